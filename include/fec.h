@@ -1,0 +1,142 @@
+/*
+ * fec.h — C ABI of the B200 (sm_100a) FEC hot path: fixed-radius connected components
+ * of a 3-D point cloud with a cluster-size noise filter and min-index labels.
+ *
+ * What is computed (PAPER.md = arXiv 2208.07678 text; readings A1..A16 in DESIGN.md §2):
+ *
+ *   d = fp32(d_th), t2 = fl32(d*d)                                       (reading A3)
+ *   pred(i,j) <=> fl(fl(fl(dx*dx) + fl(dy*dy)) + fl(dz*dz)) <= t2,  dx = fl(x_j - x_i) ...
+ *       -- Eq. 1, PAPER.md L187-194 (§2.2 "Fast Euclidean Clustering"), boundary inclusive
+ *          (reading A1), every operation one fp32 round-to-nearest, no FMA (reading A2).
+ *   C(i) = connected component of i in the graph {i~j : pred(i,j)}
+ *       -- the clusters Algorithm 1 outputs as P.lab; the paper's loop
+ *          is replaced by a grid index + lock-free union-find computing the same partition
+ *          as EC.
+ *   labels_out[i] = min C(i)  if min_size <= |C(i)| <= max_size,  else -1
+ *       -- size filter of the EC interface (reading A7, inclusive),
+ *          canonical min-index label (reading A8), -1 = noise (reading A10).
+ *
+ * Exactly one output is correct for every input (reading A16), so the result is
+ * deterministic and bitwise comparable.  There is no CPU fallback: every step runs in the
+ * library's sm_100a kernels.
+ *
+ * Pointers: unless a function says "host", pointers are CUDA device pointers on the
+ * calling thread's current device.  `points` is row-major [n][3] fp32 (x,y,z interleaved),
+ * 4-byte aligned.  `labels_out` is int32[n], in the caller's input order.
+ *
+ * Ownership: the caller owns `points`, `labels_out` and `workspace`; the library never
+ * frees or retains them past the call.  `workspace` is scratch device memory of at least
+ * fec_workspace_bytes(n) bytes, 256-byte aligned (any cudaMalloc / PyTorch allocation).
+ *
+ * Errors: argument errors are returned before any launch and leave labels_out untouched.
+ * FEC_ERR_NONFINITE / FEC_ERR_GRID_RANGE are detected on the device after the first
+ * kernel and returned before any write to labels_out.  FEC_ERR_CUDA leaves labels_out
+ * unspecified; fec_last_error() then holds the CUDA error string (thread-local).
+ */
+#ifndef FEC_H_
+#define FEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t fec_status_t;
+
+#define FEC_OK 0
+#define FEC_ERR_INVALID_ARGUMENT (-1) /* n<0 or n>INT32_MAX; d_th not finite > 0 or t2 not a
+                                         finite normal fp32 (reading A13); min>max;
+                                         max<1; min<0; null/host pointer where a device
+                                         pointer is required; workspace too small */
+#define FEC_ERR_NONFINITE (-2)        /* a coordinate is NaN or +-inf (reading A12) */
+#define FEC_ERR_GRID_RANGE (-3)       /* bbox extent / (d_th*(1+2^-16)) >= 2^20 on an axis
+                                         (reading A14): cannot be indexed */
+#define FEC_ERR_OUT_OF_MEMORY (-4)    /* fec_cluster / fec_cluster_host could not allocate */
+#define FEC_ERR_CUDA (-5)             /* a CUDA runtime error; see fec_last_error() */
+
+/* Statistics of the last successful call on this thread (instrumentation). */
+typedef struct {
+    int64_t n;              /* points */
+    int64_t cells;          /* nonempty grid cells (edge c = d_th*(1+2^-16)) */
+    int64_t groups;         /* hash mode: nonempty sub-cells (edge c/2: cliques under pred) */
+    int64_t components;     /* connected components before the size filter */
+    int64_t pair_tests;     /* predicate evaluations in the neighbour scan */
+    int64_t group_pairs;    /* sub-cell pairs examined by the neighbour scan */
+    int64_t dense_cells;    /* dense-grid mode: cells holding > 16 points (octant-grouped) */
+    int64_t dense_points;   /* dense-grid mode: points in those cells */
+    int64_t dense_tests;    /* dense-grid mode: predicate evaluations of the dense-cell kernel */
+    int64_t key_bits;       /* significant Morton-key bits sorted */
+    int32_t radix_passes;   /* LSD passes of the key sort */
+    int32_t dense_table;    /* 1: dense cell grid (counting sort), 0: Morton radix sort + hash */
+    int32_t dims[3];        /* cells per axis */
+    int32_t launches;       /* kernel launches of the call (all of them the library's own) */
+} fec_stats_t;
+
+/* Bytes of device workspace fec_cluster_ws needs for n points (an upper bound that does
+ * not depend on the coordinates).  Returns 0 for n <= 0. */
+size_t fec_workspace_bytes(int64_t n);
+
+/* Enqueue the whole path on `stream` (cudaStream_t; NULL = legacy default stream) using
+ * caller-provided workspace.  Host-synchronises once, after the bbox/validation kernel,
+ * to size the grid; returns after the remaining kernels are enqueued (they complete
+ * in stream order; labels_out is valid once the stream reaches that point).
+ * n == 0 returns FEC_OK without launching anything. */
+fec_status_t fec_cluster_ws(const float* points, int64_t n, float d_th, int64_t min_size,
+                            int64_t max_size, int32_t* labels_out, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* Synchronous convenience form: allocates the workspace itself (stream-ordered
+ * cudaMallocAsync on the legacy default stream), runs, synchronises, frees. */
+fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min_size,
+                         int64_t max_size, int32_t* labels_out);
+
+/* End-to-end form with HOST buffers: points_host [n][3] fp32 and labels_host int32[n] are
+ * host memory (pinned memory gives asynchronous copies).  Copies the points into the
+ * workspace, clusters, copies the labels back, and synchronises `stream` before
+ * returning.  `workspace` must hold fec_workspace_bytes_host(n) bytes of device memory. */
+size_t fec_workspace_bytes_host(int64_t n);
+fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th,
+                              int64_t min_size, int64_t max_size, int32_t* labels_host,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Fills *out with the statistics of this thread's last call whose status was FEC_OK.
+ * Counters that need a device read-back (components, pair_tests, group_pairs) are
+ * gathered only when fec_set_instrumentation(1) was set before that call. */
+fec_status_t fec_get_stats(fec_stats_t* out);
+void fec_set_instrumentation(int enable);
+
+/* Grid-mode override for testing (thread-local): 0 = automatic (dense cell grid whenever
+ * the bbox holds <= 4n + 2^22 cells, else Morton radix sort + hashed cells), 1 = hashed
+ * mode always.  Both modes compute identical labels. */
+void fec_set_grid_mode(int mode);
+
+/* Per-stage device timing.  With fec_set_timing(1), each call records CUDA events on its
+ * stream at the stage boundaries (a1 validate+bbox incl. the host sync, a2 keys, a3 sort,
+ * a4 gather, a5 tables, a6+a7 scan+union, a8 flatten, a9 stats, a10 relabel).
+ * fec_get_stage_times() waits for the last event of this thread's last call and writes up
+ * to max_stages durations in milliseconds; it returns the number of stages (or <0). */
+void fec_set_timing(int enable);
+int32_t fec_get_stage_times(float* ms_out, int32_t max_stages);
+const char* fec_stage_name(int32_t stage);
+
+/* Human-readable status text (static storage) and the last error detail of this thread. */
+const char* fec_status_string(fec_status_t status);
+const char* fec_last_error(void);
+
+/* Library version string, e.g. "fec-b200 0.1 sm_100a". */
+const char* fec_version(void);
+
+/* Diagnostic: evaluate the device predicate on m point pairs (a[k], b[k]), each [m][3]
+ * fp32 device arrays; out[k] = pred (uint8 0/1), d2_out[k] = the fp32 squared distance
+ * (d2_out may be NULL).  Exists so tests can check the fp32 operation order / no-FMA
+ * contract of Eq. 1 on the GPU itself.  Synchronises `stream`. */
+fec_status_t fec_debug_pred(const float* a, const float* b, int64_t m, float d_th, uint8_t* out,
+                            float* d2_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEC_H_ */

@@ -1,0 +1,225 @@
+"""Python binding of the FEC B200 library (argument marshalling only).
+
+Every step of the path runs in libfec.so's sm_100a kernels behind the C ABI declared in
+include/fec.h; this module only converts tensors to pointers, takes device memory for the
+workspace from PyTorch's caching allocator and passes PyTorch's current CUDA stream.
+There is no CPU fallback: if libfec.so is missing or no CUDA device is present, calls
+raise.
+
+    labels = cluster(points_cuda_f32_nx3, d_th, min_size, max_size)   # int32 [n], device
+    labels = cluster_host(points_np, d_th, min_size, max_size)        # host in, host out
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["cluster", "cluster_host", "workspace_bytes", "workspace_bytes_host", "stats",
+           "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfec.so")
+
+OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_CUDA = 0, -1, -2, -3, -4, -5
+
+# every symbol include/fec.h declares
+EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
+           "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
+           "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
+           "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode")
+
+
+class FecStats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("cells", ctypes.c_int64), ("groups", ctypes.c_int64),
+                ("components", ctypes.c_int64), ("pair_tests", ctypes.c_int64),
+                ("group_pairs", ctypes.c_int64), ("dense_cells", ctypes.c_int64),
+                ("dense_points", ctypes.c_int64), ("dense_tests", ctypes.c_int64),
+                ("key_bits", ctypes.c_int64),
+                ("radix_passes", ctypes.c_int32), ("dense_table", ctypes.c_int32),
+                ("dims", ctypes.c_int32 * 3), ("launches", ctypes.c_int32)]
+
+
+class FecError(RuntimeError):
+    def __init__(self, code: int, detail: str):
+        super().__init__(f"{_status_string(code)}: {detail}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libfec.so (raises if it has not been built: no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build() "
+                              "(the FEC path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, f32, vp, sz = ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t
+        L.fec_workspace_bytes.restype = sz
+        L.fec_workspace_bytes.argtypes = [i64]
+        L.fec_workspace_bytes_host.restype = sz
+        L.fec_workspace_bytes_host.argtypes = [i64]
+        L.fec_cluster_ws.restype = ctypes.c_int32
+        L.fec_cluster_ws.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
+        L.fec_cluster.restype = ctypes.c_int32
+        L.fec_cluster.argtypes = [vp, i64, f32, i64, i64, vp]
+        L.fec_cluster_host.restype = ctypes.c_int32
+        L.fec_cluster_host.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
+        L.fec_get_stats.restype = ctypes.c_int32
+        L.fec_get_stats.argtypes = [ctypes.POINTER(FecStats)]
+        L.fec_set_instrumentation.restype = None
+        L.fec_set_instrumentation.argtypes = [ctypes.c_int]
+        L.fec_status_string.restype = ctypes.c_char_p
+        L.fec_status_string.argtypes = [ctypes.c_int32]
+        L.fec_last_error.restype = ctypes.c_char_p
+        L.fec_last_error.argtypes = []
+        L.fec_version.restype = ctypes.c_char_p
+        L.fec_version.argtypes = []
+        L.fec_set_grid_mode.restype = None
+        L.fec_set_grid_mode.argtypes = [ctypes.c_int]
+        L.fec_set_timing.restype = None
+        L.fec_set_timing.argtypes = [ctypes.c_int]
+        L.fec_get_stage_times.restype = ctypes.c_int32
+        L.fec_get_stage_times.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int32]
+        L.fec_stage_name.restype = ctypes.c_char_p
+        L.fec_stage_name.argtypes = [ctypes.c_int32]
+        L.fec_debug_pred.restype = ctypes.c_int32
+        L.fec_debug_pred.argtypes = [vp, vp, i64, f32, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _status_string(code: int) -> str:
+    try:
+        return lib().fec_status_string(code).decode()
+    except Exception:  # pragma: no cover
+        return str(code)
+
+
+def _check(code: int):
+    if code != OK:
+        raise FecError(code, lib().fec_last_error().decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def workspace_bytes(n: int) -> int:
+    return int(lib().fec_workspace_bytes(int(n)))
+
+
+def workspace_bytes_host(n: int) -> int:
+    return int(lib().fec_workspace_bytes_host(int(n)))
+
+
+def _f32(d_th: float) -> float:
+    # the C ABI takes d_th as fp32; round here so callers and the oracle see the same value
+    return float(np.float32(d_th))
+
+
+def cluster(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
+            workspace=None, stream=None):
+    """Labels of `points` (CUDA float32 tensor [n, 3], contiguous) on the current device.
+
+    Returns an int32 CUDA tensor [n]: min input index of the point's component, or -1
+    when the component size is outside [min_size, max_size].  Enqueued on PyTorch's
+    current stream (or `stream`); the result is ready in stream order."""
+    torch = _torch()
+    if not (isinstance(points, torch.Tensor) and points.is_cuda):
+        raise TypeError("points must be a CUDA tensor (use cluster_host for host arrays)")
+    if points.dtype != torch.float32 or points.dim() != 2 or points.shape[1] != 3:
+        raise TypeError("points must be float32 [n, 3]")
+    points = points.contiguous()
+    n = points.shape[0]
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=points.device)
+    if n == 0:
+        _check(lib().fec_cluster_ws(None, 0, _f32(d_th), int(min_size), int(max_size), None, None, 0, None))
+        return out
+    nb = workspace_bytes(n)
+    if workspace is None or workspace.numel() < nb:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=points.device)
+    st = stream if stream is not None else torch.cuda.current_stream(points.device)
+    _check(lib().fec_cluster_ws(points.data_ptr(), n, _f32(d_th), int(min_size), int(max_size),
+                                out.data_ptr(), workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    return out
+
+
+def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
+                 workspace=None, stream=None, device=None):
+    """End-to-end form: host float32 [n, 3] in (numpy or CPU tensor; pinned memory gives
+    asynchronous copies), host int32 [n] labels out.  The host<->device copies run inside
+    the C ABI call (fec_cluster_host)."""
+    torch = _torch()
+    if isinstance(points, torch.Tensor):
+        if points.is_cuda:
+            raise TypeError("cluster_host takes host memory")
+        p = points.contiguous()
+        n = p.shape[0]
+        ptr = p.data_ptr()
+        keep = p
+    else:
+        p = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        n = p.shape[0]
+        ptr = p.ctypes.data
+        keep = p
+    if out is None:
+        out = np.empty(n, dtype=np.int32)
+    out_ptr = out.data_ptr() if isinstance(out, torch.Tensor) else out.ctypes.data
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    nb = workspace_bytes_host(n)
+    if n and (workspace is None or workspace.numel() < nb):
+        workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().fec_cluster_host(ptr if n else None, n, _f32(d_th), int(min_size), int(max_size),
+                                  out_ptr if n else None, workspace.data_ptr() if n else None,
+                                  workspace.numel() if n else 0, st.cuda_stream))
+    del keep
+    return out
+
+
+def set_instrumentation(enable: bool):
+    lib().fec_set_instrumentation(1 if enable else 0)
+
+
+def stats() -> dict:
+    s = FecStats()
+    _check(lib().fec_get_stats(ctypes.byref(s)))
+    d = {k: getattr(s, k) for k, _ in FecStats._fields_ if k != "dims"}
+    d["dims"] = list(s.dims)
+    return d
+
+
+def set_grid_mode(mode: int):
+    """0 = automatic, 1 = always the hashed (Morton radix-sort) mode.  Testing aid."""
+    lib().fec_set_grid_mode(int(mode))
+
+
+def set_timing(enable: bool):
+    lib().fec_set_timing(1 if enable else 0)
+
+
+def stage_times() -> dict:
+    """{stage name: ms} of this thread's last timed call (waits for its last event)."""
+    buf = (ctypes.c_float * 16)()
+    k = lib().fec_get_stage_times(buf, 16)
+    if k < 0:
+        raise FecError(ERR_INVALID_ARGUMENT, lib().fec_last_error().decode())
+    return {lib().fec_stage_name(i).decode(): float(buf[i]) for i in range(k)}
+
+
+def debug_pred(a, b, d_th: float):
+    """Device predicate on pairs (CUDA float32 [m,3] tensors) -> (bool tensor, d2 tensor)."""
+    torch = _torch()
+    m = a.shape[0]
+    out = torch.empty(m, dtype=torch.uint8, device=a.device)
+    d2 = torch.empty(m, dtype=torch.float32, device=a.device)
+    st = torch.cuda.current_stream(a.device)
+    _check(lib().fec_debug_pred(a.contiguous().data_ptr(), b.contiguous().data_ptr(), m, _f32(d_th),
+                                out.data_ptr(), d2.data_ptr(), st.cuda_stream))
+    return out.bool(), d2

@@ -1,0 +1,501 @@
+// C ABI (include/fec.h) and host orchestration of the FEC sm_100a pipeline.
+#include <float.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "fec.h"
+#include "fec_kernels.cuh"
+
+using namespace fec;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local fec_stats_t g_stats;
+thread_local bool g_stats_valid = false;
+thread_local int g_instrument = 0;
+thread_local Meta* g_pinned_meta = nullptr;
+thread_local int g_timing = 0;
+thread_local int g_grid_mode = 0;
+
+constexpr int kStages = 10;
+const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",       "a3_sort",
+                                          "a4_gather_fixup",  "a5_tables_init",    "a6a7_union_sparse",
+                                          "a6a7_union_dense", "a8_flatten",        "a9_stats",
+                                          "a10_relabel"};
+struct StageEvents {
+    cudaEvent_t ev[kStages + 1] = {};
+    bool created = false;
+    bool recorded = false;
+};
+thread_local StageEvents g_ev;
+
+// Records the boundary event `i` (0 = start ... kStages = end) when timing is enabled.
+inline void mark(int i, cudaStream_t st) {
+    if (!g_timing) return;
+    if (!g_ev.created) {
+        for (auto& e : g_ev.ev) cudaEventCreate(&e);
+        g_ev.created = true;
+    }
+    cudaEventRecord(g_ev.ev[i], st);
+    if (i == kStages) g_ev.recorded = true;
+}
+
+constexpr int kMaxBBoxBlocks = 148 * 8;
+
+fec_status_t fail_cuda(cudaError_t e, const char* where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return FEC_ERR_CUDA;
+}
+#define FEC_CUDA(call)                                   \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return fail_cuda(e_, #call); \
+    } while (0)
+
+struct DevInfo {
+    int sms = 0;
+    int scan_blocks_per_sm = 0;
+};
+DevInfo dev_info() {
+    static DevInfo cache[64];
+    int d = 0;
+    cudaGetDevice(&d);
+    DevInfo& di = cache[d & 63];
+    if (di.sms == 0) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_scan_union, SCAN_THREADS, 0);
+        di.scan_blocks_per_sm = b > 0 ? b : 1;
+    }
+    return di;
+}
+
+int64_t dense_cap(int64_t n) { return 4 * n + (int64_t(1) << 22); }
+int64_t hash_cap(int64_t n) {
+    int64_t c = 1024;
+    while (c < 2 * n) c <<= 1;
+    return c;
+}
+
+// Workspace = common part + max(radix/hash-mode part, dense-grid-mode part).
+struct Layout {
+    // common
+    Meta* meta;
+    float* part;
+    float4* spts;
+    int *parent, *size, *minidx;
+    // radix / hash mode
+    u64 *keyA, *keyB;
+    int *valA, *valB;
+    u64* flags;
+    u64* scan64;
+    uint32_t* counts;
+    uint32_t* scan32;
+    Tables T;
+    int num_tiles;
+    // dense-grid mode
+    uint32_t* cstart;   // [cells+1] counts, then exclusive prefix (cell start)
+    int* crec;          // [cells]   dense record id of a dense cell
+    uint32_t* dscan;    // scan scratch
+    uint32_t* slot;     // [n]
+    int* sidx;          // [n] input index of each sorted position
+    uint32_t* pcell;    // [n] linear cell of each sorted position
+    uint8_t* octs;      // [n]
+    int* dlist;         // dense cells
+    DenseRec* drec;     // their records
+    float4* tmp_pts;    // staging for very large dense cells
+    int* tmp_idx;
+    size_t total;
+};
+
+Layout carve(char* base, int64_t n) {
+    Layout L{};
+    Carver cv{base, 0, 0};
+    L.meta = cv.take<Meta>(1);
+    L.part = cv.take<float>(6 * kMaxBBoxBlocks);
+    L.spts = cv.take<float4>(n);
+    L.parent = cv.take<int>(n);
+    L.size = cv.take<int>(n);
+    L.minidx = cv.take<int>(n);
+    const size_t common = (cv.off + 255) & ~size_t(255);
+    // radix / hash mode
+    Carver a{base, common, 0};
+    L.keyA = a.take<u64>(n);
+    L.keyB = a.take<u64>(n);
+    L.valA = a.take<int>(n);
+    L.valB = a.take<int>(n);
+    L.flags = a.take<u64>(n + 1);
+    L.scan64 = a.take<u64>(scan_scratch_elems(n + 1));
+    L.num_tiles = (int)((n + RS_TILE - 1) / RS_TILE);
+    L.counts = a.take<uint32_t>((size_t)256 * L.num_tiles);
+    L.scan32 = a.take<uint32_t>(scan_scratch_elems((int64_t)256 * L.num_tiles));
+    L.T.gstart = a.take<int>(n + 1);
+    L.T.goct = a.take<uint8_t>(n);
+    L.T.cell_gstart = a.take<int>(n + 1);
+    L.T.cell_pc = a.take<u64>(n);
+    const int64_t hc = hash_cap(n);
+    L.T.hkey = a.take<u64>(hc);
+    L.T.hval = a.take<int>(hc);
+    L.T.dense = nullptr;
+    // dense-grid mode
+    const int64_t dc = dense_cap(n);
+    Carver b{base, common, 0};
+    L.cstart = b.take<uint32_t>(dc + 1);
+    L.crec = b.take<int>(dc);
+    L.dscan = b.take<uint32_t>(scan_scratch_elems(dc + 1));
+    L.slot = b.take<uint32_t>(n);
+    L.sidx = b.take<int>(n);
+    L.pcell = b.take<uint32_t>(n);
+    L.octs = b.take<uint8_t>(n);
+    L.dlist = b.take<int>(n / (SPARSE_MAX + 1) + 16);
+    L.drec = b.take<DenseRec>(n / (SPARSE_MAX + 1) + 16);
+    L.tmp_pts = b.take<float4>(n);
+    L.tmp_idx = b.take<int>(n);
+    L.total = std::max(a.off, b.off) + 256;
+    return L;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int ceil_log2(int64_t v) {
+    int b = 0;
+    while ((int64_t(1) << b) < v) ++b;
+    return b;
+}
+
+fec_status_t check_args(int64_t n, float d, int64_t mn, int64_t mx, float* t2_out) {
+    if (n < 0 || n > INT32_MAX) { g_err = "n out of range [0, INT32_MAX]"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!(d > 0.0f) || !std::isfinite(d)) { g_err = "d_th must be finite and > 0"; return FEC_ERR_INVALID_ARGUMENT; }
+    volatile float dv = d;
+    const float t2 = dv * dv;  // one fp32 rounding (reading A3)
+    if (!std::isfinite(t2) || t2 < FLT_MIN) {
+        g_err = "d_th*d_th must be a finite normal fp32 (reading A13)";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    if (mn < 0 || mx < 1 || mn > mx) { g_err = "need 0 <= min_size <= max_size, max_size >= 1"; return FEC_ERR_INVALID_ARGUMENT; }
+    *t2_out = t2;
+    return FEC_OK;
+}
+
+inline unsigned grid_for(int64_t work, int per_block, int cap) {
+    int64_t b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t max_size, int32_t* labels,
+                 void* ws, size_t ws_bytes, cudaStream_t st) {
+    g_stats_valid = false;
+    g_ev.recorded = false;
+    int launches = 0;
+    float t2 = 0.f;
+    fec_status_t rc = check_args(n, d, min_size, max_size, &t2);
+    if (rc != FEC_OK) return rc;
+    if (n == 0) {
+        std::memset(&g_stats, 0, sizeof(g_stats));
+        g_stats_valid = true;
+        return FEC_OK;
+    }
+    if (!pts || !labels || !ws) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!is_device_ptr(pts) || !is_device_ptr(labels) || !is_device_ptr(ws)) {
+        g_err = "points, labels_out and workspace must be device pointers";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    Layout L = carve(static_cast<char*>(ws), n);
+    if (ws_bytes < L.total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!g_pinned_meta) FEC_CUDA(cudaMallocHost(&g_pinned_meta, sizeof(Meta)));
+    const DevInfo di = dev_info();
+    const int cap = di.sms * 8;
+
+    // ---- a1: validate + bbox, then the only host synchronisation ----------------------
+    mark(0, st);
+    FEC_CUDA(cudaMemsetAsync(L.meta, 0, sizeof(Meta), st));
+    const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
+    const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
+    k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite);
+    k_bbox_final<<<1, 32, 0, st>>>(L.part, (int)bb_blocks, L.meta);
+    launches += 2;
+    FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    FEC_CUDA(cudaStreamSynchronize(st));
+    const Meta hm = *g_pinned_meta;
+    if (hm.nonfinite) { g_err = "non-finite coordinate"; return FEC_ERR_NONFINITE; }
+
+    // ---- grid parameters (reading A6): cell c = d(1+2^-16), sub-cell h = c/2 -----------
+    Grid g{};
+    const double c = (double)d * (1.0 + std::ldexp(1.0, -16));
+    g.h = c * 0.5;
+    g.inv_h = 1.0 / g.h;
+    int64_t cells_total = 1;
+    int key_bits = 3;
+    for (int a = 0; a < 3; ++a) {
+        g.lo[a] = (double)hm.bbox[a];
+        // the same double operations as sub_coord() on the device
+        const double smax = std::floor(((double)hm.bbox[3 + a] - g.lo[a]) * g.inv_h);
+        if (!(smax < 2097152.0)) { g_err = "bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
+        g.dims[a] = (int32_t)(((int64_t)smax >> 1) + 1);
+        g.bits[a] = ceil_log2(g.dims[a]);
+        key_bits += g.bits[a];
+        cells_total *= g.dims[a];
+    }
+    g.key_bits = key_bits;
+    g.t2 = t2;
+    const int64_t hc = hash_cap(n);
+    g.hash_mask = (u64)(hc - 1);
+    g.dense = (g_grid_mode != 1 && cells_total <= dense_cap(n) && cells_total < (int64_t)0xfffffff0ll) ? 1 : 0;
+    int passes = 0;
+    FEC_CUDA(cudaMemsetAsync(&L.meta->instrument, 0, sizeof(int), st));
+    if (g_instrument) {
+        static const int one = 1;
+        FEC_CUDA(cudaMemcpyAsync(&L.meta->instrument, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    const unsigned ew = grid_for(n, 256, cap * 4);
+    const int* val = nullptr;
+
+    if (g.dense) {
+        // smallest dimension fastest in the linear cell id (L2 locality of the slow axis)
+        int perm[3] = {0, 1, 2};
+        for (int i = 0; i < 3; ++i)
+            for (int j = i + 1; j < 3; ++j)
+                if (g.dims[perm[j]] < g.dims[perm[i]]) std::swap(perm[i], perm[j]);
+        for (int i = 0; i < 3; ++i) g.perm[i] = perm[i];
+        g.stride[perm[0]] = 1;
+        g.stride[perm[1]] = (uint32_t)g.dims[perm[0]];
+        g.stride[perm[2]] = (uint32_t)g.dims[perm[0]] * (uint32_t)g.dims[perm[1]];
+        g.sdiv[0] = g.stride[perm[2]];
+        g.sdiv[1] = g.stride[perm[1]];
+        // a2: counts
+        mark(1, st);
+        FEC_CUDA(cudaMemsetAsync(L.cstart, 0, (size_t)(cells_total + 1) * 4, st));
+        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.dlist, L.meta);
+        ++launches;
+        // a3: counting sort = scan + scatter
+        mark(2, st);
+        launches += exclusive_scan<uint32_t>(L.cstart, L.cstart, cells_total + 1, L.dscan, st);
+        k_dscatter<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.spts);
+        ++launches;
+        // a4/a5: sorted-order init, then dense-cell octant fix-up
+        mark(3, st);
+        k_dinit<<<ew, 256, 0, st>>>(L.spts, n, L.parent, L.size, L.minidx, L.sidx);
+        mark(4, st);
+        k_dfixup<<<di.sms * 4, 256, 0, st>>>(L.cstart, L.dlist, L.meta, g, L.spts, L.sidx, L.parent, L.drec, L.crec,
+                                             L.tmp_pts);
+        launches += 2;
+        // a6+a7: one sweep over all grid cells (sparse cells: lane; dense cells: warp)
+        mark(5, st);
+        k_union_sparse<<<(unsigned)((cells_total + 255) / 256), 256, 0, st>>>(L.spts, L.cstart,
+                                                                             (uint32_t)cells_total, g, L.parent,
+                                                                             L.meta);
+        mark(6, st);
+        k_union_dense<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, L.cstart, L.drec, L.crec, g,
+                                                                              L.parent, L.meta);
+        launches += 2;
+        mark(7, st);
+        val = L.sidx;
+    } else {
+        // ---- a2: keys ----------------------------------------------------------------------
+        mark(1, st);
+        k_keys<<<ew, 256, 0, st>>>(pts, n, g, L.keyA, L.valA);
+        ++launches;
+        mark(2, st);
+        // ---- a3: LSD radix sort over the significant key bits -------------------------------
+        passes = (key_bits + 7) / 8;
+        u64 *kin = L.keyA, *kout = L.keyB;
+        int *vin = L.valA, *vout = L.valB;
+        for (int p = 0; p < passes; ++p) {
+            const int shift = 8 * p;
+            k_radix_hist<<<L.num_tiles, RS_THREADS, 0, st>>>(kin, n, shift, L.counts, L.num_tiles);
+            launches += exclusive_scan<uint32_t>(L.counts, L.counts, (int64_t)256 * L.num_tiles, L.scan32, st);
+            k_radix_scatter<<<L.num_tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, L.counts,
+                                                                L.num_tiles);
+            launches += 2;
+            std::swap(kin, kout);
+            std::swap(vin, vout);
+        }
+        const u64* key = kin;
+        val = vin;
+        // ---- a4: gather ----------------------------------------------------------------------
+        mark(3, st);
+        k_gather<<<ew, 256, 0, st>>>(pts, val, n, L.spts);
+        ++launches;
+        mark(4, st);
+        // ---- a5: group / cell tables -----------------------------------------------------------
+        k_heads<<<grid_for(n + 1, 256, cap * 4), 256, 0, st>>>(key, n, L.flags);
+        launches += 1 + exclusive_scan<u64>(L.flags, L.flags, n + 1, L.scan64, st);
+        FEC_CUDA(cudaMemsetAsync(L.T.hkey, 0xFF, (size_t)hc * 8, st));
+        k_fill_tables<<<ew, 256, 0, st>>>(key, L.flags, n, g, L.T, L.meta);
+        k_init_uf<<<ew, 256, 0, st>>>(L.flags, L.T.gstart, n, L.parent, L.size, L.minidx);
+        launches += 2;
+        mark(5, st);
+        mark(6, st);
+        // ---- a6+a7: neighbour scan + union (persistent warps, dynamic cell counter) -----------
+        k_scan_union<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, g, L.T, L.parent, L.meta);
+        ++launches;
+        mark(7, st);
+    }
+
+    // ---- a8..a10 ---------------------------------------------------------------------------
+    k_flatten<<<ew, 256, 0, st>>>(L.parent, n);
+    mark(8, st);
+    k_stats<<<ew, 256, 0, st>>>(L.parent, val, n, L.size, L.minidx, L.meta);
+    mark(9, st);
+    k_relabel<<<ew, 256, 0, st>>>(L.parent, val, L.size, L.minidx, n, (long long)min_size, (long long)max_size,
+                                  labels);
+    launches += 3;
+    mark(10, st);
+    FEC_CUDA(cudaGetLastError());
+
+    std::memset(&g_stats, 0, sizeof(g_stats));
+    g_stats.n = n;
+    g_stats.cells = g_stats.groups = g_stats.components = g_stats.pair_tests = g_stats.group_pairs = -1;
+    g_stats.dense_cells = g_stats.dense_points = g_stats.dense_tests = -1;
+    g_stats.key_bits = key_bits;
+    g_stats.radix_passes = passes;
+    g_stats.dense_table = g.dense;
+    for (int a = 0; a < 3; ++a) g_stats.dims[a] = g.dims[a];
+    g_stats.launches = launches;
+    if (g_instrument) {
+        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+        FEC_CUDA(cudaStreamSynchronize(st));
+        g_stats.cells = g_pinned_meta->cells;
+        g_stats.groups = g.dense ? -1 : g_pinned_meta->groups;
+        g_stats.dense_cells = g.dense ? g_pinned_meta->ndense : -1;
+        g_stats.dense_points = g.dense ? (int64_t)g_pinned_meta->dense_points : -1;
+        g_stats.components = (int64_t)g_pinned_meta->components;
+        g_stats.pair_tests = (int64_t)(g_pinned_meta->pair_tests + g_pinned_meta->dense_tests);
+        g_stats.dense_tests = g.dense ? (int64_t)g_pinned_meta->dense_tests : -1;
+        g_stats.group_pairs = (int64_t)g_pinned_meta->group_pairs;
+    }
+    g_stats_valid = true;
+    return FEC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t fec_workspace_bytes(int64_t n) {
+    if (n <= 0) return 0;
+    return carve(nullptr, n).total;
+}
+
+size_t fec_workspace_bytes_host(int64_t n) {
+    if (n <= 0) return 0;
+    return fec_workspace_bytes(n) + ((size_t)12 * n + 256) + ((size_t)4 * n + 256);
+}
+
+fec_status_t fec_cluster_ws(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
+                            int32_t* labels_out, void* workspace, size_t workspace_bytes, void* stream) {
+    return run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes,
+               static_cast<cudaStream_t>(stream));
+}
+
+fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
+                         int32_t* labels_out) {
+    float t2;
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK || n == 0) return run(points, n, d_th, min_size, max_size, labels_out, nullptr, 0, 0);
+    const size_t b = fec_workspace_bytes(n);
+    void* ws = nullptr;
+    cudaError_t e = cudaMallocAsync(&ws, b, 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_err = std::string("cudaMallocAsync: ") + cudaGetErrorString(e);
+        return FEC_ERR_OUT_OF_MEMORY;
+    }
+    rc = run(points, n, d_th, min_size, max_size, labels_out, ws, b, 0);
+    cudaError_t e2 = cudaStreamSynchronize(0);
+    cudaFreeAsync(ws, 0);
+    cudaStreamSynchronize(0);
+    if (rc == FEC_OK && e2 != cudaSuccess) return fail_cuda(e2, "fec_cluster sync");
+    return rc;
+}
+
+fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th, int64_t min_size, int64_t max_size,
+                              int32_t* labels_host, void* workspace, size_t workspace_bytes, void* stream) {
+    float t2;
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK) return rc;
+    if (n == 0) return run(nullptr, 0, d_th, min_size, max_size, nullptr, nullptr, 0, 0);
+    if (!points_host || !labels_host || !workspace) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (workspace_bytes < fec_workspace_bytes_host(n)) { g_err = "workspace too small (see fec_workspace_bytes_host)"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t main_b = fec_workspace_bytes(n);
+    char* base = static_cast<char*>(workspace);
+    float* dpts = reinterpret_cast<float*>(base + ((main_b + 255) & ~size_t(255)));
+    int32_t* dlab = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dpts) + (((size_t)12 * n + 255) & ~size_t(255)));
+    FEC_CUDA(cudaMemcpyAsync(dpts, points_host, (size_t)12 * n, cudaMemcpyHostToDevice, st));
+    rc = run(dpts, n, d_th, min_size, max_size, dlab, workspace, main_b, st);
+    if (rc == FEC_OK) FEC_CUDA(cudaMemcpyAsync(labels_host, dlab, (size_t)4 * n, cudaMemcpyDeviceToHost, st));
+    FEC_CUDA(cudaStreamSynchronize(st));
+    return rc;
+}
+
+fec_status_t fec_get_stats(fec_stats_t* out) {
+    if (!out) return FEC_ERR_INVALID_ARGUMENT;
+    if (!g_stats_valid) { g_err = "no successful call on this thread"; return FEC_ERR_INVALID_ARGUMENT; }
+    *out = g_stats;
+    return FEC_OK;
+}
+
+void fec_set_instrumentation(int enable) { g_instrument = enable ? 1 : 0; }
+
+void fec_set_timing(int enable) { g_timing = enable ? 1 : 0; }
+
+void fec_set_grid_mode(int mode) { g_grid_mode = mode; }
+
+int32_t fec_get_stage_times(float* ms_out, int32_t max_stages) {
+    if (!g_ev.recorded) { g_err = "no timed call on this thread (fec_set_timing(1) first)"; return -1; }
+    cudaError_t e = cudaEventSynchronize(g_ev.ev[kStages]);
+    if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return -1; }
+    for (int i = 0; i < kStages && i < max_stages; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_ev.ev[i], g_ev.ev[i + 1]);
+        ms_out[i] = ms;
+    }
+    return kStages;
+}
+
+const char* fec_stage_name(int32_t stage) { return (stage >= 0 && stage < kStages) ? kStageNames[stage] : ""; }
+
+const char* fec_status_string(fec_status_t s) {
+    switch (s) {
+        case FEC_OK: return "FEC_OK";
+        case FEC_ERR_INVALID_ARGUMENT: return "FEC_ERR_INVALID_ARGUMENT";
+        case FEC_ERR_NONFINITE: return "FEC_ERR_NONFINITE";
+        case FEC_ERR_GRID_RANGE: return "FEC_ERR_GRID_RANGE";
+        case FEC_ERR_OUT_OF_MEMORY: return "FEC_ERR_OUT_OF_MEMORY";
+        case FEC_ERR_CUDA: return "FEC_ERR_CUDA";
+        default: return "FEC_ERR_UNKNOWN";
+    }
+}
+
+const char* fec_last_error(void) { return g_err.c_str(); }
+
+const char* fec_version(void) { return "fec-b200 0.1 sm_100a"; }
+
+fec_status_t fec_debug_pred(const float* a, const float* b, int64_t m, float d_th, uint8_t* out, float* d2_out,
+                            void* stream) {
+    float t2;
+    fec_status_t rc = check_args(0, d_th, 1, 1, &t2);
+    if (rc != FEC_OK) return rc;
+    if (m <= 0) return FEC_OK;
+    if (!is_device_ptr(a) || !is_device_ptr(b) || !is_device_ptr(out)) { g_err = "device pointers required"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_debug_pred<<<grid_for(m, 256, 1024), 256, 0, st>>>(a, b, m, t2, out, d2_out);
+    FEC_CUDA(cudaGetLastError());
+    FEC_CUDA(cudaStreamSynchronize(st));
+    return FEC_OK;
+}
+
+}  // extern "C"

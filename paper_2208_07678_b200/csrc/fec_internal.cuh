@@ -1,0 +1,142 @@
+// Internal device helpers and launch declarations of the FEC sm_100a path.
+// Not part of the C ABI (include/fec.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fec {
+
+using u64 = unsigned long long;
+constexpr int kWarp = 32;
+
+// ---- the predicate: Eq. 1, readings A1-A3 --------------------------
+// Each operation is an explicit round-to-nearest intrinsic, which nvcc never contracts
+// into an FMA; the library is additionally compiled with -fmad=false and without
+// fast-math / flush-to-zero.
+__device__ __forceinline__ float d2_rn(float4 a, float4 b) {
+    float dx = __fsub_rn(b.x, a.x);
+    float dy = __fsub_rn(b.y, a.y);
+    float dz = __fsub_rn(b.z, a.z);
+    float s = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+    return __fadd_rn(s, __fmul_rn(dz, dz));
+}
+__device__ __forceinline__ bool pred(float4 a, float4 b, float t2) { return d2_rn(a, b) <= t2; }
+
+// ---- grid geometry (host-computed once per call, passed by value) ---------------------
+struct Grid {
+    double lo[3];       // bbox minimum (fp32 values widened)
+    double inv_h;       // 1/h (double): sub-cell coordinate = floor((x - lo) * inv_h)
+    double h;           // sub-cell edge = c/2, c = d*(1+2^-16)
+    int32_t dims[3];    // cells per axis
+    int32_t bits[3];    // ceil(log2(dims)) per axis (cell-level Morton bits, hash mode)
+    int32_t key_bits;   // 3 + sum(bits): significant bits of the sub-cell Morton key
+    int32_t dense;      // 1: dense cell grid (counting sort), 0: Morton radix sort + hash
+    uint32_t stride[3]; // dense mode: linear cell id = sum_a c[a]*stride[a] (smallest dim fastest)
+    int32_t perm[3];    // dense mode: axes from fastest to slowest
+    uint32_t sdiv[2];   // dense mode: stride[perm[2]], stride[perm[1]] (for decoding)
+    u64 hash_mask;
+    float t2;
+};
+
+// Sub-cell coordinate on one axis: floor((x - lo) * inv_h).  Cell = sub >> 1 and the octant
+// bit = sub & 1, so cell and sub-cell always agree.  Monotone in x (DESIGN.md §4.2 shows
+// that pred-true pairs differ by <= 2 sub-cells and <= 1 cell on every axis).
+__device__ __forceinline__ uint32_t sub_coord(float x, double lo, double inv_h) {
+    return (uint32_t)floor(__dmul_rn(__dadd_rn((double)x, -lo), inv_h));
+}
+
+// Generalised Morton interleave of cell coordinates with per-axis bit counts: level l takes
+// bit l of x, y, z (each only while l < bits[axis]).  Prefixed (low bits) by the octant.
+__device__ __forceinline__ u64 subcell_key(uint32_t sx, uint32_t sy, uint32_t sz, const Grid& g) {
+    u64 key = (u64)((sx & 1u) | ((sy & 1u) << 1) | ((sz & 1u) << 2));
+    uint32_t c[3] = {sx >> 1, sy >> 1, sz >> 1};
+    int pos = 3;
+    int maxb = max(g.bits[0], max(g.bits[1], g.bits[2]));
+    for (int l = 0; l < maxb; ++l) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (l < g.bits[a]) {
+                key |= (u64)((c[a] >> l) & 1u) << pos;
+                ++pos;
+            }
+        }
+    }
+    return key;
+}
+
+__device__ __forceinline__ u64 pack_cell(uint32_t cx, uint32_t cy, uint32_t cz) {
+    return (u64)cx | ((u64)cy << 21) | ((u64)cz << 42);
+}
+__device__ __forceinline__ u64 hash_cell(u64 pc) {
+    pc ^= pc >> 31;
+    pc *= 0x7fb5d329728ea185ull;
+    pc ^= pc >> 27;
+    pc *= 0x81dadef4bc2dd44dull;
+    pc ^= pc >> 33;
+    return pc;
+}
+
+// ---- union-find over sorted positions (ECL-CC style) ----------------------------------
+// Invariant: parent[x] >= x, and a root r has parent[r] == r.  Hooks attach the SMALLER
+// root under the larger one with atomicCAS (performed at L2, always on the current value);
+// path compression only ever raises a parent.  Roots are therefore the highest sorted
+// position of their set: the kernels sweep the sorted order upwards, so the roots that
+// finds reach sit near the sweep front (in L2), not at the far start of the array.
+// Reads are plain (L1-cacheable) loads: a stale value is still an ancestor, so a find may
+// return a non-root; the hook's CAS then fails and returns the current parent, and the loop
+// continues from there (values strictly increase, so it terminates).  Two finds that return
+// the same node prove the inputs are connected, so skipping on equal roots is always
+// sound.  The loads/stores are inline PTX so the compiler cannot merge or hoist them.
+__device__ __forceinline__ int ld_parent(const int* p, int x) {
+    int v;
+    asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p + x) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_parent(int* p, int x, int v) {
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p + x), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int uf_find(int* parent, int v) {
+    int curr = ld_parent(parent, v);
+    if (curr != v) {
+        int prev = v, next;
+        while (curr < (next = ld_parent(parent, curr))) {
+            st_parent(parent, prev, next);  // pointer jumping: prev skips to its grandparent
+            prev = curr;
+            curr = next;
+        }
+    }
+    return curr;
+}
+
+__device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
+    int ra = uf_find(parent, a), rb = uf_find(parent, b);
+    while (ra != rb) {
+        if (ra > rb) { int t = ra; ra = rb; rb = t; }
+        int old = atomicCAS(parent + ra, ra, rb);  // hook smaller root under larger
+        if (old == ra) return;
+        ra = uf_find(parent, old);
+        rb = uf_find(parent, rb);
+    }
+}
+
+// ---- device-wide exclusive scan (host recursion over tiles) ---------------------------
+template <typename T>
+int exclusive_scan(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st);  // returns launches
+size_t scan_scratch_elems(int64_t n);
+
+// ---- workspace carving -----------------------------------------------------------------
+struct Carver {
+    char* base;
+    size_t off = 0, cap;
+    template <typename T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+}  // namespace fec

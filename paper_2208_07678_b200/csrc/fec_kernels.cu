@@ -1,0 +1,451 @@
+// FEC hot-path kernels for sm_100a.  Step numbering follows SURVEY.md §8(a) / DESIGN.md §4:
+//   a1 K0 bbox+validate | a2 K1 keys | a3 K2 radix sort | a4 K3 gather | a5 K4 group/cell
+//   tables | a6+a7 K5 neighbour scan + union | a8 K6 flatten | a9 K7 stats | a10 K8 relabel
+#include <float.h>
+
+#include "fec_internal.cuh"
+#include "fec_kernels.cuh"
+#include "fec_pairs.cuh"
+
+namespace fec {
+
+// =====================================================================================
+// a1  K0: validation + bounding box (isfinite over all 3n floats; per-axis min/max)
+// =====================================================================================
+__device__ __forceinline__ void bb_acc(float v, float& mn, float& mx, int& bad) {
+    bad |= !isfinite(v);
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+}
+
+__global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ p, int64_t n, int vec4,
+                                                     float* __restrict__ part, int* __restrict__ nonfinite) {
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    int bad = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t tail_start = 0;
+    if (vec4) {
+        // 4 points = 12 floats = 3 float4 per quad; the pointer is 16-byte aligned
+        const float4* q = reinterpret_cast<const float4*>(p);
+        const int64_t nq = n >> 2;
+        for (int64_t i = t0; i < nq; i += stride) {
+            float4 a = __ldg(q + 3 * i), b = __ldg(q + 3 * i + 1), c = __ldg(q + 3 * i + 2);
+            float v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int k = 0; k < 12; ++k) bb_acc(v[k], mn[k % 3], mx[k % 3], bad);
+        }
+        tail_start = nq << 2;
+    }
+    for (int64_t i = tail_start + t0; i < n; i += stride) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) bb_acc(__ldg(p + 3 * i + k), mn[k], mx[k], bad);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    __shared__ float s[8][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { s[w][k] = mn[k]; s[w][3 + k] = mx[k]; }
+        if (bad) atomicOr(nonfinite, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        part[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+__global__ void k_bbox_final(const float* __restrict__ part, int nblocks, Meta* __restrict__ meta) {
+    const int k = threadIdx.x;  // 6 threads
+    if (k >= 6) return;
+    float v = part[k];
+    for (int b = 1; b < nblocks; ++b) v = k < 3 ? fminf(v, part[b * 6 + k]) : fmaxf(v, part[b * 6 + k]);
+    meta->bbox[k] = v;
+}
+
+// =====================================================================================
+// a2  K1: sub-cell Morton keys; idx = iota
+// =====================================================================================
+__global__ void __launch_bounds__(256) k_keys(const float* __restrict__ p, int64_t n, Grid g,
+                                             u64* __restrict__ key, int* __restrict__ val) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t sx = sub_coord(__ldg(p + 3 * i), g.lo[0], g.inv_h);
+        uint32_t sy = sub_coord(__ldg(p + 3 * i + 1), g.lo[1], g.inv_h);
+        uint32_t sz = sub_coord(__ldg(p + 3 * i + 2), g.lo[2], g.inv_h);
+        key[i] = subcell_key(sx, sy, sz, g);
+        val[i] = (int)i;
+    }
+}
+
+// =====================================================================================
+// a3  K2: LSD radix sort, 8-bit digits, stable (reduce-then-scan per pass)
+// =====================================================================================
+__global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const u64* __restrict__ key, int64_t n, int shift,
+                                                          uint32_t* __restrict__ counts, int num_tiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+    for (int k = 0; k < RS_ITEMS; ++k) {
+        int64_t i = base + k * RS_THREADS + threadIdx.x;
+        if (i < n) atomicAdd(&h[(unsigned)(key[i] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * num_tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter.  Warp w of a tile owns the contiguous keys [w*512, w*512+512); iteration
+// `it` covers 32 consecutive keys, so (warp, it, lane) order equals input order.  Ranks:
+// (digit offset of this tile) + (same-digit keys in earlier warps) + (in earlier
+// iterations of this warp) + (in lower lanes of this iteration).
+__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restrict__ kin, const int* __restrict__ vin,
+                                                             u64* __restrict__ kout, int* __restrict__ vout,
+                                                             int64_t n, int shift, const uint32_t* __restrict__ offs,
+                                                             int num_tiles) {
+    __shared__ uint32_t wcnt[RS_THREADS / kWarp][256];
+    __shared__ uint32_t goff[256];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < (RS_THREADS / kWarp) * 256; d += RS_THREADS) (&wcnt[0][0])[d] = 0;
+    goff[threadIdx.x] = offs[(int64_t)threadIdx.x * num_tiles + blockIdx.x];
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * (RS_ITEMS * kWarp);
+    const unsigned lt = (1u << lane) - 1u;
+    u64 k[RS_ITEMS];
+    int v[RS_ITEMS];
+    uint32_t rank[RS_ITEMS];
+    int dig[RS_ITEMS];
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        int64_t i = base + it * kWarp + lane;
+        bool ok = i < n;
+        k[it] = ok ? kin[i] : 0ull;
+        v[it] = ok ? vin[i] : 0;
+        dig[it] = ok ? (int)((unsigned)(k[it] >> shift) & 255u) : 256;
+    }
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        const int d = dig[it];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t c = d < 256 ? wcnt[w][d] : 0u;
+        __syncwarp();
+        rank[it] = c + __popc(peers & lt);
+        if (d < 256 && (peers & lt) == 0u) wcnt[w][d] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_THREADS / kWarp; ++ww) {
+            uint32_t t = wcnt[ww][d];
+            wcnt[ww][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        const int d = dig[it];
+        if (d < 256) {
+            uint32_t pos = goff[d] + wcnt[w][d] + rank[it];
+            kout[pos] = k[it];
+            vout[pos] = v[it];
+        }
+    }
+}
+
+// =====================================================================================
+// a4  K3: gather points into sorted order as float4 (x, y, z, idx)
+// =====================================================================================
+__global__ void __launch_bounds__(256) k_gather(const float* __restrict__ p, const int* __restrict__ val, int64_t n,
+                                               float4* __restrict__ spts) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        int i = val[s];
+        spts[s] = make_float4(__ldg(p + 3 * (int64_t)i), __ldg(p + 3 * (int64_t)i + 1), __ldg(p + 3 * (int64_t)i + 2),
+                              __int_as_float(i));
+    }
+}
+
+// =====================================================================================
+// a5  K4: group (sub-cell) and cell tables
+// =====================================================================================
+// flags[s] = groupHead | cellHead << 32 ; flags[n] = 0 (so the exclusive scan yields totals)
+__global__ void __launch_bounds__(256) k_heads(const u64* __restrict__ key, int64_t n, u64* __restrict__ flags) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= n; s += (int64_t)gridDim.x * blockDim.x) {
+        u64 f = 0;
+        if (s < n) {
+            u64 k = key[s];
+            if (s == 0) {
+                f = 1ull | (1ull << 32);
+            } else {
+                u64 kp = key[s - 1];
+                f = (u64)(k != kp) | ((u64)((k >> 3) != (kp >> 3)) << 32);
+            }
+        }
+        flags[s] = f;
+    }
+}
+
+__device__ __forceinline__ void decode_cell(u64 key, const Grid& g, uint32_t& cx, uint32_t& cy, uint32_t& cz) {
+    uint32_t c[3] = {0u, 0u, 0u};
+    int pos = 3;
+    int maxb = max(g.bits[0], max(g.bits[1], g.bits[2]));
+    for (int l = 0; l < maxb; ++l) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (l < g.bits[a]) {
+                c[a] |= (uint32_t)((key >> pos) & 1ull) << l;
+                ++pos;
+            }
+        }
+    }
+    cx = c[0]; cy = c[1]; cz = c[2];
+}
+
+__global__ void __launch_bounds__(256) k_fill_tables(const u64* __restrict__ key, const u64* __restrict__ ex, int64_t n,
+                                                    Grid g, Tables T, Meta* __restrict__ meta) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const u64 e0 = ex[s], e1 = ex[s + 1];
+        const u64 d = e1 - e0;
+        const int gidx = (int)(uint32_t)e0;
+        const int cidx = (int)(e0 >> 32);
+        if (d & 1ull) {  // group head
+            const u64 k = key[s];
+            T.gstart[gidx] = (int)s;
+            T.goct[gidx] = (uint8_t)(k & 7ull);
+            if (d >> 32) {  // cell head
+                T.cell_gstart[cidx] = gidx;
+                uint32_t cx, cy, cz;
+                decode_cell(k, g, cx, cy, cz);
+                const u64 pc = pack_cell(cx, cy, cz);
+                T.cell_pc[cidx] = pc;
+                if (g.dense) {
+                    T.dense[((int64_t)cz * g.dims[1] + cy) * g.dims[0] + cx] = cidx;
+                } else {
+                    u64 slot = hash_cell(pc) & g.hash_mask;
+                    while (true) {
+                        u64 prev = atomicCAS(T.hkey + slot, ~0ull, pc);
+                        if (prev == ~0ull) { T.hval[slot] = cidx; break; }
+                        slot = (slot + 1) & g.hash_mask;
+                    }
+                }
+            }
+        }
+        if (s == n - 1) {
+            const u64 tot = ex[n];
+            const int G = (int)(uint32_t)tot, U = (int)(tot >> 32);
+            T.gstart[G] = (int)n;
+            T.cell_gstart[U] = G;
+            meta->groups = G;
+            meta->cells = U;
+        }
+    }
+}
+
+// parent[s] = last point of s's sub-cell (sub-cells are cliques under pred: DESIGN.md §4.5);
+// size/minidx accumulators initialised here too.
+__global__ void __launch_bounds__(256) k_init_uf(const u64* __restrict__ ex, const int* __restrict__ gstart, int64_t n,
+                                                int* __restrict__ parent, int* __restrict__ size,
+                                                int* __restrict__ minidx) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const int gidx = (int)(uint32_t)ex[s + 1] - 1;
+        parent[s] = gstart[gidx + 1] - 1;
+        size[s] = 0;
+        minidx[s] = 0x7fffffff;
+    }
+}
+
+// =====================================================================================
+// a6+a7  K5: neighbour scan fused with union (warp per cell; sub-cell group pairs)
+// =====================================================================================
+__device__ __forceinline__ int cell_lookup(const Grid& g, const Tables& T, int cx, int cy, int cz) {
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= g.dims[0] || cy >= g.dims[1] || cz >= g.dims[2]) return -1;
+    const u64 pc = pack_cell((uint32_t)cx, (uint32_t)cy, (uint32_t)cz);
+    u64 slot = hash_cell(pc) & g.hash_mask;
+    while (true) {
+        const u64 k = __ldg(T.hkey + slot);
+        if (k == pc) return __ldg(T.hval + slot);
+        if (k == ~0ull) return -1;
+        slot = (slot + 1) & g.hash_mask;
+    }
+}
+
+constexpr int kCellChunk = 8;  // cells taken per atomic on the dynamic work counter
+
+// Hash mode (sparse, huge bounding boxes): warp per nonempty cell, cells visited in Morton
+// order, groups = octants of the cell.
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_union(const float4* __restrict__ spts, Grid g, Tables T,
+                                                           int* __restrict__ parent, Meta* __restrict__ meta) {
+    __shared__ PairSmem sm[SCAN_THREADS / kWarp];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    PairSmem& S = sm[w];
+    const int U = meta->cells;
+    const float t2 = g.t2;
+    unsigned long long n_tests = 0, n_pairs = 0;
+
+    while (true) {
+        int c0 = 0;
+        if (lane == 0) c0 = atomicAdd(&meta->work, kCellChunk);
+        c0 = __shfl_sync(0xffffffffu, c0, 0);
+        if (c0 >= U) break;
+        const int c1 = min(U, c0 + kCellChunk);
+        for (int c = c0; c < c1; ++c) {
+            const int gs = __ldg(T.cell_gstart + c), ge = __ldg(T.cell_gstart + c + 1);
+            const int np = ge - gs;
+            if (lane <= np) S.ps[lane] = __ldg(T.gstart + gs + lane);
+            if (lane < np) S.po[lane] = __ldg(T.goct + gs + lane);
+            const u64 pc = __ldg(T.cell_pc + c);
+            const int cx = (int)(pc & 0x1fffff), cy = (int)((pc >> 21) & 0x1fffff), cz = (int)(pc >> 42);
+            int qcell = -1;
+            if (lane < 13) qcell = cell_lookup(g, T, cx + c_fwd[lane][0], cy + c_fwd[lane][1], cz + c_fwd[lane][2]);
+            __syncwarp();
+            for (int k = -1; k < 13; ++k) {
+                const int q = k < 0 ? c : __shfl_sync(0xffffffffu, qcell, k);
+                if (q < 0) continue;
+                int nq;
+                if (k < 0) {
+                    nq = np;
+                    if (lane <= np) S.qs[lane] = S.ps[lane];
+                    if (lane < np) S.qo[lane] = S.po[lane];
+                } else {
+                    const int qgs = __ldg(T.cell_gstart + q), qge = __ldg(T.cell_gstart + q + 1);
+                    nq = qge - qgs;
+                    if (lane <= nq) S.qs[lane] = __ldg(T.gstart + qgs + lane);
+                    if (lane < nq) S.qo[lane] = __ldg(T.goct + qgs + lane);
+                }
+                __syncwarp();
+                const int nqueue = k < 0 ? build_queue(S, np, nq, true, 0, 0, 0, lane)
+                                         : build_queue(S, np, nq, false, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], lane);
+                n_pairs += (lane == 0) ? (unsigned long long)nqueue : 0ull;
+                load_roots(S, np, nq, parent, lane);
+            process_queue(S, nqueue, spts, parent, t2, lane, n_tests);
+            }
+        }
+    }
+    if (meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
+            n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&meta->pair_tests, n_tests);
+            atomicAdd(&meta->group_pairs, n_pairs);
+        }
+    }
+}
+
+// =====================================================================================
+// a8  K6: flatten   a9  K7: component stats   a10  K8: filter + relabel + scatter
+// =====================================================================================
+// Read-only root walk, then one store per element.  (A compressing find here would let a
+// thread's late path-halving store overwrite another thread's final root with a stale
+// intermediate; each parent[s] must be written only by its own thread.)
+__global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64_t n) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        int curr = ld_parent(parent, (int)s), next;
+        if (curr == (int)s) continue;
+        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        st_parent(parent, (int)s, curr);
+    }
+}
+
+// Component size and minimum input index per root.  Atomics are aggregated per warp (one
+// per distinct root in the warp) and then per block through a small shared-memory table,
+// so a giant component (C5: ~40% of all points) costs one global atomic per block instead
+// of one per warp.  Blocks own contiguous ranges (the sorted order is spatial).
+constexpr int HH_SLOTS = 256;
+__global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+                                              int* __restrict__ size, int* __restrict__ minidx,
+                                              Meta* __restrict__ meta) {
+    __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
+    for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned long long roots = 0;
+    const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    for (int64_t s0 = b0; s0 < b1; s0 += blockDim.x) {
+        const int64_t s = s0 + threadIdx.x;
+        const bool ok = s < b1;
+        const int r = ok ? __ldg(parent + s) : -1;
+        const int v = ok ? __ldg(val + s) : 0x7fffffff;
+        roots += (ok && r == (int)s) ? 1ull : 0ull;
+        unsigned todo = __ballot_sync(0xffffffffu, ok);
+        while (todo) {
+            const int leader = __ffs(todo) - 1;
+            const int key = __shfl_sync(0xffffffffu, r, leader);
+            const bool mem = ok && r == key;
+            const unsigned peers = __ballot_sync(0xffffffffu, mem);
+            const int mn = __reduce_min_sync(0xffffffffu, mem ? v : 0x7fffffff);
+            if (lane == leader) {
+                const int cnt = __popc(peers);
+                unsigned h = ((unsigned)key * 2654435761u) >> 24;  // 256 slots
+                bool done = false;
+                for (int probe = 0; probe < 4 && !done; ++probe, h = (h + 1) & (HH_SLOTS - 1)) {
+                    int cur = hkey[h];
+                    if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
+                    if (cur == -1 || cur == key) {
+                        atomicAdd(&hcnt[h], cnt);
+                        atomicMin(&hmin[h], mn);
+                        done = true;
+                    }
+                }
+                if (!done) {
+                    atomicAdd(size + key, cnt);
+                    atomicMin(minidx + key, mn);
+                }
+            }
+            todo &= ~peers;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) {
+        if (hkey[k] >= 0) {
+            atomicAdd(size + hkey[k], hcnt[k]);
+            atomicMin(minidx + hkey[k], hmin[k]);
+        }
+    }
+    if (meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) roots += __shfl_xor_sync(0xffffffffu, roots, o);
+        if (lane == 0 && roots) atomicAdd(&meta->components, roots);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent, const int* __restrict__ val,
+                                                const int* __restrict__ size, const int* __restrict__ minidx,
+                                                int64_t n, long long min_size, long long max_size,
+                                                int* __restrict__ labels) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const int r = __ldg(parent + s);
+        const long long sz = __ldg(size + r);
+        labels[__ldg(val + s)] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r) : -1;
+    }
+}
+
+// =====================================================================================
+// diagnostic: the device predicate on m pairs (tests the fp32 order / no-FMA contract)
+// =====================================================================================
+__global__ void k_debug_pred(const float* __restrict__ a, const float* __restrict__ b, int64_t m, float t2,
+                             uint8_t* __restrict__ out, float* __restrict__ d2out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 pa = make_float4(a[3 * i], a[3 * i + 1], a[3 * i + 2], 0.f);
+        float4 pb = make_float4(b[3 * i], b[3 * i + 1], b[3 * i + 2], 0.f);
+        const float d2 = d2_rn(pa, pb);
+        out[i] = d2 <= t2;
+        if (d2out) d2out[i] = d2;
+    }
+}
+
+}  // namespace fec
