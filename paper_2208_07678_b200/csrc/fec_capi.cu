@@ -58,6 +58,7 @@ fec_status_t fail_cuda(cudaError_t e, const char* where) {
 struct DevInfo {
     int sms = 0;
     int scan_blocks_per_sm = 0;
+    int sparse_blocks_per_sm = 0;
 };
 DevInfo dev_info() {
     static DevInfo cache[64];
@@ -67,8 +68,10 @@ DevInfo dev_info() {
     if (di.sms == 0) {
         cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_scan_union, SCAN_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_dense, SCAN_THREADS, 0);
         di.scan_blocks_per_sm = b > 0 ? b : 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_sparse, 256, 0);
+        di.sparse_blocks_per_sm = b > 0 ? b : 1;
     }
     return di;
 }
@@ -106,6 +109,7 @@ struct Layout {
     uint8_t* octs;      // [n]
     int* dlist;         // dense cells
     DenseRec* drec;     // their records
+    int* dorder;        // processing order of the records (heavy first)
     float4* tmp_pts;    // staging for very large dense cells
     int* tmp_idx;
     size_t total;
@@ -152,6 +156,7 @@ Layout carve(char* base, int64_t n) {
     L.octs = b.take<uint8_t>(n);
     L.dlist = b.take<int>(n / (SPARSE_MAX + 1) + 16);
     L.drec = b.take<DenseRec>(n / (SPARSE_MAX + 1) + 16);
+    L.dorder = b.take<int>(n / (SPARSE_MAX + 1) + 16);
     L.tmp_pts = b.take<float4>(n);
     L.tmp_idx = b.take<int>(n);
     L.total = std::max(a.off, b.off) + 256;
@@ -289,17 +294,18 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
         k_dinit<<<ew, 256, 0, st>>>(L.spts, n, L.parent, L.size, L.minidx, L.sidx);
         mark(4, st);
         k_dfixup<<<di.sms * 4, 256, 0, st>>>(L.cstart, L.dlist, L.meta, g, L.spts, L.sidx, L.parent, L.drec, L.crec,
-                                             L.tmp_pts);
+                                             L.dorder, L.tmp_pts);
         launches += 2;
         // a6+a7: one sweep over all grid cells (sparse cells: lane; dense cells: warp)
         mark(5, st);
-        k_union_sparse<<<(unsigned)((cells_total + 255) / 256), 256, 0, st>>>(L.spts, L.cstart,
-                                                                             (uint32_t)cells_total, g, L.parent,
-                                                                             L.meta);
+        k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cstart, (uint32_t)cells_total, g,
+                                                                         L.parent, L.meta);
         mark(6, st);
-        k_union_dense<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, L.cstart, L.drec, L.crec, g,
-                                                                              L.parent, L.meta);
-        launches += 2;
+        for (int phase = 0; phase < 2; ++phase)
+            k_union_dense<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, L.cstart, L.drec, L.crec,
+                                                                                  L.dorder, phase, g, L.parent,
+                                                                                  L.meta);
+        launches += 3;
         mark(7, st);
         val = L.sidx;
     } else {

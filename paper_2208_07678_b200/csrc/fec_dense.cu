@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
 }
 
 // ---- a4: dense cells -> octant order, group records, group-leader parents ------------------
+constexpr int HEAVY_POINTS = 512;  // dense cells scheduled first by the union kernel
 constexpr int FIX_THREADS = 256;
 constexpr int FIX_CAP = 2048;  // points staged in shared memory (40 KB); larger cells stage in global
 
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(FIX_THREADS) k_dfixup(const uint32_t* __restri
                                                        const int* __restrict__ dlist, Meta* __restrict__ meta, Grid g,
                                                        float4* __restrict__ spts, int* __restrict__ sidx,
                                                        int* __restrict__ parent, DenseRec* __restrict__ drec,
-                                                       int* __restrict__ crec, float4* __restrict__ tmp_pts) {
+                                                       int* __restrict__ crec, int* __restrict__ order,
+                                                       float4* __restrict__ tmp_pts) {
     __shared__ float4 sp[FIX_CAP];
     __shared__ int cnt[8], off[9], cur[8];
     const int nd = meta->ndense;
@@ -132,6 +134,9 @@ __global__ void __launch_bounds__(FIX_THREADS) k_dfixup(const uint32_t* __restri
             drec[r] = R;
             crec[cell] = r;
             atomicAdd(&meta->dense_points, (unsigned long long)m);
+            // heavy cells first in the union kernel's schedule (long tails otherwise)
+            if (m > HEAVY_POINTS) order[atomicAdd(&meta->nheavy, 1)] = r;
+            else order[nd - 1 - atomicAdd(&meta->nlight, 1)] = r;
         }
         __syncthreads();
         for (int q = threadIdx.x; q < m; q += FIX_THREADS) {
@@ -156,24 +161,152 @@ __global__ void __launch_bounds__(FIX_THREADS) k_dfixup(const uint32_t* __restri
     }
 }
 
-// ---- a6+a7: one fused sweep over the grid cells ------------------------------------------
-// Thread per linear cell; a warp covers 32 consecutive cells, so the cell-table reads of a
-// neighbour offset are coalesced, and blocks run in launch order, sweeping the sorted order
-// upwards (roots of the union-find sit near the sweep front).
-//   sparse cell P (1..SPARSE_MAX points): its lane tests every pair (s, t) with t in P
-//       (t > s) or in a SPARSE forward neighbour Q;
-//   dense cell P: the whole warp evaluates sub-cell group pairs of P with itself, with every
+// ---- a6+a7: neighbour scan + union --------------------------------------------------------
+// Responsibilities (each unordered pair of adjacent cells is examined exactly once,
+// DESIGN.md §4.6):
+//   sparse cell P (1..SPARSE_MAX points): one lane tests every pair (s, t) with t in P
+//       (t > s) or in a SPARSE forward neighbour Q                       -> k_union_sparse
+//   dense cell P: one warp evaluates sub-cell group pairs of P with itself, with every
 //       forward neighbour (dense: octant groups; sparse: single points) and with every
-//       SPARSE backward neighbour.
-// So each unordered pair of adjacent cells is examined exactly once.
-__device__ __forceinline__ void dense_cell_work(int r, PairSmem& S, const float4* __restrict__ spts,
-                                                const uint32_t* __restrict__ cstart,
-                                                const DenseRec* __restrict__ drec, const int* __restrict__ crec,
-                                                const Grid& g, int* __restrict__ parent, int lane,
-                                                unsigned long long& n_tests, unsigned long long& n_pairs) {
+//       SPARSE backward neighbour                                         -> k_union_dense
+
+constexpr int QG_CAP = 13 * 8 + 13 * SPARSE_MAX;  // Q groups of one dense cell (all neighbours)
+constexpr int PQ_CAP = 256;                        // pair queue capacity
+
+struct DenseSmem {
+    int ps[9];                 // P octant groups: [ps[a], ps[a+1])
+    uint8_t po[8];
+    int proot[8];
+    int qs[QG_CAP], qe[QG_CAP];  // Q groups: [qs[b], qe[b])
+    uint8_t qo[QG_CAP];        // octant, or 0xFF for a single point (no octant filter)
+    uint8_t qk[QG_CAP];        // neighbour slot (0..12 forward, 13..25 backward, 26 own)
+    int qroot[QG_CAP];
+    uint16_t small[PQ_CAP], big[PQ_CAP];  // (a << 8) | b
+    int slot_q[26], slot_rec[26], slot_cnt[26], slot_off[27];
+};
+
+__device__ __forceinline__ void slot_offset(int k, int& ox, int& oy, int& oz) {
+    const int kk = k < 13 ? k : k - 13;
+    const int sg = k < 13 ? 1 : -1;
+    ox = sg * c_fwd[kk][0];
+    oy = sg * c_fwd[kk][1];
+    oz = sg * c_fwd[kk][2];
+}
+
+// Small pairs one lane each, big pairs the whole warp; both stop at the first pred-true pair.
+__device__ __forceinline__ void run_pairs(DenseSmem& S, int nsmall, int nbig, int nq_total,
+                                          const float4* __restrict__ spts, int* parent, float t2, int lane,
+                                          unsigned long long& n_tests) {
+    for (int e0 = 0; e0 < nsmall; e0 += 32) {
+        const int e = e0 + lane;
+        if (e < nsmall) {
+            const int a = S.small[e] >> 8, b = S.small[e] & 255;
+            const int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qe[b];
+            bool hit = false;
+            for (int i = sa; i < ea && !hit; ++i) {
+                const float4 pi = __ldg(spts + i);
+                for (int j = sb; j < eb; ++j) {
+                    ++n_tests;
+                    if (pred(pi, __ldg(spts + j), t2)) { hit = true; break; }
+                }
+            }
+            if (hit) uf_unite(parent, sa, sb);
+        }
+        __syncwarp();
+    }
+    for (int e = 0; e < nbig; ++e) {
+        const int a = S.big[e] >> 8, b = S.big[e] & 255;
+        if (S.proot[a] == S.qroot[b]) continue;  // joined by an earlier big pair
+        int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qe[b];
+        if (eb - sb > ea - sa) { int t = sa; sa = sb; sb = t; t = ea; ea = eb; eb = t; }
+        bool found = false;
+        for (int i0 = sa; i0 < ea && !found; i0 += 32) {
+            const int i = i0 + lane;
+            const bool vi = i < ea;
+            const float4 pi = vi ? __ldg(spts + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = sb; j < eb; ++j) {
+                const float4 pj = __ldg(spts + j);
+                n_tests += vi ? 1ull : 0ull;
+                if (__any_sync(0xffffffffu, vi && pred(pi, pj, t2))) { found = true; break; }
+            }
+        }
+        if (found) {
+            const int ra = S.proot[a], rb = S.qroot[b];
+            int rn = 0;
+            if (lane == 0) {
+                uf_unite(parent, S.ps[a], S.qs[b]);
+                rn = uf_find(parent, S.ps[a]);
+            }
+            rn = __shfl_sync(0xffffffffu, rn, 0);
+            __syncwarp();
+            // every cached root equal to either old root now maps to the merged root
+            if (lane < 8 && (S.proot[lane] == ra || S.proot[lane] == rb)) S.proot[lane] = rn;
+            for (int q = lane; q < nq_total; q += 32)
+                if (S.qroot[q] == ra || S.qroot[q] == rb) S.qroot[q] = rn;
+            __syncwarp();
+        }
+    }
+}
+
+// Enumerate (a, b) for a < np and b in [b0, b1), keep those whose cached roots differ and
+// whose sub-cell offset can hold a pred-true pair, and run them through run_pairs in
+// batches of at most PQ_CAP.  `own`: the Q groups are P's own groups (only b > a).
+__device__ __forceinline__ void pair_sweep(DenseSmem& S, int np, int b0, int b1, bool own,
+                                           const float4* __restrict__ spts, int* parent, float t2, int lane,
+                                           unsigned long long& n_tests, unsigned long long& n_pairs) {
+    const int nb = b1 - b0;
+    const int total = np * nb;
+    int nsmall = 0, nbig = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int pid = base + lane;
+        bool ok = pid < total;
+        int a = 0, b = 0;
+        bool big = false;
+        if (ok) {
+            b = b0 + pid / np;
+            a = pid - (b - b0) * np;
+            if (own) {
+                ok = b > a;
+            } else if (S.qo[b] != 0xFF) {
+                int ox, oy, oz;
+                slot_offset(S.qk[b], ox, oy, oz);
+                const int oa = S.po[a], ob = S.qo[b];
+                const int dx = 2 * ox + (ob & 1) - (oa & 1);
+                const int dy = 2 * oy + ((ob >> 1) & 1) - ((oa >> 1) & 1);
+                const int dz = 2 * oz + ((ob >> 2) & 1) - ((oa >> 2) & 1);
+                ok = dx <= 2 && dx >= -2 && dy <= 2 && dy >= -2 && dz <= 2 && dz >= -2;
+            }
+            ok = ok && S.proot[a] != S.qroot[b];
+            big = (S.ps[a + 1] - S.ps[a]) * (S.qe[b] - S.qs[b]) > SMALL_PAIR;
+        }
+        const unsigned ms = __ballot_sync(0xffffffffu, ok && !big);
+        const unsigned mb = __ballot_sync(0xffffffffu, ok && big);
+        const unsigned lt = (1u << lane) - 1u;
+        if (ok && !big) S.small[nsmall + __popc(ms & lt)] = (uint16_t)((a << 8) | b);
+        if (ok && big) S.big[nbig + __popc(mb & lt)] = (uint16_t)((a << 8) | b);
+        nsmall += __popc(ms);
+        nbig += __popc(mb);
+        __syncwarp();
+        if (nsmall > PQ_CAP - 32 || nbig > PQ_CAP - 32 || base + 32 >= total) {
+            n_pairs += lane == 0 ? (unsigned long long)(nsmall + nbig) : 0ull;
+            run_pairs(S, nsmall, nbig, b1, spts, parent, t2, lane, n_tests);
+            nsmall = nbig = 0;
+            __syncwarp();
+        }
+    }
+}
+
+// phase 0: the cell's own octant-group pairs; phase 1: its neighbour pairs.  Running all
+// cells' phase 0 first means phase 1 sees every dense cell's groups joined already, so
+// after the first contact between two cells all their group pairs skip on cached roots.
+__device__ void dense_cell_work(int r, int phase, DenseSmem& S, const float4* __restrict__ spts,
+                                const uint32_t* __restrict__ cstart, const DenseRec* __restrict__ drec,
+                                const int* __restrict__ crec, const Grid& g, int* __restrict__ parent, int lane,
+                                unsigned long long& n_tests, unsigned long long& n_pairs) {
     const float t2 = g.t2;
     const DenseRec* R = drec + r;
-    int np = 0;
+    // P: nonempty octant groups
+    int np;
     {
         const int k = lane < 8 ? lane : 7;
         const int o0 = __ldg(&R->off[k]), o1 = __ldg(&R->off[k + 1]);
@@ -187,135 +320,106 @@ __device__ __forceinline__ void dense_cell_work(int r, PairSmem& S, const float4
         np = __popc(m);
         if (lane == 0) S.ps[np] = __ldg(&R->off[8]);
     }
-    int c[3];
-    dense_decode((uint32_t)__ldg(&R->cell), g, c);
-    // neighbour table: lanes 0..12 forward, 13..25 backward
-    int qstart = 0, qend = 0;
+    __syncwarp();
+    // own-cell group pairs
+    if (phase == 0) {
+        if (np < 2) return;
+        if (lane < np) {
+            S.proot[lane] = uf_find(parent, S.ps[lane]);
+            S.qs[lane] = S.ps[lane];
+            S.qe[lane] = S.ps[lane + 1];
+            S.qo[lane] = S.po[lane];
+            S.qk[lane] = 26;
+        }
+        __syncwarp();
+        if (lane < np) S.qroot[lane] = S.proot[lane];
+        __syncwarp();
+        pair_sweep(S, np, 0, np, true, spts, parent, t2, lane, n_tests, n_pairs);
+        return;
+    }
+    // neighbour slots: lanes 0..25 (0..12 forward, 13..25 backward)
+    int cnt = 0;
     if (lane < 26) {
-        const int k = lane < 13 ? lane : lane - 13;
-        const int sg = lane < 13 ? 1 : -1;
+        int c[3];
+        dense_decode((uint32_t)__ldg(&R->cell), g, c);
+        int ox, oy, oz;
+        slot_offset(lane, ox, oy, oz);
         uint32_t Q;
-        if (dense_neighbor(g, c, sg * c_fwd[k][0], sg * c_fwd[k][1], sg * c_fwd[k][2], Q)) {
-            qstart = (int)__ldg(cstart + Q);
-            qend = (int)__ldg(cstart + Q + 1);
-            if (qend - qstart > SPARSE_MAX) {
-                if (lane >= 13) qend = qstart;       // dense backward: handled by that cell
-                else qstart = -1 - __ldg(crec + Q);  // dense forward: encode record id
+        int rec = -1, qs = 0, qe = 0;
+        if (dense_neighbor(g, c, ox, oy, oz, Q)) {
+            qs = (int)__ldg(cstart + Q);
+            qe = (int)__ldg(cstart + Q + 1);
+            if (qe - qs > SPARSE_MAX) {
+                if (lane < 13) {
+                    rec = __ldg(crec + Q);
+                    const DenseRec* RQ = drec + rec;
+                    for (int k = 0; k < 8; ++k) cnt += __ldg(&RQ->off[k + 1]) > __ldg(&RQ->off[k]);
+                }
+            } else {
+                cnt = qe - qs;
+            }
+        }
+        S.slot_q[lane] = qs;
+        S.slot_rec[lane] = rec;
+        S.slot_cnt[lane] = cnt;
+    }
+    // exclusive scan of the group counts over the 26 slots
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    const int nq = __shfl_sync(0xffffffffu, x, 25);
+    if (lane < 26) S.slot_off[lane] = x - cnt;
+    __syncwarp();
+    if (nq == 0) return;
+    if (lane < 26 && cnt > 0) {
+        int o = x - cnt;
+        const int rec = S.slot_rec[lane];
+        if (rec >= 0) {
+            const DenseRec* RQ = drec + rec;
+            for (int k = 0; k < 8; ++k) {
+                const int a0 = __ldg(&RQ->off[k]), a1 = __ldg(&RQ->off[k + 1]);
+                if (a1 > a0) {
+                    S.qs[o] = a0; S.qe[o] = a1; S.qo[o] = (uint8_t)k; S.qk[o] = (uint8_t)lane;
+                    ++o;
+                }
+            }
+        } else {
+            const int qs = S.slot_q[lane];
+            for (int k = 0; k < cnt; ++k) {
+                S.qs[o] = qs + k; S.qe[o] = qs + k + 1; S.qo[o] = 0xFF; S.qk[o] = (uint8_t)lane;
+                ++o;
             }
         }
     }
     __syncwarp();
-    for (int k = -1; k < 26; ++k) {
-        int nq;
-        const bool same = k < 0;
-        if (same) {
-            nq = np;
-            if (lane <= np) S.qs[lane] = S.ps[lane];
-            if (lane < np) S.qo[lane] = S.po[lane];
-        } else {
-            const int qs = __shfl_sync(0xffffffffu, qstart, k);
-            const int qe = __shfl_sync(0xffffffffu, qend, k);
-            if (qs >= 0 && qe <= qs) continue;
-            if (qs < 0) {  // dense forward neighbour: its octant groups
-                const DenseRec* RQ = drec + (-1 - qs);
-                const int kk = lane < 8 ? lane : 7;
-                const int o0 = __ldg(&RQ->off[kk]), o1 = __ldg(&RQ->off[kk + 1]);
-                const bool ne = lane < 8 && o1 > o0;
-                const unsigned m = __ballot_sync(0xffffffffu, ne);
-                if (ne) {
-                    const int j = __popc(m & ((1u << lane) - 1u));
-                    S.qs[j] = o0;
-                    S.qo[j] = (uint8_t)kk;
-                }
-                nq = __popc(m);
-                if (lane == 0) S.qs[nq] = __ldg(&RQ->off[8]);
-            } else {       // sparse neighbour: every point is its own group
-                nq = qe - qs;
-                if (lane <= nq) S.qs[lane] = qs + lane;
-                if (lane < nq) S.qo[lane] = 0xFF;
-            }
-        }
-        __syncwarp();
-        const int kk = k < 13 ? k : k - 13;
-        const int sg = k < 13 ? 1 : -1;
-        const int nqueue = same ? build_queue(S, np, nq, true, 0, 0, 0, lane)
-                                : build_queue(S, np, nq, false, sg * c_fwd[kk][0], sg * c_fwd[kk][1],
-                                              sg * c_fwd[kk][2], lane);
-        n_pairs += (lane == 0) ? (unsigned long long)nqueue : 0ull;
-        load_roots(S, np, nq, parent, lane);
-        process_queue(S, nqueue, spts, parent, t2, lane, n_tests);
-    }
+    // current roots (P's own groups were just joined)
+    if (lane < np) S.proot[lane] = uf_find(parent, S.ps[lane]);
+    for (int b = lane; b < nq; b += 32) S.qroot[b] = uf_find(parent, S.qs[b]);
+    __syncwarp();
+    pair_sweep(S, np, 0, nq, false, spts, parent, t2, lane, n_tests, n_pairs);
 }
 
-__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts,
-                                                     const uint32_t* __restrict__ cstart, uint32_t cells, Grid g,
-                                                     int* __restrict__ parent, Meta* __restrict__ meta) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long n_tests = 0, n_pairs = 0;
-    const float t2 = g.t2;
-    const uint32_t P = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool ok = P < cells;
-    int ps = 0, pe = 0;
-    if (ok) {
-        ps = (int)__ldg(cstart + P);
-        pe = (int)__ldg(cstart + P + 1);
-    }
-    const bool sparse = ok && pe > ps && pe - ps <= SPARSE_MAX;
-    if (sparse) {
-        for (int s = ps; s < pe; ++s) {
-            const float4 a = __ldg(spts + s);
-            for (int t = s + 1; t < pe; ++t) {
-                ++n_tests;
-                if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-            }
-        }
-        int c[3];
-        dense_decode(P, g, c);
-#pragma unroll 1
-        for (int k = 0; k < 13; ++k) {
-            uint32_t Q;
-            if (!dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], Q)) continue;
-            const int qs = (int)__ldg(cstart + Q), qe = (int)__ldg(cstart + Q + 1);
-            if (qe == qs || qe - qs > SPARSE_MAX) continue;
-            for (int s = ps; s < pe; ++s) {
-                const float4 a = __ldg(spts + s);
-                for (int t = qs; t < qe; ++t) {
-                    ++n_tests;
-                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-                }
-            }
-        }
-    }
-    if (meta->instrument) {
-        for (int o = 16; o > 0; o >>= 1) {
-            n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
-            n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
-        }
-        if (lane == 0 && (n_tests || n_pairs)) {
-            atomicAdd(&meta->pair_tests, n_tests);
-            atomicAdd(&meta->group_pairs, n_pairs);
-        }
-    }
-}
-
-// Dense cells: warp per cell, dynamic scheduling over the dense records (load balance:
-// a few cells hold thousands of points).
 __global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __restrict__ spts,
                                                             const uint32_t* __restrict__ cstart,
                                                             const DenseRec* __restrict__ drec,
-                                                            const int* __restrict__ crec, Grid g,
+                                                            const int* __restrict__ crec,
+                                                            const int* __restrict__ order, int phase, Grid g,
                                                             int* __restrict__ parent, Meta* __restrict__ meta) {
-    __shared__ PairSmem sm[SCAN_THREADS / kWarp];
+    __shared__ DenseSmem sm[SCAN_THREADS / kWarp];
     const int lane = threadIdx.x & 31;
-    PairSmem& S = sm[threadIdx.x >> 5];
+    DenseSmem& S = sm[threadIdx.x >> 5];
     const int nd = meta->ndense;
     unsigned long long n_tests = 0, n_pairs = 0;
     while (true) {
-        int r = 0;
-        if (lane == 0) r = atomicAdd(&meta->work, 1);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        if (r >= nd) break;
-        dense_cell_work(r, S, spts, cstart, drec, crec, g, parent, lane, n_tests, n_pairs);
+        int it = 0;
+        if (lane == 0) it = atomicAdd(phase == 0 ? &meta->work : &meta->work2, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= nd) break;
+        dense_cell_work(__ldg(order + it), phase, S, spts, cstart, drec, crec, g, parent, lane, n_tests, n_pairs);
+        __syncwarp();
     }
     if (meta->instrument) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -326,6 +430,80 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __re
             atomicAdd(&meta->dense_tests, n_tests);
             atomicAdd(&meta->group_pairs, n_pairs);
         }
+    }
+}
+
+// Sparse cells.  The grid is one resident wave; each warp grid-strides over chunks of
+// 128 consecutive cells (so the wave sweeps the sorted order upwards), compacts the
+// chunk's nonempty sparse cells into a per-warp list and gives every lane a real cell.
+// Loops are warp-uniform with a reconvergence point per neighbour (SIMT efficiency).
+constexpr int SP_CHUNK = 128;
+
+__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts,
+                                                     const uint32_t* __restrict__ cstart, uint32_t cells, Grid g,
+                                                     int* __restrict__ parent, Meta* __restrict__ meta) {
+    __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
+    unsigned long long n_tests = 0;
+    const float t2 = g.t2;
+    const int lane = threadIdx.x & 31;
+    uint32_t* list = lists[threadIdx.x >> 5];
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t base = warp * SP_CHUNK; base < cells; base += nwarps * SP_CHUNK) {
+        int total = 0;
+#pragma unroll
+        for (int j = 0; j < SP_CHUNK / 32; ++j) {
+            const uint32_t P = base + j * 32 + lane;
+            bool act = false;
+            if (P < cells) {
+                const int cnt = (int)__ldg(cstart + P + 1) - (int)__ldg(cstart + P);
+                act = cnt > 0 && cnt <= SPARSE_MAX;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, act);
+            if (act) list[total + __popc(m & ((1u << lane) - 1u))] = P;
+            total += __popc(m);
+        }
+        __syncwarp();
+        for (int e0 = 0; e0 < total; e0 += 32) {
+            const int e = e0 + lane;
+            const bool v = e < total;
+            const uint32_t P = v ? list[e] : 0u;
+            const int ps = v ? (int)__ldg(cstart + P) : 0;
+            const int pe = v ? (int)__ldg(cstart + P + 1) : 0;
+            for (int s = ps; s < pe; ++s) {
+                const float4 a = __ldg(spts + s);
+                for (int t = s + 1; t < pe; ++t) {
+                    ++n_tests;
+                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                }
+            }
+            __syncwarp();
+            int c[3];
+            dense_decode(P, g, c);
+#pragma unroll 1
+            for (int k = 0; k < 13; ++k) {
+                uint32_t Q;
+                int qs = 0, qe = 0;
+                if (v && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], Q)) {
+                    qs = (int)__ldg(cstart + Q);
+                    qe = (int)__ldg(cstart + Q + 1);
+                    if (qe - qs > SPARSE_MAX) qe = qs;
+                }
+                for (int s = ps; s < pe && qe > qs; ++s) {
+                    const float4 a = __ldg(spts + s);
+                    for (int t = qs; t < qe; ++t) {
+                        ++n_tests;
+                        if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    }
+    if (meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
+        if (lane == 0 && n_tests) atomicAdd(&meta->pair_tests, n_tests);
     }
 }
 

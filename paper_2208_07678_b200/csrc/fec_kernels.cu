@@ -326,11 +326,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_union(const float4* __res
                     if (lane < nq) S.qo[lane] = __ldg(T.goct + qgs + lane);
                 }
                 __syncwarp();
-                const int nqueue = k < 0 ? build_queue(S, np, nq, true, 0, 0, 0, lane)
-                                         : build_queue(S, np, nq, false, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], lane);
-                n_pairs += (lane == 0) ? (unsigned long long)nqueue : 0ull;
                 load_roots(S, np, nq, parent, lane);
-            process_queue(S, nqueue, spts, parent, t2, lane, n_tests);
+                const int2 nqueue = k < 0 ? build_queue(S, np, nq, true, 0, 0, 0, lane)
+                                          : build_queue(S, np, nq, false, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], lane);
+                n_pairs += (lane == 0) ? (unsigned long long)(nqueue.x + nqueue.y) : 0ull;
+                process_queue(S, nqueue, spts, parent, t2, lane, n_tests);
             }
         }
     }

@@ -8,7 +8,7 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int SCAN_THREADS = 256;
-constexpr int SPARSE_MAX = 16;  // dense-grid mode: cells with <= SPARSE_MAX points are "sparse"
+constexpr int SPARSE_MAX = 6;   // dense-grid mode: cells with <= SPARSE_MAX points are "sparse"
 
 // Small device-resident header at the start of the workspace.
 struct Meta {
@@ -24,6 +24,8 @@ struct Meta {
     unsigned long long components;
     unsigned long long dense_points;
     unsigned long long dense_tests;
+    int nheavy, nlight;               // dense-grid mode: schedule of the dense cells
+    int work2;                        // second dynamic work counter
 };
 
 struct Tables {
@@ -62,11 +64,11 @@ __global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint32_t* cs
                            float4* spts);
 __global__ void k_dinit(const float4* spts, int64_t n, int* parent, int* size, int* minidx, int* sidx);
 __global__ void k_dfixup(const uint32_t* cstart, const int* dlist, Meta* meta, Grid g, float4* spts, int* sidx,
-                         int* parent, DenseRec* drec, int* crec, float4* tmp_pts);
+                         int* parent, DenseRec* drec, int* crec, int* order, float4* tmp_pts);
 __global__ void k_union_sparse(const float4* spts, const uint32_t* cstart, uint32_t cells, Grid g, int* parent,
                                Meta* meta);
 __global__ void k_union_dense(const float4* spts, const uint32_t* cstart, const DenseRec* drec, const int* crec,
-                              Grid g, int* parent, Meta* meta);
+                              const int* order, int phase, Grid g, int* parent, Meta* meta);
 __global__ void k_debug_pred(const float* a, const float* b, int64_t m, float t2, uint8_t* out, float* d2out);
 
 }  // namespace fec

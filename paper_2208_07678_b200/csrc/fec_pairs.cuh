@@ -19,7 +19,8 @@ struct PairSmem {
     int qs[QMAX + 1];          // Q group starts (+ end)
     uint8_t po[8];             // P octants
     uint8_t qo[QMAX];          // Q octants (0xFF: single point, no octant filter)
-    uint16_t queue[8 * QMAX];  // candidate group pairs (a << 8 | b)
+    uint16_t queue[8 * QMAX];  // small candidate group pairs (a << 8 | b), one lane each
+    uint16_t bigq[8 * QMAX];   // big candidate group pairs, whole warp each
     int proot[8];              // cached roots of the P groups (may be stale: see below)
     int qroot[QMAX];           // cached roots of the Q groups
 };
@@ -39,18 +40,20 @@ __constant__ signed char c_fwd[13][3] = {
     {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},  {1, 1, 0},  {-1, -1, 1}, {0, -1, 1}, {1, -1, 1},
     {-1, 0, 1}, {0, 0, 1},  {1, 0, 1},  {-1, 1, 1}, {0, 1, 1},   {1, 1, 1}};
 
-// Enumerate candidate pairs (a in P groups, b in Q groups) into S.queue.  `same_cell`: only
-// b > a.  Otherwise octant pairs whose sub-cell offset exceeds 2 on an axis are dropped
-// (they are > c > d apart), unless a Q group is a single point (qo == 0xFF).
-// `off` is the cell offset Q - P.  Returns the queue length (warp-uniform).
-__device__ __forceinline__ int build_queue(PairSmem& S, int np, int nq, bool same_cell, int ox, int oy, int oz,
-                                           int lane) {
-    int nqueue = 0;
+// Enumerate candidate pairs (a in P groups, b in Q groups) that still need a test: their
+// cached roots differ, and (unless a Q group is a single point, qo == 0xFF) their sub-cell
+// offset is at most 2 on every axis (larger offsets are > c > d apart).  `same_cell`: only
+// b > a.  (ox, oy, oz) is the cell offset Q - P.  Small pairs (|A|*|B| <= SMALL_PAIR) go to
+// S.queue, big ones to S.bigq.  Call after load_roots().  Returns both lengths.
+__device__ __forceinline__ int2 build_queue(PairSmem& S, int np, int nq, bool same_cell, int ox, int oy, int oz,
+                                            int lane) {
+    int nsmall = 0, nbig = 0;
     const int npairs = np * nq;
     for (int base = 0; base < npairs; base += 32) {
         const int pid = base + lane;
         bool ok = pid < npairs;
         int a = 0, b = 0;
+        bool big = false;
         if (ok) {
             a = pid / nq;
             b = pid - a * nq;
@@ -63,25 +66,28 @@ __device__ __forceinline__ int build_queue(PairSmem& S, int np, int nq, bool sam
                 const int dz = 2 * oz + ((ob >> 2) & 1) - ((oa >> 2) & 1);
                 ok = dx <= 2 && dx >= -2 && dy <= 2 && dy >= -2 && dz <= 2 && dz >= -2;
             }
+            ok = ok && S.proot[a] != S.qroot[b];
+            big = (S.ps[a + 1] - S.ps[a]) * (S.qs[b + 1] - S.qs[b]) > SMALL_PAIR;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (ok) S.queue[nqueue + __popc(m & ((1u << lane) - 1u))] = (uint16_t)((a << 8) | b);
-        nqueue += __popc(m);
+        const unsigned ms = __ballot_sync(0xffffffffu, ok && !big);
+        const unsigned mb = __ballot_sync(0xffffffffu, ok && big);
+        const unsigned lt = (1u << lane) - 1u;
+        if (ok && !big) S.queue[nsmall + __popc(ms & lt)] = (uint16_t)((a << 8) | b);
+        if (ok && big) S.bigq[nbig + __popc(mb & lt)] = (uint16_t)((a << 8) | b);
+        nsmall += __popc(ms);
+        nbig += __popc(mb);
     }
     __syncwarp();
-    return nqueue;
+    return make_int2(nsmall, nbig);
 }
 
-// Evaluate the queued group pairs: small ones one lane each, big ones by the whole warp
-// with an early exit at the first pred-true pair; skip pairs whose cached roots agree.
-__device__ __forceinline__ void process_queue(PairSmem& S, int nqueue, const float4* __restrict__ spts,
+// Evaluate the queued group pairs: small ones one lane each, big ones by the whole warp,
+// both with an early exit at the first pred-true pair.
+__device__ __forceinline__ void process_queue(PairSmem& S, int2 nq2, const float4* __restrict__ spts,
                                               int* parent, float t2, int lane, unsigned long long& n_tests) {
-    for (int e = lane; e < nqueue; e += 32) {
+    for (int e = lane; e < nq2.x; e += 32) {
         const int a = S.queue[e] >> 8, b = S.queue[e] & 255;
-        if (S.proot[a] == S.qroot[b]) continue;
         const int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qs[b + 1];
-        const int na = ea - sa, nb = eb - sb;
-        if (na * nb > SMALL_PAIR) continue;
         bool hit = false;
         for (int i = sa; i < ea && !hit; ++i) {
             const float4 pi = __ldg(spts + i);
@@ -93,11 +99,10 @@ __device__ __forceinline__ void process_queue(PairSmem& S, int nqueue, const flo
         if (hit) uf_unite(parent, sa, sb);
     }
     __syncwarp();
-    for (int e = 0; e < nqueue; ++e) {
-        const int a = S.queue[e] >> 8, b = S.queue[e] & 255;
+    for (int e = 0; e < nq2.y; ++e) {
+        const int a = S.bigq[e] >> 8, b = S.bigq[e] & 255;
+        if (S.proot[a] == S.qroot[b]) continue;   // joined by an earlier big pair of this queue
         int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qs[b + 1];
-        if ((ea - sa) * (eb - sb) <= SMALL_PAIR) continue;
-        if (S.proot[a] == S.qroot[b]) continue;
         // lanes stride over the larger group, the smaller one is broadcast
         if (eb - sb > ea - sa) { int t = sa; sa = sb; sb = t; t = ea; ea = eb; eb = t; }
         bool found = false;
