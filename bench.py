@@ -130,10 +130,10 @@ def algorithmic_bytes(stage: str, n: int, st: dict) -> float:
         md = max(st.get("dense_points", 0), 0)
         model = {
             "a1_bbox_validate": 12.0 * n,
-            "a2_bin_keys": 12.0 * n + 4.0 * n + 4.0 * C,          # read xyz, write slot, zero counts
+            "a2_bin_keys": 4.0 * C + 2 * 12.0 * n + 4.0 * n + 4.0 * md,  # zero counts, 2 reads of xyz, slots
             "a3_sort": 8.0 * C + 12.0 * n + 4.0 * n + 16.0 * n,   # scan counts, read xyz+slot, write float4
-            "a4_gather_fixup": 16.0 * n + 16.0 * n,                # read float4, write parent/size/min/idx
-            "a5_tables_init": 32.0 * md + 24.0 * md,               # dense cells: read twice, write float4+idx+parent
+            "a4_gather_init": 16.0 * n + 16.0 * n,                 # read float4, write parent/size/min/idx
+            "a5_tables": 0.0,
             "a6a7_union_sparse": 4.0 * C + 16.0 * (n - md) + 8.0 * (n - md),  # cell table; sparse points, parents
             "a6a7_union_dense": 16.0 * md + 8.0 * md,              # dense points read; parents r/w
             "a8_flatten": 8.0 * n,
@@ -146,8 +146,8 @@ def algorithmic_bytes(stage: str, n: int, st: dict) -> float:
             "a1_bbox_validate": 12.0 * n,
             "a2_bin_keys": 12.0 * n + 12.0 * n,
             "a3_sort": P * (8.0 * n + 24.0 * n),
-            "a4_gather_fixup": 4.0 * n + 12.0 * n + 16.0 * n,
-            "a5_tables_init": 72.0 * n + 5.0 * G + 16.0 * U,
+            "a4_gather_init": 4.0 * n + 12.0 * n + 16.0 * n,
+            "a5_tables": 72.0 * n + 5.0 * G + 16.0 * U,
             "a6a7_union_sparse": 0.0,
             "a6a7_union_dense": 16.0 * n + 8.0 * n + 5.0 * G + 12.0 * U,
             "a8_flatten": 8.0 * n,

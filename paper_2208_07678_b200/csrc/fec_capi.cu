@@ -22,7 +22,7 @@ thread_local int g_grid_mode = 0;
 
 constexpr int kStages = 10;
 const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",       "a3_sort",
-                                          "a4_gather_fixup",  "a5_tables_init",    "a6a7_union_sparse",
+                                          "a4_gather_init",   "a5_tables",    "a6a7_union_sparse",
                                           "a6a7_union_dense", "a8_flatten",        "a9_stats",
                                           "a10_relabel"};
 struct StageEvents {
@@ -59,6 +59,7 @@ struct DevInfo {
     int sms = 0;
     int scan_blocks_per_sm = 0;
     int sparse_blocks_per_sm = 0;
+    int wfix_blocks_per_sm = 0;
 };
 DevInfo dev_info() {
     static DevInfo cache[64];
@@ -109,9 +110,9 @@ struct Layout {
     uint8_t* octs;      // [n]
     int* dlist;         // dense cells
     DenseRec* drec;     // their records
-    int* dorder;        // processing order of the records (heavy first)
-    float4* tmp_pts;    // staging for very large dense cells
-    int* tmp_idx;
+    uint32_t* dbits;    // [cells/32+1] bitmap of dense cells
+    uint32_t* dwpos;    // [cells/32+2] popcount prefix of the bitmap words
+    uint32_t* ocnt;     // per dense record: points per octant
     size_t total;
 };
 
@@ -156,9 +157,9 @@ Layout carve(char* base, int64_t n) {
     L.octs = b.take<uint8_t>(n);
     L.dlist = b.take<int>(n / (SPARSE_MAX + 1) + 16);
     L.drec = b.take<DenseRec>(n / (SPARSE_MAX + 1) + 16);
-    L.dorder = b.take<int>(n / (SPARSE_MAX + 1) + 16);
-    L.tmp_pts = b.take<float4>(n);
-    L.tmp_idx = b.take<int>(n);
+    L.dbits = b.take<uint32_t>(dc / 32 + 2);
+    L.dwpos = b.take<uint32_t>(dc / 32 + 2);
+    L.ocnt = b.take<uint32_t>((size_t)8 * (n / (SPARSE_MAX + 1) + 16));
     L.total = std::max(a.off, b.off) + 256;
     return L;
 }
@@ -279,23 +280,30 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
         g.stride[perm[2]] = (uint32_t)g.dims[perm[0]] * (uint32_t)g.dims[perm[1]];
         g.sdiv[0] = g.stride[perm[2]];
         g.sdiv[1] = g.stride[perm[1]];
-        // a2: counts
+        // a2: counts per cell; dense cells get records and octant-ordered slots
         mark(1, st);
         FEC_CUDA(cudaMemsetAsync(L.cstart, 0, (size_t)(cells_total + 1) * 4, st));
-        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.dlist, L.meta);
-        ++launches;
+        const int64_t words = (cells_total + 31) / 32;
+        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(words + 1) * 4, st));
+        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.dbits, L.meta);
+        const unsigned wb = grid_for(words + 1, 256, cap * 4);
+        k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, words, L.dwpos);
+        launches += 2 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, words + 1, L.dscan, st);
+        k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, words, L.dwpos, L.dlist, L.crec, L.ocnt, L.meta);
+        k_dcount_oct<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.crec, L.ocnt, L.slot);
+        launches += 2;
         // a3: counting sort = scan + scatter
         mark(2, st);
         launches += exclusive_scan<uint32_t>(L.cstart, L.cstart, cells_total + 1, L.dscan, st);
-        k_dscatter<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.spts);
-        ++launches;
-        // a4/a5: sorted-order init, then dense-cell octant fix-up
-        mark(3, st);
-        k_dinit<<<ew, 256, 0, st>>>(L.spts, n, L.parent, L.size, L.minidx, L.sidx);
-        mark(4, st);
-        k_dfixup<<<di.sms * 4, 256, 0, st>>>(L.cstart, L.dlist, L.meta, g, L.spts, L.sidx, L.parent, L.drec, L.crec,
-                                             L.dorder, L.tmp_pts);
+        k_drec_fin<<<grid_for(n / (SPARSE_MAX + 1) + 1, 256, cap), 256, 0, st>>>(L.dlist, L.meta, L.cstart, L.ocnt,
+                                                                                 L.drec);
+        k_dscatter<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.crec, L.drec, L.spts);
         launches += 2;
+        // a4: sorted-order init (parents = clique-group leaders)
+        mark(3, st);
+        k_dinit<<<ew, 256, 0, st>>>(L.spts, n, g, L.cstart, L.crec, L.drec, L.parent, L.size, L.minidx, L.sidx);
+        ++launches;
+        mark(4, st);
         // a6+a7: one sweep over all grid cells (sparse cells: lane; dense cells: warp)
         mark(5, st);
         k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cstart, (uint32_t)cells_total, g,
@@ -303,7 +311,7 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
         mark(6, st);
         for (int phase = 0; phase < 2; ++phase)
             k_union_dense<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, L.cstart, L.drec, L.crec,
-                                                                                  L.dorder, phase, g, L.parent,
+                                                                                  phase, g, L.parent,
                                                                                   L.meta);
         launches += 3;
         mark(7, st);

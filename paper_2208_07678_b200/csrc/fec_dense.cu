@@ -40,7 +40,7 @@ __device__ __forceinline__ bool dense_neighbor(const Grid& g, const int c[3], in
 // ---- a2: per-cell counts; slot[i] = rank of point i inside its cell -----------------------
 __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
                                                uint32_t* __restrict__ count, uint32_t* __restrict__ slot,
-                                               int* __restrict__ dlist, Meta* __restrict__ meta) {
+                                               uint32_t* __restrict__ dbits, Meta* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
         if (ok && lane == leader) {
             old = atomicAdd(count + lin, cnt);
             if (old <= (uint32_t)SPARSE_MAX && old + cnt > (uint32_t)SPARSE_MAX)
-                dlist[atomicAdd(&meta->ndense, 1)] = (int)lin;
+                atomicOr(dbits + (lin >> 5), 1u << (lin & 31u));   // the cell just became dense
             if (old == 0 && meta->instrument) atomicAdd(&meta->cells, 1);
         }
         old = __shfl_sync(0xffffffffu, old, leader);
@@ -66,98 +66,125 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
     }
 }
 
+// ---- a2b: dense cells get records (in ascending cell order); their points get
+// octant-ordered slots.  A cell with more than SPARSE_MAX points is laid out octant by
+// octant (octant k = the sub-cell (sx&1, sy&1, sz&1)), so each octant is a contiguous
+// clique group.
+__global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
+                                                   uint32_t* __restrict__ wcount) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
+        wcount[w] = w < words ? (uint32_t)__popc(__ldg(dbits + w)) : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__ dbits, int64_t words,
+                                                   const uint32_t* __restrict__ wpos, int* __restrict__ dlist,
+                                                   int* __restrict__ crec, uint32_t* __restrict__ ocnt,
+                                                   Meta* __restrict__ meta) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
+        if (w == words) { meta->ndense = (int)wpos[words]; continue; }
+        uint32_t bits = __ldg(dbits + w);
+        int r = (int)__ldg(wpos + w);
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int cell = (int)(w * 32 + b);
+            dlist[r] = cell;
+            crec[cell] = r;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ocnt[8 * r + k] = 0u;
+            ++r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dcount_oct(const float* __restrict__ p, int64_t n, Grid g,
+                                                   const uint32_t* __restrict__ count, const int* __restrict__ crec,
+                                                   uint32_t* __restrict__ ocnt, uint32_t* __restrict__ slot) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        uint32_t key = 0xffffffffu;
+        if (i < n) {
+            uint32_t lin;
+            int oct;
+            dense_cell_of(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2), g, lin, oct);
+            if (__ldg(count + lin) > (uint32_t)SPARSE_MAX) key = 8u * (uint32_t)__ldg(crec + lin) + (uint32_t)oct;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (key != 0xffffffffu && lane == leader) old = atomicAdd(ocnt + key, (uint32_t)__popc(peers));
+        old = __shfl_sync(0xffffffffu, old, leader);
+        if (key != 0xffffffffu) slot[i] = old + __popc(peers & lt);
+    }
+}
+
+// After the scan: octant offsets of every dense record.
+__global__ void __launch_bounds__(256) k_drec_fin(const int* __restrict__ dlist, Meta* __restrict__ meta,
+                                                 const uint32_t* __restrict__ cstart,
+                                                 const uint32_t* __restrict__ ocnt, DenseRec* __restrict__ drec) {
+    const int nd = meta->ndense;
+    unsigned long long pts = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
+        const int cell = __ldg(dlist + r);
+        const int start = (int)__ldg(cstart + cell), m = (int)__ldg(cstart + cell + 1) - start;
+        DenseRec R;
+        R.cell = cell;
+        int run = start;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            R.off[k] = run;
+            run += (int)__ldg(ocnt + 8 * r + k);
+        }
+        R.off[8] = run;
+        drec[r] = R;
+        pts += (unsigned long long)m;
+    }
+    for (int o = 16; o > 0; o >>= 1) pts += __shfl_xor_sync(0xffffffffu, pts, o);
+    if ((threadIdx.x & 31) == 0 && pts) atomicAdd(&meta->dense_points, pts);
+}
+
 // ---- a3: scatter into cell order (after the exclusive scan of count -> cstart) ------------
 // Only the float4 (x, y, z, idx) is scattered: for shuffled inputs every scattered array
 // costs a DRAM read-modify-write per point, so everything else is derived in sorted order.
 __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n, Grid g,
                                                  const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ slot,
+                                                 const int* __restrict__ crec, const DenseRec* __restrict__ drec,
                                                  float4* __restrict__ spts) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float x = __ldg(p + 3 * i), y = __ldg(p + 3 * i + 1), z = __ldg(p + 3 * i + 2);
         uint32_t lin;
         int oct;
         dense_cell_of(x, y, z, g, lin, oct);
-        const uint32_t pos = __ldg(cstart + lin) + __ldg(slot + i);
-        spts[pos] = make_float4(x, y, z, __int_as_float((int)i));
+        const uint32_t c0 = __ldg(cstart + lin), c1 = __ldg(cstart + lin + 1);
+        uint32_t base = c0;
+        if (c1 - c0 > (uint32_t)SPARSE_MAX) base = (uint32_t)__ldg(&drec[__ldg(crec + lin)].off[oct]);
+        spts[base + __ldg(slot + i)] = make_float4(x, y, z, __int_as_float((int)i));
     }
 }
 
-// Sorted-order initialisation (coalesced): singleton sets, accumulators, input index.
-__global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, int* __restrict__ parent,
+// Sorted-order initialisation (coalesced): parent = self for points of sparse cells, the
+// last point of the octant group for points of dense cells (groups are cliques, DESIGN.md
+// §4.5); accumulators; input index.
+__global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, Grid g,
+                                              const uint32_t* __restrict__ cstart, const int* __restrict__ crec,
+                                              const DenseRec* __restrict__ drec, int* __restrict__ parent,
                                               int* __restrict__ size, int* __restrict__ minidx,
                                               int* __restrict__ sidx) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        parent[s] = (int)s;
+        const float4 v = __ldg(spts + s);
+        uint32_t lin;
+        int oct;
+        dense_cell_of(v.x, v.y, v.z, g, lin, oct);
+        const uint32_t c0 = __ldg(cstart + lin), c1 = __ldg(cstart + lin + 1);
+        int par = (int)s;
+        if (c1 - c0 > (uint32_t)SPARSE_MAX) par = __ldg(&drec[__ldg(crec + lin)].off[oct + 1]) - 1;
+        parent[s] = par;
         size[s] = 0;
         minidx[s] = 0x7fffffff;
-        sidx[s] = __float_as_int(__ldg(&spts[s].w));
-    }
-}
-
-// ---- a4: dense cells -> octant order, group records, group-leader parents ------------------
-constexpr int HEAVY_POINTS = 512;  // dense cells scheduled first by the union kernel
-constexpr int FIX_THREADS = 256;
-constexpr int FIX_CAP = 2048;  // points staged in shared memory (40 KB); larger cells stage in global
-
-__global__ void __launch_bounds__(FIX_THREADS) k_dfixup(const uint32_t* __restrict__ cstart,
-                                                       const int* __restrict__ dlist, Meta* __restrict__ meta, Grid g,
-                                                       float4* __restrict__ spts, int* __restrict__ sidx,
-                                                       int* __restrict__ parent, DenseRec* __restrict__ drec,
-                                                       int* __restrict__ crec, int* __restrict__ order,
-                                                       float4* __restrict__ tmp_pts) {
-    __shared__ float4 sp[FIX_CAP];
-    __shared__ int cnt[8], off[9], cur[8];
-    const int nd = meta->ndense;
-    for (int r = blockIdx.x; r < nd; r += gridDim.x) {
-        const int cell = dlist[r];
-        const int start = (int)cstart[cell], end = (int)cstart[cell + 1];
-        const int m = end - start;
-        if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
-        __syncthreads();
-        const bool in_smem = m <= FIX_CAP;
-        // octants from the coordinates (same arithmetic as the binning kernels)
-        for (int q = threadIdx.x; q < m; q += FIX_THREADS) {
-            const float4 v = spts[start + q];
-            uint32_t lin;
-            int o;
-            dense_cell_of(v.x, v.y, v.z, g, lin, o);
-            atomicAdd(&cnt[o], 1);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int k = 0; k < 8; ++k) { off[k] = run; cur[k] = run; run += cnt[k]; }
-            off[8] = run;
-            DenseRec R;
-            R.cell = cell;
-            for (int k = 0; k < 9; ++k) R.off[k] = start + off[k];
-            drec[r] = R;
-            crec[cell] = r;
-            atomicAdd(&meta->dense_points, (unsigned long long)m);
-            // heavy cells first in the union kernel's schedule (long tails otherwise)
-            if (m > HEAVY_POINTS) order[atomicAdd(&meta->nheavy, 1)] = r;
-            else order[nd - 1 - atomicAdd(&meta->nlight, 1)] = r;
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < m; q += FIX_THREADS) {
-            const float4 v = spts[start + q];
-            uint32_t lin;
-            int o;
-            dense_cell_of(v.x, v.y, v.z, g, lin, o);
-            const int d = atomicAdd(&cur[o], 1);
-            if (in_smem) sp[d] = v;
-            else tmp_pts[start + d] = v;
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < m; q += FIX_THREADS) {
-            int k = 0;
-            while (q >= off[k + 1]) ++k;
-            const float4 v = in_smem ? sp[q] : tmp_pts[start + q];
-            spts[start + q] = v;
-            sidx[start + q] = __float_as_int(v.w);
-            parent[start + q] = start + off[k + 1] - 1;   // leader = last point of the octant group
-        }
-        __syncthreads();
+        sidx[s] = __float_as_int(v.w);
     }
 }
 
@@ -395,18 +422,39 @@ __device__ void dense_cell_work(int r, int phase, DenseSmem& S, const float4* __
         }
     }
     __syncwarp();
-    // current roots (P's own groups were just joined)
+    // current roots (P's own groups were joined in phase 0)
     if (lane < np) S.proot[lane] = uf_find(parent, S.ps[lane]);
     for (int b = lane; b < nq; b += 32) S.qroot[b] = uf_find(parent, S.qs[b]);
     __syncwarp();
-    pair_sweep(S, np, 0, nq, false, spts, parent, t2, lane, n_tests, n_pairs);
+    // keep only Q groups that can still need a test: when all P groups share one root R
+    // (the usual case), a Q group already rooted at R is skipped as a whole
+    const int R0 = S.proot[0];
+    const bool allsame = __all_sync(0xffffffffu, lane >= np || S.proot[lane] == R0);
+    int live_n = 0;
+    for (int b0 = 0; b0 < nq; b0 += 32) {
+        const int b = b0 + lane;
+        const bool live = b < nq && (!allsame || S.qroot[b] != R0);
+        int qs_ = 0, qe_ = 0, qr_ = 0;
+        uint8_t qo_ = 0, qk_ = 0;
+        if (live) { qs_ = S.qs[b]; qe_ = S.qe[b]; qr_ = S.qroot[b]; qo_ = S.qo[b]; qk_ = S.qk[b]; }
+        const unsigned m = __ballot_sync(0xffffffffu, live);
+        __syncwarp();
+        if (live) {
+            const int d = live_n + __popc(m & ((1u << lane) - 1u));
+            S.qs[d] = qs_; S.qe[d] = qe_; S.qroot[d] = qr_; S.qo[d] = qo_; S.qk[d] = qk_;
+        }
+        live_n += __popc(m);
+        __syncwarp();
+    }
+    if (live_n == 0) return;
+    pair_sweep(S, np, 0, live_n, false, spts, parent, t2, lane, n_tests, n_pairs);
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __restrict__ spts,
                                                             const uint32_t* __restrict__ cstart,
                                                             const DenseRec* __restrict__ drec,
                                                             const int* __restrict__ crec,
-                                                            const int* __restrict__ order, int phase, Grid g,
+                                                            int phase, Grid g,
                                                             int* __restrict__ parent, Meta* __restrict__ meta) {
     __shared__ DenseSmem sm[SCAN_THREADS / kWarp];
     const int lane = threadIdx.x & 31;
@@ -418,7 +466,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __re
         if (lane == 0) it = atomicAdd(phase == 0 ? &meta->work : &meta->work2, 1);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= nd) break;
-        dense_cell_work(__ldg(order + it), phase, S, spts, cstart, drec, crec, g, parent, lane, n_tests, n_pairs);
+        // phase 1 visits the cells in a scattered order (a multiplicative permutation):
+        // cells processed at the same time are then rarely neighbours, so each cell sees
+        // the unions its neighbours already made and most group pairs skip on roots
+        // (a sweep in cell order processes ~7k adjacent cells at once and tests 3x more).
+        const int r = phase == 0 ? it : (int)(((unsigned long long)it * 2654435761ull) % (unsigned long long)nd);
+        dense_cell_work(r, phase, S, spts, cstart, drec, crec, g, parent, lane, n_tests, n_pairs);
         __syncwarp();
     }
     if (meta->instrument) {

@@ -59,16 +59,22 @@ __global__ void k_flatten(int* parent, int64_t n);
 __global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
 __global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
                           long long min_size, long long max_size, int* labels);
-__global__ void k_dcount(const float* p, int64_t n, Grid g, uint32_t* count, uint32_t* slot, int* dlist, Meta* meta);
+__global__ void k_dcount(const float* p, int64_t n, Grid g, uint32_t* count, uint32_t* slot, uint32_t* dbits,
+                         Meta* meta);
+__global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount);
+__global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
+                             uint32_t* ocnt, Meta* meta);
+__global__ void k_dcount_oct(const float* p, int64_t n, Grid g, const uint32_t* count, const int* crec, uint32_t* ocnt,
+                             uint32_t* slot);
+__global__ void k_drec_fin(const int* dlist, Meta* meta, const uint32_t* cstart, const uint32_t* ocnt, DenseRec* drec);
 __global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint32_t* cstart, const uint32_t* slot,
-                           float4* spts);
-__global__ void k_dinit(const float4* spts, int64_t n, int* parent, int* size, int* minidx, int* sidx);
-__global__ void k_dfixup(const uint32_t* cstart, const int* dlist, Meta* meta, Grid g, float4* spts, int* sidx,
-                         int* parent, DenseRec* drec, int* crec, int* order, float4* tmp_pts);
+                           const int* crec, const DenseRec* drec, float4* spts);
+__global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint32_t* cstart, const int* crec,
+                        const DenseRec* drec, int* parent, int* size, int* minidx, int* sidx);
 __global__ void k_union_sparse(const float4* spts, const uint32_t* cstart, uint32_t cells, Grid g, int* parent,
                                Meta* meta);
 __global__ void k_union_dense(const float4* spts, const uint32_t* cstart, const DenseRec* drec, const int* crec,
-                              const int* order, int phase, Grid g, int* parent, Meta* meta);
+                              int phase, Grid g, int* parent, Meta* meta);
 __global__ void k_debug_pred(const float* a, const float* b, int64_t m, float t2, uint8_t* out, float* d2out);
 
 }  // namespace fec

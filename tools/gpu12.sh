@@ -1,0 +1,6 @@
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pytest_gpu.log
+for c in C3 C4 C5; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo $c=$?; tail -3 gpurun_out/bench_$c.err; python -c "
+import json; d=json.load(open('gpurun_out/bench_$c.json')); print(d['value'], d['ms_per_step'], d['roofline']['kernel'], d['roofline']['frac']); print({k: round(v,3) for k,v in d['stages_ms'].items()}); print({k:d['config'][k] for k in ('n_points','cells','components','pair_tests','dense_tests','group_pairs','dense_cells','dense_points')})"; done
+python tools/prof_run.py C4 1.0 2 > gpurun_out/prof_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 25 --csv --log-file gpurun_out/launches_c4.csv python tools/prof_run.py C4 1.0 2 > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?
