@@ -38,7 +38,7 @@ WORKLOAD_TEXT = {
     "C5": "C5: 100M uniform pts at mean degree 2.8 + 50 balls x 200k pts, shuffled; d_th=0.1 m, min 1, max 1e9",
 }
 # bounded oracle samples (prefixes in acquisition order for the LiDAR maps)
-CPU_SAMPLE = {"C1": None, "C2": None, "C3": 3_000_000, "C4": 6_000_000, "C5": 5_000_000}
+CPU_SAMPLE = {"C1": None, "C2": None, "C3": 4_000_000, "C4": 12_000_000, "C5": 8_000_000}
 REF_STEP_SAMPLE = {"C1": None, "C2": None, "C3": 600_000, "C4": 1_200_000, "C5": 1_000_000}
 
 

@@ -230,7 +230,7 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
     const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
     k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite);
-    k_bbox_final<<<1, 32, 0, st>>>(L.part, (int)bb_blocks, L.meta);
+    k_bbox_final<<<1, 256, 0, st>>>(L.part, (int)bb_blocks, L.meta);
     launches += 2;
     FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
     FEC_CUDA(cudaStreamSynchronize(st));

@@ -65,12 +65,36 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ 
     }
 }
 
-__global__ void k_bbox_final(const float* __restrict__ part, int nblocks, Meta* __restrict__ meta) {
-    const int k = threadIdx.x;  // 6 threads
-    if (k >= 6) return;
-    float v = part[k];
-    for (int b = 1; b < nblocks; ++b) v = k < 3 ? fminf(v, part[b * 6 + k]) : fmaxf(v, part[b * 6 + k]);
-    meta->bbox[k] = v;
+__global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ part, int nblocks,
+                                                   Meta* __restrict__ meta) {
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mn[k] = fminf(mn[k], part[b * 6 + k]);
+            mx[k] = fmaxf(mx[k], part[b * 6 + 3 + k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+    }
+    __shared__ float s[8][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { s[w][k] = mn[k]; s[w][3 + k] = mx[k]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        meta->bbox[threadIdx.x] = v;
+    }
 }
 
 // =====================================================================================
