@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="also verify the labels bit-exactly (untimed)")
+    ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even at N=1 (testing)")
     return ap.parse_args()
 
 
@@ -212,7 +213,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": "Mpoints/s clustered", "value": value, "unit": "Mpoints/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.config], "n_points_per_step": n, "sample": desc},
         "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": 1, "kind": "oracle", "sample": desc},
@@ -232,11 +233,160 @@ def cpu_baseline(name: str, scale: float):
             "sample": f"{desc}; {dt:.1f} s single-threaded"}
 
 
+def run_slab(args, rank: int, world: int, local: int):
+    """N > 1: the cloud is sharded into spatial slabs (+ one-cell halo) before the timed
+    region (north_star: "sharded across the 8xB200 box into spatial slabs"); a step is
+    fec_slab_local -> NCCL all-gather of boundary records -> fec_slab_merge on every rank.
+    Total work is the fixed workload, so scaling is strong."""
+    import torch
+    import torch.distributed as tdist
+    import paper_2208_07678_b200 as fec
+    from paper_2208_07678_b200 import dist as fdist
+
+    multi = world > 1
+
+    def barrier():
+        if multi:
+            tdist.barrier()
+
+    def allreduce(t, op=tdist.ReduceOp.SUM):
+        if multi:
+            tdist.all_reduce(t, op=op)
+        return t
+
+    fec.lib()
+    d_th, mn, mx = synth.CONFIGS[args.config]
+    w = synth.make_config(args.config, scale=args.scale)
+    n_total = w.n
+    plan = fdist.plan_slabs(w.points, d_th, world)  # identical on every rank
+    sh = fdist.shard(w.points, plan, rank)
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(sh.points).to(dev)
+    g = torch.from_numpy(sh.gidx).to(dev)
+    runner = fdist.SlabRunner(x, g, sh.n_owned, sh.n_first, plan.rec_cap, d_th, mn, mx, world, rank)
+    stream = torch.cuda.current_stream(dev)
+    fec.set_instrumentation(True)
+    runner.step()
+    torch.cuda.synchronize()
+    st = fec.stats()
+    fec.set_instrumentation(False)
+    check = None
+    if args.check:
+        import oracle
+        parts = [None] * world
+        mine = (sh.gidx[:sh.n_owned], runner.labels.cpu().numpy())
+        if multi:
+            tdist.all_gather_object(parts, mine)
+        else:
+            parts = [mine]
+        if rank == 0:
+            full = np.full(n_total, -7, np.int32)
+            for gi, lab in parts:
+                full[gi] = lab
+            check = bool(np.array_equal(full, oracle.fec(w.points, d_th, mn, mx)))
+    for _ in range(args.warmup):
+        runner.step()
+    torch.cuda.synchronize()
+    barrier()
+    fec.set_timing(True)
+    stage_sum: dict[str, float] = {}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            runner.step()
+            for k, v in fec.stage_times().items():
+                stage_sum[k] = stage_sum.get(k, 0.0) + v
+        e1.record(stream)
+        torch.cuda.synchronize()
+    fec.set_timing(False)
+    barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], device=dev)
+    allreduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = n_total / (ms * 1e-3) / 1e6
+
+    # e2e: this rank's slab from pinned host memory, labels back to host, every step
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(sh.points).pin_memory()
+        hg = torch.from_numpy(sh.gidx).pin_memory()
+        hl = torch.empty(sh.n_owned, dtype=torch.int32).pin_memory()
+
+        def host_step():
+            runner.points.copy_(hp, non_blocking=True)
+            runner.gidx.copy_(hg, non_blocking=True)
+            lab = runner.step()
+            hl.copy_(lab, non_blocking=True)
+            stream.synchronize()
+
+        for _ in range(max(1, args.warmup // 2)):
+            host_step()
+        barrier()
+        ksteps = max(3, args.steps // 2)
+        e0.record(stream)
+        for _ in range(ksteps):
+            host_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / ksteps], device=dev)
+        allreduce(t, op=tdist.ReduceOp.MAX)
+        ems = float(t.item())
+        nb = torch.tensor([16 * sh.points.shape[0], 4 * sh.n_owned], device=dev, dtype=torch.int64)
+        allreduce(nb)  # bytes copied by all ranks together
+        e2e = {"value": n_total / (ems * 1e-3) / 1e6, "unit": "Mpoints/s",
+               "h2d_bytes_per_step": int(nb[0].item()), "d2h_bytes_per_step": int(nb[1].item()),
+               "ms_per_step": ems}
+
+    n_local = sh.points.shape[0]
+    stages = {k: v / args.steps for k, v in stage_sum.items()}
+    dom = max((k for k in stages if k != "a1_bbox_validate"), key=lambda k: stages[k])
+    peak, peak_src = load_peaks()
+    ab = algorithmic_bytes(dom, n_local, st)
+    ach = ab / (stages[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "peak_source": peak_src, "algorithmic_bytes": ab, "rank": rank}
+    launches = torch.tensor([st["launches"] + 5], device=dev)  # + merge kernels
+    allreduce(launches, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": "Mpoints/s clustered", "value": value, "unit": "Mpoints/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT[args.config] + ("" if args.scale == 1.0 else f" (scale {args.scale})"),
+                       "n_points": n_total, "d_th": d_th, "min_size": mn, "max_size": mx,
+                       "parallelism": f"slab{world} (axis {'xyz'[plan.axis]}, one-cell halo, NCCL all-gather "
+                                      f"of boundary records)",
+                       "slab_points": [int(v) for v in plan.n_owned], "halo_points": [int(v) for v in plan.n_halo],
+                       "rec_cap": plan.rec_cap,
+                       "l2": "no flush: per-rank inputs and working set exceed the 126 MB L2"
+                             if 12 * n_local > 126e6 else "per-rank input below L2 size; working set "
+                             f"({fec.slab_workspace_bytes(n_local, world, plan.rec_cap) / 1e9:.2f} GB) exceeds it"},
+            "e2e": e2e,
+            "roofline": roofline,
+            "cpu_baseline": None,
+            "gpu_launches": int(launches.item()) * args.steps,
+            "clocks": clk.summary(),
+            "stages_ms_rank0": stages,
+        }
+        if check is not None:
+            line["parity_bit_exact"] = check
+        print(json.dumps(line), flush=True)
+    if multi:
+        tdist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if world > 1 or args.slab:
+        run_slab(args, rank, world, local)
         return
     import torch
     import paper_2208_07678_b200 as fec
@@ -342,10 +492,10 @@ def main():
         line = {
             "metric": "Mpoints/s clustered", "value": value, "unit": "Mpoints/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.config] + ("" if args.scale == 1.0 else f" (scale {args.scale})"),
                        "n_points": n, "d_th": d_th, "min_size": mn, "max_size": mx,
-                       "parallelism": "single" if world == 1 else f"replicas{world}",
+                       "parallelism": "single",
                        "l2": f"no flush: inputs ({12 * n / 1e6:.0f} MB) and working set "
                              f"({fec.workspace_bytes(n) / 1e9:.1f} GB) exceed the 126 MB L2"
                              if 12 * n > 126e6 else "small input: L2-resident (latency-bound)",

@@ -121,6 +121,65 @@ void fec_set_timing(int enable);
 int32_t fec_get_stage_times(float* ms_out, int32_t max_stages);
 const char* fec_stage_name(int32_t stage);
 
+/* ---- Multi-GPU slab path ------------------------------------
+ *
+ * PAPER.md's FEC is serial (L480 lists a parallel version as future work); the sharding is
+ * this library's: the cloud is cut into spatial slabs along one axis at boundaries of a
+ * grid whose cell edge exceeds d_th (reading A6), so every edge of the graph of Eq. 1
+ * (L187-194) joins points of the same or of adjacent slabs.  Each rank holds its slab plus
+ * a one-cell halo (the first cell layer of the next slab) and calls, on its own device:
+ *
+ *   1. fec_slab_local   clusters owned ∪ halo (a1..a8) and packs boundary records;
+ *   2. an all-gather of the record buffers (NCCL, by the caller — the library does no
+ *      communication; `world` buffers of fec_slab_record_words(rec_cap) int32 each,
+ *      rank r's buffer at offset r);
+ *   3. fec_slab_merge   replays the same boundary union-find on every rank and writes the
+ *      global labels of the rank's owned points.
+ *
+ * The result over all ranks equals fec_cluster on the whole cloud: labels_owned[i] = the
+ * minimum GLOBAL index (gidx) of the point's component, or -1 when the component's total
+ * size (over all slabs) is outside [min_size, max_size].
+ *
+ * Local input order (caller's contract): points[0 .. n_first) are owned points in the slab's
+ * first cell layer (the halo of the previous rank), points[n_first .. n_owned) the other
+ * owned points, points[n_owned .. n_local) the halo (owned by the next rank).  gidx[i] is
+ * the global input index of local point i (int32, unique over the owned points of all
+ * ranks).  rec_cap must be the same on every rank and >= n_first + (n_local - n_owned) on
+ * every rank.  Record buffer layout (int32 words): [nP, nC, 0, 0], then rec_cap (gidx, key)
+ * pairs (space for rec_cap rounded up to even), then rec_cap (key, owned size, owned min
+ * gidx, local root) quads — 16-byte aligned when the buffer is.
+ * If the caller's halo/first-layer sets are not exactly one cell layer of a grid with edge
+ * > d_th, the result is unspecified (not detected). */
+typedef struct {
+    int64_t opaque[8]; /* host memory; filled by fec_slab_local, read by fec_slab_merge */
+} fec_slab_state_t;
+
+/* int32 words of one rank's record buffer: 4 + 2*(rec_cap rounded up to even) + 4*rec_cap
+ * (-1 if rec_cap < 0); a multiple of 4, so gathered buffers stay 16-byte aligned. */
+int64_t fec_slab_record_words(int64_t rec_cap);
+
+/* Device workspace for fec_slab_local + fec_slab_merge on n_local points (one buffer for
+ * both calls; it carries the local forest from the first call to the second). */
+size_t fec_slab_workspace_bytes(int64_t n_local, int32_t world, int64_t rec_cap);
+
+/* Step 1 (device pointers; enqueued on `stream`, one host sync after the bbox kernel like
+ * fec_cluster_ws).  Writes the rank's record buffer `records` (fec_slab_record_words(rec_cap)
+ * words) and fills *state.  Errors: as fec_cluster_ws, plus FEC_ERR_INVALID_ARGUMENT for
+ * n_first/n_owned/n_local out of order or rec_cap too small.  n_local == 0 is valid (the
+ * header is zeroed, nothing else is launched). */
+fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_local, int64_t n_owned,
+                            int64_t n_first, float d_th, int32_t* records, int64_t rec_cap, void* workspace,
+                            size_t workspace_bytes, fec_slab_state_t* state, void* stream);
+
+/* Step 3.  all_records: world * fec_slab_record_words(rec_cap) int32 (device), the gathered
+ * buffers in rank order.  labels_owned: int32[n_owned] (device), in local order.  The
+ * workspace and state must be those of this rank's fec_slab_local, with the workspace
+ * sized by fec_slab_workspace_bytes(n_local, world, rec_cap).  Enqueued on `stream`; no
+ * host synchronisation. */
+fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t rank, int64_t min_size,
+                            int64_t max_size, int32_t* labels_owned, void* workspace, size_t workspace_bytes,
+                            const fec_slab_state_t* state, void* stream);
+
 /* Human-readable status text (static storage) and the last error detail of this thread. */
 const char* fec_status_string(fec_status_t status);
 const char* fec_last_error(void);

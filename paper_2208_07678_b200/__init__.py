@@ -16,7 +16,8 @@ import os
 
 import numpy as np
 
-__all__ = ["cluster", "cluster_host", "workspace_bytes", "workspace_bytes_host", "stats",
+__all__ = ["cluster", "cluster_host", "slab_local", "slab_merge", "slab_record_words",
+           "slab_workspace_bytes", "SlabState", "workspace_bytes", "workspace_bytes_host", "stats",
            "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfec.so")
@@ -27,7 +28,8 @@ OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_
 EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
            "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
-           "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode")
+           "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
+           "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge")
 
 
 class FecStats(ctypes.Structure):
@@ -38,6 +40,11 @@ class FecStats(ctypes.Structure):
                 ("key_bits", ctypes.c_int64),
                 ("radix_passes", ctypes.c_int32), ("dense_table", ctypes.c_int32),
                 ("dims", ctypes.c_int32 * 3), ("launches", ctypes.c_int32)]
+
+
+class SlabState(ctypes.Structure):
+    """Opaque host-side state carried from slab_local to slab_merge (fec_slab_state_t)."""
+    _fields_ = [("opaque", ctypes.c_int64 * 8)]
 
 
 class FecError(RuntimeError):
@@ -86,6 +93,15 @@ def lib():
         L.fec_get_stage_times.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int32]
         L.fec_stage_name.restype = ctypes.c_char_p
         L.fec_stage_name.argtypes = [ctypes.c_int32]
+        L.fec_slab_record_words.restype = i64
+        L.fec_slab_record_words.argtypes = [i64]
+        L.fec_slab_workspace_bytes.restype = sz
+        L.fec_slab_workspace_bytes.argtypes = [i64, ctypes.c_int32, i64]
+        L.fec_slab_local.restype = ctypes.c_int32
+        L.fec_slab_local.argtypes = [vp, vp, i64, i64, i64, f32, vp, i64, vp, sz, ctypes.POINTER(SlabState), vp]
+        L.fec_slab_merge.restype = ctypes.c_int32
+        L.fec_slab_merge.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, i64, i64, vp, vp, sz,
+                                     ctypes.POINTER(SlabState), vp]
         L.fec_debug_pred.restype = ctypes.c_int32
         L.fec_debug_pred.argtypes = [vp, vp, i64, f32, vp, vp, vp]
         _lib = L
@@ -223,3 +239,48 @@ def debug_pred(a, b, d_th: float):
     _check(lib().fec_debug_pred(a.contiguous().data_ptr(), b.contiguous().data_ptr(), m, _f32(d_th),
                                 out.data_ptr(), d2.data_ptr(), st.cuda_stream))
     return out.bool(), d2
+
+
+# ---- multi-GPU slab path (include/fec.h "Multi-GPU slab path"; driver in .dist) ---------------
+def slab_record_words(rec_cap: int) -> int:
+    return int(lib().fec_slab_record_words(int(rec_cap)))
+
+
+def slab_workspace_bytes(n_local: int, world: int, rec_cap: int) -> int:
+    return int(lib().fec_slab_workspace_bytes(int(n_local), int(world), int(rec_cap)))
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None and t.numel() else None
+
+
+def slab_local(points, gidx, n_owned: int, n_first: int, d_th: float, records, rec_cap: int, workspace,
+               stream=None) -> SlabState:
+    """Step 1 on this rank: cluster owned ∪ halo (CUDA float32 [n_local, 3], local order
+    first-layer | other owned | halo) and pack boundary records into `records` (CUDA int32
+    [slab_record_words(rec_cap)]).  Returns the state slab_merge needs."""
+    torch = _torch()
+    if not (isinstance(points, torch.Tensor) and points.is_cuda and points.dtype == torch.float32):
+        raise TypeError("points must be a CUDA float32 tensor [n, 3]")
+    if gidx.dtype != torch.int32 or records.dtype != torch.int32 or not gidx.is_cuda or not records.is_cuda:
+        raise TypeError("gidx and records must be CUDA int32 tensors")
+    points = points.contiguous()
+    n_local = points.shape[0]
+    st = stream if stream is not None else torch.cuda.current_stream(records.device)
+    state = SlabState()
+    _check(lib().fec_slab_local(_ptr(points), _ptr(gidx), n_local, int(n_owned), int(n_first), _f32(d_th),
+                                records.data_ptr(), int(rec_cap), workspace.data_ptr(), workspace.numel(),
+                                ctypes.byref(state), st.cuda_stream))
+    return state
+
+
+def slab_merge(all_records, world: int, rank: int, min_size: int, max_size: int, labels_owned, workspace,
+               state: SlabState, stream=None):
+    """Step 3 on this rank: replicated boundary union-find over the gathered records, then
+    the global labels (min global index, or -1) of the rank's owned points."""
+    torch = _torch()
+    st = stream if stream is not None else torch.cuda.current_stream(all_records.device)
+    _check(lib().fec_slab_merge(all_records.data_ptr(), int(world), int(rank), int(min_size), int(max_size),
+                                _ptr(labels_owned), workspace.data_ptr(), workspace.numel(), ctypes.byref(state),
+                                st.cuda_stream))
+    return labels_owned

@@ -7,6 +7,7 @@
 
 #include "fec.h"
 #include "fec_kernels.cuh"
+#include "fec_slab.cuh"
 
 using namespace fec;
 
@@ -200,26 +201,21 @@ inline unsigned grid_for(int64_t work, int per_block, int cap) {
     return (unsigned)b;
 }
 
-fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t max_size, int32_t* labels,
-                 void* ws, size_t ws_bytes, cudaStream_t st) {
-    g_stats_valid = false;
-    g_ev.recorded = false;
+// State of a call after a1..a8 (flattened forest over sorted positions), shared by the
+// single-GPU tail (a9, a10) and the slab tail (owned-only stats + boundary records).
+struct Core {
+    Layout L;
+    Grid g;
+    const int* val = nullptr;  // local input index of each sorted position
     int launches = 0;
-    float t2 = 0.f;
-    fec_status_t rc = check_args(n, d, min_size, max_size, &t2);
-    if (rc != FEC_OK) return rc;
-    if (n == 0) {
-        std::memset(&g_stats, 0, sizeof(g_stats));
-        g_stats_valid = true;
-        return FEC_OK;
-    }
-    if (!pts || !labels || !ws) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
-    if (!is_device_ptr(pts) || !is_device_ptr(labels) || !is_device_ptr(ws)) {
-        g_err = "points, labels_out and workspace must be device pointers";
-        return FEC_ERR_INVALID_ARGUMENT;
-    }
-    Layout L = carve(static_cast<char*>(ws), n);
-    if (ws_bytes < L.total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    int passes = 0;
+};
+
+// a1..a8 on n > 0 points (arguments already checked, pointers validated).
+fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C) {
+    Layout& L = C.L;
+    L = carve(static_cast<char*>(ws), n);
+    int launches = 0;
     if (!g_pinned_meta) FEC_CUDA(cudaMallocHost(&g_pinned_meta, sizeof(Meta)));
     const DevInfo di = dev_info();
     const int cap = di.sms * 8;
@@ -358,17 +354,24 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
         mark(7, st);
     }
 
-    // ---- a8..a10 ---------------------------------------------------------------------------
+    // ---- a8 ----------------------------------------------------------------------------------
     k_flatten<<<ew, 256, 0, st>>>(L.parent, n);
+    ++launches;
     mark(8, st);
-    k_stats<<<ew, 256, 0, st>>>(L.parent, val, n, L.size, L.minidx, L.meta);
-    mark(9, st);
-    k_relabel<<<ew, 256, 0, st>>>(L.parent, val, L.size, L.minidx, n, (long long)min_size, (long long)max_size,
-                                  labels);
-    launches += 3;
-    mark(10, st);
-    FEC_CUDA(cudaGetLastError());
+    C.g = g;
+    C.val = val;
+    C.launches = launches;
+    C.passes = passes;
+    return FEC_OK;
+}
 
+// Fills g_stats after a successful call (instrumented counters need one read-back).
+fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
+    const Grid& g = C.g;
+    const Layout& L = C.L;
+    const int launches = C.launches;
+    const int passes = C.passes;
+    const int key_bits = g.key_bits;
     std::memset(&g_stats, 0, sizeof(g_stats));
     g_stats.n = n;
     g_stats.cells = g_stats.groups = g_stats.components = g_stats.pair_tests = g_stats.group_pairs = -1;
@@ -394,6 +397,75 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     return FEC_OK;
 }
 
+fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t max_size, int32_t* labels,
+                 void* ws, size_t ws_bytes, cudaStream_t st) {
+    g_stats_valid = false;
+    g_ev.recorded = false;
+    float t2 = 0.f;
+    fec_status_t rc = check_args(n, d, min_size, max_size, &t2);
+    if (rc != FEC_OK) return rc;
+    if (n == 0) {
+        std::memset(&g_stats, 0, sizeof(g_stats));
+        g_stats_valid = true;
+        return FEC_OK;
+    }
+    if (!pts || !labels || !ws) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!is_device_ptr(pts) || !is_device_ptr(labels) || !is_device_ptr(ws)) {
+        g_err = "points, labels_out and workspace must be device pointers";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    if (ws_bytes < carve(nullptr, n).total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    Core C;
+    rc = run_core(pts, n, d, t2, ws, st, C);
+    if (rc != FEC_OK) return rc;
+    const Layout& L = C.L;
+    const unsigned ew = grid_for(n, 256, dev_info().sms * 8 * 4);
+    // ---- a9, a10 -------------------------------------------------------------------------------
+    k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
+    mark(9, st);
+    k_relabel<<<ew, 256, 0, st>>>(L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size,
+                                  labels);
+    C.launches += 2;
+    mark(10, st);
+    FEC_CUDA(cudaGetLastError());
+    return finish_stats(C, n, st);
+}
+
+
+// ---- slab (multi-GPU) path ----------------------------------------------------------------
+constexpr int64_t kSlabMagic = 0x46454353'4c414231ll;  // "FECSLAB1"
+struct SlabState {       // lives in the caller's fec_slab_state_t (host memory)
+    int64_t magic;
+    int64_t n_local, n_owned, n_first, rec_cap;
+    int64_t val_off;     // byte offset of the sorted-position -> local-index array in the workspace
+    int64_t pad[2];
+};
+static_assert(sizeof(SlabState) == sizeof(fec_slab_state_t), "opaque state size");
+
+int64_t slab_hash_cap(int32_t world, int64_t rec_cap) {
+    int64_t c = 1024;
+    while (c < 2 * (int64_t)world * rec_cap) c <<= 1;
+    return c;
+}
+struct SlabLayout {
+    size_t core;  // fec_workspace_bytes(n_local)
+    int* ckey;
+    int *hkey, *hpar, *gsize, *gmin;
+    size_t total;
+};
+SlabLayout slab_carve(char* base, int64_t n_local, int32_t world, int64_t rec_cap) {
+    SlabLayout S{};
+    S.core = n_local > 0 ? carve(nullptr, n_local).total : 0;
+    Carver cv{base, S.core, 0};
+    S.ckey = cv.take<int>(n_local > 0 ? n_local : 1);
+    const int64_t hc = slab_hash_cap(world, rec_cap);
+    S.hkey = cv.take<int>(hc);
+    S.hpar = cv.take<int>(hc);
+    S.gsize = cv.take<int>(hc);
+    S.gmin = cv.take<int>(hc);
+    S.total = cv.off + 256;
+    return S;
+}
 }  // namespace
 
 extern "C" {
@@ -453,6 +525,113 @@ fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th, i
     if (rc == FEC_OK) FEC_CUDA(cudaMemcpyAsync(labels_host, dlab, (size_t)4 * n, cudaMemcpyDeviceToHost, st));
     FEC_CUDA(cudaStreamSynchronize(st));
     return rc;
+}
+
+
+int64_t fec_slab_record_words(int64_t rec_cap) { return rec_cap < 0 ? -1 : slab_c_off(rec_cap) + 4 * rec_cap; }
+
+size_t fec_slab_workspace_bytes(int64_t n_local, int32_t world, int64_t rec_cap) {
+    if (n_local < 0 || world < 1 || rec_cap < 0) return 0;
+    return slab_carve(nullptr, n_local, world, rec_cap).total;
+}
+
+fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_local, int64_t n_owned,
+                            int64_t n_first, float d_th, int32_t* records, int64_t rec_cap, void* workspace,
+                            size_t workspace_bytes, fec_slab_state_t* state, void* stream) {
+    g_stats_valid = false;
+    g_ev.recorded = false;
+    float t2 = 0.f;
+    fec_status_t rc = check_args(n_local, d_th, 1, 1, &t2);
+    if (rc != FEC_OK) return rc;
+    if (!state) { g_err = "state is NULL"; return FEC_ERR_INVALID_ARGUMENT; }
+    std::memset(state, 0, sizeof(*state));
+    if (n_first < 0 || n_owned < n_first || n_local < n_owned) {
+        g_err = "need 0 <= n_first <= n_owned <= n_local";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    if (rec_cap < n_first + (n_local - n_owned) || rec_cap > (int64_t)(INT32_MAX - SLAB_HDR) / 6) {
+        g_err = "rec_cap must be >= n_first + (n_local - n_owned) (boundary points) and < 2^31/6";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    if (!records || !workspace || (n_local > 0 && (!points || !gidx))) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!is_device_ptr(records) || !is_device_ptr(workspace) ||
+        (n_local > 0 && (!is_device_ptr(points) || !is_device_ptr(gidx)))) {
+        g_err = "points, gidx, records and workspace must be device pointers";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    const SlabLayout S = slab_carve(static_cast<char*>(workspace), n_local, 1, 0);
+    if (workspace_bytes < S.total) { g_err = "workspace too small (see fec_slab_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FEC_CUDA(cudaMemsetAsync(records, 0, SLAB_HDR * sizeof(int32_t), st));
+    SlabState ss{kSlabMagic, n_local, n_owned, n_first, rec_cap, 0, {0, 0}};
+    if (n_local == 0) {
+        std::memcpy(state, &ss, sizeof(ss));
+        std::memset(&g_stats, 0, sizeof(g_stats));
+        g_stats_valid = true;
+        return FEC_OK;
+    }
+    Core C;
+    rc = run_core(points, n_local, d_th, t2, workspace, st, C);
+    if (rc != FEC_OK) return rc;
+    const Layout& L = C.L;
+    const unsigned ew = grid_for(n_local, 256, dev_info().sms * 8 * 4);
+    FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)n_local * 4, st));
+    k_slab_stats<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
+                                     S.ckey, L.meta);
+    mark(9, st);
+    k_slab_pack<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
+                                    S.ckey, records, (int)rec_cap);
+    C.launches += 2;
+    mark(10, st);
+    FEC_CUDA(cudaGetLastError());
+    ss.val_off = reinterpret_cast<const char*>(C.val) - static_cast<const char*>(workspace);
+    std::memcpy(state, &ss, sizeof(ss));
+    return finish_stats(C, n_local, st);
+}
+
+fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t rank, int64_t min_size,
+                            int64_t max_size, int32_t* labels_owned, void* workspace, size_t workspace_bytes,
+                            const fec_slab_state_t* state, void* stream) {
+    SlabState ss;
+    if (!state) { g_err = "state is NULL"; return FEC_ERR_INVALID_ARGUMENT; }
+    std::memcpy(&ss, state, sizeof(ss));
+    if (ss.magic != kSlabMagic) { g_err = "state was not filled by a successful fec_slab_local"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (world < 1 || rank < 0 || rank >= world) { g_err = "need 0 <= rank < world"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (min_size < 0 || max_size < 1 || min_size > max_size) { g_err = "need 0 <= min_size <= max_size, max_size >= 1"; return FEC_ERR_INVALID_ARGUMENT; }
+    if ((int64_t)world * ss.rec_cap > INT32_MAX / 2) { g_err = "world * rec_cap too large"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!all_records || !workspace || (ss.n_owned > 0 && !labels_owned)) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (!is_device_ptr(all_records) || !is_device_ptr(workspace) || (ss.n_owned > 0 && !is_device_ptr(labels_owned))) {
+        g_err = "all_records, labels_owned and workspace must be device pointers";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    const SlabLayout S = slab_carve(static_cast<char*>(workspace), ss.n_local, world, ss.rec_cap);
+    if (workspace_bytes < S.total) { g_err = "workspace too small (see fec_slab_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t hc = slab_hash_cap(world, ss.rec_cap);
+    const unsigned mask = (unsigned)(hc - 1);
+    const int64_t words = fec_slab_record_words(ss.rec_cap);
+    const int cap = dev_info().sms * 8 * 4;
+    k_merge_init<<<grid_for(hc, 256, cap), 256, 0, st>>>(S.hkey, S.hpar, S.gsize, S.gmin, hc);
+    const int64_t total = (int64_t)world * ss.rec_cap;
+    if (total > 0) {
+        k_merge_link<<<grid_for(total, 256, cap), 256, 0, st>>>(all_records, world, words, (int)ss.rec_cap, S.hkey,
+                                                                mask, S.hpar);
+        k_merge_stats<<<grid_for(total, 256, cap), 256, 0, st>>>(all_records, world, words, (int)ss.rec_cap, S.hkey,
+                                                                 mask, S.hpar, S.gsize, S.gmin);
+    }
+    if (ss.n_local > 0) {
+        const Layout L = carve(static_cast<char*>(workspace), ss.n_local);
+        const int* val = reinterpret_cast<const int*>(static_cast<const char*>(workspace) + ss.val_off);
+        if (ss.rec_cap > 0)
+            k_merge_resolve<<<grid_for(ss.rec_cap, 256, cap), 256, 0, st>>>(all_records + rank * words, (int)ss.rec_cap,
+                                                                            S.hkey, mask, S.hpar, S.gsize, S.gmin,
+                                                                            L.size, L.minidx);
+        k_slab_relabel<<<grid_for(ss.n_local, 256, cap), 256, 0, st>>>(L.parent, val, L.size, L.minidx, ss.n_local,
+                                                                       (int)ss.n_owned, (long long)min_size,
+                                                                       (long long)max_size, labels_owned);
+    }
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
 }
 
 fec_status_t fec_get_stats(fec_stats_t* out) {
