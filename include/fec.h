@@ -112,6 +112,11 @@ void fec_set_instrumentation(int enable);
  * mode always.  Both modes compute identical labels. */
 void fec_set_grid_mode(int mode);
 
+/* Test hook (thread-local): cap the queue of "uncertain" dense component pairs (DESIGN.md
+ * §4) at `cap` entries (0 = default, n/8 + 65536).  Pairs beyond the cap are tested in
+ * place by one thread each; labels are identical either way. */
+void fec_set_item_cap(int64_t cap);
+
 /* Per-stage device timing.  With fec_set_timing(1), each call records CUDA events on its
  * stream at the stage boundaries (a1 validate+bbox incl. the host sync, a2 keys, a3 sort,
  * a4 gather, a5 tables, a6+a7 scan+union, a8 flatten, a9 stats, a10 relabel).

@@ -29,7 +29,7 @@ EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspac
            "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
-           "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge")
+           "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap")
 
 
 class FecStats(ctypes.Structure):
@@ -85,6 +85,8 @@ def lib():
         L.fec_last_error.argtypes = []
         L.fec_version.restype = ctypes.c_char_p
         L.fec_version.argtypes = []
+        L.fec_set_item_cap.restype = None
+        L.fec_set_item_cap.argtypes = [i64]
         L.fec_set_grid_mode.restype = None
         L.fec_set_grid_mode.argtypes = [ctypes.c_int]
         L.fec_set_timing.restype = None
@@ -214,6 +216,11 @@ def stats() -> dict:
 def set_grid_mode(mode: int):
     """0 = automatic, 1 = always the hashed (Morton radix-sort) mode.  Testing aid."""
     lib().fec_set_grid_mode(int(mode))
+
+
+def set_item_cap(cap: int):
+    """Testing aid: cap the queued uncertain dense pairs (0 = default); labels do not change."""
+    lib().fec_set_item_cap(int(cap))
 
 
 def set_timing(enable: bool):

@@ -20,6 +20,7 @@ thread_local int g_instrument = 0;
 thread_local Meta* g_pinned_meta = nullptr;
 thread_local int g_timing = 0;
 thread_local int g_grid_mode = 0;
+thread_local int64_t g_item_cap = 0;  // test hook: cap on the queued uncertain pairs (0 = default)
 
 constexpr int kStages = 10;
 const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",       "a3_sort",
@@ -70,7 +71,7 @@ DevInfo dev_info() {
     if (di.sms == 0) {
         cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_dense, SCAN_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_scan_union, SCAN_THREADS, 0);
         di.scan_blocks_per_sm = b > 0 ? b : 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_sparse, 256, 0);
         di.sparse_blocks_per_sm = b > 0 ? b : 1;
@@ -78,7 +79,10 @@ DevInfo dev_info() {
     return di;
 }
 
-int64_t dense_cap(int64_t n) { return 4 * n + (int64_t(1) << 22); }
+// dense-grid mode needs 1/4 B per grid cell (occupancy bitmap + word bases + scan)
+int64_t dense_cap(int64_t n) { return 32 * n + (int64_t(1) << 26); }
+int64_t dense_max(int64_t n) { return n / (SPARSE_MAX + 1) + 16; }
+int64_t nodes_max(int64_t n) { return n + 8 * dense_max(n); }
 int64_t hash_cap(int64_t n) {
     int64_t c = 1024;
     while (c < 2 * n) c <<= 1;
@@ -101,19 +105,27 @@ struct Layout {
     uint32_t* scan32;
     Tables T;
     int num_tiles;
-    // dense-grid mode
-    uint32_t* cstart;   // [cells+1] counts, then exclusive prefix (cell start)
-    int* crec;          // [cells]   dense record id of a dense cell
+    // dense-grid mode (per-cell tables indexed by compact id of the occupied cells)
+    uint2* cw;          // [W+1] occupancy bitmap words {bits, occupied cells before the word}
+    uint32_t* cwpos;    // [W+2] popcount scan scratch
+    uint32_t* clin;     // [n]   linear cell id of each compact id
+    uint32_t* cstart;   // [n+1] counts, then exclusive prefix (cell start)
+    int* crec;          // [n]   dense record id of a dense cell
     uint32_t* dscan;    // scan scratch
     uint32_t* slot;     // [n]
     int* sidx;          // [n] input index of each sorted position
-    uint32_t* pcell;    // [n] linear cell of each sorted position
-    uint8_t* octs;      // [n]
-    int* dlist;         // dense cells
-    DenseRec* drec;     // their records
-    uint32_t* dbits;    // [cells/32+1] bitmap of dense cells
-    uint32_t* dwpos;    // [cells/32+2] popcount prefix of the bitmap words
-    uint32_t* ocnt;     // per dense record: points per octant
+    int* dlist;         // dense record -> compact cell id
+    uint32_t* dbits;    // [n/32+2] bitmap of dense compact ids
+    uint32_t* dwpos;    // [n/32+2] popcount prefix of the bitmap words
+    u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
+    u64* ccoord;        // [n]   cell coordinates of each occupied cell, 21 bits each
+    int* ncomp;         // per dense record: certain-connected components (<= 8)
+    uint32_t* dflag;    // per dense record: neighbour slots left for the uncertain pass
+    u64* dcoord;        // per dense record: cell coordinates, 21 bits each
+    int* dflist;        // dense records left for the uncertain pass
+    u64* cmask;         // per dense record: 8 component masks
+    int4* items;        // uncertain component pairs
+    int item_cap;
     size_t total;
 };
 
@@ -123,9 +135,10 @@ Layout carve(char* base, int64_t n) {
     L.meta = cv.take<Meta>(1);
     L.part = cv.take<float>(6 * kMaxBBoxBlocks);
     L.spts = cv.take<float4>(n);
-    L.parent = cv.take<int>(n);
-    L.size = cv.take<int>(n);
-    L.minidx = cv.take<int>(n);
+    // union-find nodes: the n points, then (dense-grid mode) 8 component nodes per dense cell
+    L.parent = cv.take<int>(nodes_max(n));
+    L.size = cv.take<int>(nodes_max(n));
+    L.minidx = cv.take<int>(nodes_max(n));
     const size_t common = (cv.off + 255) & ~size_t(255);
     // radix / hash mode
     Carver a{base, common, 0};
@@ -148,19 +161,28 @@ Layout carve(char* base, int64_t n) {
     L.T.dense = nullptr;
     // dense-grid mode
     const int64_t dc = dense_cap(n);
+    const int64_t W = dc / 32 + 1;
     Carver b{base, common, 0};
-    L.cstart = b.take<uint32_t>(dc + 1);
-    L.crec = b.take<int>(dc);
-    L.dscan = b.take<uint32_t>(scan_scratch_elems(dc + 1));
+    L.cw = b.take<uint2>(W + 1);
+    L.cwpos = b.take<uint32_t>(W + 2);
+    L.clin = b.take<uint32_t>(n);
+    L.cstart = b.take<uint32_t>(n + 1);
+    L.crec = b.take<int>(n);
+    L.dscan = b.take<uint32_t>(scan_scratch_elems(std::max<int64_t>(W + 2, n + 1)));
     L.slot = b.take<uint32_t>(n);
     L.sidx = b.take<int>(n);
-    L.pcell = b.take<uint32_t>(n);
-    L.octs = b.take<uint8_t>(n);
-    L.dlist = b.take<int>(n / (SPARSE_MAX + 1) + 16);
-    L.drec = b.take<DenseRec>(n / (SPARSE_MAX + 1) + 16);
-    L.dbits = b.take<uint32_t>(dc / 32 + 2);
-    L.dwpos = b.take<uint32_t>(dc / 32 + 2);
-    L.ocnt = b.take<uint32_t>((size_t)8 * (n / (SPARSE_MAX + 1) + 16));
+    L.dlist = b.take<int>(dense_max(n));
+    L.dbits = b.take<uint32_t>(n / 32 + 2);
+    L.dwpos = b.take<uint32_t>(n / 32 + 2);
+    L.cocc = b.take<u64>(n);
+    L.ccoord = b.take<u64>(n);
+    L.ncomp = b.take<int>(dense_max(n));
+    L.dflag = b.take<uint32_t>(dense_max(n));
+    L.dcoord = b.take<u64>(dense_max(n));
+    L.dflist = b.take<int>(dense_max(n));
+    L.cmask = b.take<u64>((size_t)8 * dense_max(n));
+    L.item_cap = (int)std::min<int64_t>(n / 8 + 65536, INT32_MAX / 2);
+    L.items = b.take<int4>(L.item_cap);
     L.total = std::max(a.off, b.off) + 256;
     return L;
 }
@@ -238,6 +260,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const double c = (double)d * (1.0 + std::ldexp(1.0, -16));
     g.h = c * 0.5;
     g.inv_h = 1.0 / g.h;
+    g.inv_q = 2.0 * g.inv_h;
     int64_t cells_total = 1;
     int key_bits = 3;
     for (int a = 0; a < 3; ++a) {
@@ -262,9 +285,12 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         FEC_CUDA(cudaMemcpyAsync(&L.meta->instrument, &one, sizeof(int), cudaMemcpyHostToDevice, st));
     }
     const unsigned ew = grid_for(n, 256, cap * 4);
+    const unsigned ew4 = grid_for((n + 3) / 4, 256, cap * 4);  // kernels taking 4 points per thread
     const int* val = nullptr;
+    DenseCtx dctx{};
 
     if (g.dense) {
+        FEC_CUDA(ensure_subcell_tables());
         // smallest dimension fastest in the linear cell id (L2 locality of the slow axis)
         int perm[3] = {0, 1, 2};
         for (int i = 0; i < 3; ++i)
@@ -276,40 +302,66 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         g.stride[perm[2]] = (uint32_t)g.dims[perm[0]] * (uint32_t)g.dims[perm[1]];
         g.sdiv[0] = g.stride[perm[2]];
         g.sdiv[1] = g.stride[perm[1]];
-        // a2: counts per cell; dense cells get records and octant-ordered slots
+        // a2: occupancy bitmap -> compact cell ids; counts per cell; dense cells get records
+        // and octant-ordered slots
         mark(1, st);
-        FEC_CUDA(cudaMemsetAsync(L.cstart, 0, (size_t)(cells_total + 1) * 4, st));
-        const int64_t words = (cells_total + 31) / 32;
-        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(words + 1) * 4, st));
-        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.dbits, L.meta);
-        const unsigned wb = grid_for(words + 1, 256, cap * 4);
-        k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, words, L.dwpos);
-        launches += 2 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, words + 1, L.dscan, st);
-        k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, words, L.dwpos, L.dlist, L.crec, L.ocnt, L.meta);
-        k_dcount_oct<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.crec, L.ocnt, L.slot);
+        const int64_t W = (cells_total + 31) / 32;
+        FEC_CUDA(cudaMemsetAsync(L.cw, 0, (size_t)(W + 1) * sizeof(uint2), st));
+        k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
+        const unsigned cwb = grid_for(W + 1, 256, cap * 4);
+        k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
+        launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
+        k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc, L.ccoord,
+                                                                       g, L.meta);
+        const int64_t dwords = n / 32 + 1;
+        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(dwords + 1) * 4, st));
+        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
+        const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
+        k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
+        launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
+        k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+        // dense cells: certain-connected components of the fine occupancy (component nodes)
+        dctx.spts = L.spts;
+        dctx.cstart = L.cstart;
+        dctx.dlist = L.dlist;
+        dctx.clin = L.clin;
+        dctx.cmask = L.cmask;
+        dctx.parent = L.parent;
+        dctx.items = L.items;
+        dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
+        dctx.nbase = (int)n;
+        dctx.meta = L.meta;
+        k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx, L.dcoord,
+                                                                  L.dflag, dctx);
         launches += 2;
-        // a3: counting sort = scan + scatter
+        // a3: counting sort = scan (over the occupied cells only) + scatter
         mark(2, st);
-        launches += exclusive_scan<uint32_t>(L.cstart, L.cstart, cells_total + 1, L.dscan, st);
-        k_drec_fin<<<grid_for(n / (SPARSE_MAX + 1) + 1, 256, cap), 256, 0, st>>>(L.dlist, L.meta, L.cstart, L.ocnt,
-                                                                                 L.drec);
-        k_dscatter<<<ew, 256, 0, st>>>(pts, n, g, L.cstart, L.slot, L.crec, L.drec, L.spts);
-        launches += 2;
-        // a4: sorted-order init (parents = clique-group leaders)
+        launches += exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
+        k_dscatter<<<ew4, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.spts);
+        ++launches;
+        // a4: sorted-order init (parents: self, or the point's component node)
         mark(3, st);
-        k_dinit<<<ew, 256, 0, st>>>(L.spts, n, g, L.cstart, L.crec, L.drec, L.parent, L.size, L.minidx, L.sidx);
+        k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
+                                     L.sidx);
         ++launches;
         mark(4, st);
-        // a6+a7: one sweep over all grid cells (sparse cells: lane; dense cells: warp)
+        // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
+        // queued uncertain pairs
         mark(5, st);
-        k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cstart, (uint32_t)cells_total, g,
+        k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
                                                                          L.parent, L.meta);
         mark(6, st);
-        for (int phase = 0; phase < 2; ++phase)
-            k_union_dense<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, L.cstart, L.drec, L.crec,
-                                                                                  phase, g, L.parent,
-                                                                                  L.meta);
-        launches += 3;
+        const unsigned lb = grid_for(dense_max(n), 256, cap * 4);
+        k_dense_link0<<<dim3(grid_for(dense_max(n), 256, cap), 27), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord,
+                                                                              L.dflag, L.dflist, dctx);
+        k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
+        k_dense_link1<<<lb, 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.dflag, L.dflist, dctx);
+        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx);
+        launches += 5;
+        if (g_instrument) {
+            k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);
+            ++launches;
+        }
         mark(7, st);
         val = L.sidx;
     } else {
@@ -355,7 +407,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     }
 
     // ---- a8 ----------------------------------------------------------------------------------
-    k_flatten<<<ew, 256, 0, st>>>(L.parent, n);
+    k_flatten<<<ew, 256, 0, st>>>(L.parent, n, L.size, L.minidx);
     ++launches;
     mark(8, st);
     C.g = g;
@@ -391,7 +443,8 @@ fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
         g_stats.components = (int64_t)g_pinned_meta->components;
         g_stats.pair_tests = (int64_t)(g_pinned_meta->pair_tests + g_pinned_meta->dense_tests);
         g_stats.dense_tests = g.dense ? (int64_t)g_pinned_meta->dense_tests : -1;
-        g_stats.group_pairs = (int64_t)g_pinned_meta->group_pairs;
+        g_stats.group_pairs = g.dense ? (int64_t)g_pinned_meta->nitems : (int64_t)g_pinned_meta->group_pairs;
+        if (g_pinned_meta->internal_error) { g_err = "internal invariant failed (component bound)"; return FEC_ERR_CUDA; }
     }
     g_stats_valid = true;
     return FEC_OK;
@@ -457,7 +510,7 @@ SlabLayout slab_carve(char* base, int64_t n_local, int32_t world, int64_t rec_ca
     SlabLayout S{};
     S.core = n_local > 0 ? carve(nullptr, n_local).total : 0;
     Carver cv{base, S.core, 0};
-    S.ckey = cv.take<int>(n_local > 0 ? n_local : 1);
+    S.ckey = cv.take<int>(n_local > 0 ? nodes_max(n_local) : 1);
     const int64_t hc = slab_hash_cap(world, rec_cap);
     S.hkey = cv.take<int>(hc);
     S.hpar = cv.take<int>(hc);
@@ -575,12 +628,13 @@ fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n_local, 256, dev_info().sms * 8 * 4);
-    FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)n_local * 4, st));
+    FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)nodes_max(n_local) * 4, st));
     k_slab_stats<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
                                      S.ckey, L.meta);
     mark(9, st);
-    k_slab_pack<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
-                                    S.ckey, records, (int)rec_cap);
+    k_slab_pack<<<grid_for(nodes_max(n_local), 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
+        L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx, S.ckey, records, (int)rec_cap,
+        L.meta);
     C.launches += 2;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
@@ -646,6 +700,8 @@ void fec_set_instrumentation(int enable) { g_instrument = enable ? 1 : 0; }
 void fec_set_timing(int enable) { g_timing = enable ? 1 : 0; }
 
 void fec_set_grid_mode(int mode) { g_grid_mode = mode; }
+
+void fec_set_item_cap(int64_t cap) { g_item_cap = cap > 0 ? cap : 0; }
 
 int32_t fec_get_stage_times(float* ms_out, int32_t max_stages) {
     if (!g_ev.recorded) { g_err = "no timed call on this thread (fec_set_timing(1) first)"; return -1; }

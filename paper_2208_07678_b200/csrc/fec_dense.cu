@@ -1,22 +1,32 @@
-// Dense-grid path (the default whenever the bbox holds <= 4n + 2^22 cells): the points are
-// counting-sorted by cell into a dense row-major cell table, cells holding more than
-// SPARSE_MAX points are re-ordered by octant (sub-cell cliques), then
-//   * sparse cells: one thread per point tests every candidate directly,
-//   * dense cells:  one warp per cell evaluates sub-cell group pairs (fec_pairs.cuh).
-// DESIGN.md §4 describes the responsibilities that make every adjacent cell pair examined
-// exactly once.
+// Dense-grid path (the default whenever the bbox holds <= 32n + 2^26 grid cells).
+//
+// Binning: an occupancy bitmap over the linear grid cells gives every occupied cell a
+// compact id; points are counting-sorted by compact cell id (a3).  Cells holding more than
+// SPARSE_MAX points are "dense": each keeps a 64-bit occupancy mask of its 4x4x4 fine
+// sub-cells (fec_subcell.cuh), split into at most 8 certain-connected components that
+// become union-find nodes of their own (ids n + 8*record + k).  Then
+//   * sparse cells: every point pair with a sparse forward neighbour is tested directly;
+//   * dense cells: components of adjacent cells are united without any distance test when
+//     a certain sub-cell pair joins them, and the rare pairs that are only "uncertain" go
+//     to a queue of point tests (early exit at the first pred-true pair).
+// DESIGN.md §4 describes why every edge of the graph of Eq. 1 is covered exactly.
 #include "fec_internal.cuh"
 #include "fec_kernels.cuh"
 #include "fec_pairs.cuh"
+#include "fec_subcell.cuh"
 
 namespace fec {
 
-__device__ __forceinline__ void dense_cell_of(float x, float y, float z, const Grid& g, uint32_t& lin, int& oct) {
-    const uint32_t sx = sub_coord(x, g.lo[0], g.inv_h);
-    const uint32_t sy = sub_coord(y, g.lo[1], g.inv_h);
-    const uint32_t sz = sub_coord(z, g.lo[2], g.inv_h);
-    oct = (int)((sx & 1u) | ((sy & 1u) << 1) | ((sz & 1u) << 2));
-    lin = (sx >> 1) * g.stride[0] + (sy >> 1) * g.stride[1] + (sz >> 1) * g.stride[2];
+__device__ SubcellTables d_sc;  // filled once per device (fec_capi.cu)
+
+// Fine sub-cell coordinates f = floor((x - lo) * inv_q) (inv_q = 4/c exactly twice inv_h,
+// so cell = f >> 2 equals the coarse computation floor((x - lo) * inv_h) >> 1).
+__device__ __forceinline__ void dense_cell_of(float x, float y, float z, const Grid& g, uint32_t& lin, int& q) {
+    const uint32_t fx = sub_coord(x, g.lo[0], g.inv_q);
+    const uint32_t fy = sub_coord(y, g.lo[1], g.inv_q);
+    const uint32_t fz = sub_coord(z, g.lo[2], g.inv_q);
+    q = (int)((fx & 3u) | ((fy & 3u) << 2) | ((fz & 3u) << 4));
+    lin = (fx >> 2) * g.stride[0] + (fy >> 2) * g.stride[1] + (fz >> 2) * g.stride[2];
 }
 
 __device__ __forceinline__ void dense_decode(uint32_t lin, const Grid& g, int c[3]) {
@@ -37,39 +47,224 @@ __device__ __forceinline__ bool dense_neighbor(const Grid& g, const int c[3], in
     return true;
 }
 
-// ---- a2: per-cell counts; slot[i] = rank of point i inside its cell -----------------------
-__global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
-                                               uint32_t* __restrict__ count, uint32_t* __restrict__ slot,
-                                               uint32_t* __restrict__ dbits, Meta* __restrict__ meta) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool ok = i < n;
-        uint32_t lin = 0xffffffffu;
-        int oct;
-        if (ok) dense_cell_of(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2), g, lin, oct);
-        // warp-aggregated atomics: one atomicAdd per distinct cell in the warp
-        const unsigned peers = __match_any_sync(0xffffffffu, lin);
-        const int leader = __ffs(peers) - 1;
-        const uint32_t cnt = __popc(peers);
-        uint32_t old = 0;
-        if (ok && lane == leader) {
-            old = atomicAdd(count + lin, cnt);
-            if (old <= (uint32_t)SPARSE_MAX && old + cnt > (uint32_t)SPARSE_MAX)
-                atomicOr(dbits + (lin >> 5), 1u << (lin & 31u));   // the cell just became dense
-            if (old == 0 && meta->instrument) atomicAdd(&meta->cells, 1);
+// Four consecutive input points per thread: three 16-byte loads when `points` is 16-byte
+// aligned (more bytes in flight per thread than one scalar load per coordinate).
+struct Pts4 {
+    float x[4], y[4], z[4];
+};
+__device__ __forceinline__ void load_pts4(const float* __restrict__ p, int64_t n, int64_t base, bool vec, Pts4& P) {
+    if (vec && base + 4 <= n) {
+        const float4* q = reinterpret_cast<const float4*>(p + 3 * base);
+        const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+        P.x[0] = a.x; P.y[0] = a.y; P.z[0] = a.z;
+        P.x[1] = a.w; P.y[1] = b.x; P.z[1] = b.y;
+        P.x[2] = b.z; P.y[2] = b.w; P.z[2] = c.x;
+        P.x[3] = c.y; P.y[3] = c.z; P.z[3] = c.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = base + j;
+            P.x[j] = i < n ? __ldg(p + 3 * i) : 0.f;
+            P.y[j] = i < n ? __ldg(p + 3 * i + 1) : 0.f;
+            P.z[j] = i < n ? __ldg(p + 3 * i + 2) : 0.f;
         }
-        old = __shfl_sync(0xffffffffu, old, leader);
-        if (ok) slot[i] = old + __popc(peers & lt);
     }
 }
 
-// ---- a2b: dense cells get records (in ascending cell order); their points get
-// octant-ordered slots.  A cell with more than SPARSE_MAX points is laid out octant by
-// octant (octant k = the sub-cell (sx&1, sy&1, sz&1)), so each octant is a contiguous
-// clique group.
+// ---- compact cell ids ---------------------------------------------------------------------
+// Only occupied cells get storage: an occupancy bitmap over the linear cell ids, each 32-bit
+// word paired with the number of occupied cells before it (uint2 {bits, base}), gives the
+// compact id of an occupied cell with one 8-byte load and a popcount.  The bitmap is 1/32 B
+// per grid cell (C4: 89M grid cells, 358k occupied -> 11 MB, L2-resident), so per-cell tables
+// (counts / starts, dense records) are sized by the occupied cells, not the bounding box.
+__device__ __forceinline__ uint32_t cid_of(const uint2* __restrict__ cw, uint32_t lin) {
+    const uint2 v = __ldg(cw + (lin >> 5));
+    return v.y + (uint32_t)__popc(v.x & ((1u << (lin & 31u)) - 1u));
+}
+__device__ __forceinline__ int cid_lookup(const uint2* __restrict__ cw, uint32_t lin) {
+    const uint2 v = __ldg(cw + (lin >> 5));
+    const uint32_t b = 1u << (lin & 31u);
+    return (v.x & b) ? (int)(v.y + (uint32_t)__popc(v.x & (b - 1u))) : -1;
+}
+
+// ---- a2: occupancy bitmap ------------------------------------------------------------------
+// Binning kernels aggregate per block through a small shared-memory hash table (keys = bitmap
+// word or compact cell id): one global atomic per distinct key per tile of kBinTile points.
+constexpr int kBinThreads = 256;
+constexpr int kBinIpt = 4;
+constexpr int kBinTile = kBinThreads * kBinIpt;
+constexpr int kBinSlots = 2 * kBinTile;
+
+__device__ __forceinline__ int bin_slot(int* keys, uint32_t key) {
+    uint32_t h = (key * 2654435761u) & (kBinSlots - 1);
+    while (true) {
+        const int cur = keys[h];
+        if (cur == (int)key) return (int)h;
+        if (cur == -1) {
+            const int old = atomicCAS(keys + h, -1, (int)key);
+            if (old == -1 || old == (int)key) return (int)h;
+        }
+        h = (h + 1) & (kBinSlots - 1);
+    }
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__ p, int64_t n, Grid g,
+                                                       uint2* __restrict__ cw) {
+    __shared__ int keys[kBinSlots];
+    __shared__ uint32_t bits[kBinSlots];
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) { keys[k] = -1; bits[k] = 0u; }
+    __syncthreads();
+    for (int64_t t0 = (int64_t)blockIdx.x * kBinTile; t0 < n; t0 += (int64_t)gridDim.x * kBinTile) {
+        const int64_t b4 = t0 + kBinIpt * threadIdx.x;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
+#pragma unroll
+        for (int j = 0; j < kBinIpt; ++j) {
+            if (b4 + j < n) {
+                uint32_t lin;
+                int q;
+                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                atomicOr(bits + bin_slot(keys, lin >> 5), 1u << (lin & 31u));
+            }
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
+            if (keys[k] != -1) {
+                atomicOr(reinterpret_cast<unsigned int*>(cw + keys[k]), bits[k]);
+                keys[k] = -1;
+                bits[k] = 0u;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_cpopc(const uint2* __restrict__ cw, int64_t words, uint32_t* __restrict__ cnt) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
+        cnt[w] = w < words ? (uint32_t)__popc(__ldg(cw + w).x) : 0u;
+}
+
+// Word bases, compact-id -> linear cell list (ascending), zeroed per-cell counts, U.
+// Four words per thread, loaded with vector loads before any dependent work.
+__global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t words, const uint32_t* __restrict__ wpos,
+                                              uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
+                                              u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
+                                              Meta* __restrict__ meta) {
+    const int64_t groups = (words + 4) / 4;  // words + 1 entries of wpos (the last holds U)
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w0 = 4 * gi;
+        uint32_t r0[4], bw[4];
+        if (w0 + 4 <= words) {
+            const uint4 pv = __ldg(reinterpret_cast<const uint4*>(wpos + w0));
+            const uint4 c01 = *reinterpret_cast<const uint4*>(cw + w0);
+            const uint4 c23 = *reinterpret_cast<const uint4*>(cw + w0 + 2);
+            r0[0] = pv.x; r0[1] = pv.y; r0[2] = pv.z; r0[3] = pv.w;
+            bw[0] = c01.x; bw[1] = c01.z; bw[2] = c23.x; bw[3] = c23.z;
+            *reinterpret_cast<uint4*>(cw + w0) = make_uint4(bw[0], r0[0], bw[1], r0[1]);
+            *reinterpret_cast<uint4*>(cw + w0 + 2) = make_uint4(bw[2], r0[2], bw[3], r0[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t w = w0 + j;
+                r0[j] = w <= words ? __ldg(wpos + w) : 0u;
+                bw[j] = w < words ? cw[w].x : 0u;
+                if (w < words) cw[w].y = r0[j];
+                if (w == words) {
+                    meta->cells = (int)r0[j];
+                    meta->cells1 = (int)r0[j] + 1;
+                    count[r0[j]] = 0u;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t bits = bw[j];
+            uint32_t r = r0[j];
+            while (bits) {
+                const int b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const uint32_t lin = (uint32_t)((w0 + j) * 32 + b);
+                int cc[3];
+                dense_decode(lin, g, cc);
+                clin[r] = lin;
+                ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
+                count[r] = 0u;
+                cocc[r] = 0ull;
+                ++r;
+            }
+        }
+    }
+}
+
+// ---- a2: per-cell counts, slot[i] = rank of point i inside its cell, fine occupancy ------
+__global__ void __launch_bounds__(kBinThreads) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
+                                                        const uint2* __restrict__ cw, uint32_t* __restrict__ count,
+                                                        uint32_t* __restrict__ slot, uint32_t* __restrict__ dbits,
+                                                        u64* __restrict__ cocc) {
+    __shared__ int keys[kBinSlots];
+    __shared__ uint32_t cnt[kBinSlots], olo[kBinSlots], ohi[kBinSlots], base[kBinSlots];
+    for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
+        keys[k] = -1;
+        cnt[k] = 0u;
+        olo[k] = 0u;
+        ohi[k] = 0u;
+    }
+    __syncthreads();
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    for (int64_t t0 = (int64_t)blockIdx.x * kBinTile; t0 < n; t0 += (int64_t)gridDim.x * kBinTile) {
+        int hs[kBinIpt];
+        uint32_t rk[kBinIpt];
+        const int64_t b4 = t0 + kBinIpt * threadIdx.x;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
+#pragma unroll
+        for (int j = 0; j < kBinIpt; ++j) {
+            hs[j] = -1;
+            if (b4 + j < n) {
+                uint32_t lin;
+                int q;
+                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                const int h = bin_slot(keys, cid_of(cw, lin));
+                hs[j] = h;
+                rk[j] = atomicAdd(cnt + h, 1u);
+                if (q < 32) atomicOr(olo + h, 1u << q);
+                else atomicOr(ohi + h, 1u << (q - 32));
+            }
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
+            const int cid = keys[k];
+            if (cid != -1) {
+                const uint32_t c = cnt[k];
+                const uint32_t old = atomicAdd(count + cid, c);
+                base[k] = old;
+                if (old <= (uint32_t)SPARSE_MAX && old + c > (uint32_t)SPARSE_MAX)
+                    atomicOr(dbits + (cid >> 5), 1u << (cid & 31u));   // the cell just became dense
+                atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
+            }
+        }
+        __syncthreads();
+        if (b4 + kBinIpt <= n) {
+            *reinterpret_cast<uint4*>(slot + b4) =
+                make_uint4(base[hs[0]] + rk[0], base[hs[1]] + rk[1], base[hs[2]] + rk[2], base[hs[3]] + rk[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kBinIpt; ++j)
+                if (hs[j] >= 0) slot[b4 + j] = base[hs[j]] + rk[j];
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
+            keys[k] = -1;
+            cnt[k] = 0u;
+            olo[k] = 0u;
+            ohi[k] = 0u;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- dense records: compact ids of the dense cells in ascending order -----------------------
 __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
                                                    uint32_t* __restrict__ wcount) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
@@ -78,8 +273,7 @@ __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__
 
 __global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__ dbits, int64_t words,
                                                    const uint32_t* __restrict__ wpos, int* __restrict__ dlist,
-                                                   int* __restrict__ crec, uint32_t* __restrict__ ocnt,
-                                                   Meta* __restrict__ meta) {
+                                                   int* __restrict__ crec, Meta* __restrict__ meta) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
         if (w == words) { meta->ndense = (int)wpos[words]; continue; }
         uint32_t bits = __ldg(dbits + w);
@@ -90,128 +284,210 @@ __global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__
             const int cell = (int)(w * 32 + b);
             dlist[r] = cell;
             crec[cell] = r;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) ocnt[8 * r + k] = 0u;
             ++r;
         }
     }
 }
 
-__global__ void __launch_bounds__(256) k_dcount_oct(const float* __restrict__ p, int64_t n, Grid g,
-                                                   const uint32_t* __restrict__ count, const int* __restrict__ crec,
-                                                   uint32_t* __restrict__ ocnt, uint32_t* __restrict__ slot) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        uint32_t key = 0xffffffffu;
-        if (i < n) {
-            uint32_t lin;
-            int oct;
-            dense_cell_of(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2), g, lin, oct);
-            if (__ldg(count + lin) > (uint32_t)SPARSE_MAX) key = 8u * (uint32_t)__ldg(crec + lin) + (uint32_t)oct;
+// ---- uncertain component pairs: queued, or tested in place when the queue is full ----------
+// item = (P record, P component, Q record or point, Q component or -1 for a point)
+
+__device__ __forceinline__ int cell_slot_of(const Grid& g, uint32_t lin_p, uint32_t lin_q) {
+    int a[3], b[3];
+    dense_decode(lin_p, g, a);
+    dense_decode(lin_q, g, b);
+    return sc_slot(b[0] - a[0], b[1] - a[1], b[2] - a[2]);
+}
+
+__device__ __forceinline__ u64 reach_of(const u64 m, int slot) {
+    u64 r = 0;
+    u64 b = m & d_sc.F[slot];
+    while (b) {
+        const int a = __ffsll((long long)b) - 1;
+        b &= b - 1;
+        r |= d_sc.U[slot][a];
+    }
+    return r;
+}
+
+// One thread tests an uncertain item by itself (queue overflow path; slow but rare).
+__device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, int4 it) {
+    const float t2 = g.t2;
+    const int cp = __ldg(C.dlist + it.x);
+    const uint32_t lp = __ldg(C.clin + cp);
+    const u64 ma = C.cmask[8 * it.x + it.y];
+    const int na = C.nbase + 8 * it.x + it.y;
+    int nb, b0, b1;
+    u64 mb;
+    int slot;
+    if (it.w >= 0) {
+        const int cq = __ldg(C.dlist + it.z);
+        mb = C.cmask[8 * it.z + it.w];
+        nb = C.nbase + 8 * it.z + it.w;
+        b0 = (int)__ldg(C.cstart + cq);
+        b1 = (int)__ldg(C.cstart + cq + 1);
+        slot = cell_slot_of(g, lp, __ldg(C.clin + cq));
+    } else {
+        mb = ~0ull;
+        nb = it.z;
+        b0 = it.z;
+        b1 = it.z + 1;
+        uint32_t lq;
+        int qq;
+        const float4 v = C.spts[it.z];
+        dense_cell_of(v.x, v.y, v.z, g, lq, qq);
+        slot = cell_slot_of(g, lp, lq);
+    }
+    const int a0 = (int)__ldg(C.cstart + cp), a1 = (int)__ldg(C.cstart + cp + 1);
+    for (int i = a0; i < a1; ++i) {
+        const float4 pa = C.spts[i];
+        uint32_t l;
+        int qa;
+        dense_cell_of(pa.x, pa.y, pa.z, g, l, qa);
+        if (!((ma >> qa) & 1ull)) continue;
+        const u64 reach = d_sc.U[slot][qa];
+        for (int j = b0; j < b1; ++j) {
+            const float4 pb = C.spts[j];
+            int qb;
+            dense_cell_of(pb.x, pb.y, pb.z, g, l, qb);
+            if (it.w >= 0 && !(((mb & reach) >> qb) & 1ull)) continue;
+            if (pred(pa, pb, t2)) {
+                uf_unite(C.parent, na, nb);
+                return;
+            }
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const int leader = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (key != 0xffffffffu && lane == leader) old = atomicAdd(ocnt + key, (uint32_t)__popc(peers));
-        old = __shfl_sync(0xffffffffu, old, leader);
-        if (key != 0xffffffffu) slot[i] = old + __popc(peers & lt);
     }
 }
 
-// After the scan: octant offsets of every dense record.
-__global__ void __launch_bounds__(256) k_drec_fin(const int* __restrict__ dlist, Meta* __restrict__ meta,
-                                                 const uint32_t* __restrict__ cstart,
-                                                 const uint32_t* __restrict__ ocnt, DenseRec* __restrict__ drec) {
-    const int nd = meta->ndense;
-    unsigned long long pts = 0;
+// Queue an uncertain pair unless the two nodes are already connected.  The lanes that push
+// together share one atomicAdd.
+__device__ __forceinline__ void push_item(const DenseCtx& C, const Grid& g, int4 it, int na, int nb) {
+    if (uf_find(C.parent, na) == uf_find(C.parent, nb)) return;
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&C.meta->nitems, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    const int k = base + __popc(m & ((1u << lane) - 1u));
+    if (k < C.item_cap) C.items[k] = it;
+    else test_item_serial(C, g, it);
+}
+
+// ---- dense records: components of the fine occupancy, node init, in-cell uncertain pairs --
+__global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ cocc, const u64* __restrict__ ccoord,
+                                               int* __restrict__ ncomp,
+                                               int* __restrict__ size, int* __restrict__ minidx,
+                                               u64* __restrict__ dcoord, uint32_t* __restrict__ flags, DenseCtx C) {
+    const int nd = C.meta->ndense;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
-        const int cell = __ldg(dlist + r);
-        const int start = (int)__ldg(cstart + cell), m = (int)__ldg(cstart + cell + 1) - start;
-        DenseRec R;
-        R.cell = cell;
-        int run = start;
+        const int cid = __ldg(C.dlist + r);
+        const u64 occ = __ldg(cocc + cid);
+        dcoord[r] = __ldg(ccoord + cid);
+        flags[r] = 0u;
+        u64 comp[kMaxComp];
+        u64 rest;
+        const int k = sc_components(occ, comp, rest);
+        if (rest) atomicOr(&C.meta->internal_error, 1);  // impossible by the 8-component bound
+        ncomp[r] = k;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            R.off[k] = run;
-            run += (int)__ldg(ocnt + 8 * r + k);
+        for (int j = 0; j < kMaxComp; ++j) {
+            const int node = C.nbase + 8 * r + j;
+            C.parent[node] = node;
+            size[node] = 0;
+            minidx[node] = 0x7fffffff;
+            C.cmask[8 * r + j] = j < k ? comp[j] : 0ull;
         }
-        R.off[8] = run;
-        drec[r] = R;
-        pts += (unsigned long long)m;
     }
-    for (int o = 16; o > 0; o >>= 1) pts += __shfl_xor_sync(0xffffffffu, pts, o);
-    if ((threadIdx.x & 31) == 0 && pts) atomicAdd(&meta->dense_points, pts);
 }
 
 // ---- a3: scatter into cell order (after the exclusive scan of count -> cstart) ------------
 // Only the float4 (x, y, z, idx) is scattered: for shuffled inputs every scattered array
 // costs a DRAM read-modify-write per point, so everything else is derived in sorted order.
 __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n, Grid g,
-                                                 const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ slot,
-                                                 const int* __restrict__ crec, const DenseRec* __restrict__ drec,
-                                                 float4* __restrict__ spts) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float x = __ldg(p + 3 * i), y = __ldg(p + 3 * i + 1), z = __ldg(p + 3 * i + 2);
-        uint32_t lin;
-        int oct;
-        dense_cell_of(x, y, z, g, lin, oct);
-        const uint32_t c0 = __ldg(cstart + lin), c1 = __ldg(cstart + lin + 1);
-        uint32_t base = c0;
-        if (c1 - c0 > (uint32_t)SPARSE_MAX) base = (uint32_t)__ldg(&drec[__ldg(crec + lin)].off[oct]);
-        spts[base + __ldg(slot + i)] = make_float4(x, y, z, __int_as_float((int)i));
+                                                 const uint2* __restrict__ cw, const uint32_t* __restrict__ cstart,
+                                                 const uint32_t* __restrict__ slot, float4* __restrict__ spts) {
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b4 = 4 * gi;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
+        uint32_t sl[4];
+        if (b4 + 4 <= n) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(slot + b4));
+            sl[0] = v.x; sl[1] = v.y; sl[2] = v.z; sl[3] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sl[j] = b4 + j < n ? __ldg(slot + b4 + j) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (b4 + j < n) {
+                uint32_t lin;
+                int q;
+                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                spts[__ldg(cstart + cid_of(cw, lin)) + sl[j]] =
+                    make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
+            }
+        }
     }
 }
 
-// Sorted-order initialisation (coalesced): parent = self for points of sparse cells, the
-// last point of the octant group for points of dense cells (groups are cliques, DESIGN.md
-// §4.5); accumulators; input index.
+// Sorted-order initialisation (coalesced): points of sparse cells are their own parents,
+// points of dense cells hang under their component's node; accumulators; input index.
 __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, Grid g,
-                                              const uint32_t* __restrict__ cstart, const int* __restrict__ crec,
-                                              const DenseRec* __restrict__ drec, int* __restrict__ parent,
-                                              int* __restrict__ size, int* __restrict__ minidx,
+                                              const uint2* __restrict__ cw, const uint32_t* __restrict__ cstart,
+                                              const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                              const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
                                               int* __restrict__ sidx) {
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        const float4 v = __ldg(spts + s);
-        uint32_t lin;
-        int oct;
-        dense_cell_of(v.x, v.y, v.z, g, lin, oct);
-        const uint32_t c0 = __ldg(cstart + lin), c1 = __ldg(cstart + lin + 1);
-        int par = (int)s;
-        if (c1 - c0 > (uint32_t)SPARSE_MAX) par = __ldg(&drec[__ldg(crec + lin)].off[oct + 1]) - 1;
-        parent[s] = par;
-        size[s] = 0;
-        minidx[s] = 0x7fffffff;
-        sidx[s] = __float_as_int(v.w);
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b4 = 4 * gi;
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = b4 + j < n ? __ldg(spts + b4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        int par[4], si[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t lin;
+            int q;
+            dense_cell_of(v[j].x, v[j].y, v[j].z, g, lin, q);
+            const uint32_t cid = cid_of(cw, lin);
+            par[j] = (int)(b4 + j);
+            si[j] = __float_as_int(v[j].w);
+            if (b4 + j < n && __ldg(cstart + cid + 1) - __ldg(cstart + cid) > (uint32_t)SPARSE_MAX) {
+                const int r = __ldg(crec + cid);
+                const int k = __ldg(ncomp + r);
+                int c = 0;
+                if (k > 1)
+                    while (c < k - 1 && !((__ldg(cmask + 8 * r + c) >> q) & 1ull)) ++c;
+                par[j] = nbase + 8 * r + c;
+            }
+        }
+        // size / minidx of root points are set by k_flatten
+        if (b4 + 4 <= n) {
+            *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
+            *reinterpret_cast<int4*>(sidx + b4) = make_int4(si[0], si[1], si[2], si[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (b4 + j < n) {
+                    parent[b4 + j] = par[j];
+                    sidx[b4 + j] = si[j];
+                }
+        }
     }
 }
 
-// ---- a6+a7: neighbour scan + union --------------------------------------------------------
-// Responsibilities (each unordered pair of adjacent cells is examined exactly once,
-// DESIGN.md §4.6):
-//   sparse cell P (1..SPARSE_MAX points): one lane tests every pair (s, t) with t in P
-//       (t > s) or in a SPARSE forward neighbour Q                       -> k_union_sparse
-//   dense cell P: one warp evaluates sub-cell group pairs of P with itself, with every
-//       forward neighbour (dense: octant groups; sparse: single points) and with every
-//       SPARSE backward neighbour                                         -> k_union_dense
-
-constexpr int QG_CAP = 13 * 8 + 13 * SPARSE_MAX;  // Q groups of one dense cell (all neighbours)
-constexpr int PQ_CAP = 256;                        // pair queue capacity
-
-struct DenseSmem {
-    int ps[9];                 // P octant groups: [ps[a], ps[a+1])
-    uint8_t po[8];
-    int proot[8];
-    int qs[QG_CAP], qe[QG_CAP];  // Q groups: [qs[b], qe[b])
-    uint8_t qo[QG_CAP];        // octant, or 0xFF for a single point (no octant filter)
-    uint8_t qk[QG_CAP];        // neighbour slot (0..12 forward, 13..25 backward, 26 own)
-    int qroot[QG_CAP];
-    uint16_t small[PQ_CAP], big[PQ_CAP];  // (a << 8) | b
-    int slot_q[26], slot_rec[26], slot_cnt[26], slot_off[27];
-};
-
+// ---- a6+a7: dense cells — certain unions across cells, uncertain pairs queued -------------
+// Thread per dense record P, looping over the 26 neighbour slots in the same order in every
+// thread (warp-uniform slot -> broadcast table reads): forward dense neighbours give
+// component pairs, sparse neighbours (both directions) give their points against P's
+// components; slot 26 stands for the pairs of P's own components.  Each unordered pair of
+// adjacent cells is therefore handled once.  Pass 0 makes the certain
+// unions and records, per record, the slots that still hold a non-certain pair within
+// reach; pass 1 (after all certain unions) queues those pairs whose nodes are still apart.
 __device__ __forceinline__ void slot_offset(int k, int& ox, int& oy, int& oz) {
     const int kk = k < 13 ? k : k - 13;
     const int sg = k < 13 ? 1 : -1;
@@ -220,269 +496,258 @@ __device__ __forceinline__ void slot_offset(int k, int& ox, int& oy, int& oz) {
     oz = sg * c_fwd[kk][2];
 }
 
-// Small pairs one lane each, big pairs the whole warp; both stop at the first pred-true pair.
-__device__ __forceinline__ void run_pairs(DenseSmem& S, int nsmall, int nbig, int nq_total,
-                                          const float4* __restrict__ spts, int* parent, float t2, int lane,
-                                          unsigned long long& n_tests) {
-    for (int e0 = 0; e0 < nsmall; e0 += 32) {
-        const int e = e0 + lane;
-        if (e < nsmall) {
-            const int a = S.small[e] >> 8, b = S.small[e] & 255;
-            const int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qe[b];
-            bool hit = false;
-            for (int i = sa; i < ea && !hit; ++i) {
-                const float4 pi = __ldg(spts + i);
-                for (int j = sb; j < eb; ++j) {
-                    ++n_tests;
-                    if (pred(pi, __ldg(spts + j), t2)) { hit = true; break; }
+// One (dense record r, slot k) item.  Returns whether pass 0 left work for pass 1.
+template <int pass>
+__device__ __forceinline__ bool dense_link_item(int r, int k, const Grid& g, const uint2* __restrict__ cw,
+                                                const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                                const u64* __restrict__ dcoord, const DenseCtx& C) {
+    const int kp = __ldg(ncomp + r);
+    const u64* mp = C.cmask + 8 * r;
+    if (k == 26) {
+        // P's own components within reach of each other (never certain-adjacent)
+        if (kp < 2) return false;
+        if constexpr (pass == 1) {
+            for (int i = 0; i + 1 < kp; ++i) {
+                const u64 ri = reach_of(mp[i], 13);
+                for (int j = i + 1; j < kp; ++j)
+                    if (ri & mp[j]) push_item(C, g, make_int4(r, i, r, j), C.nbase + 8 * r + i, C.nbase + 8 * r + j);
+            }
+        }
+        return true;
+    }
+    const u64 pc = __ldg(dcoord + r);
+    const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
+    int ox, oy, oz;
+    slot_offset(k, ox, oy, oz);
+    uint32_t lq;
+    if (!dense_neighbor(g, c, ox, oy, oz, lq)) return false;
+    const int cq = cid_lookup(cw, lq);
+    if (cq < 0) return false;
+    const int q0 = (int)__ldg(C.cstart + cq), q1 = (int)__ldg(C.cstart + cq + 1);
+    const int slot = sc_slot(ox, oy, oz);
+    bool flag = false;
+    if (q1 - q0 > SPARSE_MAX) {
+        if (k >= 13) return false;  // backward dense pairs belong to the other cell
+        const int rq = __ldg(crec + cq);
+        const int kq = __ldg(ncomp + rq);
+        for (int x = 0; x < kp; ++x) {
+            const u64 mx = mp[x];
+            const u64 dc = sc_certain_across(d_sc, mx, slot);
+            const int na = C.nbase + 8 * r + x;
+            for (int y = 0; y < kq; ++y) {
+                const u64 my = C.cmask[8 * rq + y];
+                const int nb = C.nbase + 8 * rq + y;
+                if (dc & my) {
+                    if constexpr (pass == 0) uf_unite(C.parent, na, nb);
+                } else if constexpr (pass == 0) {
+                    flag = true;  // exact reach is checked in pass 1, only if still apart
+                } else if (uf_find(C.parent, na) != uf_find(C.parent, nb) && (reach_of(mx, slot) & my)) {
+                    push_item(C, g, make_int4(r, x, rq, y), na, nb);
                 }
             }
-            if (hit) uf_unite(parent, sa, sb);
         }
-        __syncwarp();
+    } else {
+        const int opp = 26 - slot;
+        for (int t = q0; t < q1; ++t) {
+            const float4 v = C.spts[t];
+            uint32_t l;
+            int qb;
+            dense_cell_of(v.x, v.y, v.z, g, l, qb);
+            const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
+            for (int x = 0; x < kp; ++x) {
+                const int na = C.nbase + 8 * r + x;
+                const u64 mx = mp[x];
+                if (tc & mx) {
+                    if constexpr (pass == 0) uf_unite(C.parent, t, na);
+                } else if (tu & mx) {
+                    if constexpr (pass == 0) flag = true;
+                    else push_item(C, g, make_int4(r, x, t, -1), na, t);
+                }
+            }
+        }
     }
-    for (int e = 0; e < nbig; ++e) {
-        const int a = S.big[e] >> 8, b = S.big[e] & 255;
-        if (S.proot[a] == S.qroot[b]) continue;  // joined by an earlier big pair
-        int sa = S.ps[a], ea = S.ps[a + 1], sb = S.qs[b], eb = S.qe[b];
-        if (eb - sb > ea - sa) { int t = sa; sa = sb; sb = t; t = ea; ea = eb; eb = t; }
-        bool found = false;
-        for (int i0 = sa; i0 < ea && !found; i0 += 32) {
-            const int i = i0 + lane;
-            const bool vi = i < ea;
-            const float4 pi = vi ? __ldg(spts + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int j = sb; j < eb; ++j) {
-                const float4 pj = __ldg(spts + j);
-                n_tests += vi ? 1ull : 0ull;
-                if (__any_sync(0xffffffffu, vi && pred(pi, pj, t2))) { found = true; break; }
-            }
-        }
-        if (found) {
-            const int ra = S.proot[a], rb = S.qroot[b];
-            int rn = 0;
-            if (lane == 0) {
-                uf_unite(parent, S.ps[a], S.qs[b]);
-                rn = uf_find(parent, S.ps[a]);
-            }
-            rn = __shfl_sync(0xffffffffu, rn, 0);
-            __syncwarp();
-            // every cached root equal to either old root now maps to the merged root
-            if (lane < 8 && (S.proot[lane] == ra || S.proot[lane] == rb)) S.proot[lane] = rn;
-            for (int q = lane; q < nq_total; q += 32)
-                if (S.qroot[q] == ra || S.qroot[q] == rb) S.qroot[q] = rn;
-            __syncwarp();
+    return flag;
+}
+
+// Pass 0: every (record, slot) item; blockIdx.y = slot, so a warp shares its slot (uniform
+// table reads); records left with work are listed once for pass 1.
+__global__ void __launch_bounds__(256) k_dense_link0(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
+                                                    const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
+                                                    uint32_t* __restrict__ flags, int* __restrict__ flist, DenseCtx C) {
+    const int nd = C.meta->ndense;
+    const int k = blockIdx.y;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
+        if (dense_link_item<0>(r, k, g, cw, crec, ncomp, dcoord, C)) {
+            if (atomicOr(flags + r, 1u << k) == 0u) flist[atomicAdd(&C.meta->nflag, 1)] = r;
         }
     }
 }
 
-// Enumerate (a, b) for a < np and b in [b0, b1), keep those whose cached roots differ and
-// whose sub-cell offset can hold a pred-true pair, and run them through run_pairs in
-// batches of at most PQ_CAP.  `own`: the Q groups are P's own groups (only b > a).
-__device__ __forceinline__ void pair_sweep(DenseSmem& S, int np, int b0, int b1, bool own,
-                                           const float4* __restrict__ spts, int* parent, float t2, int lane,
-                                           unsigned long long& n_tests, unsigned long long& n_pairs) {
-    const int nb = b1 - b0;
-    const int total = np * nb;
-    int nsmall = 0, nbig = 0;
-    for (int base = 0; base < total; base += 32) {
-        const int pid = base + lane;
-        bool ok = pid < total;
-        int a = 0, b = 0;
-        bool big = false;
-        if (ok) {
-            b = b0 + pid / np;
-            a = pid - (b - b0) * np;
-            if (own) {
-                ok = b > a;
-            } else if (S.qo[b] != 0xFF) {
-                int ox, oy, oz;
-                slot_offset(S.qk[b], ox, oy, oz);
-                const int oa = S.po[a], ob = S.qo[b];
-                const int dx = 2 * ox + (ob & 1) - (oa & 1);
-                const int dy = 2 * oy + ((ob >> 1) & 1) - ((oa >> 1) & 1);
-                const int dz = 2 * oz + ((ob >> 2) & 1) - ((oa >> 2) & 1);
-                ok = dx <= 2 && dx >= -2 && dy <= 2 && dy >= -2 && dz <= 2 && dz >= -2;
-            }
-            ok = ok && S.proot[a] != S.qroot[b];
-            big = (S.ps[a + 1] - S.ps[a]) * (S.qe[b] - S.qs[b]) > SMALL_PAIR;
-        }
-        const unsigned ms = __ballot_sync(0xffffffffu, ok && !big);
-        const unsigned mb = __ballot_sync(0xffffffffu, ok && big);
-        const unsigned lt = (1u << lane) - 1u;
-        if (ok && !big) S.small[nsmall + __popc(ms & lt)] = (uint16_t)((a << 8) | b);
-        if (ok && big) S.big[nbig + __popc(mb & lt)] = (uint16_t)((a << 8) | b);
-        nsmall += __popc(ms);
-        nbig += __popc(mb);
-        __syncwarp();
-        if (nsmall > PQ_CAP - 32 || nbig > PQ_CAP - 32 || base + 32 >= total) {
-            n_pairs += lane == 0 ? (unsigned long long)(nsmall + nbig) : 0ull;
-            run_pairs(S, nsmall, nbig, b1, spts, parent, t2, lane, n_tests);
-            nsmall = nbig = 0;
-            __syncwarp();
+// Pass 1: the listed records, their flagged slots only.
+__global__ void __launch_bounds__(256) k_dense_link1(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
+                                                    const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
+                                                    const uint32_t* __restrict__ flags, const int* __restrict__ flist,
+                                                    DenseCtx C) {
+    const int nf = C.meta->nflag;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf; e += gridDim.x * blockDim.x) {
+        const int r = flist[e];
+        uint32_t fl = flags[r];
+        while (fl) {
+            const int k = __ffs(fl) - 1;
+            fl &= fl - 1;
+            dense_link_item<1>(r, k, g, cw, crec, ncomp, dcoord, C);
         }
     }
 }
 
-// phase 0: the cell's own octant-group pairs; phase 1: its neighbour pairs.  Running all
-// cells' phase 0 first means phase 1 sees every dense cell's groups joined already, so
-// after the first contact between two cells all their group pairs skip on cached roots.
-__device__ void dense_cell_work(int r, int phase, DenseSmem& S, const float4* __restrict__ spts,
-                                const uint32_t* __restrict__ cstart, const DenseRec* __restrict__ drec,
-                                const int* __restrict__ crec, const Grid& g, int* __restrict__ parent, int lane,
-                                unsigned long long& n_tests, unsigned long long& n_pairs) {
-    const float t2 = g.t2;
-    const DenseRec* R = drec + r;
-    // P: nonempty octant groups
-    int np;
-    {
-        const int k = lane < 8 ? lane : 7;
-        const int o0 = __ldg(&R->off[k]), o1 = __ldg(&R->off[k + 1]);
-        const bool ne = lane < 8 && o1 > o0;
-        const unsigned m = __ballot_sync(0xffffffffu, ne);
-        if (ne) {
-            const int j = __popc(m & ((1u << lane) - 1u));
-            S.ps[j] = o0;
-            S.po[j] = (uint8_t)k;
-        }
-        np = __popc(m);
-        if (lane == 0) S.ps[np] = __ldg(&R->off[8]);
+// Component nodes -> their roots (shortens the finds of the uncertain pass).
+__global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta) {
+    const int64_t nn = 8 * (int64_t)meta->ndense;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
+        const int s = nbase + (int)t;
+        int curr = ld_parent(parent, s), next;
+        if (curr == s) continue;
+        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        st_parent(parent, s, curr);
     }
-    __syncwarp();
-    // own-cell group pairs
-    if (phase == 0) {
-        if (np < 2) return;
-        if (lane < np) {
-            S.proot[lane] = uf_find(parent, S.ps[lane]);
-            S.qs[lane] = S.ps[lane];
-            S.qe[lane] = S.ps[lane + 1];
-            S.qo[lane] = S.po[lane];
-            S.qk[lane] = 26;
-        }
-        __syncwarp();
-        if (lane < np) S.qroot[lane] = S.proot[lane];
-        __syncwarp();
-        pair_sweep(S, np, 0, np, true, spts, parent, t2, lane, n_tests, n_pairs);
-        return;
-    }
-    // neighbour slots: lanes 0..25 (0..12 forward, 13..25 backward)
-    int cnt = 0;
-    if (lane < 26) {
-        int c[3];
-        dense_decode((uint32_t)__ldg(&R->cell), g, c);
-        int ox, oy, oz;
-        slot_offset(lane, ox, oy, oz);
-        uint32_t Q;
-        int rec = -1, qs = 0, qe = 0;
-        if (dense_neighbor(g, c, ox, oy, oz, Q)) {
-            qs = (int)__ldg(cstart + Q);
-            qe = (int)__ldg(cstart + Q + 1);
-            if (qe - qs > SPARSE_MAX) {
-                if (lane < 13) {
-                    rec = __ldg(crec + Q);
-                    const DenseRec* RQ = drec + rec;
-                    for (int k = 0; k < 8; ++k) cnt += __ldg(&RQ->off[k + 1]) > __ldg(&RQ->off[k]);
-                }
-            } else {
-                cnt = qe - qs;
-            }
-        }
-        S.slot_q[lane] = qs;
-        S.slot_rec[lane] = rec;
-        S.slot_cnt[lane] = cnt;
-    }
-    // exclusive scan of the group counts over the 26 slots
-    int x = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    const int nq = __shfl_sync(0xffffffffu, x, 25);
-    if (lane < 26) S.slot_off[lane] = x - cnt;
-    __syncwarp();
-    if (nq == 0) return;
-    if (lane < 26 && cnt > 0) {
-        int o = x - cnt;
-        const int rec = S.slot_rec[lane];
-        if (rec >= 0) {
-            const DenseRec* RQ = drec + rec;
-            for (int k = 0; k < 8; ++k) {
-                const int a0 = __ldg(&RQ->off[k]), a1 = __ldg(&RQ->off[k + 1]);
-                if (a1 > a0) {
-                    S.qs[o] = a0; S.qe[o] = a1; S.qo[o] = (uint8_t)k; S.qk[o] = (uint8_t)lane;
-                    ++o;
-                }
-            }
-        } else {
-            const int qs = S.slot_q[lane];
-            for (int k = 0; k < cnt; ++k) {
-                S.qs[o] = qs + k; S.qe[o] = qs + k + 1; S.qo[o] = 0xFF; S.qk[o] = (uint8_t)lane;
-                ++o;
-            }
-        }
-    }
-    __syncwarp();
-    // current roots (P's own groups were joined in phase 0)
-    if (lane < np) S.proot[lane] = uf_find(parent, S.ps[lane]);
-    for (int b = lane; b < nq; b += 32) S.qroot[b] = uf_find(parent, S.qs[b]);
-    __syncwarp();
-    // keep only Q groups that can still need a test: when all P groups share one root R
-    // (the usual case), a Q group already rooted at R is skipped as a whole
-    const int R0 = S.proot[0];
-    const bool allsame = __all_sync(0xffffffffu, lane >= np || S.proot[lane] == R0);
-    int live_n = 0;
-    for (int b0 = 0; b0 < nq; b0 += 32) {
-        const int b = b0 + lane;
-        const bool live = b < nq && (!allsame || S.qroot[b] != R0);
-        int qs_ = 0, qe_ = 0, qr_ = 0;
-        uint8_t qo_ = 0, qk_ = 0;
-        if (live) { qs_ = S.qs[b]; qe_ = S.qe[b]; qr_ = S.qroot[b]; qo_ = S.qo[b]; qk_ = S.qk[b]; }
-        const unsigned m = __ballot_sync(0xffffffffu, live);
-        __syncwarp();
-        if (live) {
-            const int d = live_n + __popc(m & ((1u << lane) - 1u));
-            S.qs[d] = qs_; S.qe[d] = qe_; S.qroot[d] = qr_; S.qo[d] = qo_; S.qk[d] = qk_;
-        }
-        live_n += __popc(m);
-        __syncwarp();
-    }
-    if (live_n == 0) return;
-    pair_sweep(S, np, 0, live_n, false, spts, parent, t2, lane, n_tests, n_pairs);
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __restrict__ spts,
-                                                            const uint32_t* __restrict__ cstart,
-                                                            const DenseRec* __restrict__ drec,
-                                                            const int* __restrict__ crec,
-                                                            int phase, Grid g,
-                                                            int* __restrict__ parent, Meta* __restrict__ meta) {
-    __shared__ DenseSmem sm[SCAN_THREADS / kWarp];
+// ---- a6+a7: queued uncertain pairs, warp per item, early exit ------------------------------
+// A's points in sub-cells within reach of B are staged per lane (up to kAPer each, in
+// batches); B's points stream through the warp 32 at a time and are broadcast by shuffle.
+constexpr int kAPer = 4;
+
+__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C) {
+    __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
-    DenseSmem& S = sm[threadIdx.x >> 5];
-    const int nd = meta->ndense;
-    unsigned long long n_tests = 0, n_pairs = 0;
-    while (true) {
-        int it = 0;
-        if (lane == 0) it = atomicAdd(phase == 0 ? &meta->work : &meta->work2, 1);
-        it = __shfl_sync(0xffffffffu, it, 0);
-        if (it >= nd) break;
-        // phase 1 visits the cells in a scattered order (a multiplicative permutation):
-        // cells processed at the same time are then rarely neighbours, so each cell sees
-        // the unions its neighbours already made and most group pairs skip on roots
-        // (a sweep in cell order processes ~7k adjacent cells at once and tests 3x more).
-        const int r = phase == 0 ? it : (int)(((unsigned long long)it * 2654435761ull) % (unsigned long long)nd);
-        dense_cell_work(r, phase, S, spts, cstart, drec, crec, g, parent, lane, n_tests, n_pairs);
+    float4* abuf = abuf_all[threadIdx.x >> 5];
+    const float t2 = g.t2;
+    const int ni = min(C.meta->nitems, C.item_cap);
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long n_tests = 0;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ni; w += warps) {
+        const int4 it = C.items[w];
+        const int na = C.nbase + 8 * it.x + it.y;
+        const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
+        int same = 0;
+        if (lane == 0) same = uf_find(C.parent, na) == uf_find(C.parent, nb);
+        if (__shfl_sync(0xffffffffu, same, 0)) continue;
+        const int cp = __ldg(C.dlist + it.x);
+        const uint32_t lp = __ldg(C.clin + cp);
+        const u64 ma = C.cmask[8 * it.x + it.y];
+        int b0, b1, slot;
+        u64 fa, fb;  // sub-cells of A within reach of B, and of B within reach of A
+        if (it.w >= 0) {
+            const int cq = __ldg(C.dlist + it.z);
+            const u64 mb = C.cmask[8 * it.z + it.w];
+            b0 = (int)__ldg(C.cstart + cq);
+            b1 = (int)__ldg(C.cstart + cq + 1);
+            slot = cell_slot_of(g, lp, __ldg(C.clin + cq));
+            fb = reach_of(ma, slot) & mb;
+            fa = reach_of(mb, 26 - slot) & ma;
+        } else {
+            b0 = it.z;
+            b1 = it.z + 1;
+            const float4 v = C.spts[it.z];
+            uint32_t lq;
+            int qb;
+            dense_cell_of(v.x, v.y, v.z, g, lq, qb);
+            slot = cell_slot_of(g, lp, lq);
+            fb = ~0ull;
+            fa = d_sc.U[26 - slot][qb] & ma;
+        }
+        const int a0 = (int)__ldg(C.cstart + cp), a1 = (int)__ldg(C.cstart + cp + 1);
+        bool found = false;
+        int ai = a0;
+        while (ai < a1 && !found) {
+            // stage the next batch of A points (via shared memory): batch position k ends up in
+            // lane k % 32, entry k / 32
+            float4 pa[kAPer];
+#pragma unroll
+            for (int e = 0; e < kAPer; ++e) pa[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            int total = 0;
+            while (ai < a1) {
+                const int i = ai + lane;
+                bool v = false;
+                float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < a1) {
+                    p = C.spts[i];
+                    uint32_t l;
+                    int qa;
+                    dense_cell_of(p.x, p.y, p.z, g, l, qa);
+                    v = (fa >> qa) & 1ull;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, v);
+                const int cnt = __popc(m);
+                if (total + cnt > 32 * kAPer) break;  // this chunk starts the next batch
+                if (v) abuf[total + __popc(m & ((1u << lane) - 1u))] = p;
+                total += cnt;
+                ai += 32;
+            }
+            __syncwarp();
+            if (total == 0) continue;
+            int na_l = (total - lane + 31) / 32;  // entries this lane holds
+            na_l = na_l > kAPer ? kAPer : (na_l < 0 ? 0 : na_l);
+#pragma unroll
+            for (int e = 0; e < kAPer; ++e)
+                if (e < na_l) pa[e] = abuf[e * 32 + lane];
+            __syncwarp();
+            for (int j0 = b0; j0 < b1 && !found; j0 += 32) {
+                const int j = j0 + lane;
+                float4 pb = make_float4(0.f, 0.f, 0.f, 0.f);
+                bool vb = false;
+                if (j < b1) {
+                    pb = C.spts[j];
+                    uint32_t l;
+                    int qb;
+                    dense_cell_of(pb.x, pb.y, pb.z, g, l, qb);
+                    vb = (fb >> qb) & 1ull;
+                }
+                unsigned mb = __ballot_sync(0xffffffffu, vb);
+                while (mb && !found) {
+                    const int src = __ffs(mb) - 1;
+                    mb &= mb - 1;
+                    float4 q;
+                    q.x = __shfl_sync(0xffffffffu, pb.x, src);
+                    q.y = __shfl_sync(0xffffffffu, pb.y, src);
+                    q.z = __shfl_sync(0xffffffffu, pb.z, src);
+                    bool hit = false;
+#pragma unroll
+                    for (int e = 0; e < kAPer; ++e)
+                        if (e < na_l) hit |= pred(pa[e], q, t2);
+                    n_tests += (unsigned long long)na_l;
+                    found = __any_sync(0xffffffffu, hit);
+                }
+            }
+        }
+        if (found && lane == 0) uf_unite(C.parent, na, nb);
         __syncwarp();
     }
-    if (meta->instrument) {
-        for (int o = 16; o > 0; o >>= 1) {
-            n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
-            n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
-        }
-        if (lane == 0 && (n_tests || n_pairs)) {
-            atomicAdd(&meta->dense_tests, n_tests);
-            atomicAdd(&meta->group_pairs, n_pairs);
-        }
+    if (C.meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
+        if (lane == 0 && n_tests) atomicAdd(&C.meta->dense_tests, n_tests);
+    }
+}
+
+// Instrumentation: dense-mode roots that are component nodes (points count themselves in
+// k_stats) and the number of dense points.
+__global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ ncomp, const int* __restrict__ dlist,
+                                                    const uint32_t* __restrict__ cstart, DenseCtx C) {
+    const int nd = C.meta->ndense;
+    unsigned long long roots = 0, pts = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
+        const int k = ncomp[r];
+        for (int j = 0; j < k; ++j) roots += C.parent[C.nbase + 8 * r + j] == C.nbase + 8 * r + j;
+        const int cid = dlist[r];
+        pts += cstart[cid + 1] - cstart[cid];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        roots += __shfl_xor_sync(0xffffffffu, roots, o);
+        pts += __shfl_xor_sync(0xffffffffu, pts, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (roots) atomicAdd(&C.meta->components, roots);
+        if (pts) atomicAdd(&C.meta->dense_points, pts);
     }
 }
 
@@ -490,11 +755,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_union_dense(const float4* __re
 // 128 consecutive cells (so the wave sweeps the sorted order upwards), compacts the
 // chunk's nonempty sparse cells into a per-warp list and gives every lane a real cell.
 // Loops are warp-uniform with a reconvergence point per neighbour (SIMT efficiency).
-constexpr int SP_CHUNK = 128;
+constexpr int SP_CHUNK = 32;
 
-__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts,
-                                                     const uint32_t* __restrict__ cstart, uint32_t cells, Grid g,
+__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
+                                                     const u64* __restrict__ ccoord,
+                                                     const uint32_t* __restrict__ cstart, Grid g,
                                                      int* __restrict__ parent, Meta* __restrict__ meta) {
+    const uint32_t cells = (uint32_t)meta->cells;  // occupied cells (compact ids)
     __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
     unsigned long long n_tests = 0;
     const float t2 = g.t2;
@@ -531,16 +798,17 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                 }
             }
             __syncwarp();
-            int c[3];
-            dense_decode(P, g, c);
+            const u64 pc = v ? __ldg(ccoord + P) : 0ull;
+            const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
 #pragma unroll 1
             for (int k = 0; k < 13; ++k) {
                 uint32_t Q;
-                int qs = 0, qe = 0;
-                if (v && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], Q)) {
-                    qs = (int)__ldg(cstart + Q);
-                    qe = (int)__ldg(cstart + Q + 1);
-                    if (qe - qs > SPARSE_MAX) qe = qs;
+                int qs = 0, qe = 0, qc = -1;
+                if (v && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], Q)) qc = cid_lookup(cw, Q);
+                if (qc >= 0) {
+                    qs = (int)__ldg(cstart + qc);
+                    qe = (int)__ldg(cstart + qc + 1);
+                    if (qe - qs > SPARSE_MAX) qe = qs;  // dense neighbours are handled by k_dense_link
                 }
                 for (int s = ps; s < pe && qe > qs; ++s) {
                     const float4 a = __ldg(spts + s);
@@ -558,6 +826,39 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
         for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
         if (lane == 0 && n_tests) atomicAdd(&meta->pair_tests, n_tests);
     }
+}
+
+}  // namespace fec
+
+// ---- host: sub-cell tables, uploaded once per device -------------------------------------
+#include <mutex>
+
+namespace fec {
+
+cudaError_t ensure_subcell_tables() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[dev & 63]) return cudaSuccess;
+    static SubcellTables t;
+    sc_build_tables(t);
+    // the bit-operation dilation used by the flood fill must equal the table's certain
+    // relation inside a cell (slot 13); checked once on the host
+    for (int a = 0; a < 64; ++a)
+        if ((sc_dilate(1ull << a) | (1ull << a)) != (t.T[13][a] | (1ull << a))) return cudaErrorInvalidValue;
+    // so must the whole-mask shift lists across the 26 neighbour slots
+    for (int sl = 0; sl < 27; ++sl) {
+        if (sl == 13) continue;
+        if (t.nsh[sl] < 0) return cudaErrorInvalidValue;
+        for (int a = 0; a < 64; ++a)
+            if (sc_certain_across(t, 1ull << a, sl) != t.T[sl][a]) return cudaErrorInvalidValue;
+    }
+    e = cudaMemcpyToSymbol(d_sc, &t, sizeof(t));
+    if (e == cudaSuccess) done[dev & 63] = true;
+    return e;
 }
 
 }  // namespace fec

@@ -28,6 +28,7 @@ struct Grid {
     double lo[3];       // bbox minimum (fp32 values widened)
     double inv_h;       // 1/h (double): sub-cell coordinate = floor((x - lo) * inv_h)
     double h;           // sub-cell edge = c/2, c = d*(1+2^-16)
+    double inv_q;       // 2*inv_h (exact): fine sub-cell coordinate = floor((x - lo) * inv_q), edge c/4
     int32_t dims[3];    // cells per axis
     int32_t bits[3];    // ceil(log2(dims)) per axis (cell-level Morton bits, hash mode)
     int32_t key_bits;   // 3 + sum(bits): significant bits of the sub-cell Morton key
@@ -124,6 +125,9 @@ __device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
 // ---- device-wide exclusive scan (host recursion over tiles) ---------------------------
 template <typename T>
 int exclusive_scan(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st);  // returns launches
+// same, over the first min(n, *ndev) elements (ndev: device int written by an earlier kernel)
+template <typename T>
+int exclusive_scan_dn(const T* in, T* out, int64_t n, const int* ndev, T* scratch, cudaStream_t st);
 size_t scan_scratch_elems(int64_t n);
 
 // ---- workspace carving -----------------------------------------------------------------

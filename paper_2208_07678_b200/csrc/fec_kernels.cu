@@ -376,10 +376,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_union(const float4* __res
 // Read-only root walk, then one store per element.  (A compressing find here would let a
 // thread's late path-halving store overwrite another thread's final root with a stale
 // intermediate; each parent[s] must be written only by its own thread.)
-__global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64_t n) {
+// Also initialises the accumulators of root points (component nodes get theirs in k_dcomps).
+__global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64_t n, int* __restrict__ size,
+                                                int* __restrict__ minidx) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         int curr = ld_parent(parent, (int)s), next;
-        if (curr == (int)s) continue;
+        if (curr == (int)s) {
+            size[s] = 0;
+            minidx[s] = 0x7fffffff;
+            continue;
+        }
         while (curr < (next = ld_parent(parent, curr))) curr = next;
         st_parent(parent, (int)s, curr);
     }

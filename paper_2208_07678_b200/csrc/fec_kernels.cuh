@@ -26,6 +26,10 @@ struct Meta {
     unsigned long long dense_tests;
     int nheavy, nlight;               // dense-grid mode: schedule of the dense cells
     int work2;                        // second dynamic work counter
+    int cells1;                       // dense-grid mode: occupied cells + 1 (scan length)
+    int nitems;                       // dense-grid mode: uncertain component pairs pushed
+    int internal_error;               // != 0: an internal invariant failed (never expected)
+    int nflag;                        // dense-grid mode: records left for the uncertain pass
 };
 
 struct Tables {
@@ -38,11 +42,6 @@ struct Tables {
     int* hval;          // hash mode: cell id
 };
 
-// Dense-grid mode: a cell holding more than SPARSE_MAX points, re-ordered by octant.
-struct DenseRec {
-    int cell;    // linear cell id
-    int off[9];  // sorted positions: octant k occupies [off[k], off[k+1])
-};
 
 __global__ void k_bbox_partial(const float* p, int64_t n, int vec4, float* part, int* nonfinite);
 __global__ void k_bbox_final(const float* part, int nblocks, Meta* meta);
@@ -55,26 +54,49 @@ __global__ void k_heads(const u64* key, int64_t n, u64* flags);
 __global__ void k_fill_tables(const u64* key, const u64* ex, int64_t n, Grid g, Tables T, Meta* meta);
 __global__ void k_init_uf(const u64* ex, const int* gstart, int64_t n, int* parent, int* size, int* minidx);
 __global__ void k_scan_union(const float4* spts, Grid g, Tables T, int* parent, Meta* meta);
-__global__ void k_flatten(int* parent, int64_t n);
+__global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx);
 __global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
 __global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
                           long long min_size, long long max_size, int* labels);
-__global__ void k_dcount(const float* p, int64_t n, Grid g, uint32_t* count, uint32_t* slot, uint32_t* dbits,
-                         Meta* meta);
+__global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
+__global__ void k_cpopc(const uint2* cw, int64_t words, uint32_t* cnt);
+__global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t* clin, uint32_t* count, u64* cocc,
+                        u64* ccoord, Grid g, Meta* meta);
+__global__ void k_dcount(const float* p, int64_t n, Grid g, const uint2* cw, uint32_t* count, uint32_t* slot,
+                         uint32_t* dbits, u64* cocc);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
-                             uint32_t* ocnt, Meta* meta);
-__global__ void k_dcount_oct(const float* p, int64_t n, Grid g, const uint32_t* count, const int* crec, uint32_t* ocnt,
-                             uint32_t* slot);
-__global__ void k_drec_fin(const int* dlist, Meta* meta, const uint32_t* cstart, const uint32_t* ocnt, DenseRec* drec);
-__global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint32_t* cstart, const uint32_t* slot,
-                           const int* crec, const DenseRec* drec, float4* spts);
-__global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint32_t* cstart, const int* crec,
-                        const DenseRec* drec, int* parent, int* size, int* minidx, int* sidx);
-__global__ void k_union_sparse(const float4* spts, const uint32_t* cstart, uint32_t cells, Grid g, int* parent,
-                               Meta* meta);
-__global__ void k_union_dense(const float4* spts, const uint32_t* cstart, const DenseRec* drec, const int* crec,
-                              int phase, Grid g, int* parent, Meta* meta);
+                             Meta* meta);
+// Dense-grid mode: what the component kernels share (item = (P record, P component,
+// Q record or point, Q component or -1 for a point)).
+struct DenseCtx {
+    const float4* spts;
+    const uint32_t* cstart;
+    const int* dlist;
+    const uint32_t* clin;
+    u64* cmask;         // [8*nd] component masks
+    int* parent;
+    int4* items;
+    int item_cap;
+    int nbase;          // node id of component k of record r: nbase + 8r + k
+    Meta* meta;
+};
+__global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp, int* size, int* minidx, u64* dcoord, uint32_t* flags,
+                         DenseCtx C);
+__global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
+                           const uint32_t* slot, float4* spts);
+__global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
+                        const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* sidx);
+__global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
+                               int* parent, Meta* meta);
+__global__ void k_dense_link0(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
+                              uint32_t* flags, int* flist, DenseCtx C);
+__global__ void k_dense_link1(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
+                              const uint32_t* flags, const int* flist, DenseCtx C);
+__global__ void k_dense_items(Grid g, DenseCtx C);
+__global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta);
+__global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);
+cudaError_t ensure_subcell_tables();  // host: upload the fine sub-cell tables (once per device)
 __global__ void k_debug_pred(const float* a, const float* b, int64_t m, float t2, uint8_t* out, float* d2out);
 
 }  // namespace fec

@@ -8,13 +8,20 @@ constexpr int SC_THREADS = 256;
 constexpr int SC_ITEMS = 8;
 constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 
+// `ndev` (optional): the length is min(n, *ndev), read on the device (tiles past it only
+// publish a zero tile sum), so a scan can be sized by a count a previous kernel produced.
 template <typename T>
 __global__ void __launch_bounds__(SC_THREADS) k_scan_tile(const T* __restrict__ in, T* __restrict__ out,
-                                                         int64_t n, T* __restrict__ sums) {
+                                                         int64_t n, T* __restrict__ sums, const int* ndev) {
     __shared__ T s[SC_TILE];
     __shared__ T wsum[SC_THREADS / kWarp];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    if (ndev) n = min(n, (int64_t)*ndev);
+    if (base >= n) {
+        if (tid == 0) sums[blockIdx.x] = T(0);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         int64_t i = base + k * SC_THREADS + tid;
@@ -61,9 +68,12 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_tile(const T* __restrict__ 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SC_THREADS) k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__ sums) {
-    const T add = sums[blockIdx.x];
+__global__ void __launch_bounds__(SC_THREADS) k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__ sums,
+                                                        const int* ndev) {
+    if (ndev) n = min(n, (int64_t)*ndev);
     const int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    if (base >= n) return;
+    const T add = sums[blockIdx.x];
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         int64_t i = base + k * SC_THREADS + threadIdx.x;
@@ -83,20 +93,26 @@ size_t scan_scratch_elems(int64_t n) {
 }
 
 template <typename T>
-int exclusive_scan(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st) {
+int exclusive_scan_dn(const T* in, T* out, int64_t n, const int* ndev, T* scratch, cudaStream_t st) {
     if (n <= 0) return 0;
     int launches = 1;
     int64_t nb = (n + SC_TILE - 1) / SC_TILE;
-    k_scan_tile<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, scratch);
+    k_scan_tile<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, scratch, ndev);
     if (nb > 1) {
         T* next = scratch + ((nb + 63) / 64) * 64 + 64;
-        launches += exclusive_scan<T>(scratch, scratch, nb, next, st);
-        k_scan_add<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(out, n, scratch);
+        launches += exclusive_scan_dn<T>(scratch, scratch, nb, nullptr, next, st);
+        k_scan_add<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(out, n, scratch, ndev);
         ++launches;
     }
     return launches;
 }
 
+template <typename T>
+int exclusive_scan(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st) {
+    return exclusive_scan_dn<T>(in, out, n, nullptr, scratch, st);
+}
+
+template int exclusive_scan_dn<uint32_t>(const uint32_t*, uint32_t*, int64_t, const int*, uint32_t*, cudaStream_t);
 template int exclusive_scan<uint32_t>(const uint32_t*, uint32_t*, int64_t, uint32_t*, cudaStream_t);
 template int exclusive_scan<unsigned long long>(const unsigned long long*, unsigned long long*, int64_t,
                                                 unsigned long long*, cudaStream_t);

@@ -114,20 +114,24 @@ __device__ __forceinline__ int warp_append(int* counter, bool want) {
 }
 
 // P records for every boundary point, C records for every boundary-touching local root.
+// Roots are points or (dense-grid mode) component nodes n + 8r + k, so the loop runs over
+// all n + 8 * ndense union-find nodes.
 __global__ void __launch_bounds__(256) k_slab_pack(const int* __restrict__ parent, const int* __restrict__ val,
                                                   const int* __restrict__ gidx, int64_t n, int n_owned,
                                                   int n_first, const int* __restrict__ size,
                                                   const int* __restrict__ minidx, const int* __restrict__ ckey,
-                                                  int* __restrict__ rec, int rec_cap) {
+                                                  int* __restrict__ rec, int rec_cap, const Meta* __restrict__ meta) {
     int* P = rec + SLAB_HDR;
     int* Cr = rec + slab_c_off(rec_cap);
+    const int64_t nodes = n + 8 * (int64_t)meta->ndense;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t nr = (n + 31) & ~int64_t(31);  // whole warps stay in the loop
+    const int64_t nr = (nodes + 31) & ~int64_t(31);  // whole warps stay in the loop
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += stride) {
-        const bool ok = s < n;
+        const bool ok = s < nodes;
+        const bool pt = s < n;
         const int r = ok ? __ldg(parent + s) : 0;
-        const int i = ok ? __ldg(val + s) : 0;
-        const bool bnd = ok && (i < n_first || i >= n_owned);
+        const int i = pt ? __ldg(val + s) : 0;
+        const bool bnd = pt && (i < n_first || i >= n_owned);
         const bool is_root = ok && r == (int)s;
         const int k = (bnd || is_root) ? __ldg(ckey + r) : -1;
         const int ps = warp_append(rec + 0, bnd);

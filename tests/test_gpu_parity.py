@@ -212,3 +212,25 @@ def test_instrumentation_counts(fec):
         fec.set_grid_mode(0)
     assert h["dense_table"] == 0 and h["components"] == s["components"]
     assert h["cells"] == s["cells"] and h["cells"] <= h["groups"] <= w.n
+
+
+@pytest.mark.parametrize("cap", [1, 7])
+def test_uncertain_queue_overflow_path(fec, cap):
+    """Dense cells: uncertain component pairs beyond the queue cap are tested in place by one
+    thread; the labels must not change."""
+    fec.set_item_cap(cap)
+    try:
+        for name, scale in [("C3", 0.02), ("C4", 0.01), ("C5", 0.005)]:
+            w = synth.make_config(name, scale=scale)
+            got = run_gpu(fec, w.points, w.d_th, 1, 2**62)
+            assert_same(got, oracle.fec(w.points, w.d_th, 1, 2**62), f"{name} cap {cap}")
+        rng = np.random.default_rng(11)
+        for k in range(20):
+            n = int(rng.integers(50, 3000))
+            c = rng.uniform(0, 3, size=(6, 3))
+            pts = (c[rng.integers(0, 6, n)] + rng.normal(0, 0.15, (n, 3))).astype(np.float32)
+            d = float(rng.uniform(0.05, 0.4))
+            got = run_gpu(fec, pts, d)
+            assert_same(got, oracle.fec(pts, d, 1, 2**62), f"blobs {k} cap {cap}")
+    finally:
+        fec.set_item_cap(0)
