@@ -120,11 +120,11 @@ struct Layout {
     u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
     u64* ccoord;        // [n]   cell coordinates of each occupied cell, 21 bits each
     int* ncomp;         // per dense record: certain-connected components (<= 8)
-    uint32_t* dflag;    // per dense record: neighbour slots left for the uncertain pass
     u64* dcoord;        // per dense record: cell coordinates, 21 bits each
-    int* dflist;        // dense records left for the uncertain pass
+    uint32_t* oflag;    // per dense record: slots whose pairs overflowed the queue
     u64* cmask;         // per dense record: 8 component masks
-    int4* items;        // uncertain component pairs
+    int4* items;        // queued component pairs (not certain, possibly within reach)
+    int4* items2;       // those still apart after all certain unions
     int item_cap;
     size_t total;
 };
@@ -177,12 +177,12 @@ Layout carve(char* base, int64_t n) {
     L.cocc = b.take<u64>(n);
     L.ccoord = b.take<u64>(n);
     L.ncomp = b.take<int>(dense_max(n));
-    L.dflag = b.take<uint32_t>(dense_max(n));
     L.dcoord = b.take<u64>(dense_max(n));
-    L.dflist = b.take<int>(dense_max(n));
+    L.oflag = b.take<uint32_t>(dense_max(n));
     L.cmask = b.take<u64>((size_t)8 * dense_max(n));
     L.item_cap = (int)std::min<int64_t>(n / 8 + 65536, INT32_MAX / 2);
     L.items = b.take<int4>(L.item_cap);
+    L.items2 = b.take<int4>(L.item_cap);
     L.total = std::max(a.off, b.off) + 256;
     return L;
 }
@@ -331,8 +331,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
         dctx.nbase = (int)n;
         dctx.meta = L.meta;
-        k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx, L.dcoord,
-                                                                  L.dflag, dctx);
+        k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
+                                                                  L.dcoord, L.oflag, dctx);
         launches += 2;
         // a3: counting sort = scan (over the occupied cells only) + scatter
         mark(2, st);
@@ -351,13 +351,15 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
                                                                          L.parent, L.meta);
         mark(6, st);
-        const unsigned lb = grid_for(dense_max(n), 256, cap * 4);
-        k_dense_link0<<<dim3(grid_for(dense_max(n), 256, cap), 27), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord,
-                                                                              L.dflag, L.dflist, dctx);
+        const unsigned lx = grid_for(dense_max(n), 256, cap);
+        k_dense_link<<<dim3(lx, 3), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
+        k_dense_link<<<dim3(lx, 24), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 3);
+        k_dense_overflow<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag,
+                                                                          dctx);
         k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
-        k_dense_link1<<<lb, 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.dflag, L.dflist, dctx);
-        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx);
-        launches += 5;
+        k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(dctx, L.items2);
+        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2);
+        launches += 7;
         if (g_instrument) {
             k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);
             ++launches;
@@ -443,7 +445,7 @@ fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
         g_stats.components = (int64_t)g_pinned_meta->components;
         g_stats.pair_tests = (int64_t)(g_pinned_meta->pair_tests + g_pinned_meta->dense_tests);
         g_stats.dense_tests = g.dense ? (int64_t)g_pinned_meta->dense_tests : -1;
-        g_stats.group_pairs = g.dense ? (int64_t)g_pinned_meta->nitems : (int64_t)g_pinned_meta->group_pairs;
+        g_stats.group_pairs = g.dense ? (int64_t)g_pinned_meta->nitems2 : (int64_t)g_pinned_meta->group_pairs;
         if (g_pinned_meta->internal_error) { g_err = "internal invariant failed (component bound)"; return FEC_ERR_CUDA; }
     }
     g_stats_valid = true;

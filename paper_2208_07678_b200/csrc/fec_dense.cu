@@ -359,10 +359,10 @@ __device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, 
     }
 }
 
-// Queue an uncertain pair unless the two nodes are already connected.  The lanes that push
-// together share one atomicAdd.
-__device__ __forceinline__ void push_item(const DenseCtx& C, const Grid& g, int4 it, int na, int nb) {
-    if (uf_find(C.parent, na) == uf_find(C.parent, nb)) return;
+// Queue a pair of nodes that may need point tests.  The lanes that push together share one
+// atomicAdd.  Returns false when the queue is full (the caller marks the slot for
+// k_dense_overflow, which tests such pairs in place).
+__device__ __forceinline__ bool queue_item(const DenseCtx& C, int4 it) {
     const unsigned m = __activemask();
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(m) - 1;
@@ -370,21 +370,22 @@ __device__ __forceinline__ void push_item(const DenseCtx& C, const Grid& g, int4
     if (lane == leader) base = atomicAdd(&C.meta->nitems, __popc(m));
     base = __shfl_sync(m, base, leader);
     const int k = base + __popc(m & ((1u << lane) - 1u));
-    if (k < C.item_cap) C.items[k] = it;
-    else test_item_serial(C, g, it);
+    if (k >= C.item_cap) return false;
+    C.items[k] = it;
+    return true;
 }
 
 // ---- dense records: components of the fine occupancy, node init, in-cell uncertain pairs --
 __global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ cocc, const u64* __restrict__ ccoord,
                                                int* __restrict__ ncomp,
                                                int* __restrict__ size, int* __restrict__ minidx,
-                                               u64* __restrict__ dcoord, uint32_t* __restrict__ flags, DenseCtx C) {
+                                               u64* __restrict__ dcoord, uint32_t* __restrict__ oflags, DenseCtx C) {
     const int nd = C.meta->ndense;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
         const int cid = __ldg(C.dlist + r);
         const u64 occ = __ldg(cocc + cid);
         dcoord[r] = __ldg(ccoord + cid);
-        flags[r] = 0u;
+        oflags[r] = 0u;
         u64 comp[kMaxComp];
         u64 rest;
         const int k = sc_components(occ, comp, rest);
@@ -488,115 +489,130 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
 // adjacent cells is therefore handled once.  Pass 0 makes the certain
 // unions and records, per record, the slots that still hold a non-certain pair within
 // reach; pass 1 (after all certain unions) queues those pairs whose nodes are still apart.
-__device__ __forceinline__ void slot_offset(int k, int& ox, int& oy, int& oz) {
-    const int kk = k < 13 ? k : k - 13;
-    const int sg = k < 13 ? 1 : -1;
-    ox = sg * c_fwd[kk][0];
-    oy = sg * c_fwd[kk][1];
-    oz = sg * c_fwd[kk][2];
-}
 
-// One (dense record r, slot k) item.  Returns whether pass 0 left work for pass 1.
-template <int pass>
-__device__ __forceinline__ bool dense_link_item(int r, int k, const Grid& g, const uint2* __restrict__ cw,
+// One (dense record r, slot k) item: certain component pairs are united at once; pairs that
+// are not certain but may be within reach and whose nodes are (so far) apart are queued
+// (k_dense_filter re-checks them after every certain union, k_dense_items tests the rest).
+// `serial` (overflow path): such pairs are tested in place by this thread instead.
+// Slot order: 0-2 forward faces, 3-12 forward edges and corners, 13-25 backward, 26 = P's own
+// components.
+__constant__ signed char c_slot[26][3] = {
+    {1, 0, 0},   {0, 1, 0},   {0, 0, 1},                                         // forward faces
+    {-1, 1, 0},  {1, 1, 0},   {0, -1, 1}, {-1, 0, 1}, {1, 0, 1}, {0, 1, 1},      // forward edges
+    {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1}, {1, 1, 1},                             // forward corners
+    {-1, 0, 0},  {0, -1, 0},  {0, 0, -1},                                        // backward ...
+    {1, -1, 0},  {-1, -1, 0}, {0, 1, -1}, {1, 0, -1}, {-1, 0, -1}, {0, -1, -1},
+    {1, 1, -1},  {-1, 1, -1}, {1, -1, -1}, {-1, -1, -1}};
+
+template <bool serial>
+__device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, const uint2* __restrict__ cw,
                                                 const int* __restrict__ crec, const int* __restrict__ ncomp,
-                                                const u64* __restrict__ dcoord, const DenseCtx& C) {
+                                                const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
+                                                const DenseCtx& C) {
     const int kp = __ldg(ncomp + r);
     const u64* mp = C.cmask + 8 * r;
+    bool overflow = false;
     if (k == 26) {
-        // P's own components within reach of each other (never certain-adjacent)
-        if (kp < 2) return false;
-        if constexpr (pass == 1) {
-            for (int i = 0; i + 1 < kp; ++i) {
-                const u64 ri = reach_of(mp[i], 13);
-                for (int j = i + 1; j < kp; ++j)
-                    if (ri & mp[j]) push_item(C, g, make_int4(r, i, r, j), C.nbase + 8 * r + i, C.nbase + 8 * r + j);
+        // P's own components (never certain-adjacent to each other)
+        for (int i = 0; i + 1 < kp; ++i)
+            for (int j = i + 1; j < kp; ++j) {
+                const int na = C.nbase + 8 * r + i, nb = C.nbase + 8 * r + j;
+                if (uf_find(C.parent, na) == uf_find(C.parent, nb)) continue;
+                if constexpr (serial) test_item_serial(C, g, make_int4(r, i, r, j));
+                else overflow |= !queue_item(C, make_int4(r, i, r, j));
             }
-        }
-        return true;
-    }
-    const u64 pc = __ldg(dcoord + r);
-    const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
-    int ox, oy, oz;
-    slot_offset(k, ox, oy, oz);
-    uint32_t lq;
-    if (!dense_neighbor(g, c, ox, oy, oz, lq)) return false;
-    const int cq = cid_lookup(cw, lq);
-    if (cq < 0) return false;
-    const int q0 = (int)__ldg(C.cstart + cq), q1 = (int)__ldg(C.cstart + cq + 1);
-    const int slot = sc_slot(ox, oy, oz);
-    bool flag = false;
-    if (q1 - q0 > SPARSE_MAX) {
-        if (k >= 13) return false;  // backward dense pairs belong to the other cell
-        const int rq = __ldg(crec + cq);
-        const int kq = __ldg(ncomp + rq);
-        for (int x = 0; x < kp; ++x) {
-            const u64 mx = mp[x];
-            const u64 dc = sc_certain_across(d_sc, mx, slot);
-            const int na = C.nbase + 8 * r + x;
-            for (int y = 0; y < kq; ++y) {
-                const u64 my = C.cmask[8 * rq + y];
-                const int nb = C.nbase + 8 * rq + y;
-                if (dc & my) {
-                    if constexpr (pass == 0) uf_unite(C.parent, na, nb);
-                } else if constexpr (pass == 0) {
-                    flag = true;  // exact reach is checked in pass 1, only if still apart
-                } else if (uf_find(C.parent, na) != uf_find(C.parent, nb) && (reach_of(mx, slot) & my)) {
-                    push_item(C, g, make_int4(r, x, rq, y), na, nb);
-                }
-            }
-        }
     } else {
-        const int opp = 26 - slot;
-        for (int t = q0; t < q1; ++t) {
-            const float4 v = C.spts[t];
-            uint32_t l;
-            int qb;
-            dense_cell_of(v.x, v.y, v.z, g, l, qb);
-            const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
+        const u64 pc = __ldg(dcoord + r);
+        const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
+        const int ox = c_slot[k][0], oy = c_slot[k][1], oz = c_slot[k][2];
+        uint32_t lq;
+        const int cq = dense_neighbor(g, c, ox, oy, oz, lq) ? cid_lookup(cw, lq) : -1;
+        if (cq < 0) return;
+        const int q0 = (int)__ldg(C.cstart + cq), q1 = (int)__ldg(C.cstart + cq + 1);
+        const int slot = sc_slot(ox, oy, oz);
+        if (q1 - q0 > SPARSE_MAX) {
+            if (k >= 13) return;  // backward dense pairs belong to the other cell
+            const int rq = __ldg(crec + cq);
+            const int kq = __ldg(ncomp + rq);
             for (int x = 0; x < kp; ++x) {
-                const int na = C.nbase + 8 * r + x;
                 const u64 mx = mp[x];
-                if (tc & mx) {
-                    if constexpr (pass == 0) uf_unite(C.parent, t, na);
-                } else if (tu & mx) {
-                    if constexpr (pass == 0) flag = true;
-                    else push_item(C, g, make_int4(r, x, t, -1), na, t);
+                const u64 dc = sc_certain_across(d_sc, mx, slot);
+                const bool near_p = (mx & d_sc.F[slot]) != 0;
+                const int na = C.nbase + 8 * r + x;
+                for (int y = 0; y < kq; ++y) {
+                    const u64 my = C.cmask[8 * rq + y];
+                    const int nb = C.nbase + 8 * rq + y;
+                    if (dc & my) {
+                        if constexpr (!serial) uf_unite(C.parent, na, nb);
+                    } else if (near_p && (my & d_sc.F[26 - slot]) &&
+                               uf_find(C.parent, na) != uf_find(C.parent, nb)) {
+                        if constexpr (serial) test_item_serial(C, g, make_int4(r, x, rq, y));
+                        else overflow |= !queue_item(C, make_int4(r, x, rq, y));
+                    }
+                }
+            }
+        } else {
+            const int opp = 26 - slot;
+            for (int t = q0; t < q1; ++t) {
+                const float4 v = C.spts[t];
+                uint32_t l;
+                int qb;
+                dense_cell_of(v.x, v.y, v.z, g, l, qb);
+                const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
+                for (int x = 0; x < kp; ++x) {
+                    const u64 mx = mp[x];
+                    const int na = C.nbase + 8 * r + x;
+                    if (tc & mx) {
+                        if constexpr (!serial) uf_unite(C.parent, t, na);
+                    } else if ((tu & mx) && uf_find(C.parent, na) != uf_find(C.parent, t)) {
+                        if constexpr (serial) test_item_serial(C, g, make_int4(r, x, t, -1));
+                        else overflow |= !queue_item(C, make_int4(r, x, t, -1));
+                    }
                 }
             }
         }
     }
-    return flag;
+    if (overflow) atomicOr(oflags + r, 1u << k);
 }
 
-// Pass 0: every (record, slot) item; blockIdx.y = slot, so a warp shares its slot (uniform
-// table reads); records left with work are listed once for pass 1.
-__global__ void __launch_bounds__(256) k_dense_link0(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
-                                                    const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
-                                                    uint32_t* __restrict__ flags, int* __restrict__ flist, DenseCtx C) {
+// Slots [k0, k0 + gridDim.y) of every record (blockIdx.y = slot: a warp shares its slot).
+// Launched for the face slots first, then the rest: by then most non-certain pairs of
+// edge/corner neighbours are already connected through faces and are not queued.
+__global__ void __launch_bounds__(256) k_dense_link(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
+                                                   const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
+                                                   uint32_t* __restrict__ oflags, DenseCtx C, int k0) {
     const int nd = C.meta->ndense;
-    const int k = blockIdx.y;
+    const int k = k0 + blockIdx.y;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x)
+        dense_link_item<false>(r, k, g, cw, crec, ncomp, dcoord, oflags, C);
+}
+
+// Queue overflow: the marked slots' pairs are tested in place (one thread per record).
+__global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __restrict__ cw,
+                                                       const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                                       const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
+                                                       DenseCtx C) {
+    const int nd = C.meta->ndense;
+    if (C.meta->nitems <= C.item_cap) return;  // nothing overflowed
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
-        if (dense_link_item<0>(r, k, g, cw, crec, ncomp, dcoord, C)) {
-            if (atomicOr(flags + r, 1u << k) == 0u) flist[atomicAdd(&C.meta->nflag, 1)] = r;
+        uint32_t f = oflags[r];
+        while (f) {
+            const int k = __ffs(f) - 1;
+            f &= f - 1;
+            dense_link_item<true>(r, k, g, cw, crec, ncomp, dcoord, oflags, C);
         }
     }
 }
 
-// Pass 1: the listed records, their flagged slots only.
-__global__ void __launch_bounds__(256) k_dense_link1(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
-                                                    const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
-                                                    const uint32_t* __restrict__ flags, const int* __restrict__ flist,
-                                                    DenseCtx C) {
-    const int nf = C.meta->nflag;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nf; e += gridDim.x * blockDim.x) {
-        const int r = flist[e];
-        uint32_t fl = flags[r];
-        while (fl) {
-            const int k = __ffs(fl) - 1;
-            fl &= fl - 1;
-            dense_link_item<1>(r, k, g, cw, crec, ncomp, dcoord, C);
-        }
+// Queued pairs whose nodes are already connected (after all certain unions) are dropped;
+// the others are compacted into items2 for k_dense_items.
+__global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restrict__ items2) {
+    const int ni = min(C.meta->nitems, C.item_cap);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
+        const int4 it = C.items[e];  // queued before every certain union was done: re-check
+        const int na = C.nbase + 8 * it.x + it.y;
+        const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
+        if (uf_find(C.parent, na) != uf_find(C.parent, nb)) items2[atomicAdd(&C.meta->nitems2, 1)] = it;
     }
 }
 
@@ -617,16 +633,16 @@ __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent,
 // batches); B's points stream through the warp 32 at a time and are broadcast by shuffle.
 constexpr int kAPer = 4;
 
-__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C) {
+__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const int4* __restrict__ items2) {
     __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
     float4* abuf = abuf_all[threadIdx.x >> 5];
     const float t2 = g.t2;
-    const int ni = min(C.meta->nitems, C.item_cap);
+    const int ni = C.meta->nitems2;
     const int warps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long n_tests = 0;
     for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ni; w += warps) {
-        const int4 it = C.items[w];
+        const int4 it = items2[w];
         const int na = C.nbase + 8 * it.x + it.y;
         const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
         int same = 0;

@@ -29,7 +29,7 @@ struct Meta {
     int cells1;                       // dense-grid mode: occupied cells + 1 (scan length)
     int nitems;                       // dense-grid mode: uncertain component pairs pushed
     int internal_error;               // != 0: an internal invariant failed (never expected)
-    int nflag;                        // dense-grid mode: records left for the uncertain pass
+    int nitems2;                      // dense-grid mode: queued pairs still apart after the certain unions
 };
 
 struct Tables {
@@ -81,19 +81,20 @@ struct DenseCtx {
     int nbase;          // node id of component k of record r: nbase + 8r + k
     Meta* meta;
 };
-__global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp, int* size, int* minidx, u64* dcoord, uint32_t* flags,
-                         DenseCtx C);
+__global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp, int* size, int* minidx, u64* dcoord,
+                         uint32_t* oflags, DenseCtx C);
 __global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                            const uint32_t* slot, float4* spts);
 __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                         const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* sidx);
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
                                int* parent, Meta* meta);
-__global__ void k_dense_link0(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
-                              uint32_t* flags, int* flist, DenseCtx C);
-__global__ void k_dense_link1(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
-                              const uint32_t* flags, const int* flist, DenseCtx C);
-__global__ void k_dense_items(Grid g, DenseCtx C);
+__global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
+                             uint32_t* oflags, DenseCtx C, int k0);
+__global__ void k_dense_overflow(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
+                                 uint32_t* oflags, DenseCtx C);
+__global__ void k_dense_filter(DenseCtx C, int4* items2);
+__global__ void k_dense_items(Grid g, DenseCtx C, const int4* items2);
 __global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta);
 __global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);
 cudaError_t ensure_subcell_tables();  // host: upload the fine sub-cell tables (once per device)
