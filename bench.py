@@ -127,19 +127,24 @@ def algorithmic_bytes(stage: str, n: int, st: dict) -> float:
     """Bytes each stage must move: n points, C grid cells (dense mode),
     md points in dense cells, G groups / U cells and P radix passes (hashed mode)."""
     if st["dense_table"]:
-        C = float(np.prod(st["dims"]))
-        md = max(st.get("dense_points", 0), 0)
+        C = float(np.prod(st["dims"]))          # grid cells (occupancy bitmap: 1 bit each)
+        U = float(max(st.get("cells", 0), 0))  # occupied cells
+        nd = float(max(st.get("dense_cells", 0), 0))
+        md = float(max(st.get("dense_points", 0), 0))
+        ns = n - md                             # points of sparse cells
         model = {
             "a1_bbox_validate": 12.0 * n,
-            "a2_bin_keys": 4.0 * C + 2 * 12.0 * n + 4.0 * n + 4.0 * md,  # zero counts, 2 reads of xyz, slots
-            "a3_sort": 8.0 * C + 12.0 * n + 4.0 * n + 16.0 * n,   # scan counts, read xyz+slot, write float4
-            "a4_gather_init": 16.0 * n + 16.0 * n,                 # read float4, write parent/size/min/idx
+            # occupancy bitmap + word bases (C/8 B, ~9 touches), cell lists (28 B/cell), two
+            # reads of xyz, slots, per-cell counts + fine masks, dense components (~180 B/cell)
+            "a2_bin_keys": 24.0 * n + 4.0 * n + 1.125 * C + 44.0 * U + 180.0 * nd,
+            "a3_sort": 8.0 * U + 12.0 * n + 4.0 * n + 16.0 * n,  # scan counts; xyz + slot -> float4
+            "a4_gather_init": 16.0 * n + 8.0 * n + 8.0 * ns,      # float4 -> parent, idx (+ root accumulators)
             "a5_tables": 0.0,
-            "a6a7_union_sparse": 4.0 * C + 16.0 * (n - md) + 8.0 * (n - md),  # cell table; sparse points, parents
-            "a6a7_union_dense": 16.0 * md + 8.0 * md,              # dense points read; parents r/w
-            "a8_flatten": 8.0 * n,
-            "a9_stats": 8.0 * n,
-            "a10_relabel": 20.0 * n,
+            "a6a7_union_sparse": 24.0 * ns + 8.0 * U,             # sparse points + parents, cell starts
+            "a6a7_union_dense": 128.0 * nd,                       # component masks + node parents
+            "a8_flatten": 8.0 * n if 4 * U > n else 0.0,          # separate flatten (sparse-dominated only)
+            "a9_stats": 12.0 * n,                                 # parent r/w + input index
+            "a10_relabel": 12.0 * n,                              # parent + index -> label
         }
     else:
         G, U, P = st["groups"], st["cells"], st["radix_passes"]

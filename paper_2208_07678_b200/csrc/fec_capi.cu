@@ -26,7 +26,7 @@ constexpr int kStages = 10;
 const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",       "a3_sort",
                                           "a4_gather_init",   "a5_tables",    "a6a7_union_sparse",
                                           "a6a7_union_dense", "a8_flatten",        "a9_stats",
-                                          "a10_relabel"};
+                                          "a10_relabel"};  // single-GPU path: a8 = separate flatten (sparse-dominated clouds only), a9 = k_flat_stats
 struct StageEvents {
     cudaEvent_t ev[kStages + 1] = {};
     bool created = false;
@@ -342,7 +342,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         // a4: sorted-order init (parents: self, or the point's component node)
         mark(3, st);
         k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
-                                     L.sidx);
+                                     L.size, L.minidx, L.sidx);
         ++launches;
         mark(4, st);
         // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
@@ -408,10 +408,6 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         mark(7, st);
     }
 
-    // ---- a8 ----------------------------------------------------------------------------------
-    k_flatten<<<ew, 256, 0, st>>>(L.parent, n, L.size, L.minidx);
-    ++launches;
-    mark(8, st);
     C.g = g;
     C.val = val;
     C.launches = launches;
@@ -475,12 +471,15 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n, 256, dev_info().sms * 8 * 4);
-    // ---- a9, a10 -------------------------------------------------------------------------------
-    k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
+    // ---- a8+a9 fused (flatten + stats), a10 -----------------------------------------------------
+    k_flatten_if<<<ew, 256, 0, st>>>(L.parent, n, L.meta);
+    mark(8, st);
+    k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
+    k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
     mark(9, st);
-    k_relabel<<<ew, 256, 0, st>>>(L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size,
-                                  labels);
-    C.launches += 2;
+    k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
+        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels);
+    C.launches += 4;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
     return finish_stats(C, n, st);
@@ -630,6 +629,9 @@ fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n_local, 256, dev_info().sms * 8 * 4);
+    k_flatten<<<ew, 256, 0, st>>>(L.parent, n_local, L.size, L.minidx);
+    mark(8, st);
+    ++C.launches;
     FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)nodes_max(n_local) * 4, st));
     k_slab_stats<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
                                      S.ckey, L.meta);

@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                                               const uint2* __restrict__ cw, const uint32_t* __restrict__ cstart,
                                               const int* __restrict__ crec, const int* __restrict__ ncomp,
                                               const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
+                                              int* __restrict__ size, int* __restrict__ minidx,
                                               int* __restrict__ sidx) {
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -466,7 +467,14 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                 par[j] = nbase + 8 * r + c;
             }
         }
-        // size / minidx of root points are set by k_flatten
+        // accumulators of the possible root points (points of sparse cells); points of dense
+        // cells hang under component nodes and never become roots
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (b4 + j < n && par[j] == (int)(b4 + j)) {
+                size[b4 + j] = 0;
+                minidx[b4 + j] = 0x7fffffff;
+            }
         if (b4 + 4 <= n) {
             *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
             *reinterpret_cast<int4*>(sidx + b4) = make_int4(si[0], si[1], si[2], si[3]);

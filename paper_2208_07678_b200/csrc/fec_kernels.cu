@@ -396,9 +396,12 @@ __global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64
 // so a giant component (C5: ~40% of all points) costs one global atomic per block instead
 // of one per warp.  Blocks own contiguous ranges (the sorted order is spatial).
 constexpr int HH_SLOTS = 256;
+// `only_sparse`: run only for sparse-dominated clouds (occupied cells > n/4; the forest was
+// flattened by k_flatten_if), where per-lane aggregation of this form is the faster one.
 __global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                               int* __restrict__ size, int* __restrict__ minidx,
-                                              Meta* __restrict__ meta) {
+                                              Meta* __restrict__ meta, int only_sparse) {
+    if (only_sparse && 4 * (int64_t)meta->cells <= n) return;
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
     for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
     __syncthreads();
@@ -453,14 +456,129 @@ __global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, c
     }
 }
 
+// Sparse-dominated clouds (many small components, deep forests: occupied cells > n/4)
+// flatten in a separate pass first; k_flat_stats's walks are then one load each.
+__global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, int64_t n, const Meta* __restrict__ meta) {
+    if (4 * (int64_t)meta->cells <= n) return;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        int curr = ld_parent(parent, (int)s), next;
+        if (curr == (int)s) continue;
+        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        st_parent(parent, (int)s, curr);
+    }
+}
+
+// Single-GPU tail, a8+a9 fused: every point's root (read-only walk; the root is written back,
+// which flattens the forest for k_relabel) and the component size + minimum input index,
+// aggregated per warp and per block as in k_stats.  Roots' accumulators were initialised
+// earlier (sparse points in k_dinit, component nodes in k_dcomps, hashed mode in k_init_uf).
+__global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+                                                   int* __restrict__ size, int* __restrict__ minidx,
+                                                   Meta* __restrict__ meta) {
+    if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_flatten_if + k_stats
+    __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
+    for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned long long roots = 0;
+    const int64_t per = 4 * (int64_t)blockDim.x;
+    const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + per - 1) / per * per;
+    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    for (int64_t s0 = b0; s0 < b1; s0 += per) {
+        // round j covers positions s0 + j*blockDim + threadIdx.x: a warp holds 32 consecutive
+        // positions per round (equal roots meet in one aggregation step); the 4 rounds' loads
+        // are issued together
+        int r[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t s = s0 + j * (int64_t)blockDim.x + threadIdx.x;
+            r[j] = s < b1 ? ld_parent(parent, (int)s) : -1;
+            v[j] = s < b1 ? __ldg(val + s) : 0x7fffffff;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r[j] < 0) continue;
+            const int s = (int)(s0 + j * (int64_t)blockDim.x + threadIdx.x);
+            if (r[j] == s) {
+                ++roots;
+                continue;
+            }
+            int curr = r[j], next;
+            while (curr < (next = ld_parent(parent, curr))) curr = next;
+            if (curr != r[j]) st_parent(parent, s, curr);
+            r[j] = curr;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool ok = r[j] >= 0;
+            unsigned todo = __ballot_sync(0xffffffffu, ok);
+            while (todo) {
+                const int leader = __ffs(todo) - 1;
+                const int key = __shfl_sync(0xffffffffu, r[j], leader);
+                const bool mem = ok && r[j] == key;
+                const unsigned peers = __ballot_sync(0xffffffffu, mem);
+                const int mn = __reduce_min_sync(0xffffffffu, mem ? v[j] : 0x7fffffff);
+                if (lane == leader) {
+                    const int cnt = __popc(peers);
+                    unsigned h = ((unsigned)key * 2654435761u) >> 24;
+                    bool done = false;
+                    for (int probe = 0; probe < 4 && !done; ++probe, h = (h + 1) & (HH_SLOTS - 1)) {
+                        int cur = hkey[h];
+                        if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
+                        if (cur == -1 || cur == key) {
+                            atomicAdd(&hcnt[h], cnt);
+                            atomicMin(&hmin[h], mn);
+                            done = true;
+                        }
+                    }
+                    if (!done) {
+                        atomicAdd(size + key, cnt);
+                        atomicMin(minidx + key, mn);
+                    }
+                }
+                todo &= ~peers;
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) {
+        if (hkey[k] >= 0) {
+            atomicAdd(size + hkey[k], hcnt[k]);
+            atomicMin(minidx + hkey[k], hmin[k]);
+        }
+    }
+    if (meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) roots += __shfl_xor_sync(0xffffffffu, roots, o);
+        if (lane == 0 && roots) atomicAdd(&meta->components, roots);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent, const int* __restrict__ val,
                                                 const int* __restrict__ size, const int* __restrict__ minidx,
                                                 int64_t n, long long min_size, long long max_size,
                                                 int* __restrict__ labels) {
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        const int r = __ldg(parent + s);
-        const long long sz = __ldg(size + r);
-        labels[__ldg(val + s)] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r) : -1;
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sb = 4 * gi;
+        int r[4], v[4];
+        if (sb + 4 <= n) {
+            const int4 pr = __ldg(reinterpret_cast<const int4*>(parent + sb));
+            const int4 vv = __ldg(reinterpret_cast<const int4*>(val + sb));
+            r[0] = pr.x; r[1] = pr.y; r[2] = pr.z; r[3] = pr.w;
+            v[0] = vv.x; v[1] = vv.y; v[2] = vv.z; v[3] = vv.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                r[j] = sb + j < n ? __ldg(parent + sb + j) : -1;
+                v[j] = sb + j < n ? __ldg(val + sb + j) : -1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r[j] < 0) continue;
+            const long long sz = __ldg(size + r[j]);
+            labels[v[j]] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
+        }
     }
 }
 

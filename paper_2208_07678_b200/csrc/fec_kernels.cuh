@@ -55,7 +55,9 @@ __global__ void k_fill_tables(const u64* key, const u64* ex, int64_t n, Grid g, 
 __global__ void k_init_uf(const u64* ex, const int* gstart, int64_t n, int* parent, int* size, int* minidx);
 __global__ void k_scan_union(const float4* spts, Grid g, Tables T, int* parent, Meta* meta);
 __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx);
-__global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
+__global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
+__global__ void k_flat_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
+__global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta, int only_sparse);
 __global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
                           long long min_size, long long max_size, int* labels);
 __global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
@@ -86,7 +88,8 @@ __global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp,
 __global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                            const uint32_t* slot, float4* spts);
 __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
-                        const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* sidx);
+                        const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* size,
+                        int* minidx, int* sidx);
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
                                int* parent, Meta* meta);
 __global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
