@@ -199,6 +199,18 @@ const char* fec_version(void);
 fec_status_t fec_debug_pred(const float* a, const float* b, int64_t m, float d_th, uint8_t* out,
                             float* d2_out, void* stream);
 
+/* Host-only diagnostics of the fine sub-cell relations of the dense-grid path (DESIGN.md
+ * §4; no device needed).  A grid cell is split into 4x4x4 sub-cells, bit x + 4y + 16z.
+ *   fec_debug_subcell_tables: certain[64*s + a] / reach[64*s + a] (27*64 host uint64 each)
+ *     = masks of the sub-cells b of the neighbour cell at slot s (offset (s%3-1, s/3%3-1,
+ *     s/9-1)) that are certain-adjacent to / within reach of sub-cell a.  Returns 0.
+ *   fec_debug_subcell_dilate(m): m plus every sub-cell certain-adjacent to one of m's.
+ *   fec_debug_subcell_components(occ, comps): splits occ into certain-connected components
+ *     (comps: 8 host uint64); returns their number, or -1 if more than 8 (never). */
+int32_t fec_debug_subcell_tables(unsigned long long* certain, unsigned long long* reach);
+unsigned long long fec_debug_subcell_dilate(unsigned long long m);
+int32_t fec_debug_subcell_components(unsigned long long occ, unsigned long long* comps);
+
 #ifdef __cplusplus
 }
 #endif

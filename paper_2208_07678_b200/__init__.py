@@ -29,7 +29,8 @@ EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspac
            "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
-           "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap")
+           "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap",
+           "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components")
 
 
 class FecStats(ctypes.Structure):
@@ -85,6 +86,13 @@ def lib():
         L.fec_last_error.argtypes = []
         L.fec_version.restype = ctypes.c_char_p
         L.fec_version.argtypes = []
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        L.fec_debug_subcell_tables.restype = ctypes.c_int32
+        L.fec_debug_subcell_tables.argtypes = [u64p, u64p]
+        L.fec_debug_subcell_dilate.restype = ctypes.c_uint64
+        L.fec_debug_subcell_dilate.argtypes = [ctypes.c_uint64]
+        L.fec_debug_subcell_components.restype = ctypes.c_int32
+        L.fec_debug_subcell_components.argtypes = [ctypes.c_uint64, u64p]
         L.fec_set_item_cap.restype = None
         L.fec_set_item_cap.argtypes = [i64]
         L.fec_set_grid_mode.restype = None
@@ -291,3 +299,22 @@ def slab_merge(all_records, world: int, rank: int, min_size: int, max_size: int,
                                 _ptr(labels_owned), workspace.data_ptr(), workspace.numel(), ctypes.byref(state),
                                 st.cuda_stream))
     return labels_owned
+
+
+def subcell_tables():
+    """(certain, reach) uint64 arrays [27, 64] of the dense path's sub-cell relations (host)."""
+    c = np.zeros(27 * 64, np.uint64)
+    r = np.zeros(27 * 64, np.uint64)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib().fec_debug_subcell_tables(c.ctypes.data_as(u64p), r.ctypes.data_as(u64p))
+    return c.reshape(27, 64), r.reshape(27, 64)
+
+
+def subcell_dilate(m: int) -> int:
+    return int(lib().fec_debug_subcell_dilate(int(m)))
+
+
+def subcell_components(occ: int):
+    out = np.zeros(8, np.uint64)
+    k = lib().fec_debug_subcell_components(int(occ), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return [int(x) for x in out[:k]] if k >= 0 else None

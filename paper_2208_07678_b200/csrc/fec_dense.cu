@@ -886,3 +886,24 @@ cudaError_t ensure_subcell_tables() {
 }
 
 }  // namespace fec
+
+// ---- host-side diagnostics of the sub-cell relations (C ABI: fec_debug_subcell_*) -------------
+extern "C" int32_t fec_debug_subcell_tables(unsigned long long* certain, unsigned long long* reach) {
+    static fec::SubcellTables t;
+    fec::sc_build_tables(t);
+    for (int s = 0; s < 27; ++s)
+        for (int a = 0; a < 64; ++a) {
+            certain[64 * s + a] = t.T[s][a];
+            reach[64 * s + a] = t.U[s][a];
+        }
+    return 0;
+}
+
+extern "C" unsigned long long fec_debug_subcell_dilate(unsigned long long m) { return fec::sc_dilate(m) | m; }
+
+extern "C" int32_t fec_debug_subcell_components(unsigned long long occ, unsigned long long* comps) {
+    fec::u64s c[fec::kMaxComp], rest;
+    const int k = fec::sc_components(occ, c, rest);
+    for (int i = 0; i < k; ++i) comps[i] = c[i];
+    return rest ? -1 : k;
+}
