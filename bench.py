@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="also verify the labels bit-exactly (untimed)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even at N=1 (testing)")
+    ap.add_argument("--grid-mode", default="auto", choices=["auto", "hashed"], help="testing: force the hashed mode")
     return ap.parse_args()
 
 
@@ -397,6 +398,7 @@ def main():
     import paper_2208_07678_b200 as fec
 
     fec.lib()
+    fec.set_grid_mode(1 if args.grid_mode == "hashed" else 0)
     d_th, mn, mx = synth.CONFIGS[args.config]
     w = synth.make_config(args.config, scale=args.scale)
     n = w.n

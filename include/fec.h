@@ -108,8 +108,11 @@ fec_status_t fec_get_stats(fec_stats_t* out);
 void fec_set_instrumentation(int enable);
 
 /* Grid-mode override for testing (thread-local): 0 = automatic (dense cell grid whenever
- * the bbox holds <= 4n + 2^22 cells, else Morton radix sort + hashed cells), 1 = hashed
- * mode always.  Both modes compute identical labels. */
+ * the bbox holds <= 32n + 2^26 cells, else Morton radix sort + hashed cells; in the dense
+ * grid, a counting sort for spatially coherent input order and a radix sort of the cell
+ * keys otherwise), 1 = hashed mode always, 2 = dense grid with the key sort, 3 = dense grid
+ * with the counting sort (when the bbox allows the dense grid).  All modes compute
+ * identical labels. */
 void fec_set_grid_mode(int mode);
 
 /* Test hook (thread-local): cap the queue of "uncertain" dense component pairs (DESIGN.md

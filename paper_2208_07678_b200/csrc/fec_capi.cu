@@ -123,6 +123,9 @@ struct Layout {
     u64* dcoord;        // per dense record: cell coordinates, 21 bits each
     uint32_t* oflag;    // per dense record: slots whose pairs overflowed the queue
     u64* cmask;         // per dense record: 8 component masks
+    uint32_t *skey0, *skey1;  // key-sort path: linear cell keys (double buffer)
+    int *sval0, *sval1;       // key-sort path: input indices (double buffer)
+    uint32_t* scounts;        // key-sort path: digit counts per tile
     int4* items;        // queued component pairs (not certain, possibly within reach)
     int4* items2;       // those still apart after all certain unions
     int item_cap;
@@ -168,13 +171,19 @@ Layout carve(char* base, int64_t n) {
     L.clin = b.take<uint32_t>(n);
     L.cstart = b.take<uint32_t>(n + 1);
     L.crec = b.take<int>(n);
-    L.dscan = b.take<uint32_t>(scan_scratch_elems(std::max<int64_t>(W + 2, n + 1)));
+    L.dscan = b.take<uint32_t>(
+        scan_scratch_elems(std::max<int64_t>(std::max<int64_t>(W + 2, n + 1), 256 * ((n + RS_TILE - 1) / RS_TILE))));
     L.slot = b.take<uint32_t>(n);
     L.sidx = b.take<int>(n);
     L.dlist = b.take<int>(dense_max(n));
     L.dbits = b.take<uint32_t>(n / 32 + 2);
     L.dwpos = b.take<uint32_t>(n / 32 + 2);
     L.cocc = b.take<u64>(n);
+    L.skey0 = b.take<uint32_t>(n);
+    L.skey1 = b.take<uint32_t>(n);
+    L.sval0 = b.take<int>(n);
+    L.sval1 = b.take<int>(n);
+    L.scounts = b.take<uint32_t>((size_t)256 * ((n + RS_TILE - 1) / RS_TILE));
     L.ccoord = b.take<u64>(n);
     L.ncomp = b.take<int>(dense_max(n));
     L.dcoord = b.take<u64>(dense_max(n));
@@ -247,7 +256,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     FEC_CUDA(cudaMemsetAsync(L.meta, 0, sizeof(Meta), st));
     const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
     const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
-    k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite);
+    const float near = (float)(2.0 * (double)d * (1.0 + std::ldexp(1.0, -16)));
+    k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite, near, &L.meta->near_pairs);
     k_bbox_final<<<1, 256, 0, st>>>(L.part, (int)bb_blocks, L.meta);
     launches += 2;
     FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
@@ -288,6 +298,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const unsigned ew4 = grid_for((n + 3) / 4, 256, cap * 4);  // kernels taking 4 points per thread
     const int* val = nullptr;
     DenseCtx dctx{};
+    bool key_sort = false;
 
     if (g.dense) {
         FEC_CUDA(ensure_subcell_tables());
@@ -302,25 +313,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         g.stride[perm[2]] = (uint32_t)g.dims[perm[0]] * (uint32_t)g.dims[perm[1]];
         g.sdiv[0] = g.stride[perm[2]];
         g.sdiv[1] = g.stride[perm[1]];
-        // a2: occupancy bitmap -> compact cell ids; counts per cell; dense cells get records
-        // and octant-ordered slots
-        mark(1, st);
-        const int64_t W = (cells_total + 31) / 32;
-        FEC_CUDA(cudaMemsetAsync(L.cw, 0, (size_t)(W + 1) * sizeof(uint2), st));
-        k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
-        const unsigned cwb = grid_for(W + 1, 256, cap * 4);
-        k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
-        launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
-        k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc, L.ccoord,
-                                                                       g, L.meta);
-        const int64_t dwords = n / 32 + 1;
-        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(dwords + 1) * 4, st));
-        k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
-        const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
-        k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
-        launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
-        k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
-        // dense cells: certain-connected components of the fine occupancy (component nodes)
+        // dense cells get certain-connected components of their fine occupancy (component nodes)
         dctx.spts = L.spts;
         dctx.cstart = L.cstart;
         dctx.dlist = L.dlist;
@@ -331,14 +324,70 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
         dctx.nbase = (int)n;
         dctx.meta = L.meta;
-        k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
-                                                                  L.dcoord, L.oflag, dctx);
-        launches += 2;
-        // a3: counting sort = scan (over the occupied cells only) + scatter
-        mark(2, st);
-        launches += exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
-        k_dscatter<<<ew4, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.spts);
-        ++launches;
+        const int64_t W = (cells_total + 31) / 32;
+        const unsigned cwb = grid_for(W + 1, 256, cap * 4);
+        const int64_t dwords = n / 32 + 1;
+        const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
+        // input order: spatially coherent (LiDAR scan order) -> counting sort; shuffled -> key sort
+        const double pairs = 3.0 * (double)(n / 4);
+        key_sort = g_grid_mode == 2 || (g_grid_mode != 3 && !(vec4 && (double)hm.near_pairs >= 0.5 * pairs));
+        FEC_CUDA(cudaMemsetAsync(L.cw, 0, (size_t)(W + 1) * sizeof(uint2), st));
+        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(dwords + 1) * 4, st));
+        if (!key_sort) {
+            // a2: occupancy bitmap -> compact cell ids; counts per cell -> slots, fine occupancy
+            mark(1, st);
+            k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
+            k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
+            launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
+            k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
+                                                                           L.ccoord, g, L.meta);
+            k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
+            k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
+            launches += 3 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
+            k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+            k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
+                                                                      L.dcoord, L.oflag, dctx);
+            launches += 2;
+            // a3: counting sort = scan (over the occupied cells only) + scatter
+            mark(2, st);
+            launches += exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
+            k_dscatter<<<ew4, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.spts);
+            ++launches;
+        } else {
+            // a2: linear cell keys, LSD radix sort over their significant bits
+            mark(1, st);
+            uint32_t* kin = reinterpret_cast<uint32_t*>(L.skey0);
+            uint32_t* kout = reinterpret_cast<uint32_t*>(L.skey1);
+            int *vin = L.sval0, *vout = L.sval1;
+            k_lkey<<<ew4, 256, 0, st>>>(pts, n, g, kin, vin);
+            ++launches;
+            const int lbits = std::max(1, ceil_log2(cells_total));
+            passes = (lbits + 7) / 8;
+            const int tiles = (int)((n + RS_TILE - 1) / RS_TILE);
+            for (int pp = 0; pp < passes; ++pp) {
+                k_radix_hist32<<<tiles, RS_THREADS, 0, st>>>(kin, n, 8 * pp, L.scounts, tiles);
+                launches += exclusive_scan<uint32_t>(L.scounts, L.scounts, (int64_t)256 * tiles, L.dscan, st);
+                k_radix_scatter32<<<tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
+                launches += 2;
+                std::swap(kin, kout);
+                std::swap(vin, vout);
+            }
+            // a3: cells = runs of equal keys -> compact ids, starts, fine occupancy; gather points
+            mark(2, st);
+            k_smark<<<ew, 256, 0, st>>>(kin, n, L.cw);
+            k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
+            launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
+            k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
+                                                                           L.ccoord, g, L.meta);
+            k_sgather<<<ew, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.meta);
+            k_scount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.meta);
+            k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
+            launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
+            k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+            k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
+                                                                      L.dcoord, L.oflag, dctx);
+            launches += 2;
+        }
         // a4: sorted-order init (parents: self, or the point's component node)
         mark(3, st);
         k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,

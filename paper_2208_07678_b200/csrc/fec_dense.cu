@@ -264,6 +264,99 @@ __global__ void __launch_bounds__(kBinThreads) k_dcount(const float* __restrict_
     }
 }
 
+// ---- a2/a3, sort path (shuffled inputs) ----------------------------------------------------
+// For inputs without spatial coherence (C1, C5) the counting sort's per-point atomics and
+// scatter hit random DRAM sectors; instead the linear cell ids are radix-sorted (coalesced
+// digit passes), cells are the runs of equal keys, and points are gathered into cell order.
+__global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64_t n, Grid g, uint32_t* __restrict__ key,
+                                             int* __restrict__ val) {
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b4 = 4 * gi;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
+        uint32_t k[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int q;
+            dense_cell_of(P.x[j], P.y[j], P.z[j], g, k[j], q);
+        }
+        if (b4 + 4 <= n) {
+            *reinterpret_cast<uint4*>(key + b4) = make_uint4(k[0], k[1], k[2], k[3]);
+            *reinterpret_cast<int4*>(val + b4) = make_int4((int)b4, (int)b4 + 1, (int)b4 + 2, (int)b4 + 3);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (b4 + j < n) {
+                    key[b4 + j] = k[j];
+                    val[b4 + j] = (int)(b4 + j);
+                }
+        }
+    }
+}
+
+// Occupancy bits of the sorted keys' distinct values (heads only; a warp's heads share words).
+__global__ void __launch_bounds__(256) k_smark(const uint32_t* __restrict__ key, int64_t n, uint2* __restrict__ cw) {
+    const int64_t nr = (n + 31) & ~int64_t(31);
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = s < n;
+        const uint32_t k = ok ? __ldg(key + s) : 0u;
+        const bool head = ok && (s == 0 || __ldg(key + s - 1) != k);
+        const uint32_t w = head ? (k >> 5) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, w);
+        const uint32_t bits = __reduce_or_sync(peers, head ? (1u << (k & 31u)) : 0u);
+        if (head && (threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(reinterpret_cast<unsigned int*>(cw + w), bits);
+    }
+}
+
+// Points into cell order (random 12-byte gathers, coalesced float4 stores), cell starts at
+// the run heads, fine occupancy OR-ed per run (segmented within the warp, one atomic per run
+// piece).
+__global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, const uint32_t* __restrict__ key,
+                                                const int* __restrict__ val, int64_t n, Grid g,
+                                                const uint2* __restrict__ cw, float4* __restrict__ spts,
+                                                uint32_t* __restrict__ cstart, u64* __restrict__ cocc,
+                                                const Meta* __restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nr = (n + 31) & ~int64_t(31);
+    if (blockIdx.x == 0 && threadIdx.x == 0) cstart[meta->cells] = (uint32_t)n;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = s < n;
+        uint32_t cid = 0xffffffffu;
+        u64 bit = 0;
+        if (ok) {
+            const uint32_t k = __ldg(key + s);
+            const int i = __ldg(val + s);
+            const float x = __ldg(p + 3 * (int64_t)i), y = __ldg(p + 3 * (int64_t)i + 1), z = __ldg(p + 3 * (int64_t)i + 2);
+            uint32_t lin;
+            int q;
+            dense_cell_of(x, y, z, g, lin, q);
+            cid = cid_of(cw, k);
+            bit = 1ull << q;
+            spts[s] = make_float4(x, y, z, __int_as_float(i));
+            if (s == 0 || __ldg(key + s - 1) != k) cstart[cid] = (uint32_t)s;
+        }
+        // equal cids are contiguous: inclusive segmented OR, the last lane of a run publishes
+        const unsigned peers = __match_any_sync(0xffffffffu, cid);
+        const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit), hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+        if (ok && lane == 31 - __clz(peers)) atomicOr(cocc + cid, ((u64)hi << 32) | lo);
+    }
+}
+
+// Dense bits of the occupied cells from the run lengths (lanes = consecutive compact ids,
+// so a warp fills one bitmap word with a plain store).
+__global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
+                                               const Meta* __restrict__ meta) {
+    const int64_t U = meta->cells;
+    const int64_t ur = (U + 31) & ~int64_t(31);
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
+        const bool dense = u < U && __ldg(cstart + u + 1) - __ldg(cstart + u) > (uint32_t)SPARSE_MAX;
+        const unsigned m = __ballot_sync(0xffffffffu, dense);
+        if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
+    }
+}
+
 // ---- dense records: compact ids of the dense cells in ascending order -----------------------
 __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
                                                    uint32_t* __restrict__ wcount) {

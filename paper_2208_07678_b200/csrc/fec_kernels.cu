@@ -18,10 +18,14 @@ __device__ __forceinline__ void bb_acc(float v, float& mn, float& mx, int& bad) 
     mx = fmaxf(mx, v);
 }
 
+// Also counts consecutive input pairs (i, i+1) within `near` on every axis (spatial coherence
+// of the input order: decides between the counting sort and the key sort).
 __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ p, int64_t n, int vec4,
-                                                     float* __restrict__ part, int* __restrict__ nonfinite) {
+                                                     float* __restrict__ part, int* __restrict__ nonfinite,
+                                                     float near, unsigned long long* __restrict__ near_pairs) {
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     int bad = 0;
+    unsigned nearc = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t tail_start = 0;
@@ -34,6 +38,10 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ 
             float v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
             for (int k = 0; k < 12; ++k) bb_acc(v[k], mn[k % 3], mx[k % 3], bad);
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                nearc += fabsf(v[3 * j + 3] - v[3 * j]) <= near && fabsf(v[3 * j + 4] - v[3 * j + 1]) <= near &&
+                         fabsf(v[3 * j + 5] - v[3 * j + 2]) <= near;
         }
         tail_start = nq << 2;
     }
@@ -49,6 +57,8 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ 
         }
     }
     bad = __any_sync(0xffffffffu, bad);
+    for (int o = 16; o > 0; o >>= 1) nearc += __shfl_xor_sync(0xffffffffu, nearc, o);
+    if ((threadIdx.x & 31) == 0 && nearc) atomicAdd(near_pairs, (unsigned long long)nearc);
     __shared__ float s[8][6];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) {
@@ -114,8 +124,9 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ p, int64
 // =====================================================================================
 // a3  K2: LSD radix sort, 8-bit digits, stable (reduce-then-scan per pass)
 // =====================================================================================
-__global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const u64* __restrict__ key, int64_t n, int shift,
-                                                          uint32_t* __restrict__ counts, int num_tiles) {
+template <typename K>
+__device__ __forceinline__ void radix_hist(const K* __restrict__ key, int64_t n, int shift, uint32_t* __restrict__ counts,
+                                           int num_tiles) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -133,10 +144,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const u64* __restrict
 // `it` covers 32 consecutive keys, so (warp, it, lane) order equals input order.  Ranks:
 // (digit offset of this tile) + (same-digit keys in earlier warps) + (in earlier
 // iterations of this warp) + (in lower lanes of this iteration).
-__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restrict__ kin, const int* __restrict__ vin,
-                                                             u64* __restrict__ kout, int* __restrict__ vout,
-                                                             int64_t n, int shift, const uint32_t* __restrict__ offs,
-                                                             int num_tiles) {
+template <typename K>
+__device__ __forceinline__ void radix_scatter(const K* __restrict__ kin, const int* __restrict__ vin,
+                                              K* __restrict__ kout, int* __restrict__ vout, int64_t n, int shift,
+                                              const uint32_t* __restrict__ offs, int num_tiles) {
     __shared__ uint32_t wcnt[RS_THREADS / kWarp][256];
     __shared__ uint32_t goff[256];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restr
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * (RS_ITEMS * kWarp);
     const unsigned lt = (1u << lane) - 1u;
-    u64 k[RS_ITEMS];
+    K k[RS_ITEMS];
     int v[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
     int dig[RS_ITEMS];
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restr
     for (int it = 0; it < RS_ITEMS; ++it) {
         int64_t i = base + it * kWarp + lane;
         bool ok = i < n;
-        k[it] = ok ? kin[i] : 0ull;
+        k[it] = ok ? kin[i] : K(0);
         v[it] = ok ? vin[i] : 0;
         dig[it] = ok ? (int)((unsigned)(k[it] >> shift) & 255u) : 256;
     }
@@ -188,6 +199,28 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restr
             vout[pos] = v[it];
         }
     }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const u64* __restrict__ key, int64_t n, int shift,
+                                                          uint32_t* __restrict__ counts, int num_tiles) {
+    radix_hist<u64>(key, n, shift, counts, num_tiles);
+}
+__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restrict__ kin, const int* __restrict__ vin,
+                                                             u64* __restrict__ kout, int* __restrict__ vout,
+                                                             int64_t n, int shift, const uint32_t* __restrict__ offs,
+                                                             int num_tiles) {
+    radix_scatter<u64>(kin, vin, kout, vout, n, shift, offs, num_tiles);
+}
+// 32-bit keys (linear cell ids of the dense grid's sort path)
+__global__ void __launch_bounds__(RS_THREADS) k_radix_hist32(const uint32_t* __restrict__ key, int64_t n, int shift,
+                                                            uint32_t* __restrict__ counts, int num_tiles) {
+    radix_hist<uint32_t>(key, n, shift, counts, num_tiles);
+}
+__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32(const uint32_t* __restrict__ kin,
+                                                               const int* __restrict__ vin, uint32_t* __restrict__ kout,
+                                                               int* __restrict__ vout, int64_t n, int shift,
+                                                               const uint32_t* __restrict__ offs, int num_tiles) {
+    radix_scatter<uint32_t>(kin, vin, kout, vout, n, shift, offs, num_tiles);
 }
 
 // =====================================================================================

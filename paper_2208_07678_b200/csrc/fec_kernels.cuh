@@ -30,6 +30,7 @@ struct Meta {
     int nitems;                       // dense-grid mode: uncertain component pairs pushed
     int internal_error;               // != 0: an internal invariant failed (never expected)
     int nitems2;                      // dense-grid mode: queued pairs still apart after the certain unions
+    unsigned long long near_pairs;    // a1: consecutive input pairs within 2 cells (input coherence)
 };
 
 struct Tables {
@@ -43,12 +44,16 @@ struct Tables {
 };
 
 
-__global__ void k_bbox_partial(const float* p, int64_t n, int vec4, float* part, int* nonfinite);
+__global__ void k_bbox_partial(const float* p, int64_t n, int vec4, float* part, int* nonfinite, float near,
+                               unsigned long long* near_pairs);
 __global__ void k_bbox_final(const float* part, int nblocks, Meta* meta);
 __global__ void k_keys(const float* p, int64_t n, Grid g, u64* key, int* val);
 __global__ void k_radix_hist(const u64* key, int64_t n, int shift, uint32_t* counts, int num_tiles);
 __global__ void k_radix_scatter(const u64* kin, const int* vin, u64* kout, int* vout, int64_t n, int shift,
                                 const uint32_t* offs, int num_tiles);
+__global__ void k_radix_hist32(const uint32_t* key, int64_t n, int shift, uint32_t* counts, int num_tiles);
+__global__ void k_radix_scatter32(const uint32_t* kin, const int* vin, uint32_t* kout, int* vout, int64_t n, int shift,
+                                  const uint32_t* offs, int num_tiles);
 __global__ void k_gather(const float* p, const int* val, int64_t n, float4* spts);
 __global__ void k_heads(const u64* key, int64_t n, u64* flags);
 __global__ void k_fill_tables(const u64* key, const u64* ex, int64_t n, Grid g, Tables T, Meta* meta);
@@ -66,6 +71,11 @@ __global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t
                         u64* ccoord, Grid g, Meta* meta);
 __global__ void k_dcount(const float* p, int64_t n, Grid g, const uint2* cw, uint32_t* count, uint32_t* slot,
                          uint32_t* dbits, u64* cocc);
+__global__ void k_lkey(const float* p, int64_t n, Grid g, uint32_t* key, int* val);
+__global__ void k_smark(const uint32_t* key, int64_t n, uint2* cw);
+__global__ void k_sgather(const float* p, const uint32_t* key, const int* val, int64_t n, Grid g, const uint2* cw,
+                          float4* spts, uint32_t* cstart, u64* cocc, const Meta* meta);
+__global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* meta);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
                              Meta* meta);

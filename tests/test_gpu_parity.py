@@ -49,7 +49,7 @@ def test_golden_examples_gpu(fec):
         assert_same(got, np.array(c["labels"], np.int32), c["name"])
 
 
-@pytest.fixture(params=[0, 1], ids=["auto", "hashed"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "hashed", "keysort", "countsort"])
 def mode(fec, request):
     fec.set_grid_mode(request.param)
     yield request.param
