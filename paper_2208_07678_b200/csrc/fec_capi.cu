@@ -339,7 +339,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
             k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
             launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
-            k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
+            k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
                                                                            L.ccoord, g, L.meta);
             k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
             k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
@@ -367,7 +367,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             for (int pp = 0; pp < passes; ++pp) {
                 k_radix_hist32<<<tiles, RS_THREADS, 0, st>>>(kin, n, 8 * pp, L.scounts, tiles);
                 launches += exclusive_scan<uint32_t>(L.scounts, L.scounts, (int64_t)256 * tiles, L.dscan, st);
-                k_radix_scatter32<<<tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
+                k_radix_scatter32l<<<tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
                 launches += 2;
                 std::swap(kin, kout);
                 std::swap(vin, vout);
@@ -377,9 +377,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             k_smark<<<ew, 256, 0, st>>>(kin, n, L.cw);
             k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
             launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
-            k_clist<<<grid_for((W + 4) / 4, 256, cap * 4), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
+            k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
                                                                            L.ccoord, g, L.meta);
-            k_sgather<<<ew, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.meta);
+            k_sgather<<<ew4, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.meta);
             k_scount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.meta);
             k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
             launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
@@ -526,9 +526,10 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
     k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
     mark(9, st);
+    k_rootlab<<<ew, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
     k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
-        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels);
-    C.launches += 4;
+        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta);
+    C.launches += 5;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
     return finish_stats(C, n, st);

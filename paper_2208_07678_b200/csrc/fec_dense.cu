@@ -71,6 +71,25 @@ __device__ __forceinline__ void load_pts4(const float* __restrict__ p, int64_t n
     }
 }
 
+// One gathered point (random index): the 16-byte aligned word(s) covering its 12 bytes,
+// so each point costs one (rarely two) memory transactions instead of three loads.
+__device__ __forceinline__ void load_point(const float* __restrict__ p, int64_t i, float& x, float& y, float& z) {
+    const int64_t f = 3 * i;  // first float
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        const float4* q = reinterpret_cast<const float4*>(p) + (f >> 2);
+        const float4 a = __ldg(q);
+        switch (f & 3) {
+            case 0: x = a.x; y = a.y; z = a.z; return;
+            case 1: x = a.y; y = a.z; z = a.w; return;
+            case 2: { const float4 b = __ldg(q + 1); x = a.z; y = a.w; z = b.x; return; }
+            default: { const float4 b = __ldg(q + 1); x = a.w; y = b.x; z = b.y; return; }
+        }
+    }
+    x = __ldg(p + f);
+    y = __ldg(p + f + 1);
+    z = __ldg(p + f + 2);
+}
+
 // ---- compact cell ids ---------------------------------------------------------------------
 // Only occupied cells get storage: an occupancy bitmap over the linear cell ids, each 32-bit
 // word paired with the number of occupied cells before it (uint2 {bits, base}), gives the
@@ -146,52 +165,42 @@ __global__ void __launch_bounds__(256) k_cpopc(const uint2* __restrict__ cw, int
 }
 
 // Word bases, compact-id -> linear cell list (ascending), zeroed per-cell counts, U.
-// Four words per thread, loaded with vector loads before any dependent work.
+// Warp per 8 bitmap words (lanes 0-7 load them), then lane per cell of each nonzero word:
+// consecutive occupied cells are written by consecutive lanes (coalesced stores even when
+// most cells are occupied) and runs of empty words cost one load per lane.
 __global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t words, const uint32_t* __restrict__ wpos,
                                               uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
                                               u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
                                               Meta* __restrict__ meta) {
-    const int64_t groups = (words + 4) / 4;  // words + 1 entries of wpos (the last holds U)
-    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t w0 = 4 * gi;
-        uint32_t r0[4], bw[4];
-        if (w0 + 4 <= words) {
-            const uint4 pv = __ldg(reinterpret_cast<const uint4*>(wpos + w0));
-            const uint4 c01 = *reinterpret_cast<const uint4*>(cw + w0);
-            const uint4 c23 = *reinterpret_cast<const uint4*>(cw + w0 + 2);
-            r0[0] = pv.x; r0[1] = pv.y; r0[2] = pv.z; r0[3] = pv.w;
-            bw[0] = c01.x; bw[1] = c01.z; bw[2] = c23.x; bw[3] = c23.z;
-            *reinterpret_cast<uint4*>(cw + w0) = make_uint4(bw[0], r0[0], bw[1], r0[1]);
-            *reinterpret_cast<uint4*>(cw + w0 + 2) = make_uint4(bw[2], r0[2], bw[3], r0[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int64_t w = w0 + j;
-                r0[j] = w <= words ? __ldg(wpos + w) : 0u;
-                bw[j] = w < words ? cw[w].x : 0u;
-                if (w < words) cw[w].y = r0[j];
-                if (w == words) {
-                    meta->cells = (int)r0[j];
-                    meta->cells1 = (int)r0[j] + 1;
-                    count[r0[j]] = 0u;
-                }
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w0 = 8 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w0 <= words; w0 += 8 * nw) {
+        uint32_t mybits = 0, myr0 = 0;
+        if (lane < 8 && w0 + lane <= words) {
+            myr0 = __ldg(wpos + w0 + lane);
+            if (w0 + lane < words) {
+                mybits = cw[w0 + lane].x;
+                cw[w0 + lane].y = myr0;
+            } else {
+                meta->cells = (int)myr0;
+                meta->cells1 = (int)myr0 + 1;
+                count[myr0] = 0u;
             }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            uint32_t bits = bw[j];
-            uint32_t r = r0[j];
-            while (bits) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const uint32_t lin = (uint32_t)((w0 + j) * 32 + b);
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t bits = __shfl_sync(0xffffffffu, mybits, j);
+            if (!bits) continue;
+            const uint32_t r0 = __shfl_sync(0xffffffffu, myr0, j);
+            if ((bits >> lane) & 1u) {
+                const uint32_t r = r0 + (uint32_t)__popc(bits & ((1u << lane) - 1u));
+                const uint32_t lin = (uint32_t)((w0 + j) * 32 + lane);
                 int cc[3];
                 dense_decode(lin, g, cc);
                 clin[r] = lin;
                 ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
                 count[r] = 0u;
                 cocc[r] = 0ull;
-                ++r;
             }
         }
     }
@@ -319,28 +328,48 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
                                                 uint32_t* __restrict__ cstart, u64* __restrict__ cocc,
                                                 const Meta* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
-    const int64_t nr = (n + 31) & ~int64_t(31);
     if (blockIdx.x == 0 && threadIdx.x == 0) cstart[meta->cells] = (uint32_t)n;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += (int64_t)gridDim.x * blockDim.x) {
-        const bool ok = s < n;
-        uint32_t cid = 0xffffffffu;
-        u64 bit = 0;
-        if (ok) {
-            const uint32_t k = __ldg(key + s);
-            const int i = __ldg(val + s);
-            const float x = __ldg(p + 3 * (int64_t)i), y = __ldg(p + 3 * (int64_t)i + 1), z = __ldg(p + 3 * (int64_t)i + 2);
-            uint32_t lin;
-            int q;
-            dense_cell_of(x, y, z, g, lin, q);
-            cid = cid_of(cw, k);
-            bit = 1ull << q;
-            spts[s] = make_float4(x, y, z, __int_as_float(i));
-            if (s == 0 || __ldg(key + s - 1) != k) cstart[cid] = (uint32_t)s;
+    // round j: positions s0 + j*256 + threadIdx.x (a warp holds 32 consecutive positions, so
+    // the run reduction below works per round); the 4 rounds' gathers are issued together
+    const int64_t per = 4 * (int64_t)blockDim.x;
+    for (int64_t s0 = (int64_t)blockIdx.x * per; s0 < n; s0 += (int64_t)gridDim.x * per) {
+        uint32_t k[4];
+        int vi[4];
+        float x[4], y[4], z[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t s = s0 + j * (int64_t)blockDim.x + threadIdx.x;
+            k[j] = s < n ? __ldg(key + s) : 0xffffffffu;
+            vi[j] = s < n ? __ldg(val + s) : 0;
         }
-        // equal cids are contiguous: inclusive segmented OR, the last lane of a run publishes
-        const unsigned peers = __match_any_sync(0xffffffffu, cid);
-        const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit), hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
-        if (ok && lane == 31 - __clz(peers)) atomicOr(cocc + cid, ((u64)hi << 32) | lo);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            x[j] = y[j] = z[j] = 0.f;
+            if (k[j] != 0xffffffffu) load_point(p, vi[j], x[j], y[j], z[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t s = s0 + j * (int64_t)blockDim.x + threadIdx.x;
+            const bool ok = s < n;
+            uint32_t cid = 0xffffffffu;
+            u64 bit = 0;
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, k[j], 1);  // all lanes take part
+            if (ok) {
+                uint32_t lin;
+                int q;
+                dense_cell_of(x[j], y[j], z[j], g, lin, q);
+                cid = cid_of(cw, k[j]);
+                bit = 1ull << q;
+                spts[s] = make_float4(x[j], y[j], z[j], __int_as_float(vi[j]));
+                const bool head = s == 0 || (lane > 0 ? prev != k[j] : __ldg(key + s - 1) != k[j]);
+                if (head) cstart[cid] = (uint32_t)s;
+            }
+            // equal cids are contiguous: the last lane of each run publishes the run's OR
+            const unsigned peers = __match_any_sync(0xffffffffu, cid);
+            const uint32_t lo = __reduce_or_sync(peers, (uint32_t)bit);
+            const uint32_t hi = __reduce_or_sync(peers, (uint32_t)(bit >> 32));
+            if (ok && lane == 31 - __clz(peers)) atomicOr(cocc + cid, ((u64)hi << 32) | lo);
+        }
     }
 }
 

@@ -211,7 +211,97 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restr
                                                              int num_tiles) {
     radix_scatter<u64>(kin, vin, kout, vout, n, shift, offs, num_tiles);
 }
-// 32-bit keys (linear cell ids of the dense grid's sort path)
+// 32-bit keys (linear cell ids of the dense grid's key-sort path).  The scatter first sorts
+// the tile by digit in shared memory, then writes each digit's run with consecutive threads
+// (coalesced stores instead of one scattered 4-byte store per key and value).
+__global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32l(const uint32_t* __restrict__ kin,
+                                                                const int* __restrict__ vin,
+                                                                uint32_t* __restrict__ kout, int* __restrict__ vout,
+                                                                int64_t n, int shift, const uint32_t* __restrict__ offs,
+                                                                int num_tiles) {
+    __shared__ uint32_t wcnt[RS_THREADS / kWarp][256];
+    __shared__ uint32_t goff[256], tstart[256];
+    __shared__ uint32_t sk[RS_TILE];
+    __shared__ int sv[RS_TILE];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < (RS_THREADS / kWarp) * 256; d += RS_THREADS) (&wcnt[0][0])[d] = 0;
+    goff[threadIdx.x] = offs[(int64_t)threadIdx.x * num_tiles + blockIdx.x];
+    __syncthreads();
+    const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
+    const int64_t base = tbase + (int64_t)w * (RS_ITEMS * kWarp);
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t k[RS_ITEMS];
+    int v[RS_ITEMS];
+    uint32_t rank[RS_ITEMS];
+    int dig[RS_ITEMS];
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        int64_t i = base + it * kWarp + lane;
+        bool ok = i < n;
+        k[it] = ok ? kin[i] : 0u;
+        v[it] = ok ? vin[i] : 0;
+        dig[it] = ok ? (int)((k[it] >> shift) & 255u) : 256;
+    }
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        const int d = dig[it];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t c = d < 256 ? wcnt[w][d] : 0u;
+        __syncwarp();
+        rank[it] = c + __popc(peers & lt);
+        if (d < 256 && (peers & lt) == 0u) wcnt[w][d] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        // per digit: exclusive offsets of the warps, and the tile's digit total
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_THREADS / kWarp; ++ww) {
+            uint32_t t = wcnt[ww][d];
+            wcnt[ww][d] = run;
+            run += t;
+        }
+        tstart[d] = run;  // digit total for now
+    }
+    __syncthreads();
+    // exclusive scan of the 256 digit totals (one warp)
+    if (w == 0) {
+        uint32_t a[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { a[j] = tstart[8 * lane + j]; sum += a[j]; }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t run = x - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { tstart[8 * lane + j] = run; run += a[j]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; ++it) {
+        const int d = dig[it];
+        if (d < 256) {
+            const uint32_t lp = tstart[d] + wcnt[w][d] + rank[it];
+            sk[lp] = k[it];
+            sv[lp] = v[it];
+        }
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)RS_TILE, n - tbase);
+    for (int lp = threadIdx.x; lp < cnt; lp += RS_THREADS) {
+        const uint32_t key = sk[lp];
+        const int d = (int)((key >> shift) & 255u);
+        const uint32_t pos = goff[d] + ((uint32_t)lp - tstart[d]);
+        kout[pos] = key;
+        vout[pos] = sv[lp];
+    }
+}
+
 __global__ void __launch_bounds__(RS_THREADS) k_radix_hist32(const uint32_t* __restrict__ key, int64_t n, int shift,
                                                             uint32_t* __restrict__ counts, int num_tiles) {
     radix_hist<uint32_t>(key, n, shift, counts, num_tiles);
@@ -586,10 +676,25 @@ __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, co
     }
 }
 
+// Sparse-dominated clouds (many components, roots scattered): fold the filter into the roots
+// (minidx[r] = final label) so k_relabel reads one root word per point instead of two.
+__global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent, const int* __restrict__ size,
+                                                int* __restrict__ minidx, int64_t n, long long min_size,
+                                                long long max_size, const Meta* __restrict__ meta) {
+    if (4 * (int64_t)meta->cells <= n) return;
+    const int64_t nodes = n + 8 * (int64_t)meta->ndense;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nodes; r += (int64_t)gridDim.x * blockDim.x) {
+        if (__ldg(parent + r) != (int)r) continue;
+        const long long sz = __ldg(size + r);
+        if (!(sz >= min_size && sz <= max_size)) minidx[r] = -1;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent, const int* __restrict__ val,
                                                 const int* __restrict__ size, const int* __restrict__ minidx,
                                                 int64_t n, long long min_size, long long max_size,
-                                                int* __restrict__ labels) {
+                                                int* __restrict__ labels, const Meta* __restrict__ meta) {
+    const bool folded = 4 * (int64_t)meta->cells > n;  // k_rootlab ran
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sb = 4 * gi;
@@ -609,8 +714,12 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (r[j] < 0) continue;
-            const long long sz = __ldg(size + r[j]);
-            labels[v[j]] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
+            if (folded) {
+                labels[v[j]] = __ldg(minidx + r[j]);
+            } else {
+                const long long sz = __ldg(size + r[j]);
+                labels[v[j]] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
+            }
         }
     }
 }

@@ -54,6 +54,8 @@ __global__ void k_radix_scatter(const u64* kin, const int* vin, u64* kout, int* 
 __global__ void k_radix_hist32(const uint32_t* key, int64_t n, int shift, uint32_t* counts, int num_tiles);
 __global__ void k_radix_scatter32(const uint32_t* kin, const int* vin, uint32_t* kout, int* vout, int64_t n, int shift,
                                   const uint32_t* offs, int num_tiles);
+__global__ void k_radix_scatter32l(const uint32_t* kin, const int* vin, uint32_t* kout, int* vout, int64_t n, int shift,
+                                   const uint32_t* offs, int num_tiles);
 __global__ void k_gather(const float* p, const int* val, int64_t n, float4* spts);
 __global__ void k_heads(const u64* key, int64_t n, u64* flags);
 __global__ void k_fill_tables(const u64* key, const u64* ex, int64_t n, Grid g, Tables T, Meta* meta);
@@ -63,8 +65,10 @@ __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx);
 __global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
 __global__ void k_flat_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
 __global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta, int only_sparse);
+__global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
+                          long long max_size, const Meta* meta);
 __global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
-                          long long min_size, long long max_size, int* labels);
+                          long long min_size, long long max_size, int* labels, const Meta* meta);
 __global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
 __global__ void k_cpopc(const uint2* cw, int64_t words, uint32_t* cnt);
 __global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t* clin, uint32_t* count, u64* cocc,
