@@ -379,7 +379,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
             k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
                                                                            L.ccoord, g, L.meta);
-            k_sgather<<<ew4, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.meta);
+            k_sgather<<<ew4, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.parent, L.sidx,
+                                           L.size, L.minidx, L.meta);
             k_scount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.meta);
             k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
             launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
@@ -388,10 +389,15 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
                                                                       L.dcoord, L.oflag, dctx);
             launches += 2;
         }
-        // a4: sorted-order init (parents: self, or the point's component node)
+        // a4: sorted-order init (parents: self, or the point's component node); the key-sort
+        // path wrote parents/indices in k_sgather and only re-parents points of dense cells
         mark(3, st);
-        k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
-                                     L.size, L.minidx, L.sidx);
+        if (key_sort)
+            k_dparent<<<grid_for(dense_max(n) * 32, 256, cap * 8), 256, 0, st>>>(L.spts, L.cstart, L.dlist, L.ncomp,
+                                                                                L.cmask, g, (int)n, L.parent, L.meta);
+        else
+            k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
+                                         L.size, L.minidx, L.sidx);
         ++launches;
         mark(4, st);
         // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the

@@ -326,6 +326,8 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
                                                 const int* __restrict__ val, int64_t n, Grid g,
                                                 const uint2* __restrict__ cw, float4* __restrict__ spts,
                                                 uint32_t* __restrict__ cstart, u64* __restrict__ cocc,
+                                                int* __restrict__ parent, int* __restrict__ sidx,
+                                                int* __restrict__ size, int* __restrict__ minidx,
                                                 const Meta* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) cstart[meta->cells] = (uint32_t)n;
@@ -361,6 +363,10 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
                 cid = cid_of(cw, k[j]);
                 bit = 1ull << q;
                 spts[s] = make_float4(x[j], y[j], z[j], __int_as_float(vi[j]));
+                sidx[s] = vi[j];
+                parent[s] = (int)s;  // points of dense cells are re-parented by k_dparent
+                size[s] = 0;
+                minidx[s] = 0x7fffffff;
                 const bool head = s == 0 || (lane > 0 ? prev != k[j] : __ldg(key + s - 1) != k[j]);
                 if (head) cstart[cid] = (uint32_t)s;
             }
@@ -610,6 +616,34 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
         }
     }
 }
+
+// Key-sort path: points of dense cells hang under their component nodes (warp per dense
+// record; the cell's points are contiguous).  k_sgather made every point its own parent.
+__global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts, const uint32_t* __restrict__ cstart,
+                                                const int* __restrict__ dlist, const int* __restrict__ ncomp,
+                                                const u64* __restrict__ cmask, Grid g, int nbase,
+                                                int* __restrict__ parent, const Meta* __restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const int nd = meta->ndense;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nd; r += warps) {
+        const int cid = __ldg(dlist + r);
+        const int k = __ldg(ncomp + r);
+        const int a0 = (int)__ldg(cstart + cid), a1 = (int)__ldg(cstart + cid + 1);
+        for (int s = a0 + lane; s < a1; s += 32) {
+            int cc = 0;
+            if (k > 1) {
+                const float4 v = __ldg(spts + s);
+                uint32_t lin;
+                int q;
+                dense_cell_of(v.x, v.y, v.z, g, lin, q);
+                while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
+            }
+            parent[s] = nbase + 8 * r + cc;
+        }
+    }
+}
+
 
 // ---- a6+a7: dense cells — certain unions across cells, uncertain pairs queued -------------
 // Thread per dense record P, looping over the 26 neighbour slots in the same order in every

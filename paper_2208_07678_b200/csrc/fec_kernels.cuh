@@ -78,7 +78,8 @@ __global__ void k_dcount(const float* p, int64_t n, Grid g, const uint2* cw, uin
 __global__ void k_lkey(const float* p, int64_t n, Grid g, uint32_t* key, int* val);
 __global__ void k_smark(const uint32_t* key, int64_t n, uint2* cw);
 __global__ void k_sgather(const float* p, const uint32_t* key, const int* val, int64_t n, Grid g, const uint2* cw,
-                          float4* spts, uint32_t* cstart, u64* cocc, const Meta* meta);
+                          float4* spts, uint32_t* cstart, u64* cocc, int* parent, int* sidx, int* size, int* minidx,
+                          const Meta* meta);
 __global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* meta);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
@@ -104,6 +105,8 @@ __global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint2* cw, c
 __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                         const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* size,
                         int* minidx, int* sidx);
+__global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int* dlist, const int* ncomp,
+                          const u64* cmask, Grid g, int nbase, int* parent, const Meta* meta);
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
                                int* parent, Meta* meta);
 __global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
