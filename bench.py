@@ -169,9 +169,12 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # testing aids (not used by the driver): FEC_DIST_BACKEND=gloo and FEC_FORCE_DEVICE=0 let
+    # several ranks share one GPU to exercise the multi-rank code path end to end
+    local = int(os.environ.get("FEC_FORCE_DEVICE", local))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "fec" else "gloo"
+        backend = os.environ.get("FEC_DIST_BACKEND", "nccl") if args.impl == "fec" else "gloo"
         if args.impl == "fec":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)

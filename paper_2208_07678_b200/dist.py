@@ -122,6 +122,11 @@ def exchange_records(send, world: int, group=None):
     recv = torch.empty(world * send.numel(), dtype=send.dtype, device=send.device)
     if world == 1:
         recv.copy_(send)
+    elif send.is_cuda and dist.get_backend(group) == "gloo":
+        # test plumbing only (several ranks sharing one GPU): gloo gathers host tensors
+        host = torch.empty(world * send.numel(), dtype=send.dtype)
+        dist.all_gather_into_tensor(host, send.cpu(), group=group)
+        recv.copy_(host)
     else:
         dist.all_gather_into_tensor(recv, send, group=group)
     return recv
