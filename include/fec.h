@@ -129,6 +129,23 @@ void fec_set_timing(int enable);
 int32_t fec_get_stage_times(float* ms_out, int32_t max_stages);
 const char* fec_stage_name(int32_t stage);
 
+/* ---- Batched clouds (the paper's per-scan mode, Table 4)
+ *
+ * nclouds independent clouds stored back to back: cloud c is points[offsets[c] ..
+ * offsets[c+1]) (offsets: HOST array of nclouds + 1 int64, offsets[0] = 0, non-decreasing,
+ * empty clouds allowed).  Every cloud is clustered as if by its own fec_cluster call: no edge
+ * joins points of different clouds, sizes are per cloud, and labels_out[i] is the minimum
+ * index INSIDE the point's cloud (0 .. size-1) of its component, or -1.  One pipeline serves
+ * all clouds (each cloud gets its own grid origin and a separate band of cells); if the
+ * stacked grid is too large for the dense mode the clouds are run one after another.
+ * Device pointers as fec_cluster_ws; workspace of fec_batch_workspace_bytes(n_total,
+ * nclouds) bytes.  Errors: as fec_cluster_ws (FEC_ERR_INVALID_ARGUMENT also for bad
+ * offsets). */
+size_t fec_batch_workspace_bytes(int64_t n_total, int32_t nclouds);
+fec_status_t fec_cluster_batch_ws(const float* points, const int64_t* offsets, int32_t nclouds, float d_th,
+                                  int64_t min_size, int64_t max_size, int32_t* labels_out, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ---- Multi-GPU slab path ------------------------------------
  *
  * PAPER.md's FEC is serial (L480 lists a parallel version as future work); the sharding is

@@ -16,7 +16,7 @@ import os
 
 import numpy as np
 
-__all__ = ["cluster", "cluster_host", "slab_local", "slab_merge", "slab_record_words",
+__all__ = ["cluster", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
            "slab_workspace_bytes", "SlabState", "workspace_bytes", "workspace_bytes_host", "stats",
            "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
 
@@ -30,7 +30,8 @@ EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspac
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
            "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap",
-           "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components")
+           "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components",
+           "fec_batch_workspace_bytes", "fec_cluster_batch_ws")
 
 
 class FecStats(ctypes.Structure):
@@ -86,6 +87,10 @@ def lib():
         L.fec_last_error.argtypes = []
         L.fec_version.restype = ctypes.c_char_p
         L.fec_version.argtypes = []
+        L.fec_batch_workspace_bytes.restype = sz
+        L.fec_batch_workspace_bytes.argtypes = [i64, ctypes.c_int32]
+        L.fec_cluster_batch_ws.restype = ctypes.c_int32
+        L.fec_cluster_batch_ws.argtypes = [vp, vp, ctypes.c_int32, f32, i64, i64, vp, vp, sz, vp]
         u64p = ctypes.POINTER(ctypes.c_uint64)
         L.fec_debug_subcell_tables.restype = ctypes.c_int32
         L.fec_debug_subcell_tables.argtypes = [u64p, u64p]
@@ -206,6 +211,36 @@ def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, 
                                   out_ptr if n else None, workspace.data_ptr() if n else None,
                                   workspace.numel() if n else 0, st.cuda_stream))
     del keep
+    return out
+
+
+def batch_workspace_bytes(n_total: int, nclouds: int) -> int:
+    return int(lib().fec_batch_workspace_bytes(int(n_total), int(nclouds)))
+
+
+def cluster_batch(points, offsets, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
+                  workspace=None, stream=None):
+    """Many independent clouds in one call (the paper's per-scan mode).  `points`: CUDA float32
+    [n_total, 3], cloud c = rows offsets[c]:offsets[c+1] (`offsets`: host ints, nclouds + 1).
+    Returns int32 CUDA labels [n_total]: minimum index inside the point's own cloud of its
+    component, or -1 (size outside [min_size, max_size] within that cloud)."""
+    torch = _torch()
+    if not (isinstance(points, torch.Tensor) and points.is_cuda and points.dtype == torch.float32):
+        raise TypeError("points must be a CUDA float32 tensor [n, 3]")
+    points = points.contiguous()
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    nc = len(off) - 1
+    n = points.shape[0]
+    if nc < 1 or off[-1] != n:
+        raise ValueError("offsets must have nclouds + 1 entries ending at len(points)")
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=points.device)
+    nb = max(batch_workspace_bytes(n, nc), 1)
+    if workspace is None or workspace.numel() < nb:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=points.device)
+    st = stream if stream is not None else torch.cuda.current_stream(points.device)
+    _check(lib().fec_cluster_batch_ws(_ptr(points), off.ctypes.data, nc, _f32(d_th), int(min_size), int(max_size),
+                                      _ptr(out), workspace.data_ptr(), workspace.numel(), st.cuda_stream))
     return out
 
 

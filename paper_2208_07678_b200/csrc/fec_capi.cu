@@ -242,8 +242,24 @@ struct Core {
     int passes = 0;
 };
 
+// Batch mode (fec_cluster_batch_ws): clouds [off[c], off[c+1]) clustered independently in one
+// pipeline; device arrays live in the batch region after the main workspace.
+struct BatchArgs {
+    int nclouds = 0;
+    const int64_t* off_host = nullptr;
+    int64_t* off_dev = nullptr;
+    float* bb_dev = nullptr;
+    double* blo_dev = nullptr;
+    int32_t* bz_dev = nullptr;
+};
+constexpr fec_status_t kNeedPerCloud = 1;  // internal: the combined grid does not fit, run clouds one by one
+
+thread_local void* g_pinned_batch = nullptr;
+thread_local size_t g_pinned_batch_bytes = 0;
+
 // a1..a8 on n > 0 points (arguments already checked, pointers validated).
-fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C) {
+fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C,
+                      const BatchArgs* B = nullptr) {
     Layout& L = C.L;
     L = carve(static_cast<char*>(ws), n);
     int launches = 0;
@@ -257,10 +273,31 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
     const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
     const float near = (float)(2.0 * (double)d * (1.0 + std::ldexp(1.0, -16)));
-    k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite, near, &L.meta->near_pairs);
-    k_bbox_final<<<1, 256, 0, st>>>(L.part, (int)bb_blocks, L.meta);
-    launches += 2;
-    FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    float* bbh = nullptr;  // batch: per-cloud bboxes on the host
+    if (!B) {
+        k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite, near,
+                                                  &L.meta->near_pairs);
+        k_bbox_final<<<1, 256, 0, st>>>(L.part, (int)bb_blocks, L.meta);
+        launches += 2;
+        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    } else {
+        const size_t need = (size_t)B->nclouds * (6 * sizeof(float) + 3 * sizeof(double) + sizeof(int32_t)) + 64;
+        if (g_pinned_batch_bytes < need) {
+            if (g_pinned_batch) cudaFreeHost(g_pinned_batch);
+            g_pinned_batch = nullptr;
+            g_pinned_batch_bytes = 0;
+            FEC_CUDA(cudaMallocHost(&g_pinned_batch, need));
+            g_pinned_batch_bytes = need;
+        }
+        bbh = static_cast<float*>(g_pinned_batch);
+        FEC_CUDA(cudaMemcpyAsync(B->off_dev, B->off_host, (size_t)(B->nclouds + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, st));
+        k_bbox_clouds<<<B->nclouds, 256, 0, st>>>(pts, B->off_dev, B->bb_dev, &L.meta->nonfinite, near,
+                                                  &L.meta->near_pairs);
+        ++launches;
+        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+        FEC_CUDA(cudaMemcpyAsync(bbh, B->bb_dev, (size_t)B->nclouds * 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
+    }
     FEC_CUDA(cudaStreamSynchronize(st));
     const Meta hm = *g_pinned_meta;
     if (hm.nonfinite) { g_err = "non-finite coordinate"; return FEC_ERR_NONFINITE; }
@@ -273,12 +310,54 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     g.inv_q = 2.0 * g.inv_h;
     int64_t cells_total = 1;
     int key_bits = 3;
+    if (!B) {
+        for (int a = 0; a < 3; ++a) {
+            g.lo[a] = (double)hm.bbox[a];
+            // the same double operations as sub_coord() on the device
+            const double smax = std::floor(((double)hm.bbox[3 + a] - g.lo[a]) * g.inv_h);
+            if (!(smax < 2097152.0)) { g_err = "bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
+            g.dims[a] = (int32_t)(((int64_t)smax >> 1) + 1);
+        }
+    } else {
+        // each cloud: its own origin and cell dims; stacked along z with one empty layer between
+        double* blo = reinterpret_cast<double*>(static_cast<char*>(g_pinned_batch) +
+                                                ((size_t)B->nclouds * 6 * sizeof(float) + 7) / 8 * 8);
+        int32_t* bz = reinterpret_cast<int32_t*>(blo + 3 * B->nclouds);
+        int64_t gx = 1, gy = 1, gz = 0;
+        for (int cidx = 0; cidx < B->nclouds; ++cidx) {
+            const float* bb = bbh + 6 * cidx;
+            bz[cidx] = (int32_t)gz;
+            if (B->off_host[cidx + 1] == B->off_host[cidx]) {
+                blo[3 * cidx] = blo[3 * cidx + 1] = blo[3 * cidx + 2] = 0.0;
+                continue;
+            }
+            int64_t dm[3];
+            for (int a = 0; a < 3; ++a) {
+                blo[3 * cidx + a] = (double)bb[a];
+                const double smax = std::floor(((double)bb[3 + a] - (double)bb[a]) * g.inv_h);
+                if (!(smax < 2097152.0)) { g_err = "a cloud's bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
+                dm[a] = ((int64_t)smax >> 1) + 1;
+            }
+            gx = std::max(gx, dm[0]);
+            gy = std::max(gy, dm[1]);
+            gz += dm[2] + 1;
+        }
+        if (gz < 1) gz = 1;
+        if (g_grid_mode == 1 || gx * gy * gz > dense_cap(n) || gx * gy * gz >= (int64_t)0xfffffff0ll || gz >= (1 << 20))
+            return kNeedPerCloud;
+        FEC_CUDA(cudaMemcpyAsync(B->blo_dev, blo, (size_t)B->nclouds * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+        FEC_CUDA(cudaMemcpyAsync(B->bz_dev, bz, (size_t)B->nclouds * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        g.lo[0] = g.lo[1] = g.lo[2] = 0.0;
+        g.dims[0] = (int32_t)gx;
+        g.dims[1] = (int32_t)gy;
+        g.dims[2] = (int32_t)gz;
+        g.batch = 1;
+        g.nclouds = B->nclouds;
+        g.boff = B->off_dev;
+        g.blo = B->blo_dev;
+        g.bz = B->bz_dev;
+    }
     for (int a = 0; a < 3; ++a) {
-        g.lo[a] = (double)hm.bbox[a];
-        // the same double operations as sub_coord() on the device
-        const double smax = std::floor(((double)hm.bbox[3 + a] - g.lo[a]) * g.inv_h);
-        if (!(smax < 2097152.0)) { g_err = "bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
-        g.dims[a] = (int32_t)(((int64_t)smax >> 1) + 1);
         g.bits[a] = ceil_log2(g.dims[a]);
         key_bits += g.bits[a];
         cells_total *= g.dims[a];
@@ -504,7 +583,7 @@ fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
 }
 
 fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t max_size, int32_t* labels,
-                 void* ws, size_t ws_bytes, cudaStream_t st) {
+                 void* ws, size_t ws_bytes, cudaStream_t st, const BatchArgs* B = nullptr) {
     g_stats_valid = false;
     g_ev.recorded = false;
     float t2 = 0.f;
@@ -522,7 +601,7 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     }
     if (ws_bytes < carve(nullptr, n).total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
     Core C;
-    rc = run_core(pts, n, d, t2, ws, st, C);
+    rc = run_core(pts, n, d, t2, ws, st, C, B);
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n, 256, dev_info().sms * 8 * 4);
@@ -534,7 +613,8 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     mark(9, st);
     k_rootlab<<<ew, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
     k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
-        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta);
+        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
+        B ? B->off_dev : nullptr, B ? B->nclouds : 0);
     C.launches += 5;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
@@ -575,6 +655,23 @@ SlabLayout slab_carve(char* base, int64_t n_local, int32_t world, int64_t rec_ca
     S.gmin = cv.take<int>(hc);
     S.total = cv.off + 256;
     return S;
+}
+
+// Batch region after the main workspace: offsets, per-cloud bboxes, origins, z offsets.
+size_t batch_region_bytes(int32_t nclouds) {
+    return (((size_t)(nclouds + 1) * 8 + 255) & ~size_t(255)) + (((size_t)nclouds * 24 + 255) & ~size_t(255)) +
+           (((size_t)nclouds * 24 + 255) & ~size_t(255)) + (((size_t)nclouds * 4 + 255) & ~size_t(255)) + 256;
+}
+BatchArgs batch_carve(char* base, int64_t n, int32_t nclouds, const int64_t* off_host) {
+    BatchArgs B;
+    B.nclouds = nclouds;
+    B.off_host = off_host;
+    Carver cv{base, n > 0 ? carve(nullptr, n).total : 0, 0};
+    B.off_dev = cv.take<int64_t>(nclouds + 1);
+    B.bb_dev = cv.take<float>((size_t)6 * nclouds);
+    B.blo_dev = cv.take<double>((size_t)3 * nclouds);
+    B.bz_dev = cv.take<int32_t>(nclouds);
+    return B;
 }
 }  // namespace
 
@@ -745,6 +842,48 @@ fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t r
                                                                        (long long)max_size, labels_owned);
     }
     FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+
+size_t fec_batch_workspace_bytes(int64_t n_total, int32_t nclouds) {
+    if (n_total < 0 || nclouds < 1) return 0;
+    return (n_total > 0 ? fec_workspace_bytes(n_total) : 0) + batch_region_bytes(nclouds);
+}
+
+fec_status_t fec_cluster_batch_ws(const float* points, const int64_t* offsets, int32_t nclouds, float d_th,
+                                  int64_t min_size, int64_t max_size, int32_t* labels_out, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    g_stats_valid = false;
+    float t2 = 0.f;
+    if (nclouds < 1 || !offsets) { g_err = "need nclouds >= 1 and host offsets[nclouds + 1]"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (offsets[0] != 0) { g_err = "offsets[0] must be 0"; return FEC_ERR_INVALID_ARGUMENT; }
+    for (int32_t c = 0; c < nclouds; ++c)
+        if (offsets[c + 1] < offsets[c]) { g_err = "offsets must be non-decreasing"; return FEC_ERR_INVALID_ARGUMENT; }
+    const int64_t n = offsets[nclouds];
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK) return rc;
+    if (n == 0) {
+        std::memset(&g_stats, 0, sizeof(g_stats));
+        g_stats_valid = true;
+        return FEC_OK;
+    }
+    if (!workspace || workspace_bytes < fec_batch_workspace_bytes(n, nclouds)) {
+        g_err = "workspace missing or too small (see fec_batch_workspace_bytes)";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    if (!is_device_ptr(workspace)) { g_err = "workspace must be device memory"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const BatchArgs B = batch_carve(static_cast<char*>(workspace), n, nclouds, offsets);
+    rc = run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes, st, &B);
+    if (rc != kNeedPerCloud) return rc;
+    // the stacked grid does not fit the dense mode: cluster the clouds one after another
+    for (int32_t c = 0; c < nclouds; ++c) {
+        const int64_t a = offsets[c], nc = offsets[c + 1] - offsets[c];
+        if (nc == 0) continue;
+        rc = run(points + 3 * a, nc, d_th, min_size, max_size, labels_out + a, workspace, workspace_bytes, st);
+        if (rc != FEC_OK) return rc;
+    }
     return FEC_OK;
 }
 

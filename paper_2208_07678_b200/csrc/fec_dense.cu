@@ -19,12 +19,37 @@ namespace fec {
 
 __device__ SubcellTables d_sc;  // filled once per device (fec_capi.cu)
 
+// Batched clouds (fec_cluster_batch_ws): the cloud holding input index i (binary search over
+// the cloud offsets, a small L1-resident array).
+__device__ __forceinline__ int cloud_of(const Grid& g, int64_t i) {
+    int lo = 0, hi = g.nclouds;  // boff[lo] <= i < boff[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(g.boff + mid) <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // Fine sub-cell coordinates f = floor((x - lo) * inv_q) (inv_q = 4/c exactly twice inv_h,
-// so cell = f >> 2 equals the coarse computation floor((x - lo) * inv_h) >> 1).
-__device__ __forceinline__ void dense_cell_of(float x, float y, float z, const Grid& g, uint32_t& lin, int& q) {
-    const uint32_t fx = sub_coord(x, g.lo[0], g.inv_q);
-    const uint32_t fy = sub_coord(y, g.lo[1], g.inv_q);
-    const uint32_t fz = sub_coord(z, g.lo[2], g.inv_q);
+// so cell = f >> 2 equals the coarse computation floor((x - lo) * inv_h) >> 1).  In batch
+// mode each cloud uses its own origin and is shifted by a whole number of cells along z,
+// with an empty cell layer between clouds, so no cell neighbourhood spans two clouds.
+// `i` is the point's input index.
+__device__ __forceinline__ void dense_cell_of(float x, float y, float z, int64_t i, const Grid& g, uint32_t& lin,
+                                              int& q) {
+    double l0 = g.lo[0], l1 = g.lo[1], l2 = g.lo[2];
+    uint32_t zoff = 0;
+    if (g.batch) {
+        const int c = cloud_of(g, i);
+        l0 = __ldg(g.blo + 3 * c);
+        l1 = __ldg(g.blo + 3 * c + 1);
+        l2 = __ldg(g.blo + 3 * c + 2);
+        zoff = 4u * (uint32_t)__ldg(g.bz + c);
+    }
+    const uint32_t fx = sub_coord(x, l0, g.inv_q);
+    const uint32_t fy = sub_coord(y, l1, g.inv_q);
+    const uint32_t fz = sub_coord(z, l2, g.inv_q) + zoff;
     q = (int)((fx & 3u) | ((fy & 3u) << 2) | ((fz & 3u) << 4));
     lin = (fx >> 2) * g.stride[0] + (fy >> 2) * g.stride[1] + (fz >> 2) * g.stride[2];
 }
@@ -143,7 +168,7 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
                 atomicOr(bits + bin_slot(keys, lin >> 5), 1u << (lin & 31u));
             }
         }
@@ -233,7 +258,7 @@ __global__ void __launch_bounds__(kBinThreads) k_dcount(const float* __restrict_
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
                 const int h = bin_slot(keys, cid_of(cw, lin));
                 hs[j] = h;
                 rk[j] = atomicAdd(cnt + h, 1u);
@@ -289,7 +314,7 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             int q;
-            dense_cell_of(P.x[j], P.y[j], P.z[j], g, k[j], q);
+            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, k[j], q);
         }
         if (b4 + 4 <= n) {
             *reinterpret_cast<uint4*>(key + b4) = make_uint4(k[0], k[1], k[2], k[3]);
@@ -359,7 +384,7 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
             if (ok) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(x[j], y[j], z[j], g, lin, q);
+                dense_cell_of(x[j], y[j], z[j], vi[j], g, lin, q);
                 cid = cid_of(cw, k[j]);
                 bit = 1ull << q;
                 spts[s] = make_float4(x[j], y[j], z[j], __int_as_float(vi[j]));
@@ -463,7 +488,7 @@ __device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, 
         uint32_t lq;
         int qq;
         const float4 v = C.spts[it.z];
-        dense_cell_of(v.x, v.y, v.z, g, lq, qq);
+        dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lq, qq);
         slot = cell_slot_of(g, lp, lq);
     }
     const int a0 = (int)__ldg(C.cstart + cp), a1 = (int)__ldg(C.cstart + cp + 1);
@@ -471,13 +496,13 @@ __device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, 
         const float4 pa = C.spts[i];
         uint32_t l;
         int qa;
-        dense_cell_of(pa.x, pa.y, pa.z, g, l, qa);
+        dense_cell_of(pa.x, pa.y, pa.z, __float_as_int(pa.w), g, l, qa);
         if (!((ma >> qa) & 1ull)) continue;
         const u64 reach = d_sc.U[slot][qa];
         for (int j = b0; j < b1; ++j) {
             const float4 pb = C.spts[j];
             int qb;
-            dense_cell_of(pb.x, pb.y, pb.z, g, l, qb);
+            dense_cell_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g, l, qb);
             if (it.w >= 0 && !(((mb & reach) >> qb) & 1ull)) continue;
             if (pred(pa, pb, t2)) {
                 uf_unite(C.parent, na, nb);
@@ -555,7 +580,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], g, lin, q);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
                 spts[__ldg(cstart + cid_of(cw, lin)) + sl[j]] =
                     make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
             }
@@ -582,7 +607,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
         for (int j = 0; j < 4; ++j) {
             uint32_t lin;
             int q;
-            dense_cell_of(v[j].x, v[j].y, v[j].z, g, lin, q);
+            dense_cell_of(v[j].x, v[j].y, v[j].z, __float_as_int(v[j].w), g, lin, q);
             const uint32_t cid = cid_of(cw, lin);
             par[j] = (int)(b4 + j);
             si[j] = __float_as_int(v[j].w);
@@ -636,7 +661,7 @@ __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts
                 const float4 v = __ldg(spts + s);
                 uint32_t lin;
                 int q;
-                dense_cell_of(v.x, v.y, v.z, g, lin, q);
+                dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lin, q);
                 while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
             }
             parent[s] = nbase + 8 * r + cc;
@@ -721,7 +746,7 @@ __device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, con
                 const float4 v = C.spts[t];
                 uint32_t l;
                 int qb;
-                dense_cell_of(v.x, v.y, v.z, g, l, qb);
+                dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, l, qb);
                 const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
                 for (int x = 0; x < kp; ++x) {
                     const u64 mx = mp[x];
@@ -831,7 +856,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
             const float4 v = C.spts[it.z];
             uint32_t lq;
             int qb;
-            dense_cell_of(v.x, v.y, v.z, g, lq, qb);
+            dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lq, qb);
             slot = cell_slot_of(g, lp, lq);
             fb = ~0ull;
             fa = d_sc.U[26 - slot][qb] & ma;
@@ -854,7 +879,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
                     p = C.spts[i];
                     uint32_t l;
                     int qa;
-                    dense_cell_of(p.x, p.y, p.z, g, l, qa);
+                    dense_cell_of(p.x, p.y, p.z, __float_as_int(p.w), g, l, qa);
                     v = (fa >> qa) & 1ull;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, v);
@@ -880,7 +905,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
                     pb = C.spts[j];
                     uint32_t l;
                     int qb;
-                    dense_cell_of(pb.x, pb.y, pb.z, g, l, qb);
+                    dense_cell_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g, l, qb);
                     vb = (fb >> qb) & 1ull;
                 }
                 unsigned mb = __ballot_sync(0xffffffffu, vb);

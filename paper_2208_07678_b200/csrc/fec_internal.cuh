@@ -38,6 +38,13 @@ struct Grid {
     uint32_t sdiv[2];   // dense mode: stride[perm[2]], stride[perm[1]] (for decoding)
     u64 hash_mask;
     float t2;
+    // batch mode (dense grid only): clouds [boff[c], boff[c+1]) with origins blo[3c..3c+2]
+    // and z cell offsets bz[c] (device arrays); batch == 0 for a single cloud
+    int32_t batch;
+    int32_t nclouds;
+    const int64_t* boff;
+    const double* blo;
+    const int32_t* bz;
 };
 
 // Sub-cell coordinate on one axis: floor((x - lo) * inv_h).  Cell = sub >> 1 and the octant

@@ -107,6 +107,53 @@ __global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ pa
     }
 }
 
+// Batch mode: one block per cloud [off[c], off[c+1]): its bbox (6 floats at bb[6c]), the
+// non-finite flag and the near-pair count (consecutive pairs inside the cloud).
+__global__ void __launch_bounds__(256) k_bbox_clouds(const float* __restrict__ p, const int64_t* __restrict__ off,
+                                                    float* __restrict__ bb, int* __restrict__ nonfinite, float near,
+                                                    unsigned long long* __restrict__ near_pairs) {
+    const int c = blockIdx.x;
+    const int64_t a = off[c], b = off[c + 1];
+    float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+    int bad = 0;
+    unsigned nearc = 0;
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        float v[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            v[k] = __ldg(p + 3 * i + k);
+            bb_acc(v[k], mn[k], mx[k], bad);
+        }
+        if (i + 1 < b)
+            nearc += fabsf(__ldg(p + 3 * i + 3) - v[0]) <= near && fabsf(__ldg(p + 3 * i + 4) - v[1]) <= near &&
+                     fabsf(__ldg(p + 3 * i + 5) - v[2]) <= near;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    for (int o = 16; o > 0; o >>= 1) nearc += __shfl_xor_sync(0xffffffffu, nearc, o);
+    __shared__ float s[8][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { s[w][k] = mn[k]; s[w][3 + k] = mx[k]; }
+        if (bad) atomicOr(nonfinite, 1);
+        if (nearc) atomicAdd(near_pairs, (unsigned long long)nearc);
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        bb[6 * c + threadIdx.x] = v;
+    }
+}
+
 // =====================================================================================
 // a2  K1: sub-cell Morton keys; idx = iota
 // =====================================================================================
@@ -694,7 +741,8 @@ __global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent,
 __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent, const int* __restrict__ val,
                                                 const int* __restrict__ size, const int* __restrict__ minidx,
                                                 int64_t n, long long min_size, long long max_size,
-                                                int* __restrict__ labels, const Meta* __restrict__ meta) {
+                                                int* __restrict__ labels, const Meta* __restrict__ meta,
+                                                const int64_t* __restrict__ boff, int nclouds) {
     const bool folded = 4 * (int64_t)meta->cells > n;  // k_rootlab ran
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -715,12 +763,24 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (r[j] < 0) continue;
+            int lab;
             if (folded) {
-                labels[v[j]] = __ldg(minidx + r[j]);
+                lab = __ldg(minidx + r[j]);
             } else {
                 const long long sz = __ldg(size + r[j]);
-                labels[v[j]] = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
+                lab = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
             }
+            if (boff && lab >= 0) {
+                // batch mode: index inside the point's own cloud (the component never spans two)
+                int lo = 0, hi = nclouds;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (__ldg(boff + mid) <= (int64_t)v[j]) lo = mid;
+                    else hi = mid;
+                }
+                lab -= (int)__ldg(boff + lo);
+            }
+            labels[v[j]] = lab;
         }
     }
 }

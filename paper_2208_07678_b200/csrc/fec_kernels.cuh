@@ -68,7 +68,10 @@ __global__ void k_stats(const int* parent, const int* val, int64_t n, int* size,
 __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
                           long long max_size, const Meta* meta);
 __global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
-                          long long min_size, long long max_size, int* labels, const Meta* meta);
+                          long long min_size, long long max_size, int* labels, const Meta* meta, const int64_t* boff,
+                          int nclouds);
+__global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
+                              unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
 __global__ void k_cpopc(const uint2* cw, int64_t words, uint32_t* cnt);
 __global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t* clin, uint32_t* count, u64* cocc,
