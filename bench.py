@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--check", action="store_true", help="also verify the labels bit-exactly (untimed)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even at N=1 (testing)")
     ap.add_argument("--grid-mode", default="auto", choices=["auto", "hashed"], help="testing: force the hashed mode")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="per-scan mode: cluster this many independent C2-recipe scans per step in one "
+                         "fec_cluster_batch_ws call (SURVEY N1)")
     return ap.parse_args()
 
 
@@ -388,11 +391,77 @@ def run_slab(args, rank: int, world: int, local: int):
         tdist.destroy_process_group()
 
 
+def run_batch(args, local: int):
+    """Per-scan mode (the paper's Table 4 setting): B independent single scans (C2 recipe,
+    seeds 1000..) per step, one batched call; the same scans through B separate calls are
+    timed beside it."""
+    import torch
+    import paper_2208_07678_b200 as fec
+    fec.lib()
+    d_th, mn, mx = synth.CONFIGS["C2"]
+    scans = [synth.lidar_scan(1000 + k) for k in range(args.batch)]
+    offs = np.concatenate([[0], np.cumsum([len(c) for c in scans])]).astype(np.int64)
+    pts = np.concatenate(scans)
+    n = pts.shape[0]
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(pts).to(dev)
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    ws = torch.empty(fec.batch_workspace_bytes(n, len(scans)), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    check = None
+    if args.check:
+        import oracle
+        fec.cluster_batch(x, offs, d_th, mn, mx, out=out, workspace=ws)
+        got = out.cpu().numpy()
+        check = all(np.array_equal(got[offs[k]:offs[k + 1]], oracle.fec(scans[k], d_th, mn, mx))
+                    for k in range(len(scans)))
+    for _ in range(args.warmup):
+        fec.cluster_batch(x, offs, d_th, mn, mx, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            fec.cluster_batch(x, offs, d_th, mn, mx, out=out, workspace=ws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    # the same scans, one call each (workspace reused)
+    wss = torch.empty(fec.workspace_bytes(max(len(c) for c in scans)), dtype=torch.uint8, device=dev)
+    xs = [x[offs[k]:offs[k + 1]] for k in range(len(scans))]
+    e0.record(stream)
+    for _ in range(max(1, args.steps // 3)):
+        for k in range(len(scans)):
+            fec.cluster(xs[k], d_th, mn, mx, out=out[offs[k]:offs[k + 1]], workspace=wss)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_seq = e0.elapsed_time(e1) / max(1, args.steps // 3)
+    line = {
+        "metric": "Mpoints/s clustered", "value": n / (ms * 1e-3) / 1e6, "unit": "Mpoints/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"per-scan mode: {len(scans)} independent C2-recipe scans (seeds 1000..) in one "
+                               f"fec_cluster_batch_ws call; d_th=0.35 m, min 50, max 25k",
+                   "n_points": int(n), "scans": len(scans), "parallelism": "single",
+                   "l2": "inputs below L2 size (latency-bound)" if 12 * n < 126e6 else "inputs exceed L2"},
+        "sequential_calls_ms_per_step": ms_seq,
+        "sequential_calls_mpts_s": n / (ms_seq * 1e-3) / 1e6,
+        "clocks": clk.summary(),
+    }
+    if check is not None:
+        line["parity_bit_exact"] = bool(check)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.batch > 1 and world == 1:
+        run_batch(args, local)
         return
     if world > 1 or args.slab:
         run_slab(args, rank, world, local)
