@@ -127,7 +127,9 @@ struct Layout {
     int *sval0, *sval1;       // key-sort path: input indices (double buffer)
     uint32_t* scounts;        // key-sort path: digit counts per tile
     int4* items;        // queued component pairs (not certain, possibly within reach)
-    int4* items2;       // those still apart after all certain unions
+    int4* items2;       // those still apart after all certain unions (split into slices)
+    int4* slices2;      // (slice, slices, queued pair) of each items2 entry
+    int* idone;         // per queued pair: a slice found a pred-true pair
     int item_cap;
     size_t total;
 };
@@ -191,7 +193,9 @@ Layout carve(char* base, int64_t n) {
     L.cmask = b.take<u64>((size_t)8 * dense_max(n));
     L.item_cap = (int)std::min<int64_t>(n / 8 + 65536, INT32_MAX / 2);
     L.items = b.take<int4>(L.item_cap);
-    L.items2 = b.take<int4>(L.item_cap);
+    L.items2 = b.take<int4>(2 * (size_t)L.item_cap);
+    L.slices2 = b.take<int4>(2 * (size_t)L.item_cap);
+    L.idone = b.take<int>(L.item_cap);
     L.total = std::max(a.off, b.off) + 256;
     return L;
 }
@@ -491,8 +495,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         k_dense_overflow<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag,
                                                                           dctx);
         k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
-        k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(dctx, L.items2);
-        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2);
+        k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
+        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
         launches += 7;
         if (g_instrument) {
             k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);

@@ -795,13 +795,38 @@ __global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __r
 
 // Queued pairs whose nodes are already connected (after all certain unions) are dropped;
 // the others are compacted into items2 for k_dense_items.
-__global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restrict__ items2) {
+// Heavy pairs (two big cells) are split over several warps along B's range: sub-item
+// (k, K) tests B's k-th of K slices, and a per-pair flag stops the others at the first hit.
+constexpr int kSliceWork = 16384;  // cell-size product per slice
+constexpr int kMaxSlices = 32;
+
+__global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* __restrict__ items2,
+                                                     int4* __restrict__ slices2, int* __restrict__ idone) {
     const int ni = min(C.meta->nitems, C.item_cap);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
         const int4 it = C.items[e];  // queued before every certain union was done: re-check
         const int na = C.nbase + 8 * it.x + it.y;
         const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
-        if (uf_find(C.parent, na) != uf_find(C.parent, nb)) items2[atomicAdd(&C.meta->nitems2, 1)] = it;
+        if (uf_find(C.parent, na) == uf_find(C.parent, nb)) continue;
+        const int cp = __ldg(C.dlist + it.x);
+        const int wa = (int)(__ldg(C.cstart + cp + 1) - __ldg(C.cstart + cp));
+        int wb = 1;
+        if (it.w >= 0) {
+            const int cq = __ldg(C.dlist + it.z);
+            wb = (int)(__ldg(C.cstart + cq + 1) - __ldg(C.cstart + cq));
+        }
+        const long long work = (long long)wa * wb;
+        int K = (int)min((long long)kMaxSlices, max(1ll, work / kSliceWork));
+        K = min(K, wb);
+        // items2 holds item_cap pairs plus item_cap extra slices: a pair whose extra slices
+        // would not fit runs as one slice (there are at most item_cap surviving pairs)
+        if (K > 1 && atomicAdd(&C.meta->nslices_extra, K - 1) + (K - 1) > C.item_cap) K = 1;
+        idone[e] = 0;
+        const int base = atomicAdd(&C.meta->nitems2, K);
+        for (int k = 0; k < K; ++k) {
+            items2[base + k] = it;
+            slices2[base + k] = make_int4(k, K, e, 0);
+        }
     }
 }
 
@@ -822,7 +847,8 @@ __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent,
 // batches); B's points stream through the warp 32 at a time and are broadcast by shuffle.
 constexpr int kAPer = 4;
 
-__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const int4* __restrict__ items2) {
+__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const int4* __restrict__ items2,
+                                                    const int4* __restrict__ slices2, int* __restrict__ idone) {
     __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
     float4* abuf = abuf_all[threadIdx.x >> 5];
@@ -832,10 +858,12 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
     unsigned long long n_tests = 0;
     for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ni; w += warps) {
         const int4 it = items2[w];
+        const int4 sl = slices2[w];
+        volatile int* done = idone + sl.z;
         const int na = C.nbase + 8 * it.x + it.y;
         const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
         int same = 0;
-        if (lane == 0) same = uf_find(C.parent, na) == uf_find(C.parent, nb);
+        if (lane == 0) same = *done || uf_find(C.parent, na) == uf_find(C.parent, nb);
         if (__shfl_sync(0xffffffffu, same, 0)) continue;
         const int cp = __ldg(C.dlist + it.x);
         const uint32_t lp = __ldg(C.clin + cp);
@@ -850,6 +878,11 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
             slot = cell_slot_of(g, lp, __ldg(C.clin + cq));
             fb = reach_of(ma, slot) & mb;
             fa = reach_of(mb, 26 - slot) & ma;
+            // this sub-item's slice of B
+            const int len = b1 - b0;
+            const int s0 = b0 + (int)(((long long)len * sl.x) / sl.y), s1 = b0 + (int)(((long long)len * (sl.x + 1)) / sl.y);
+            b0 = s0;
+            b1 = s1;
         } else {
             b0 = it.z;
             b1 = it.z + 1;
@@ -865,6 +898,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
         bool found = false;
         int ai = a0;
         while (ai < a1 && !found) {
+            if (__shfl_sync(0xffffffffu, lane == 0 ? *done : 0, 0)) break;  // another slice found it
             // stage the next batch of A points (via shared memory): batch position k ends up in
             // lane k % 32, entry k / 32
             float4 pa[kAPer];
@@ -925,7 +959,10 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
                 }
             }
         }
-        if (found && lane == 0) uf_unite(C.parent, na, nb);
+        if (found && lane == 0) {
+            *done = 1;
+            uf_unite(C.parent, na, nb);
+        }
         __syncwarp();
     }
     if (C.meta->instrument) {

@@ -31,6 +31,7 @@ struct Meta {
     int internal_error;               // != 0: an internal invariant failed (never expected)
     int nitems2;                      // dense-grid mode: queued pairs still apart after the certain unions
     unsigned long long near_pairs;    // a1: consecutive input pairs within 2 cells (input coherence)
+    int nslices_extra;                // dense-grid mode: extra slices of heavy uncertain pairs
 };
 
 struct Tables {
@@ -116,8 +117,8 @@ __global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int
                              uint32_t* oflags, DenseCtx C, int k0);
 __global__ void k_dense_overflow(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
                                  uint32_t* oflags, DenseCtx C);
-__global__ void k_dense_filter(DenseCtx C, int4* items2);
-__global__ void k_dense_items(Grid g, DenseCtx C, const int4* items2);
+__global__ void k_dense_filter(Grid g, DenseCtx C, int4* items2, int4* slices2, int* idone);
+__global__ void k_dense_items(Grid g, DenseCtx C, const int4* items2, const int4* slices2, int* idone);
 __global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta);
 __global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);
 cudaError_t ensure_subcell_tables();  // host: upload the fine sub-cell tables (once per device)
