@@ -310,11 +310,11 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
         const int64_t b4 = 4 * gi;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
-        uint32_t k[4];
+        uint32_t k[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             int q;
-            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, k[j], q);
+            if (b4 + j < n) dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, k[j], q);
         }
         if (b4 + 4 <= n) {
             *reinterpret_cast<uint4*>(key + b4) = make_uint4(k[0], k[1], k[2], k[3]);
@@ -605,13 +605,14 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
         int par[4], si[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+            par[j] = (int)(b4 + j);
+            si[j] = __float_as_int(v[j].w);
+            if (b4 + j >= n) continue;
             uint32_t lin;
             int q;
             dense_cell_of(v[j].x, v[j].y, v[j].z, __float_as_int(v[j].w), g, lin, q);
             const uint32_t cid = cid_of(cw, lin);
-            par[j] = (int)(b4 + j);
-            si[j] = __float_as_int(v[j].w);
-            if (b4 + j < n && __ldg(cstart + cid + 1) - __ldg(cstart + cid) > (uint32_t)SPARSE_MAX) {
+            if (__ldg(cstart + cid + 1) - __ldg(cstart + cid) > (uint32_t)SPARSE_MAX) {
                 const int r = __ldg(crec + cid);
                 const int k = __ldg(ncomp + r);
                 int c = 0;
