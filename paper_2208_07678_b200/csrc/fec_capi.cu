@@ -424,7 +424,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
             k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
                                                                            L.ccoord, g, L.meta);
-            k_dcount<<<ew, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
+            k_dcount<<<grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4), 256, 0, st>>>(
+                pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
             k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
             launches += 3 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
             k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);

@@ -232,69 +232,88 @@ __global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t w
 }
 
 // ---- a2: per-cell counts, slot[i] = rank of point i inside its cell, fine occupancy ------
-__global__ void __launch_bounds__(kBinThreads) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
-                                                        const uint2* __restrict__ cw, uint32_t* __restrict__ count,
-                                                        uint32_t* __restrict__ slot, uint32_t* __restrict__ dbits,
-                                                        u64* __restrict__ cocc) {
-    __shared__ int keys[kBinSlots];
-    __shared__ uint32_t cnt[kBinSlots], olo[kBinSlots], ohi[kBinSlots], base[kBinSlots];
-    for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
-        keys[k] = -1;
-        cnt[k] = 0u;
-        olo[k] = 0u;
-        ohi[k] = 0u;
+// Warp per tile of 128 consecutive points (4 per lane), aggregated through a per-warp
+// shared-memory table: one global atomicAdd (+ atomicOr) per distinct cell per tile and only
+// warp-level synchronisation (the input order is spatially coherent on this path).
+constexpr int kWTile = 128;
+constexpr int kWSlots = 256;
+
+__device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, bool& overflow) {
+    uint32_t h = (key * 2654435761u) & (kWSlots - 1);
+    for (int probe = 0; probe < kWSlots; ++probe) {
+        const int cur = keys[h];
+        if (cur == (int)key) return (int)h;
+        if (cur == -1) {
+            const int old = atomicCAS(keys + h, -1, (int)key);
+            if (old == -1 || old == (int)key) return (int)h;
+        }
+        h = (h + 1) & (kWSlots - 1);
     }
-    __syncthreads();
+    overflow = true;  // cannot happen: a tile has at most 128 distinct cells
+    return 0;
+}
+
+__global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
+                                               const uint2* __restrict__ cw, uint32_t* __restrict__ count,
+                                               uint32_t* __restrict__ slot, uint32_t* __restrict__ dbits,
+                                               u64* __restrict__ cocc) {
+    __shared__ int keys_all[256 / kWarp][kWSlots];
+    __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int* keys = keys_all[wid];
+    uint32_t *cnt = cnt_all[wid], *olo = olo_all[wid], *ohi = ohi_all[wid];
+    for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; }
+    __syncwarp();
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
-    for (int64_t t0 = (int64_t)blockIdx.x * kBinTile; t0 < n; t0 += (int64_t)gridDim.x * kBinTile) {
-        int hs[kBinIpt];
-        uint32_t rk[kBinIpt];
-        const int64_t b4 = t0 + kBinIpt * threadIdx.x;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWTile; t0 < n; t0 += nw * kWTile) {
+        const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
+        int hs[4];
+        uint32_t rk[4];
+        bool ovf = false;
 #pragma unroll
-        for (int j = 0; j < kBinIpt; ++j) {
+        for (int j = 0; j < 4; ++j) {
             hs[j] = -1;
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
                 dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                const int h = bin_slot(keys, cid_of(cw, lin));
+                const int h = wbin_slot(keys, cid_of(cw, lin), ovf);
                 hs[j] = h;
                 rk[j] = atomicAdd(cnt + h, 1u);
                 if (q < 32) atomicOr(olo + h, 1u << q);
                 else atomicOr(ohi + h, 1u << (q - 32));
             }
         }
-        __syncthreads();
-        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
+        __syncwarp();
+        // flush: lane per slot; the table's cnt[] is replaced by the cell's base slot
+        for (int k = lane; k < kWSlots; k += 32) {
             const int cid = keys[k];
             if (cid != -1) {
                 const uint32_t c = cnt[k];
                 const uint32_t old = atomicAdd(count + cid, c);
-                base[k] = old;
+                cnt[k] = old;
                 if (old <= (uint32_t)SPARSE_MAX && old + c > (uint32_t)SPARSE_MAX)
                     atomicOr(dbits + (cid >> 5), 1u << (cid & 31u));   // the cell just became dense
                 atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
             }
         }
-        __syncthreads();
-        if (b4 + kBinIpt <= n) {
-            *reinterpret_cast<uint4*>(slot + b4) =
-                make_uint4(base[hs[0]] + rk[0], base[hs[1]] + rk[1], base[hs[2]] + rk[2], base[hs[3]] + rk[3]);
+        __syncwarp();
+        uint32_t sl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sl[j] = hs[j] >= 0 ? cnt[hs[j]] + rk[j] : 0u;
+        if (b4 + 4 <= n) {
+            *reinterpret_cast<uint4*>(slot + b4) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
         } else {
 #pragma unroll
-            for (int j = 0; j < kBinIpt; ++j)
-                if (hs[j] >= 0) slot[b4 + j] = base[hs[j]] + rk[j];
+            for (int j = 0; j < 4; ++j)
+                if (b4 + j < n) slot[b4 + j] = sl[j];
         }
-        __syncthreads();
-        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
-            keys[k] = -1;
-            cnt[k] = 0u;
-            olo[k] = 0u;
-            ohi[k] = 0u;
-        }
-        __syncthreads();
+        __syncwarp();
+        for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; }
+        __syncwarp();
     }
 }
 
