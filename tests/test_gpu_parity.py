@@ -92,11 +92,43 @@ def test_device_predicate_matches_oracle_on_boundary_pairs(fec):
     assert o.any() and (~o).any()
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_config_full_size(fec, name):
     w = synth.make_config(name)
     assert_same(run_gpu(fec, w.points, w.d_th, w.min_size, w.max_size),
                 oracle.fec(w.points, w.d_th, w.min_size, w.max_size), name)
+
+
+def test_c5_full_size_properties(fec):
+    """C5 at full size (110M points, the bench's launch) — the oracle would take minutes, so the
+    labels are checked through properties that hold at any size: canonical form
+    (label[i] <= i, label[label[i]] == label[i]), every component label class is exactly the
+    set of points whose min index it is (its size within [min, max] = [1, 1e9]), and on a
+    sample of points the oracle's own component query (min index, size) agrees."""
+    w = synth.make_config("C5")
+    lab = run_gpu(fec, w.points, w.d_th, w.min_size, w.max_size)
+    n = w.n
+    idx = np.arange(n)
+    assert (lab >= 0).all()              # min 1, max 1e9: nothing is noise
+    assert (lab <= idx).all()
+    assert (lab[lab] == lab).all()
+    sizes = np.bincount(lab, minlength=n)
+    rng = np.random.default_rng(0)
+    ix = oracle.Index(w.points, w.d_th)
+    try:
+        done = 0
+        for i in rng.permutation(n)[:2000]:
+            # only small components: a query walks its whole component on one core
+            if sizes[lab[i]] > 5000:
+                continue
+            mn, sz = ix.component(int(i))
+            assert lab[i] == mn and sizes[mn] == sz, (i, lab[i], mn, sz)
+            done += 1
+            if done >= 40:
+                break
+        assert done >= 20
+    finally:
+        ix.close()
 
 
 @pytest.mark.parametrize("name,scale", [("C3", 0.05), ("C4", 0.02), ("C5", 0.02)])
