@@ -488,7 +488,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         // queued uncertain pairs
         mark(5, st);
         k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
-                                                                         L.parent, L.meta);
+                                                                         L.parent, L.meta, n);
+        k_union_sparse_local<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
+                                                                               L.parent, L.meta, n);
         mark(6, st);
         const unsigned lx = grid_for(dense_max(n), 256, cap);
         k_dense_link<<<dim3(lx, 3), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
@@ -498,7 +500,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
         k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
         k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
-        launches += 7;
+        launches += 8;
         if (g_instrument) {
             k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);
             ++launches;

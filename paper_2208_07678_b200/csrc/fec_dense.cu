@@ -1019,10 +1019,16 @@ __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ nco
 // Loops are warp-uniform with a reconvergence point per neighbour (SIMT efficiency).
 constexpr int SP_CHUNK = 32;
 
-__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
-                                                     const u64* __restrict__ ccoord,
-                                                     const uint32_t* __restrict__ cstart, Grid g,
-                                                     int* __restrict__ parent, Meta* __restrict__ meta) {
+// LOCAL (clouds with few sparse cells, e.g. LiDAR maps): a neighbour point is united once
+// per local component of P it touches (P's own pairs give 3-bit local labels) instead of
+// once per pred-true pair; sparse-dominated clouds (occupied cells > n/4, ~1-2 points per
+// cell) run the plain form.  Both are launched; the one not chosen returns at once.
+template <bool LOCAL>
+__device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spts, const uint2* __restrict__ cw,
+                                                  const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
+                                                  const Grid& g, int* __restrict__ parent, Meta* __restrict__ meta,
+                                                  int64_t n) {
+    if ((4 * (int64_t)meta->cells > n) == LOCAL) return;
     const uint32_t cells = (uint32_t)meta->cells;  // occupied cells (compact ids)
     __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
     unsigned long long n_tests = 0;
@@ -1052,11 +1058,30 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
             const uint32_t P = v ? list[e] : 0u;
             const int ps = v ? (int)__ldg(cstart + P) : 0;
             const int pe = v ? (int)__ldg(cstart + P + 1) : 0;
+            // P's own pairs; lab = 3-bit local component label (its min local index) per point,
+            // so a neighbour point needs one union per local component it touches, not one
+            // per pred-true pair
+            uint32_t lab = 0;
+            if constexpr (LOCAL)
+                for (int i = 0; i < pe - ps; ++i) lab |= (uint32_t)i << (3 * i);
             for (int s = ps; s < pe; ++s) {
                 const float4 a = __ldg(spts + s);
                 for (int t = s + 1; t < pe; ++t) {
                     ++n_tests;
-                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                    if (pred(a, __ldg(spts + t), t2)) {
+                        if constexpr (LOCAL) {
+                            const uint32_t ls = (lab >> (3 * (s - ps))) & 7u, lt = (lab >> (3 * (t - ps))) & 7u;
+                            if (ls != lt) {
+                                uf_unite(parent, s, t);
+                                const uint32_t lo = ls < lt ? ls : lt, hi = ls < lt ? lt : ls;
+                                for (int i = 0; i < pe - ps; ++i)
+                                    if (((lab >> (3 * i)) & 7u) == hi)
+                                        lab = (lab & ~(7u << (3 * i))) | (lo << (3 * i));
+                            }
+                        } else {
+                            uf_unite(parent, s, t);
+                        }
+                    }
                 }
             }
             __syncwarp();
@@ -1072,11 +1097,27 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                     qe = (int)__ldg(cstart + qc + 1);
                     if (qe - qs > SPARSE_MAX) qe = qs;  // dense neighbours are handled by k_dense_link
                 }
-                for (int s = ps; s < pe && qe > qs; ++s) {
-                    const float4 a = __ldg(spts + s);
+                if constexpr (LOCAL) {
                     for (int t = qs; t < qe; ++t) {
-                        ++n_tests;
-                        if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                        const float4 b = __ldg(spts + t);
+                        uint32_t touched = 0;  // local components of P within d of t
+                        for (int s = ps; s < pe; ++s) {
+                            ++n_tests;
+                            if (pred(__ldg(spts + s), b, t2)) touched |= 1u << ((lab >> (3 * (s - ps))) & 7u);
+                        }
+                        while (touched) {
+                            const int l = __ffs(touched) - 1;
+                            touched &= touched - 1;
+                            uf_unite(parent, ps + l, t);
+                        }
+                    }
+                } else {
+                    for (int s = ps; s < pe && qe > qs; ++s) {
+                        const float4 a = __ldg(spts + s);
+                        for (int t = qs; t < qe; ++t) {
+                            ++n_tests;
+                            if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                        }
                     }
                 }
                 __syncwarp();
@@ -1088,6 +1129,21 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
         for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(0xffffffffu, n_tests, o);
         if (lane == 0 && n_tests) atomicAdd(&meta->pair_tests, n_tests);
     }
+}
+
+__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
+                                                     const u64* __restrict__ ccoord,
+                                                     const uint32_t* __restrict__ cstart, Grid g,
+                                                     int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
+    union_sparse_body<false>(spts, cw, ccoord, cstart, g, parent, meta, n);
+}
+__global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __restrict__ spts,
+                                                           const uint2* __restrict__ cw,
+                                                           const u64* __restrict__ ccoord,
+                                                           const uint32_t* __restrict__ cstart, Grid g,
+                                                           int* __restrict__ parent, Meta* __restrict__ meta,
+                                                           int64_t n) {
+    union_sparse_body<true>(spts, cw, ccoord, cstart, g, parent, meta, n);
 }
 
 }  // namespace fec

@@ -112,7 +112,9 @@ __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, 
 __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int* dlist, const int* ncomp,
                           const u64* cmask, Grid g, int nbase, int* parent, const Meta* meta);
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
-                               int* parent, Meta* meta);
+                               int* parent, Meta* meta, int64_t n);
+__global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
+                                     Grid g, int* parent, Meta* meta, int64_t n);
 __global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
                              uint32_t* oflags, DenseCtx C, int k0);
 __global__ void k_dense_overflow(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
