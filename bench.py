@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="also verify the labels bit-exactly (untimed)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even at N=1 (testing)")
-    ap.add_argument("--grid-mode", default="auto", choices=["auto", "hashed"], help="testing: force the hashed mode")
+    ap.add_argument("--grid-mode", default="auto", choices=["auto", "hashed", "keysort", "countsort"],
+                    help="testing: force a binning mode")
     ap.add_argument("--batch", type=int, default=0,
                     help="per-scan mode: cluster this many independent C2-recipe scans per step in one "
                          "fec_cluster_batch_ws call (SURVEY N1)")
@@ -470,7 +471,7 @@ def main():
     import paper_2208_07678_b200 as fec
 
     fec.lib()
-    fec.set_grid_mode(1 if args.grid_mode == "hashed" else 0)
+    fec.set_grid_mode({"auto": 0, "hashed": 1, "keysort": 2, "countsort": 3}[args.grid_mode])
     d_th, mn, mx = synth.CONFIGS[args.config]
     w = synth.make_config(args.config, scale=args.scale)
     n = w.n
