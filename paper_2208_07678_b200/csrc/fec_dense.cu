@@ -139,14 +139,20 @@ constexpr int kBinIpt = 4;
 constexpr int kBinTile = kBinThreads * kBinIpt;
 constexpr int kBinSlots = 2 * kBinTile;
 
-__device__ __forceinline__ int bin_slot(int* keys, uint32_t key) {
+// Insert `key`; a thread that claims a new slot appends it to `used` (so the flush visits only
+// occupied slots).
+__device__ __forceinline__ int bin_slot(int* keys, uint32_t key, int* used, int* nused) {
     uint32_t h = (key * 2654435761u) & (kBinSlots - 1);
     while (true) {
         const int cur = keys[h];
         if (cur == (int)key) return (int)h;
         if (cur == -1) {
             const int old = atomicCAS(keys + h, -1, (int)key);
-            if (old == -1 || old == (int)key) return (int)h;
+            if (old == -1) {
+                used[atomicAdd(nused, 1)] = (int)h;
+                return (int)h;
+            }
+            if (old == (int)key) return (int)h;
         }
         h = (h + 1) & (kBinSlots - 1);
     }
@@ -156,8 +162,11 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
                                                        uint2* __restrict__ cw) {
     __shared__ int keys[kBinSlots];
     __shared__ uint32_t bits[kBinSlots];
+    __shared__ int used[kBinTile];
+    __shared__ int nused;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) { keys[k] = -1; bits[k] = 0u; }
+    if (threadIdx.x == 0) nused = 0;
     __syncthreads();
     for (int64_t t0 = (int64_t)blockIdx.x * kBinTile; t0 < n; t0 += (int64_t)gridDim.x * kBinTile) {
         const int64_t b4 = t0 + kBinIpt * threadIdx.x;
@@ -169,17 +178,19 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
                 uint32_t lin;
                 int q;
                 dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                atomicOr(bits + bin_slot(keys, lin >> 5), 1u << (lin & 31u));
+                atomicOr(bits + bin_slot(keys, lin >> 5, used, &nused), 1u << (lin & 31u));
             }
         }
         __syncthreads();
-        for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) {
-            if (keys[k] != -1) {
-                atomicOr(reinterpret_cast<unsigned int*>(cw + keys[k]), bits[k]);
-                keys[k] = -1;
-                bits[k] = 0u;
-            }
+        const int nu = nused;
+        for (int e = threadIdx.x; e < nu; e += kBinThreads) {
+            const int k = used[e];
+            atomicOr(reinterpret_cast<unsigned int*>(cw + keys[k]), bits[k]);
+            keys[k] = -1;
+            bits[k] = 0u;
         }
+        __syncthreads();
+        if (threadIdx.x == 0) nused = 0;
         __syncthreads();
     }
 }
@@ -238,19 +249,21 @@ __global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t w
 constexpr int kWTile = 128;
 constexpr int kWSlots = 256;
 
-__device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, bool& overflow) {
+__device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int* nused) {
     uint32_t h = (key * 2654435761u) & (kWSlots - 1);
-    for (int probe = 0; probe < kWSlots; ++probe) {
+    while (true) {  // a tile has at most 128 distinct cells: the 256-slot table never fills
         const int cur = keys[h];
         if (cur == (int)key) return (int)h;
         if (cur == -1) {
             const int old = atomicCAS(keys + h, -1, (int)key);
-            if (old == -1 || old == (int)key) return (int)h;
+            if (old == -1) {
+                used[atomicAdd(nused, 1)] = (int)h;
+                return (int)h;
+            }
+            if (old == (int)key) return (int)h;
         }
         h = (h + 1) & (kWSlots - 1);
     }
-    overflow = true;  // cannot happen: a tile has at most 128 distinct cells
-    return 0;
 }
 
 __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
@@ -259,10 +272,15 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
                                                u64* __restrict__ cocc) {
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
+    __shared__ int used_all[256 / kWarp][kWTile];
+    __shared__ int nused_all[256 / kWarp];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int* keys = keys_all[wid];
     uint32_t *cnt = cnt_all[wid], *olo = olo_all[wid], *ohi = ohi_all[wid];
+    int* used = used_all[wid];
+    int* nused = nused_all + wid;
     for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; }
+    if (lane == 0) *nused = 0;
     __syncwarp();
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -272,7 +290,6 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
         load_pts4(p, n, b4, vec, P);
         int hs[4];
         uint32_t rk[4];
-        bool ovf = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             hs[j] = -1;
@@ -280,7 +297,7 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
                 uint32_t lin;
                 int q;
                 dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                const int h = wbin_slot(keys, cid_of(cw, lin), ovf);
+                const int h = wbin_slot(keys, cid_of(cw, lin), used, nused);
                 hs[j] = h;
                 rk[j] = atomicAdd(cnt + h, 1u);
                 if (q < 32) atomicOr(olo + h, 1u << q);
@@ -288,17 +305,17 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
             }
         }
         __syncwarp();
-        // flush: lane per slot; the table's cnt[] is replaced by the cell's base slot
-        for (int k = lane; k < kWSlots; k += 32) {
+        // flush: lane per used slot; the table's cnt[] is replaced by the cell's base slot
+        const int nu = *nused;
+        for (int e = lane; e < nu; e += 32) {
+            const int k = used[e];
             const int cid = keys[k];
-            if (cid != -1) {
-                const uint32_t c = cnt[k];
-                const uint32_t old = atomicAdd(count + cid, c);
-                cnt[k] = old;
-                if (old <= (uint32_t)SPARSE_MAX && old + c > (uint32_t)SPARSE_MAX)
-                    atomicOr(dbits + (cid >> 5), 1u << (cid & 31u));   // the cell just became dense
-                atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
-            }
+            const uint32_t c = cnt[k];
+            const uint32_t old = atomicAdd(count + cid, c);
+            cnt[k] = old;
+            if (old <= (uint32_t)SPARSE_MAX && old + c > (uint32_t)SPARSE_MAX)
+                atomicOr(dbits + (cid >> 5), 1u << (cid & 31u));   // the cell just became dense
+            atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
         }
         __syncwarp();
         uint32_t sl[4];
@@ -312,7 +329,14 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
                 if (b4 + j < n) slot[b4 + j] = sl[j];
         }
         __syncwarp();
-        for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; }
+        for (int e = lane; e < nu; e += 32) {
+            const int k = used[e];
+            keys[k] = -1;
+            cnt[k] = 0u;
+            olo[k] = 0u;
+            ohi[k] = 0u;
+        }
+        if (lane == 0) *nused = 0;
         __syncwarp();
     }
 }
