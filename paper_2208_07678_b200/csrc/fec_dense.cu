@@ -172,15 +172,23 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
         const int64_t b4 = t0 + kBinIpt * threadIdx.x;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
+        // runs of this thread's points in the same bitmap word take one table update
+        uint32_t word = 0xffffffffu, wbits = 0u;
 #pragma unroll
         for (int j = 0; j < kBinIpt; ++j) {
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
                 dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                atomicOr(bits + bin_slot(keys, lin >> 5, used, &nused), 1u << (lin & 31u));
+                if ((lin >> 5) != word) {
+                    if (wbits) atomicOr(bits + bin_slot(keys, word, used, &nused), wbits);
+                    word = lin >> 5;
+                    wbits = 0u;
+                }
+                wbits |= 1u << (lin & 31u);
             }
         }
+        if (wbits) atomicOr(bits + bin_slot(keys, word, used, &nused), wbits);
         __syncthreads();
         const int nu = nused;
         for (int e = threadIdx.x; e < nu; e += kBinThreads) {
