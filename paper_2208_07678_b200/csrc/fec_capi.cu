@@ -495,8 +495,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         const unsigned lx = grid_for(dense_max(n), 256, cap);
         k_dense_link<<<dim3(lx, 3), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
         k_dense_link<<<dim3(lx, 24), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 3);
-        k_dense_overflow<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag,
-                                                                          dctx);
+        // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
+        k_dense_overflow<<<di.sms, 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
         k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
         k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
         k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
@@ -613,12 +613,14 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     const Layout& L = C.L;
     const unsigned ew = grid_for(n, 256, dev_info().sms * 8 * 4);
     // ---- a8+a9 fused (flatten + stats), a10 -----------------------------------------------------
-    k_flatten_if<<<ew, 256, 0, st>>>(L.parent, n, L.meta);
+    // one of each pair below returns at once (device-side choice)
+    const unsigned wave = grid_for(n, 256, dev_info().sms * 8);
+    k_flatten_if<<<wave, 256, 0, st>>>(L.parent, n, L.meta);
     mark(8, st);
     k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
     k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
     mark(9, st);
-    k_rootlab<<<ew, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
+    k_rootlab<<<wave, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
     k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
         L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
         B ? B->off_dev : nullptr, B ? B->nclouds : 0);
