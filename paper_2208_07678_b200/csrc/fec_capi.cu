@@ -119,6 +119,7 @@ struct Layout {
     uint32_t* dwpos;    // [n/32+2] popcount prefix of the bitmap words
     u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
     u64* ccoord;        // [n]   cell coordinates of each occupied cell, 21 bits each
+    int* slist;         // [n]   compact ids of the sparse cells (clouds with few of them)
     int* ncomp;         // per dense record: certain-connected components (<= 8)
     u64* dcoord;        // per dense record: cell coordinates, 21 bits each
     uint32_t* oflag;    // per dense record: slots whose pairs overflowed the queue
@@ -187,6 +188,7 @@ Layout carve(char* base, int64_t n) {
     L.sval1 = b.take<int>(n);
     L.scounts = b.take<uint32_t>((size_t)256 * ((n + RS_TILE - 1) / RS_TILE));
     L.ccoord = b.take<u64>(n);
+    L.slist = b.take<int>(n);
     L.ncomp = b.take<int>(dense_max(n));
     L.dcoord = b.take<u64>(dense_max(n));
     L.oflag = b.take<uint32_t>(dense_max(n));
@@ -489,8 +491,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         mark(5, st);
         k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
                                                                          L.parent, L.meta, n);
-        k_union_sparse_local<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
-                                                                               L.parent, L.meta, n);
+        k_slist<<<grid_for(n, 256, cap * 4), 256, 0, st>>>(L.cstart, L.slist, L.meta, n);
+        k_union_sparse_local<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart,
+                                                                               L.slist, g, L.parent, L.meta, n);
         mark(6, st);
         const unsigned lx = grid_for(dense_max(n), 256, cap);
         k_dense_link<<<dim3(lx, 3), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
@@ -500,7 +503,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
         k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
         k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
-        launches += 8;
+        launches += 9;
         if (g_instrument) {
             k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);
             ++launches;

@@ -1058,8 +1058,8 @@ constexpr int SP_CHUNK = 32;
 template <bool LOCAL>
 __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spts, const uint2* __restrict__ cw,
                                                   const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
-                                                  const Grid& g, int* __restrict__ parent, Meta* __restrict__ meta,
-                                                  int64_t n) {
+                                                  const int* __restrict__ slist, const Grid& g,
+                                                  int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
     if ((4 * (int64_t)meta->cells > n) == LOCAL) return;
     const uint32_t cells = (uint32_t)meta->cells;  // occupied cells (compact ids)
     __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
@@ -1069,19 +1069,26 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     uint32_t* list = lists[threadIdx.x >> 5];
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t base = warp * SP_CHUNK; base < cells; base += nwarps * SP_CHUNK) {
+    const uint32_t nitems = LOCAL ? (uint32_t)meta->nsparse : cells;
+    for (uint32_t base = warp * SP_CHUNK; base < nitems; base += nwarps * SP_CHUNK) {
         int total = 0;
+        if constexpr (LOCAL) {
+            // consecutive entries of the sparse-cell list (k_slist)
+            if (base + lane < nitems) list[lane] = (uint32_t)__ldg(slist + base + lane);
+            total = (int)min((uint32_t)SP_CHUNK, nitems - base);
+        } else {
 #pragma unroll
-        for (int j = 0; j < SP_CHUNK / 32; ++j) {
-            const uint32_t P = base + j * 32 + lane;
-            bool act = false;
-            if (P < cells) {
-                const int cnt = (int)__ldg(cstart + P + 1) - (int)__ldg(cstart + P);
-                act = cnt > 0 && cnt <= SPARSE_MAX;
+            for (int j = 0; j < SP_CHUNK / 32; ++j) {
+                const uint32_t P = base + j * 32 + lane;
+                bool act = false;
+                if (P < cells) {
+                    const int cnt = (int)__ldg(cstart + P + 1) - (int)__ldg(cstart + P);
+                    act = cnt > 0 && cnt <= SPARSE_MAX;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, act);
+                if (act) list[total + __popc(m & ((1u << lane) - 1u))] = P;
+                total += __popc(m);
             }
-            const unsigned m = __ballot_sync(0xffffffffu, act);
-            if (act) list[total + __popc(m & ((1u << lane) - 1u))] = P;
-            total += __popc(m);
         }
         __syncwarp();
         for (int e0 = 0; e0 < total; e0 += 32) {
@@ -1163,19 +1170,43 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     }
 }
 
+// LOCAL clouds: the sparse cells in one compact list, so every lane of the union kernel owns a
+// real sparse cell and all of them run in one wave.
+__global__ void __launch_bounds__(256) k_slist(const uint32_t* __restrict__ cstart, int* __restrict__ slist,
+                                              Meta* __restrict__ meta, int64_t n) {
+    if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_union_sparse walks the cells itself
+    const int64_t U = meta->cells;
+    const int64_t ur = (U + 31) & ~int64_t(31);
+    const int lane = threadIdx.x & 31;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
+        bool sp = false;
+        if (u < U) {
+            const uint32_t c = __ldg(cstart + u + 1) - __ldg(cstart + u);
+            sp = c > 0 && c <= (uint32_t)SPARSE_MAX;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, sp);
+        if (!m) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
                                                      const u64* __restrict__ ccoord,
                                                      const uint32_t* __restrict__ cstart, Grid g,
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
-    union_sparse_body<false>(spts, cw, ccoord, cstart, g, parent, meta, n);
+    union_sparse_body<false>(spts, cw, ccoord, cstart, nullptr, g, parent, meta, n);
 }
 __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __restrict__ spts,
                                                            const uint2* __restrict__ cw,
                                                            const u64* __restrict__ ccoord,
-                                                           const uint32_t* __restrict__ cstart, Grid g,
+                                                           const uint32_t* __restrict__ cstart,
+                                                           const int* __restrict__ slist, Grid g,
                                                            int* __restrict__ parent, Meta* __restrict__ meta,
                                                            int64_t n) {
-    union_sparse_body<true>(spts, cw, ccoord, cstart, g, parent, meta, n);
+    union_sparse_body<true>(spts, cw, ccoord, cstart, slist, g, parent, meta, n);
 }
 
 }  // namespace fec

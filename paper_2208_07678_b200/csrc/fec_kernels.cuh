@@ -31,6 +31,7 @@ struct Meta {
     int internal_error;               // != 0: an internal invariant failed (never expected)
     int nitems2;                      // dense-grid mode: queued pairs still apart after the certain unions
     unsigned long long near_pairs;    // a1: consecutive input pairs within 2 cells (input coherence)
+    int nsparse;                      // dense-grid mode: occupied cells with <= SPARSE_MAX points
     int nslices_extra;                // dense-grid mode: extra slices of heavy uncertain pairs
 };
 
@@ -114,7 +115,8 @@ __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int*
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
                                int* parent, Meta* meta, int64_t n);
 __global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
-                                     Grid g, int* parent, Meta* meta, int64_t n);
+                                     const int* slist, Grid g, int* parent, Meta* meta, int64_t n);
+__global__ void k_slist(const uint32_t* cstart, int* slist, Meta* meta, int64_t n);
 __global__ void k_dense_link(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
                              uint32_t* oflags, DenseCtx C, int k0);
 __global__ void k_dense_overflow(Grid g, const uint2* cw, const int* crec, const int* ncomp, const u64* dcoord,
