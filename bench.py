@@ -140,9 +140,10 @@ def algorithmic_bytes(stage: str, n: int, st: dict) -> float:
         model = {
             "a1_bbox_validate": 12.0 * n,
             # occupancy bitmap + word bases (C/8 B, ~9 touches), cell lists (28 B/cell), two
-            # reads of xyz, slots, per-cell counts + fine masks, dense components (~180 B/cell)
-            "a2_bin_keys": 24.0 * n + 4.0 * n + 1.125 * C + 44.0 * U + 180.0 * nd,
-            "a3_sort": 8.0 * U + 12.0 * n + 4.0 * n + 16.0 * n,  # scan counts; xyz + slot -> float4
+            # reads of xyz, per-cell counts + fine masks
+            "a2_bin_keys": 24.0 * n + 1.125 * C + 44.0 * U,
+            # scan counts, cursors, dense records + components (~180 B/cell), xyz -> float4
+            "a3_sort": 24.0 * U + 180.0 * nd + 12.0 * n + 16.0 * n,
             "a4_gather_init": 16.0 * n + 8.0 * n + 8.0 * ns,      # float4 -> parent, idx (+ root accumulators)
             "a5_tables": 0.0,
             "a6a7_union_sparse": 24.0 * ns + 8.0 * U,             # sparse points + parents, cell starts

@@ -426,19 +426,19 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
             k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
                                                                            L.ccoord, g, L.meta);
-            k_dcount<<<grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4), 256, 0, st>>>(
-                pts, n, g, L.cw, L.cstart, L.slot, L.dbits, L.cocc);
+            const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
+            k_dcount2<<<wt, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.cocc);
+            // a3: counting sort = scan (over the occupied cells only) + cursor scatter
+            mark(2, st);
+            launches += 2 + exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
+            k_ccount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.slot, L.meta);
             k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
-            launches += 3 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
+            launches += 2 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
             k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
             k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
                                                                       L.dcoord, L.oflag, dctx);
-            launches += 2;
-            // a3: counting sort = scan (over the occupied cells only) + scatter
-            mark(2, st);
-            launches += exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
-            k_dscatter<<<ew4, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.slot, L.spts);
-            ++launches;
+            k_dscatter2<<<wt, 256, 0, st>>>(pts, n, g, L.cw, L.slot, L.spts);  // slot = per-cell cursors here
+            launches += 3;
         } else {
             // a2: linear cell keys, LSD radix sort over their significant bits
             mark(1, st);

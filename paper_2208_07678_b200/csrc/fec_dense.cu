@@ -274,10 +274,12 @@ __device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int
     }
 }
 
-__global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int64_t n, Grid g,
-                                               const uint2* __restrict__ cw, uint32_t* __restrict__ count,
-                                               uint32_t* __restrict__ slot, uint32_t* __restrict__ dbits,
-                                               u64* __restrict__ cocc) {
+// Counting without return values: per warp-tile cell counts and fine-occupancy bits are added
+// to the cell's counters fire-and-forget (no dependent round trip); slots are assigned later
+// by k_dscatter2 against per-cell cursors.
+__global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, Grid g,
+                                                const uint2* __restrict__ cw, uint32_t* __restrict__ count,
+                                                u64* __restrict__ cocc) {
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
     __shared__ int used_all[256 / kWarp][kWTile];
@@ -296,11 +298,85 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
+        // runs of this thread's points in one cell take one table update
+        uint32_t rc = 0xffffffffu, rn = 0u;
+        u64 rb = 0ull;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (b4 + j < n) {
+                uint32_t lin;
+                int q;
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
+                const uint32_t cid = cid_of(cw, lin);
+                if (cid != rc) {
+                    if (rn) {
+                        const int h = wbin_slot(keys, rc, used, nused);
+                        atomicAdd(cnt + h, rn);
+                        if ((uint32_t)rb) atomicOr(olo + h, (uint32_t)rb);
+                        if ((uint32_t)(rb >> 32)) atomicOr(ohi + h, (uint32_t)(rb >> 32));
+                    }
+                    rc = cid;
+                    rn = 0u;
+                    rb = 0ull;
+                }
+                ++rn;
+                rb |= 1ull << q;
+            }
+        }
+        if (rn) {
+            const int h = wbin_slot(keys, rc, used, nused);
+            atomicAdd(cnt + h, rn);
+            if ((uint32_t)rb) atomicOr(olo + h, (uint32_t)rb);
+            if ((uint32_t)(rb >> 32)) atomicOr(ohi + h, (uint32_t)(rb >> 32));
+        }
+        __syncwarp();
+        const int nu = *nused;
+        for (int e = lane; e < nu; e += 32) {
+            const int k = used[e];
+            const int cid = keys[k];
+            atomicAdd(count + cid, cnt[k]);
+            atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
+            keys[k] = -1;
+            cnt[k] = 0u;
+            olo[k] = 0u;
+            ohi[k] = 0u;
+        }
+        __syncwarp();
+        if (lane == 0) *nused = 0;
+        __syncwarp();
+    }
+}
+
+// Scatter into cell order: per warp-tile, one atomicAdd on the cell's cursor (initialised to
+// the cell start) per distinct cell gives the tile's base; ranks inside the tile come from
+// the warp's shared-memory table.
+__global__ void __launch_bounds__(256) k_dscatter2(const float* __restrict__ p, int64_t n, Grid g,
+                                                  const uint2* __restrict__ cw, uint32_t* __restrict__ cursor,
+                                                  float4* __restrict__ spts) {
+    __shared__ int keys_all[256 / kWarp][kWSlots];
+    __shared__ uint32_t cnt_all[256 / kWarp][kWSlots];
+    __shared__ int used_all[256 / kWarp][kWTile];
+    __shared__ int nused_all[256 / kWarp];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int* keys = keys_all[wid];
+    uint32_t* cnt = cnt_all[wid];
+    int* used = used_all[wid];
+    int* nused = nused_all + wid;
+    for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; }
+    if (lane == 0) *nused = 0;
+    __syncwarp();
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWTile; t0 < n; t0 += nw * kWTile) {
+        const int64_t b4 = t0 + 4 * lane;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
         int hs[4];
         uint32_t rk[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             hs[j] = -1;
+            rk[j] = 0u;
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
@@ -308,44 +384,43 @@ __global__ void __launch_bounds__(256) k_dcount(const float* __restrict__ p, int
                 const int h = wbin_slot(keys, cid_of(cw, lin), used, nused);
                 hs[j] = h;
                 rk[j] = atomicAdd(cnt + h, 1u);
-                if (q < 32) atomicOr(olo + h, 1u << q);
-                else atomicOr(ohi + h, 1u << (q - 32));
             }
         }
         __syncwarp();
-        // flush: lane per used slot; the table's cnt[] is replaced by the cell's base slot
         const int nu = *nused;
         for (int e = lane; e < nu; e += 32) {
             const int k = used[e];
-            const int cid = keys[k];
-            const uint32_t c = cnt[k];
-            const uint32_t old = atomicAdd(count + cid, c);
-            cnt[k] = old;
-            if (old <= (uint32_t)SPARSE_MAX && old + c > (uint32_t)SPARSE_MAX)
-                atomicOr(dbits + (cid >> 5), 1u << (cid & 31u));   // the cell just became dense
-            atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
+            cnt[k] = atomicAdd(cursor + keys[k], cnt[k]);  // the tile's base inside the cell
         }
         __syncwarp();
-        uint32_t sl[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) sl[j] = hs[j] >= 0 ? cnt[hs[j]] + rk[j] : 0u;
-        if (b4 + 4 <= n) {
-            *reinterpret_cast<uint4*>(slot + b4) = make_uint4(sl[0], sl[1], sl[2], sl[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (b4 + j < n) slot[b4 + j] = sl[j];
-        }
+        for (int j = 0; j < 4; ++j)
+            if (hs[j] >= 0) spts[cnt[hs[j]] + rk[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
         __syncwarp();
         for (int e = lane; e < nu; e += 32) {
             const int k = used[e];
             keys[k] = -1;
             cnt[k] = 0u;
-            olo[k] = 0u;
-            ohi[k] = 0u;
         }
         if (lane == 0) *nused = 0;
         __syncwarp();
+    }
+}
+
+// Dense bits of the occupied cells from the cell starts; also the scatter cursors.
+__global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
+                                               uint32_t* __restrict__ cursor, const Meta* __restrict__ meta) {
+    const int64_t U = meta->cells;
+    const int64_t ur = (U + 31) & ~int64_t(31);
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
+        bool dense = false;
+        if (u < U) {
+            const uint32_t c0 = __ldg(cstart + u);
+            dense = __ldg(cstart + u + 1) - c0 > (uint32_t)SPARSE_MAX;
+            cursor[u] = c0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, dense);
+        if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
     }
 }
 
@@ -602,39 +677,6 @@ __global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ 
             size[node] = 0;
             minidx[node] = 0x7fffffff;
             C.cmask[8 * r + j] = j < k ? comp[j] : 0ull;
-        }
-    }
-}
-
-// ---- a3: scatter into cell order (after the exclusive scan of count -> cstart) ------------
-// Only the float4 (x, y, z, idx) is scattered: for shuffled inputs every scattered array
-// costs a DRAM read-modify-write per point, so everything else is derived in sorted order.
-__global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n, Grid g,
-                                                 const uint2* __restrict__ cw, const uint32_t* __restrict__ cstart,
-                                                 const uint32_t* __restrict__ slot, float4* __restrict__ spts) {
-    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
-    const int64_t groups = (n + 3) / 4;
-    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b4 = 4 * gi;
-        Pts4 P;
-        load_pts4(p, n, b4, vec, P);
-        uint32_t sl[4];
-        if (b4 + 4 <= n) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(slot + b4));
-            sl[0] = v.x; sl[1] = v.y; sl[2] = v.z; sl[3] = v.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) sl[j] = b4 + j < n ? __ldg(slot + b4 + j) : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (b4 + j < n) {
-                uint32_t lin;
-                int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                spts[__ldg(cstart + cid_of(cw, lin)) + sl[j]] =
-                    make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
-            }
         }
     }
 }

@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
 // Single-GPU tail, a8+a9 fused: every point's root (read-only walk; the root is written back,
 // which flattens the forest for k_relabel) and the component size + minimum input index,
 // aggregated per warp and per block as in k_stats.  Roots' accumulators were initialised
-// earlier (points of sparse cells in k_dscatter / k_sgather, component nodes in k_dcomps, hashed
+// earlier (points of sparse cells in k_dinit / k_sgather, component nodes in k_dcomps, hashed
 // mode in k_init_uf).
 __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                                    int* __restrict__ size, int* __restrict__ minidx,

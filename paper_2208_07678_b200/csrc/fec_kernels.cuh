@@ -78,14 +78,15 @@ __global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
 __global__ void k_cpopc(const uint2* cw, int64_t words, uint32_t* cnt);
 __global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t* clin, uint32_t* count, u64* cocc,
                         u64* ccoord, Grid g, Meta* meta);
-__global__ void k_dcount(const float* p, int64_t n, Grid g, const uint2* cw, uint32_t* count, uint32_t* slot,
-                         uint32_t* dbits, u64* cocc);
 __global__ void k_lkey(const float* p, int64_t n, Grid g, uint32_t* key, int* val);
 __global__ void k_smark(const uint32_t* key, int64_t n, uint2* cw);
 __global__ void k_sgather(const float* p, const uint32_t* key, const int* val, int64_t n, Grid g, const uint2* cw,
                           float4* spts, uint32_t* cstart, u64* cocc, int* parent, int* sidx, int* size, int* minidx,
                           const Meta* meta);
 __global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* meta);
+__global__ void k_dcount2(const float* p, int64_t n, Grid g, const uint2* cw, uint32_t* count, u64* cocc);
+__global__ void k_dscatter2(const float* p, int64_t n, Grid g, const uint2* cw, uint32_t* cursor, float4* spts);
+__global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
                              Meta* meta);
@@ -105,8 +106,6 @@ struct DenseCtx {
 };
 __global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp, int* size, int* minidx, u64* dcoord,
                          uint32_t* oflags, DenseCtx C);
-__global__ void k_dscatter(const float* p, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
-                           const uint32_t* slot, float4* spts);
 __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                         const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* size,
                         int* minidx, int* sidx);
