@@ -1241,6 +1241,15 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
     union_sparse_body<false>(spts, cw, ccoord, cstart, nullptr, g, parent, meta, n);
 }
+// LOCAL clouds have few sparse cells (C4: 73k of 358k cells, 0.8% of the points), so the
+// kernel is a few short waves whose time is the dependent-load chain per cell.  16 lanes per
+// sparse cell P (<= 6 points): lane l tests P's own pair l (15 pairs), the ballot gives P's
+// local components (3-bit labels = min local index) and lanes 1..5 unite each point with its
+// label; then lane k < 13 takes forward neighbour k and unites a neighbour point once per
+// local component of P it touches.
+__constant__ unsigned char c_pair_s[16] = {0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 3, 3, 4, 7};
+__constant__ unsigned char c_pair_t[16] = {1, 2, 3, 4, 5, 2, 3, 4, 5, 3, 4, 5, 4, 5, 5, 7};
+static_assert(SPARSE_MAX <= 6, "16-lane sparse kernel covers <= 15 own pairs");
 __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __restrict__ spts,
                                                            const uint2* __restrict__ cw,
                                                            const u64* __restrict__ ccoord,
@@ -1248,7 +1257,85 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
                                                            const int* __restrict__ slist, Grid g,
                                                            int* __restrict__ parent, Meta* __restrict__ meta,
                                                            int64_t n) {
-    union_sparse_body<true>(spts, cw, ccoord, cstart, slist, g, parent, meta, n);
+    if (4 * (int64_t)meta->cells > n) return;
+    const uint32_t nitems = (uint32_t)meta->nsparse;
+    const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
+    const float t2 = g.t2;
+    unsigned long long n_tests = 0;
+    const uint32_t stride = (gridDim.x * blockDim.x) >> 4;
+    const uint32_t warp0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 2;
+    for (uint32_t base = warp0; base < nitems; base += stride) {  // warp-uniform trip count
+        const uint32_t it = base + half;
+        const bool valid = it < nitems;
+        int ps = 0, np = 0;
+        uint32_t P = 0;
+        if (valid) {
+            P = (uint32_t)__ldg(slist + it);
+            ps = (int)__ldg(cstart + P);
+            np = (int)__ldg(cstart + P + 1) - ps;
+        }
+        // own pairs, one per lane
+        const int ls = c_pair_s[sub], lt = c_pair_t[sub];
+        bool e = false;
+        if (valid && lt < np) {
+            ++n_tests;
+            e = pred(__ldg(spts + ps + ls), __ldg(spts + ps + lt), t2);
+        }
+        const unsigned em = (__ballot_sync(0xffffffffu, e) >> (16 * half)) & 0x7fffu;
+        // closure over <= 6 nodes: reach[i] as 6-bit masks
+        uint32_t r[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) r[i] = 1u << i;
+#pragma unroll
+        for (int p = 0; p < 15; ++p)
+            if ((em >> p) & 1u) {
+                const int a = (p < 5) ? 0 : (p < 9) ? 1 : (p < 12) ? 2 : (p < 14) ? 3 : 4;
+                const int b = (p < 5) ? p + 1 : (p < 9) ? p - 3 : (p < 12) ? p - 6 : (p < 14) ? p - 8 : 5;
+                r[a] |= 1u << b;
+                r[b] |= 1u << a;
+            }
+#pragma unroll
+        for (int round = 0; round < 3; ++round)
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                uint32_t acc = r[i];
+#pragma unroll
+                for (int j = 0; j < 6; ++j)
+                    if ((r[i] >> j) & 1u) acc |= r[j];
+                r[i] = acc;
+            }
+        uint32_t lab = 0;  // 3-bit label (min local index of the component) per local point
+#pragma unroll
+        for (int i = 0; i < 6; ++i) lab |= (uint32_t)(__ffs(r[i]) - 1) << (3 * i);
+        if (valid && sub >= 1 && sub < np) {
+            const int l = (int)((lab >> (3 * sub)) & 7u);
+            if (l != sub) uf_unite(parent, ps + sub, ps + l);
+        }
+        // forward neighbour `sub`
+        if (!valid || sub >= 13) continue;
+        const u64 pc = __ldg(ccoord + P);
+        const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
+        uint32_t Q;
+        if (!dense_neighbor(g, c, c_fwd[sub][0], c_fwd[sub][1], c_fwd[sub][2], Q)) continue;
+        const int qc = cid_lookup(cw, Q);
+        if (qc < 0) continue;
+        const int qs = (int)__ldg(cstart + qc), qe = (int)__ldg(cstart + qc + 1);
+        if (qe - qs > SPARSE_MAX) continue;  // dense neighbours are handled by k_dense_link
+        for (int t = qs; t < qe; ++t) {
+            const float4 b = __ldg(spts + t);
+            uint32_t touched = 0;  // local components of P within d of t
+            for (int s2 = 0; s2 < np; ++s2) {
+                ++n_tests;
+                if (pred(__ldg(spts + ps + s2), b, t2)) touched |= 1u << ((lab >> (3 * s2)) & 7u);
+            }
+            while (touched) {
+                const int l = __ffs(touched) - 1;
+                touched &= touched - 1;
+                uf_unite(parent, ps + l, t);
+            }
+        }
+    }
+    if (meta->instrument && n_tests) atomicAdd(&meta->pair_tests, n_tests);
 }
 
 }  // namespace fec
