@@ -8,6 +8,8 @@ It shares no code with the CUDA path and never imports ``paper_2208_07678_b200``
 * ``fec(points, d_th, min_size, max_size)`` — grid flood fill in C (fec_oracle.c).
 * ``brute_fec(...)`` — O(n^2) definition in numpy (brute.py), for tiny inputs.
 * ``Index(points, d_th).component(i)`` — (min C(i), |C(i)|) for sampled full-size parity.
+* ``ground.ransac_ground(...)`` — RANSAC plane-fit ground removal (ground_oracle.c + numpy
+  least-squares refinement), SURVEY §8(f) N2.
 """
 from __future__ import annotations
 
@@ -21,6 +23,7 @@ from .brute import brute_fec, brute_labels_unfiltered, pred_f32, d2_f32  # noqa:
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fec_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "ground_oracle.c")]
 _LIB = os.path.join(_HERE, "_build", "liboracle.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_RANGE, ERR_NOMEM = 0, -1, -2, -3, -4
@@ -30,8 +33,8 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-shared", "
 
 def compile_oracle(force: bool = False) -> str:
     os.makedirs(os.path.dirname(_LIB), exist_ok=True)
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, *_SRCS, "-lm"])
     return _LIB
 
 
@@ -60,6 +63,19 @@ def lib():
         L.oracle_component.restype = ctypes.c_int
         L.oracle_component.argtypes = [ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.oracle_ground_plane.restype = ctypes.c_int
+        L.oracle_ground_plane.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double,
+                                          ctypes.c_void_p, i32p]
+        L.oracle_ground_residual.restype = ctypes.c_float
+        L.oracle_ground_residual.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_ground_counts.restype = None
+        L.oracle_ground_counts.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                           ctypes.c_float, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p]
+        L.oracle_ground_mask.restype = ctypes.c_int64
+        L.oracle_ground_mask.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float,
+                                         ctypes.c_void_p]
         _lib = L
     return _lib
 

@@ -29,7 +29,8 @@ import numpy as np
 
 __all__ = [
     "Workload", "CONFIGS", "make_config", "c1_blobs", "lidar_scan", "c3_map", "c4_loop",
-    "c5_stress", "random_cloud", "PARITY_GEOMETRIES", "sha256_f32",
+    "c5_stress", "random_cloud", "PARITY_GEOMETRIES", "sha256_f32", "lidar_scan_ground", "ground_map",
+    "plane_and_box", "ransac_triplets", "make_ground_config", "GROUND_PARAMS",
 ]
 
 
@@ -160,16 +161,21 @@ def _cast_cyls(ox, oy, cyls, t_best, yaw):
     np.minimum.at(t_best, (colb.ravel(), ring.ravel()), t.ravel())
 
 
-def _scan(rng, ox, oy, yaw, boxes, cyls, noise_sigma=0.02):
+def _scan(rng, ox, oy, yaw, boxes, cyls, noise_sigma=0.02, keep_ground=False):
     """One spinning scan from sensor (ox, oy, SENSOR_H) with heading ``yaw``.
-    Returns float64 [m, 3] object hits in azimuth-major acquisition order."""
+    Returns float64 [m, 3] object hits in azimuth-major acquisition order (plus the hits
+    on the ground plane z = 0 when ``keep_ground``)."""
     t_best = np.full((N_AZ, N_RINGS), np.inf)
     _cast_boxes(ox, oy, boxes, t_best, yaw)
     _cast_cyls(ox, oy, cyls, t_best, yaw)
     se = np.sin(ELEV)
     with np.errstate(divide="ignore"):
         t_ground = np.where(se < 0, -SENSOR_H / se, np.inf)[None, :]
+    if keep_ground:
+        t_best = np.minimum(t_best, t_ground)
     keep = (t_best < t_ground) & (t_best <= MAX_RANGE)
+    if keep_ground:
+        keep = t_best <= MAX_RANGE
     # range noise is drawn for every ray so the RNG stream does not depend on hits
     noise = rng.normal(0.0, noise_sigma, size=t_best.shape)
     cols, rings = np.nonzero(keep)          # row-major => azimuth-major order
@@ -215,6 +221,83 @@ def c3_map(seed: int = 2, n_poses: int = 100, n_boxes: int = 300, n_cyls: int = 
         boxes, cyls = _objects_around(rng, x, y, n_boxes, n_cyls)
         out.append(_scan(rng, x, y, yaw, boxes, cyls))
     return _f32(np.concatenate(out, 0))
+
+
+# --------------------------------------------------------------------------------------
+# Ground-removal inputs: scans WITH their ground hits, tilted as a whole
+# (a pitched sensor / sloped road), and the caller-drawn RANSAC index triplets.
+# --------------------------------------------------------------------------------------
+GROUND_PARAMS = {"threshold": 0.2, "iterations": 100, "max_tilt_deg": 30.0}  # SPEC.md L323 defaults
+
+
+def _tilt(pts: np.ndarray, tilt_deg: float, axis_deg: float = 30.0) -> np.ndarray:
+    """Rotate by ``tilt_deg`` about the horizontal axis at bearing ``axis_deg``."""
+    a = math.radians(axis_deg)
+    k = np.array([math.cos(a), math.sin(a), 0.0])
+    t = math.radians(tilt_deg)
+    K = np.array([[0, -k[2], k[1]], [k[2], 0, -k[0]], [-k[1], k[0], 0]])
+    R = np.eye(3) + math.sin(t) * K + (1 - math.cos(t)) * (K @ K)
+    return pts @ R.T
+
+
+def lidar_scan_ground(seed: int = 5, n_boxes: int = 60, n_cyls: int = 40, tilt_deg: float = 2.0) -> np.ndarray:
+    """G2: one 64-beam scan with its ground hits kept (~75% of the points), tilted."""
+    rng = np.random.default_rng(seed)
+    boxes, cyls = _objects_around(rng, 0.0, 0.0, n_boxes, n_cyls)
+    return _f32(_tilt(_scan(rng, 0.0, 0.0, 0.0, boxes, cyls, keep_ground=True), tilt_deg))
+
+
+def ground_map(seed: int = 6, n_poses: int = 100, n_boxes: int = 300, n_cyls: int = 200,
+               tilt_deg: float = 2.0) -> np.ndarray:
+    """G3: C3's recipe (scans along a gently curving path) with the ground hits kept."""
+    rng = np.random.default_rng(seed)
+    x = y = yaw = 0.0
+    out = []
+    for k in range(n_poses):
+        if k > 0:
+            yaw += math.radians(0.5)
+            x += math.cos(yaw)
+            y += math.sin(yaw)
+        boxes, cyls = _objects_around(rng, x, y, n_boxes, n_cyls)
+        out.append(_scan(rng, x, y, yaw, boxes, cyls, keep_ground=True))
+    return _f32(_tilt(np.concatenate(out, 0), tilt_deg))
+
+
+def plane_and_box(seed: int = 7, n_plane: int = 1000, n_box: int = 100) -> np.ndarray:
+    """SPEC.md L313's example: n_plane points on z = 0 then n_box points in a box at z in [1, 3]."""
+    rng = np.random.default_rng(seed)
+    g = np.zeros((n_plane, 3))
+    g[:, :2] = rng.uniform(-10.0, 10.0, size=(n_plane, 2))
+    b = rng.uniform([2.0, 2.0, 1.0], [4.0, 4.0, 3.0], size=(n_box, 3))
+    return _f32(np.concatenate([g, b], 0))
+
+
+def ransac_triplets(n: int, H: int = 100, seed: int = 0) -> np.ndarray:
+    """int32 [H, 3]: per hypothesis three distinct indices in [0, n) (the random sample a
+    RANSAC iteration draws, passed to both the oracle and the CUDA path; reading G1)."""
+    rng = np.random.default_rng(10_000 + seed)
+    if n < 3:
+        return rng.integers(0, max(n, 1), size=(H, 3)).astype(np.int32)
+    t = rng.integers(0, n, size=(H, 3))
+    for _ in range(100):
+        bad = (t[:, 0] == t[:, 1]) | (t[:, 0] == t[:, 2]) | (t[:, 1] == t[:, 2])
+        if not bad.any():
+            break
+        t[bad] = rng.integers(0, n, size=(int(bad.sum()), 3))
+    return np.ascontiguousarray(t, dtype=np.int32)
+
+
+def make_ground_config(name: str, scale: float = 1.0):
+    """(points, triplets, threshold, max_tilt_deg) for G2 / G3 (scale shrinks G3's poses)."""
+    if name == "G2":
+        pts = lidar_scan_ground(5)
+    elif name == "G3":
+        pts = ground_map(6, n_poses=max(1, int(round(100 * scale))))
+    else:
+        raise KeyError(name)
+    H = GROUND_PARAMS["iterations"]
+    return pts, ransac_triplets(pts.shape[0], H, seed=int(name[1:])), GROUND_PARAMS["threshold"], \
+        GROUND_PARAMS["max_tilt_deg"]
 
 
 C4_LATERAL_HI = 6.5
