@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0,
                     help="per-scan mode: cluster this many independent C2-recipe scans per step in one "
                          "fec_cluster_batch_ws call (SURVEY N1)")
+    ap.add_argument("--ground", default="", choices=["", "G2", "G3"],
+                    help="time the ground-removal pre-pass (SURVEY N2) on G2 (one scan) or G3 (100-scan map) "
+                         "instead of clustering")
     return ap.parse_args()
 
 
@@ -456,11 +459,132 @@ def run_batch(args, local: int):
     print(json.dumps(line), flush=True)
 
 
+def fp32_alu_peak_tflops(sm_mhz=None) -> float:
+    """Non-tensor fp32 FMA peak: 148 SMs x 128 FP32 lanes x 2 flops x clock."""
+    mhz = sm_mhz or 1965.0
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def run_ground(args, local: int):
+    """Ground removal (RANSAC plane fit) on G2/G3: H = 100 hypotheses, every
+    point tested against every plane (the dominant kernel k_g_count: 3 fused multiply-adds per
+    test), then the best plane's survivors compacted.  ALU roofline of k_g_count."""
+    import math
+    import torch
+    import paper_2208_07678_b200 as fec
+    fec.lib()
+    pts, tri, thr, tilt = synth.make_ground_config(args.ground)
+    n, H = pts.shape[0], tri.shape[0]
+    ct = math.cos(math.radians(tilt))
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(pts).to(dev)
+    t = torch.from_numpy(tri).to(dev)
+    out = (torch.empty((n, 3), dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+           torch.empty(fec.GROUND_RESULT_BYTES, dtype=torch.uint8, device=dev))
+    ws = torch.empty(fec.ground_workspace_bytes(n, H), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return fec.remove_ground(x, t, thr, cos_max_tilt=ct, out=out, workspace=ws)
+
+    step()
+    torch.cuda.synchronize()
+    info = fec.ground_result(out[2])
+    check = None
+    if args.check:
+        from oracle import ground as og
+        w = og.ransac_ground(pts, tri, thr, ct, (n + 9) // 10)
+        check = bool(w.best == info["best"] and np.array_equal(out[1][:info["n_keep"]].cpu().numpy(), w.keep_idx))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    fec.set_timing(True)   # events around k_g_count inside each call (same stream)
+    kms = 0.0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+            kms += fec.ground_count_ms()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    fec.set_timing(False)
+    kms /= args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = clk.summary()
+    # e2e: pinned host points + triplets in, result record + survivor indices out
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(pts).pin_memory()
+        ht = torch.from_numpy(tri).pin_memory()
+        hk = torch.empty(n, dtype=torch.int32).pin_memory()
+        hr = torch.empty(fec.GROUND_RESULT_BYTES, dtype=torch.uint8).pin_memory()
+
+        def host_step():
+            x.copy_(hp, non_blocking=True)
+            t.copy_(ht, non_blocking=True)
+            fec.remove_ground(x, t, thr, cos_max_tilt=ct, out=out, workspace=ws)
+            hr.copy_(out[2], non_blocking=True)
+            hk.copy_(out[1], non_blocking=True)
+
+        for _ in range(2):
+            host_step()
+        torch.cuda.synchronize()
+        k = max(3, args.steps // 2)
+        e0.record(stream)
+        for _ in range(k):
+            host_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / k
+        e2e = {"value": n / (ems * 1e-3) / 1e6, "unit": "Mpoints/s", "h2d_bytes_per_step": 12 * n + 12 * H,
+               "d2h_bytes_per_step": 4 * n + fec.GROUND_RESULT_BYTES, "ms_per_step": ems}
+    tests = float(n) * H
+    flops = 6.0 * tests  # 3 FMA per point-plane test
+    peak = fp32_alu_peak_tflops(clocks.get("sm_max_mhz"))
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import ground as og
+        hs = 4 if args.ground == "G3" else H
+        t0 = time.perf_counter()
+        og.counts(pts, tri[:hs], thr, ct)
+        dt = time.perf_counter() - t0
+        cpu = {"value": n * (hs / H) / dt / 1e6, "unit": "Mpoints/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle inlier counting of {hs} of the {H} hypotheses over all {n} points "
+                         f"(scaled to the full {H}-hypothesis step)"}
+    line = {
+        "metric": "Mpoints/s ground-removed", "value": n / (ms * 1e-3) / 1e6, "unit": "Mpoints/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.ground}: RANSAC plane-fit ground removal (SURVEY N2), {H} hypotheses, "
+                               f"threshold {thr} m, max tilt {tilt} deg, ground kept in the LiDAR recipe, tilted 2 deg",
+                   "n_points": int(n), "hypotheses": int(H), "ground_points": int(info["n_inliers"]),
+                   "parallelism": "single",
+                   "l2": "inputs exceed L2" if 12 * n > 126e6 else "inputs below L2 size"},
+        "e2e": e2e,
+        "roofline": {"bound": "alu", "kernel": "k_g_count", "achieved": flops / (kms * 1e-3) / 1e12,
+                     "peak": peak, "unit": "TFLOP/s", "frac": flops / (kms * 1e-3) / 1e12 / peak, "traffic": None,
+                     "kernel_ms": kms, "algorithmic_flops": flops,
+                     "peak_source": "derived: 148 SMs x 128 fp32 lanes x 2 x max SM clock (DESIGN.md §8c)"},
+        "cpu_baseline": cpu,
+        "gpu_launches": 8 * args.steps,
+        "clocks": clocks,
+    }
+    if check is not None:
+        line["parity_bit_exact"] = check
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.ground and world == 1:
+        run_ground(args, local)
         return
     if args.batch > 1 and world == 1:
         run_batch(args, local)

@@ -16,7 +16,8 @@ import os
 
 import numpy as np
 
-__all__ = ["cluster", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
+__all__ = ["remove_ground", "expand_labels", "cluster_nonground", "ground_result", "ground_workspace_bytes",
+           "cluster", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
            "slab_workspace_bytes", "SlabState", "workspace_bytes", "workspace_bytes_host", "stats",
            "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
 
@@ -24,14 +25,16 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfec.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_CUDA = 0, -1, -2, -3, -4, -5
 
-# every symbol include/fec.h declares
+# every symbol include/fec.h and include/fec_ground.h declare
 EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
            "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
            "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap",
            "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components",
-           "fec_batch_workspace_bytes", "fec_cluster_batch_ws")
+           "fec_batch_workspace_bytes", "fec_cluster_batch_ws",
+           # include/fec_ground.h
+           "fec_ground_workspace_bytes", "fec_ground_remove", "fec_ground_expand_labels", "fec_ground_count_ms")
 
 
 class FecStats(ctypes.Structure):
@@ -47,6 +50,12 @@ class FecStats(ctypes.Structure):
 class SlabState(ctypes.Structure):
     """Opaque host-side state carried from slab_local to slab_merge (fec_slab_state_t)."""
     _fields_ = [("opaque", ctypes.c_int64 * 8)]
+
+
+class GroundResult(ctypes.Structure):
+    """fec_ground_result_t (include/fec_ground.h)."""
+    _fields_ = [("best", ctypes.c_int32), ("n_valid", ctypes.c_int32), ("n_inliers", ctypes.c_int64),
+                ("n_keep", ctypes.c_int64), ("plane", ctypes.c_float * 4), ("refined", ctypes.c_double * 4)]
 
 
 class FecError(RuntimeError):
@@ -117,6 +126,15 @@ def lib():
         L.fec_slab_merge.restype = ctypes.c_int32
         L.fec_slab_merge.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, i64, i64, vp, vp, sz,
                                      ctypes.POINTER(SlabState), vp]
+        L.fec_ground_workspace_bytes.restype = sz
+        L.fec_ground_workspace_bytes.argtypes = [i64, ctypes.c_int32]
+        L.fec_ground_remove.restype = ctypes.c_int32
+        L.fec_ground_remove.argtypes = [vp, i64, vp, ctypes.c_int32, f32, ctypes.c_double, i64, vp, vp, vp, vp,
+                                        vp, sz, vp]
+        L.fec_ground_count_ms.restype = ctypes.c_int32
+        L.fec_ground_count_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
+        L.fec_ground_expand_labels.restype = ctypes.c_int32
+        L.fec_ground_expand_labels.argtypes = [vp, vp, vp, i64, vp, vp]
         L.fec_debug_pred.restype = ctypes.c_int32
         L.fec_debug_pred.argtypes = [vp, vp, i64, f32, vp, vp, vp]
         _lib = L
@@ -242,6 +260,95 @@ def cluster_batch(points, offsets, d_th: float, min_size: int = 1, max_size: int
     _check(lib().fec_cluster_batch_ws(_ptr(points), off.ctypes.data, nc, _f32(d_th), int(min_size), int(max_size),
                                       _ptr(out), workspace.data_ptr(), workspace.numel(), st.cuda_stream))
     return out
+
+
+# ---- ground removal (include/fec_ground.h) ----------------------------
+GROUND_RESULT_BYTES = ctypes.sizeof(GroundResult)
+
+
+def ground_workspace_bytes(n: int, n_hyp: int) -> int:
+    return int(lib().fec_ground_workspace_bytes(int(n), int(n_hyp)))
+
+
+def ground_result(buf) -> dict:
+    """Decode a device fec_ground_result_t (uint8 CUDA tensor) -- a device->host read."""
+    raw = bytes(buf[:GROUND_RESULT_BYTES].cpu().numpy().tobytes())
+    r = GroundResult.from_buffer_copy(raw)
+    return {"best": r.best, "n_valid": r.n_valid, "n_inliers": r.n_inliers, "n_keep": r.n_keep,
+            "plane": np.array(list(r.plane), dtype=np.float32), "refined": np.array(list(r.refined))}
+
+
+def remove_ground(points, triplets, threshold: float = 0.2, max_tilt_deg: float = 30.0, min_inliers=None,
+                  cos_max_tilt=None, out=None, workspace=None, stream=None, counts=False):
+    """RANSAC plane-fit ground removal on the device.  `points`: CUDA float32 [n, 3];
+    `triplets`: CUDA int32 [H, 3] point indices per hypothesis (the caller's random sample).
+    Returns (keep_points [n, 3], keep_idx [n], result_buf, counts_or_None): the first
+    n_keep rows are the survivors in input order; `result_buf` holds fec_ground_result_t on
+    the device (ground_result() reads it).  Nothing is synchronised."""
+    import math
+    torch = _torch()
+    if not (isinstance(points, torch.Tensor) and points.is_cuda and points.dtype == torch.float32):
+        raise TypeError("points must be a CUDA float32 tensor [n, 3]")
+    if not (isinstance(triplets, torch.Tensor) and triplets.is_cuda and triplets.dtype == torch.int32):
+        raise TypeError("triplets must be a CUDA int32 tensor [H, 3]")
+    points = points.contiguous()
+    triplets = triplets.contiguous()
+    n, H = points.shape[0], triplets.numel() // 3
+    if min_inliers is None:
+        min_inliers = (n + 9) // 10
+    if cos_max_tilt is None:
+        cos_max_tilt = math.cos(math.radians(max_tilt_deg))
+    dev = points.device
+    if out is None:
+        out = (torch.empty((max(n, 1), 3), dtype=torch.float32, device=dev),
+               torch.empty(max(n, 1), dtype=torch.int32, device=dev),
+               torch.empty(GROUND_RESULT_BYTES, dtype=torch.uint8, device=dev))
+    kp, ki, res = out
+    cnt = torch.empty(max(H, 1), dtype=torch.int64, device=dev) if counts else None
+    nb = ground_workspace_bytes(n, H)
+    if nb == 0:
+        raise FecError(ERR_INVALID_ARGUMENT, "bad sizes for fec_ground_remove")
+    if workspace is None or workspace.numel() < nb:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().fec_ground_remove(_ptr(points) if n else None, n, _ptr(triplets) if H else None, H,
+                                   float(np.float32(threshold)), float(cos_max_tilt), int(min_inliers),
+                                   _ptr(kp), _ptr(ki), _ptr(cnt) if cnt is not None else None, _ptr(res),
+                                   workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    return kp, ki, res, cnt
+
+
+def ground_count_ms() -> float:
+    """Duration of the last fec_ground_remove's inlier-counting kernel (needs set_timing(True))."""
+    v = ctypes.c_float(-1.0)
+    _check(lib().fec_ground_count_ms(ctypes.byref(v)))
+    return float(v.value)
+
+
+def expand_labels(keep_idx, keep_labels, result_buf, n: int, out=None, stream=None):
+    """Whole-cloud labels from the survivors' labels: -2 = ground, -1 = noise, else the
+    input-order minimum index of the point's cluster (fec_ground_expand_labels)."""
+    torch = _torch()
+    dev = keep_idx.device
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().fec_ground_expand_labels(_ptr(keep_idx), _ptr(keep_labels), _ptr(result_buf), int(n), _ptr(out),
+                                          st.cuda_stream))
+    return out[:n]
+
+
+def cluster_nonground(points, triplets, d_th: float, min_size: int = 1, max_size: int = 2**62,
+                      threshold: float = 0.2, max_tilt_deg: float = 30.0, min_inliers=None):
+    """Ground removal then clustering of the survivors ("(i) ground points
+    removal and (ii) the clustering of the remaining points").  One device->host read of
+    n_keep between the two.  Returns (labels [n] int32 CUDA: -2 ground / -1 noise / cluster
+    min index, result dict)."""
+    kp, ki, res, _ = remove_ground(points, triplets, threshold, max_tilt_deg, min_inliers)
+    info = ground_result(res)
+    nk = int(info["n_keep"])
+    lab_k = cluster(kp[:nk], d_th, min_size, max_size)
+    return expand_labels(ki, lab_k, res, points.shape[0]), info
 
 
 def set_instrumentation(enable: bool):

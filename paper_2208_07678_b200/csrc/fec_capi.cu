@@ -941,6 +941,13 @@ const char* fec_status_string(fec_status_t s) {
 }
 
 const char* fec_last_error(void) { return g_err.c_str(); }
+}  // extern "C"
+
+// the other C-ABI translation units (fec_ground.cu) report through the same thread-local slot
+void fec::set_last_error(const std::string& msg) { g_err = msg; }
+bool fec::timing_enabled() { return g_timing != 0; }
+
+extern "C" {
 
 const char* fec_version(void) { return "fec-b200 0.1 sm_100a"; }
 

@@ -5,7 +5,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace fec {
+
+void set_last_error(const std::string& msg);  // fec_last_error()'s thread-local slot
+bool timing_enabled();                         // fec_set_timing()
 
 using u64 = unsigned long long;
 constexpr int kWarp = 32;

@@ -20,7 +20,7 @@ def libpath():
 
 
 def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "fec.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("fec.h", "fec_ground.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(fec_[a-z0-9_]+)\s*\(", src)))
 
@@ -93,6 +93,35 @@ def test_argument_errors_before_launch(libpath):
     assert L.fec_cluster_ws(None, 0, 1.0, 1, 4, None, None, 0, None) == fec.OK   # empty -> OK
     assert b"d_th" in L.fec_last_error() or True
     assert L.fec_status_string(fec.ERR_NONFINITE) == b"FEC_ERR_NONFINITE"
+
+
+def test_ground_kernels_use_fused_residuals_and_reject_bad_arguments(libpath):
+    """Reading G3 fixes the residual as three FMAs: the counting kernel must contain FFMA.
+    Argument errors of fec_ground_* are reported on the host before any CUDA call."""
+    funcs = _functions(_sass(libpath))
+    body = "\n".join(next(b for nm, b in funcs.items() if "k_g_count" in nm))
+    assert "FFMA" in body
+    L = fec.lib()
+    assert fec.ground_workspace_bytes(-1, 10) == 0 and fec.ground_workspace_bytes(10, 4097) == 0
+    assert fec.ground_workspace_bytes(0, 0) > 0 and fec.ground_workspace_bytes(1000, 100) > 0
+    dummy = 256  # never dereferenced: every call below fails its host-side checks
+    bad = [
+        (dummy, -1, dummy, 10, 0.1, 0.5, 0),            # n < 0
+        (dummy, 10, dummy, 4097, 0.1, 0.5, 0),          # too many hypotheses
+        (dummy, 10, dummy, 10, float("nan"), 0.5, 0),   # threshold NaN
+        (dummy, 10, dummy, 10, -0.5, 0.5, 0),           # threshold < 0
+        (dummy, 10, dummy, 10, 0.1, float("nan"), 0),   # cos tilt NaN
+        (dummy, 10, dummy, 10, 0.1, 0.5, -1),           # min_inliers < 0
+        (None, 10, dummy, 10, 0.1, 0.5, 0),             # null points
+    ]
+    for pts, n, tri, H, thr, ct, mi in bad:
+        rc = L.fec_ground_remove(pts, n, tri, H, thr, ct, mi, dummy, dummy, None, dummy, dummy, 1 << 30, None)
+        assert rc == fec.ERR_INVALID_ARGUMENT, (n, H, thr, ct, mi)
+    # a too-small workspace
+    rc = L.fec_ground_remove(dummy, 10, dummy, 10, 0.1, 0.5, 0, dummy, dummy, None, dummy, dummy, 1, None)
+    assert rc == fec.ERR_INVALID_ARGUMENT and b"workspace" in L.fec_last_error()
+    assert L.fec_ground_expand_labels(None, None, None, -1, None, None) == fec.ERR_INVALID_ARGUMENT
+    assert L.fec_ground_count_ms(None) == fec.ERR_INVALID_ARGUMENT
 
 
 def test_product_package_never_imports_oracle():
