@@ -30,7 +30,7 @@ import numpy as np
 __all__ = [
     "Workload", "CONFIGS", "make_config", "c1_blobs", "lidar_scan", "c3_map", "c4_loop",
     "c5_stress", "random_cloud", "PARITY_GEOMETRIES", "sha256_f32", "lidar_scan_ground", "ground_map",
-    "plane_and_box", "ransac_triplets", "make_ground_config", "GROUND_PARAMS",
+    "plane_and_box", "ransac_triplets", "make_ground_config", "GROUND_PARAMS", "voxel_clusters",
 ]
 
 
@@ -298,6 +298,42 @@ def make_ground_config(name: str, scale: float = 1.0):
     H = GROUND_PARAMS["iterations"]
     return pts, ransac_triplets(pts.shape[0], H, seed=int(name[1:])), GROUND_PARAMS["threshold"], \
         GROUND_PARAMS["max_tilt_deg"]
+
+
+# --------------------------------------------------------------------------------------
+# Voxel-fill clusters with ground truth (§3.3.1): the
+# synthetic setting of the paper's Fig. 4-6, for the AP metric.
+# --------------------------------------------------------------------------------------
+def voxel_clusters(n_clusters: int, density: int, voxel_edge: float = 1.0, shift_sigma: float = 0.0,
+                   seed: int = 0):
+    """(points float32 [n*m, 3], gt int32 labels 1..n, recommended d_th).
+
+    n voxels on a stride-2 lattice (>= one voxel edge of empty space between any two), each
+    filled with the first m sites (lexicographic) of an even g^3 grid, g = ceil(m^(1/3)),
+    pitch = edge/(g-1); optional normal shift clamped to the voxel; shuffled point order."""
+    rng = np.random.default_rng(seed)
+    g = max(1, int(math.ceil(round(density ** (1.0 / 3.0), 9))))
+    while g ** 3 < density:
+        g += 1
+    pitch = voxel_edge / (g - 1) if g > 1 else 0.0
+    d_th = 1.1 * pitch if g > 1 else 0.5 * voxel_edge
+    if d_th >= voxel_edge:
+        raise ValueError("density too low for the separation guarantee (recommended d_th >= voxel edge)")
+    side = int(math.ceil(n_clusters ** (1.0 / 3.0))) + 1
+    while side ** 3 < n_clusters:
+        side += 1
+    cells = rng.choice(side ** 3, size=n_clusters, replace=False)
+    lat = np.stack([cells % side, (cells // side) % side, cells // (side * side)], 1).astype(np.float64)
+    origin = lat * (2.0 * voxel_edge)
+    sites = np.stack(np.meshgrid(np.arange(g), np.arange(g), np.arange(g), indexing="ij"), -1).reshape(-1, 3)
+    sites = sites[:density].astype(np.float64) * pitch if g > 1 else np.full((1, 3), 0.5 * voxel_edge)
+    pts = (origin[:, None, :] + sites[None, :, :]).reshape(-1, 3)
+    gt = np.repeat(np.arange(1, n_clusters + 1, dtype=np.int32), sites.shape[0])
+    if shift_sigma > 0:
+        lo = np.repeat(origin, sites.shape[0], axis=0)
+        pts = np.clip(pts + rng.normal(0.0, shift_sigma, size=pts.shape), lo, lo + voxel_edge)
+    perm = rng.permutation(pts.shape[0])
+    return _f32(pts[perm]), np.ascontiguousarray(gt[perm]), float(np.float32(d_th))
 
 
 C4_LATERAL_HI = 6.5
