@@ -16,7 +16,7 @@ import os
 
 import numpy as np
 
-__all__ = ["remove_ground", "expand_labels", "cluster_nonground", "ground_result", "ground_workspace_bytes",
+__all__ = ["average_precision", "ap_workspace_bytes", "remove_ground", "expand_labels", "cluster_nonground", "ground_result", "ground_workspace_bytes",
            "cluster", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
            "slab_workspace_bytes", "SlabState", "workspace_bytes", "workspace_bytes_host", "stats",
            "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfec.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_CUDA = 0, -1, -2, -3, -4, -5
 
-# every symbol include/fec.h and include/fec_ground.h declare
+# every symbol include/fec.h, include/fec_ground.h and include/fec_metrics.h declare
 EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
            "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
@@ -34,7 +34,9 @@ EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspac
            "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components",
            "fec_batch_workspace_bytes", "fec_cluster_batch_ws",
            # include/fec_ground.h
-           "fec_ground_workspace_bytes", "fec_ground_remove", "fec_ground_expand_labels", "fec_ground_count_ms")
+           "fec_ground_workspace_bytes", "fec_ground_remove", "fec_ground_expand_labels", "fec_ground_count_ms",
+           # include/fec_metrics.h
+           "fec_ap_workspace_bytes", "fec_average_precision")
 
 
 class FecStats(ctypes.Structure):
@@ -56,6 +58,13 @@ class GroundResult(ctypes.Structure):
     """fec_ground_result_t (include/fec_ground.h)."""
     _fields_ = [("best", ctypes.c_int32), ("n_valid", ctypes.c_int32), ("n_inliers", ctypes.c_int64),
                 ("n_keep", ctypes.c_int64), ("plane", ctypes.c_float * 4), ("refined", ctypes.c_double * 4)]
+
+
+class ApResult(ctypes.Structure):
+    """fec_ap_result_t (include/fec_metrics.h)."""
+    _fields_ = [("tp", ctypes.c_int64), ("fp", ctypes.c_int64), ("n_pred", ctypes.c_int64),
+                ("n_gt", ctypes.c_int64), ("ap", ctypes.c_double), ("status", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
 
 class FecError(RuntimeError):
@@ -131,6 +140,10 @@ def lib():
         L.fec_ground_remove.restype = ctypes.c_int32
         L.fec_ground_remove.argtypes = [vp, i64, vp, ctypes.c_int32, f32, ctypes.c_double, i64, vp, vp, vp, vp,
                                         vp, sz, vp]
+        L.fec_ap_workspace_bytes.restype = sz
+        L.fec_ap_workspace_bytes.argtypes = [i64]
+        L.fec_average_precision.restype = ctypes.c_int32
+        L.fec_average_precision.argtypes = [vp, vp, i64, ctypes.c_double, vp, vp, sz, vp]
         L.fec_ground_count_ms.restype = ctypes.c_int32
         L.fec_ground_count_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
         L.fec_ground_expand_labels.restype = ctypes.c_int32
@@ -349,6 +362,42 @@ def cluster_nonground(points, triplets, d_th: float, min_size: int = 1, max_size
     nk = int(info["n_keep"])
     lab_k = cluster(kp[:nk], d_th, min_size, max_size)
     return expand_labels(ki, lab_k, res, points.shape[0]), info
+
+
+# ---- AP metric (include/fec_metrics.h) ---------------------------------
+AP_RESULT_BYTES = ctypes.sizeof(ApResult)
+
+
+def ap_workspace_bytes(n: int) -> int:
+    return int(lib().fec_ap_workspace_bytes(int(n)))
+
+
+def average_precision(pred, gt, threshold: float = 0.75, workspace=None, stream=None, result=None,
+                      read: bool = True):
+    """AP of predicted labels `pred` (CUDA int32 [n]: -1 or a point index) against ground truth
+    `gt` (CUDA int32 [n] in [0, n], 0 = unlabelled).  Returns a dict (one device->host read)
+    or, with read=False, the device result buffer."""
+    torch = _torch()
+    for t in (pred, gt):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32):
+            raise TypeError("pred and gt must be CUDA int32 tensors")
+    if pred.numel() != gt.numel():
+        raise ValueError("pred and gt must cover the same cloud")
+    pred, gt = pred.contiguous(), gt.contiguous()
+    n = pred.numel()
+    dev = pred.device
+    nb = ap_workspace_bytes(n)
+    if workspace is None or workspace.numel() < nb:
+        workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
+    if result is None:
+        result = torch.empty(AP_RESULT_BYTES, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib().fec_average_precision(_ptr(pred), _ptr(gt), n, float(threshold), result.data_ptr(),
+                                       workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    if not read:
+        return result
+    r = ApResult.from_buffer_copy(bytes(result.cpu().numpy().tobytes()))
+    return {"tp": r.tp, "fp": r.fp, "n_pred": r.n_pred, "n_gt": r.n_gt, "ap": r.ap, "status": r.status}
 
 
 def set_instrumentation(enable: bool):

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfec.so")
-SOURCES = ["fec_capi.cu", "fec_kernels.cu", "fec_dense.cu", "fec_scan_prim.cu", "fec_slab.cu", "fec_ground.cu"]
+SOURCES = ["fec_capi.cu", "fec_kernels.cu", "fec_dense.cu", "fec_scan_prim.cu", "fec_slab.cu", "fec_ground.cu", "fec_metrics.cu"]
 HEADERS = ["fec_internal.cuh", "fec_kernels.cuh", "fec_pairs.cuh", "fec_slab.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -30,7 +30,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "fec.h"), os.path.join(INCLUDE, "fec_ground.h"), __file__]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "fec.h"), os.path.join(INCLUDE, "fec_ground.h"), os.path.join(INCLUDE, "fec_metrics.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

@@ -20,7 +20,7 @@ def libpath():
 
 
 def _declared_functions():
-    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("fec.h", "fec_ground.h"))
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("fec.h", "fec_ground.h", "fec_metrics.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(fec_[a-z0-9_]+)\s*\(", src)))
 
@@ -122,6 +122,17 @@ def test_ground_kernels_use_fused_residuals_and_reject_bad_arguments(libpath):
     assert rc == fec.ERR_INVALID_ARGUMENT and b"workspace" in L.fec_last_error()
     assert L.fec_ground_expand_labels(None, None, None, -1, None, None) == fec.ERR_INVALID_ARGUMENT
     assert L.fec_ground_count_ms(None) == fec.ERR_INVALID_ARGUMENT
+
+
+def test_ap_argument_errors_before_launch(libpath):
+    L = fec.lib()
+    assert fec.ap_workspace_bytes(-1) == 0 and fec.ap_workspace_bytes(1000) > 0
+    d = 256
+    assert L.fec_average_precision(d, d, -1, 0.75, d, d, 1 << 30, None) == fec.ERR_INVALID_ARGUMENT
+    for thr in (0.0, 1.5, float("nan")):
+        assert L.fec_average_precision(d, d, 10, thr, d, d, 1 << 30, None) == fec.ERR_INVALID_ARGUMENT
+    assert L.fec_average_precision(None, d, 10, 0.75, d, d, 1 << 30, None) == fec.ERR_INVALID_ARGUMENT
+    assert L.fec_average_precision(d, d, 10, 0.75, d, d, 1, None) == fec.ERR_INVALID_ARGUMENT
 
 
 def test_product_package_never_imports_oracle():
