@@ -264,6 +264,17 @@ thread_local void* g_pinned_batch = nullptr;
 thread_local size_t g_pinned_batch_bytes = 0;
 
 // a1..a8 on n > 0 points (arguments already checked, pointers validated).
+// word bases + compact cell list in one single-pass look-back kernel (k_cscan); the look-back
+// state lives in the scan scratch (counter in the first 256 B)
+int cell_scan(const Layout& L, int64_t W, const Grid& g, cudaStream_t st) {
+    const int64_t nb = (W + 1 + 2047) / 2048;
+    unsigned int* counter = reinterpret_cast<unsigned int*>(L.dscan);
+    unsigned long long* state = reinterpret_cast<unsigned long long*>(L.dscan + 64);
+    cudaMemsetAsync(L.dscan, 0, 256 + (size_t)nb * 8, st);
+    k_cscan<<<(unsigned)nb, 256, 0, st>>>(L.cw, W, L.clin, L.cstart, L.cocc, L.ccoord, g, L.meta, state, counter);
+    return 1;
+}
+
 fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C,
                       const BatchArgs* B = nullptr) {
     Layout& L = C.L;
@@ -422,10 +433,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             // a2: occupancy bitmap -> compact cell ids; counts per cell -> slots, fine occupancy
             mark(1, st);
             k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
-            k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
-            launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
-            k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
-                                                                           L.ccoord, g, L.meta);
+            launches += 1 + cell_scan(L, W, g, st);
             const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
             k_dcount2<<<wt, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.cocc);
             // a3: counting sort = scan (over the occupied cells only) + cursor scatter
@@ -461,10 +469,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             // a3: cells = runs of equal keys -> compact ids, starts, fine occupancy; gather points
             mark(2, st);
             k_smark<<<ew, 256, 0, st>>>(kin, n, L.cw);
-            k_cpopc<<<cwb, 256, 0, st>>>(L.cw, W, L.cwpos);
-            launches += 2 + exclusive_scan<uint32_t>(L.cwpos, L.cwpos, W + 1, L.dscan, st);
-            k_clist<<<grid_for((W + 8) / 8 * 32, 256, cap * 8), 256, 0, st>>>(L.cw, W, L.cwpos, L.clin, L.cstart, L.cocc,
-                                                                           L.ccoord, g, L.meta);
+            launches += 1 + cell_scan(L, W, g, st);
             k_sgather<<<ew4, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.parent, L.sidx,
                                            L.size, L.minidx, L.meta);
             k_scount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.meta);

@@ -209,36 +209,157 @@ __global__ void __launch_bounds__(256) k_cpopc(const uint2* __restrict__ cw, int
 }
 
 // Word bases, compact-id -> linear cell list (ascending), zeroed per-cell counts, U.
-// Warp per 8 bitmap words (lanes 0-7 load them), then lane per cell of each nonzero word:
-// consecutive occupied cells are written by consecutive lanes (coalesced stores even when
-// most cells are occupied) and runs of empty words cost one load per lane.
+// Warp per 32 bitmap words (lane per word: coalesced loads, word bases stored next to the
+// bits), then lane per cell of each nonzero word: consecutive occupied cells are written by
+// consecutive lanes (coalesced stores even when most cells are occupied).
 __global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t words, const uint32_t* __restrict__ wpos,
                                               uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
                                               u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
                                               Meta* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w0 = 8 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w0 <= words; w0 += 8 * nw) {
+    for (int64_t w0 = 32 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w0 <= words; w0 += 32 * nw) {
+        const int64_t w = w0 + lane;
         uint32_t mybits = 0, myr0 = 0;
-        if (lane < 8 && w0 + lane <= words) {
-            myr0 = __ldg(wpos + w0 + lane);
-            if (w0 + lane < words) {
-                mybits = cw[w0 + lane].x;
-                cw[w0 + lane].y = myr0;
+        if (w <= words) {
+            myr0 = __ldg(wpos + w);
+            if (w < words) {
+                mybits = cw[w].x;
+                cw[w].y = myr0;
             } else {
                 meta->cells = (int)myr0;
                 meta->cells1 = (int)myr0 + 1;
                 count[myr0] = 0u;
             }
         }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        unsigned m = __ballot_sync(0xffffffffu, mybits != 0u);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
             const uint32_t bits = __shfl_sync(0xffffffffu, mybits, j);
-            if (!bits) continue;
             const uint32_t r0 = __shfl_sync(0xffffffffu, myr0, j);
             if ((bits >> lane) & 1u) {
                 const uint32_t r = r0 + (uint32_t)__popc(bits & ((1u << lane) - 1u));
                 const uint32_t lin = (uint32_t)((w0 + j) * 32 + lane);
+                int cc[3];
+                dense_decode(lin, g, cc);
+                clin[r] = lin;
+                ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
+                count[r] = 0u;
+                cocc[r] = 0ull;
+            }
+        }
+    }
+}
+
+// Fused word bases + cell list: a single-pass scan with decoupled look-back over the popcounts
+// of the occupancy words (tiles of 2048 words, taken in order from an atomic counter), the
+// exclusive prefix stored next to each word's bits, then the tile's occupied cells emitted as
+// in k_clist.  Replaces k_cpopc + the scan + k_clist (one pass over the bitmap, one launch).
+constexpr int CS_THREADS = 256, CS_ITEMS = 8, CS_TILE = CS_THREADS * CS_ITEMS;
+
+__global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, int64_t words,
+                                                     uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
+                                                     u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
+                                                     Meta* __restrict__ meta, unsigned long long* __restrict__ state,
+                                                     unsigned int* __restrict__ counter) {
+    __shared__ uint32_t s[CS_TILE];
+    __shared__ uint32_t wsum[CS_THREADS / kWarp];
+    __shared__ unsigned int tile_sh;
+    __shared__ uint32_t prefix_sh;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) tile_sh = atomicAdd(counter, 1u);
+    __syncthreads();
+    const unsigned tile = tile_sh;
+    const int64_t n = words + 1;  // the extra element yields U = the total
+    const int64_t base = (int64_t)tile * CS_TILE;
+    if (base >= n) return;
+#pragma unroll
+    for (int k = 0; k < CS_ITEMS; ++k) {
+        const int64_t i = base + k * CS_THREADS + tid;
+        s[k * CS_THREADS + tid] = i < words ? (uint32_t)__popc(cw[i].x) : 0u;
+    }
+    __syncthreads();
+    uint32_t loc[CS_ITEMS];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < CS_ITEMS; ++k) {
+        const uint32_t v = s[tid * CS_ITEMS + k];
+        loc[k] = run;
+        run += v;
+    }
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = lane < CS_THREADS / kWarp ? wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane < CS_THREADS / kWarp) wsum[lane] = v;
+        const unsigned long long agg = __shfl_sync(0xffffffffu, v, CS_THREADS / kWarp - 1);
+        constexpr unsigned long long A = 1ull << 62, P = 2ull << 62, VAL = (1ull << 62) - 1;
+        unsigned long long prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(state, P | agg);
+        } else {
+            if (lane == 0) atomicExch(state + tile, A | agg);
+            int j = (int)tile - 1;
+            while (true) {
+                const int idx = j - lane;
+                const unsigned long long sv = idx >= 0 ? *reinterpret_cast<volatile unsigned long long*>(state + idx) : P;
+                const unsigned pmask = __ballot_sync(0xffffffffu, (sv & ~VAL) == P);
+                const int upto = pmask ? __ffs(pmask) - 1 : 31;
+                if (!__all_sync(0xffffffffu, lane > upto || (sv & ~VAL) != 0)) continue;
+                unsigned long long val = lane <= upto ? (sv & VAL) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                prefix += val;
+                if (pmask) break;
+                j -= 32;
+            }
+            if (lane == 0) atomicExch(state + tile, P | (prefix + agg));
+        }
+        if (lane == 0) prefix_sh = (uint32_t)prefix;
+    }
+    __syncthreads();
+    const uint32_t pre = prefix_sh + (x - run) + (w > 0 ? wsum[w - 1] : 0u);
+#pragma unroll
+    for (int k = 0; k < CS_ITEMS; ++k) s[tid * CS_ITEMS + k] = pre + loc[k];
+    __syncthreads();
+    // word bases next to the bits; then warp w emits the cells of words [w*256, w*256 + 256)
+#pragma unroll
+    for (int k = 0; k < CS_ITEMS; ++k) {
+        const int64_t i = base + k * CS_THREADS + tid;
+        if (i < words) {
+            cw[i].y = s[k * CS_THREADS + tid];
+        } else if (i == words) {
+            const uint32_t U = s[k * CS_THREADS + tid];
+            meta->cells = (int)U;
+            meta->cells1 = (int)U + 1;
+            count[U] = 0u;
+        }
+    }
+    for (int c = 0; c < CS_ITEMS; ++c) {
+        const int li = w * (CS_ITEMS * kWarp) + c * kWarp + lane;
+        const int64_t i = base + li;
+        const uint32_t bits = i < words ? cw[i].x : 0u;
+        unsigned m = __ballot_sync(0xffffffffu, bits != 0u);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t b = __shfl_sync(0xffffffffu, bits, j);
+            const uint32_t r0 = s[w * (CS_ITEMS * kWarp) + c * kWarp + j];
+            if ((b >> lane) & 1u) {
+                const uint32_t r = r0 + (uint32_t)__popc(b & ((1u << lane) - 1u));
+                const uint32_t lin = (uint32_t)((base + w * (CS_ITEMS * kWarp) + c * kWarp + j) * 32 + lane);
                 int cc[3];
                 dense_decode(lin, g, cc);
                 clin[r] = lin;
@@ -891,8 +1012,8 @@ __global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __r
 // the others are compacted into items2 for k_dense_items.
 // Heavy pairs (two big cells) are split over several warps along B's range: sub-item
 // (k, K) tests B's k-th of K slices, and a per-pair flag stops the others at the first hit.
-constexpr int kSliceWork = 16384;  // cell-size product per slice
-constexpr int kMaxSlices = 32;
+constexpr int kSliceWork = 4096;   // cell-size product per slice
+constexpr int kMaxSlices = 128;
 
 __global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* __restrict__ items2,
                                                      int4* __restrict__ slices2, int* __restrict__ idone) {
