@@ -572,7 +572,7 @@ def run_ground(args, local: int):
                      "kernel_ms": kms, "algorithmic_flops": flops,
                      "peak_source": "derived: 148 SMs x 128 fp32 lanes x 2 x max SM clock (DESIGN.md §8c)"},
         "cpu_baseline": cpu,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": 7 * args.steps,  # planes, count, best, flags, scan, compact, refine
         "clocks": clocks,
     }
     if check is not None:
@@ -653,7 +653,7 @@ def run_ap(args, local: int):
                      "algorithmic_bytes": model},
         "cpu_baseline": {"value": n / cpu_s / 1e6, "unit": "Mpoints/s", "cores": 1, "kind": "oracle",
                          "sample": f"oracle AP over all {n} points"},
-        "gpu_launches": (7 + 3 * passes) * args.steps, "clocks": clk.summary(),
+        "gpu_launches": (10 + 3 * passes) * args.steps,  # 2 sorts x passes x (hist, scan, scatter) + 10 "clocks": clk.summary(),
     }
     if check is not None:
         line["parity_bit_exact"] = check

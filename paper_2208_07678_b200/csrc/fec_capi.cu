@@ -107,7 +107,6 @@ struct Layout {
     int num_tiles;
     // dense-grid mode (per-cell tables indexed by compact id of the occupied cells)
     uint2* cw;          // [W+1] occupancy bitmap words {bits, occupied cells before the word}
-    uint32_t* cwpos;    // [W+2] popcount scan scratch
     uint32_t* clin;     // [n]   linear cell id of each compact id
     uint32_t* cstart;   // [n+1] counts, then exclusive prefix (cell start)
     int* crec;          // [n]   dense record id of a dense cell
@@ -170,7 +169,6 @@ Layout carve(char* base, int64_t n) {
     const int64_t W = dc / 32 + 1;
     Carver b{base, common, 0};
     L.cw = b.take<uint2>(W + 1);
-    L.cwpos = b.take<uint32_t>(W + 2);
     L.clin = b.take<uint32_t>(n);
     L.cstart = b.take<uint32_t>(n + 1);
     L.crec = b.take<int>(n);
@@ -421,7 +419,6 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         dctx.nbase = (int)n;
         dctx.meta = L.meta;
         const int64_t W = (cells_total + 31) / 32;
-        const unsigned cwb = grid_for(W + 1, 256, cap * 4);
         const int64_t dwords = n / 32 + 1;
         const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
         // input order: spatially coherent (LiDAR scan order) -> counting sort; shuffled -> key sort

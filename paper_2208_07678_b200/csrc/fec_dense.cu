@@ -203,59 +203,11 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
     }
 }
 
-__global__ void __launch_bounds__(256) k_cpopc(const uint2* __restrict__ cw, int64_t words, uint32_t* __restrict__ cnt) {
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
-        cnt[w] = w < words ? (uint32_t)__popc(__ldg(cw + w).x) : 0u;
-}
-
-// Word bases, compact-id -> linear cell list (ascending), zeroed per-cell counts, U.
-// Warp per 32 bitmap words (lane per word: coalesced loads, word bases stored next to the
-// bits), then lane per cell of each nonzero word: consecutive occupied cells are written by
-// consecutive lanes (coalesced stores even when most cells are occupied).
-__global__ void __launch_bounds__(256) k_clist(uint2* __restrict__ cw, int64_t words, const uint32_t* __restrict__ wpos,
-                                              uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
-                                              u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
-                                              Meta* __restrict__ meta) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w0 = 32 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w0 <= words; w0 += 32 * nw) {
-        const int64_t w = w0 + lane;
-        uint32_t mybits = 0, myr0 = 0;
-        if (w <= words) {
-            myr0 = __ldg(wpos + w);
-            if (w < words) {
-                mybits = cw[w].x;
-                cw[w].y = myr0;
-            } else {
-                meta->cells = (int)myr0;
-                meta->cells1 = (int)myr0 + 1;
-                count[myr0] = 0u;
-            }
-        }
-        unsigned m = __ballot_sync(0xffffffffu, mybits != 0u);
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
-            const uint32_t bits = __shfl_sync(0xffffffffu, mybits, j);
-            const uint32_t r0 = __shfl_sync(0xffffffffu, myr0, j);
-            if ((bits >> lane) & 1u) {
-                const uint32_t r = r0 + (uint32_t)__popc(bits & ((1u << lane) - 1u));
-                const uint32_t lin = (uint32_t)((w0 + j) * 32 + lane);
-                int cc[3];
-                dense_decode(lin, g, cc);
-                clin[r] = lin;
-                ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
-                count[r] = 0u;
-                cocc[r] = 0ull;
-            }
-        }
-    }
-}
-
 // Fused word bases + cell list: a single-pass scan with decoupled look-back over the popcounts
 // of the occupancy words (tiles of 2048 words, taken in order from an atomic counter), the
-// exclusive prefix stored next to each word's bits, then the tile's occupied cells emitted as
-// in k_clist.  Replaces k_cpopc + the scan + k_clist (one pass over the bitmap, one launch).
+// exclusive prefix stored next to each word's bits, then the tile's occupied cells emitted:
+// lane per cell of each nonzero word, so consecutive occupied cells are written by consecutive
+// lanes.  One pass over the bitmap, one launch (+ the state memset).
 constexpr int CS_THREADS = 256, CS_ITEMS = 8, CS_TILE = CS_THREADS * CS_ITEMS;
 
 __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, int64_t words,

@@ -14,6 +14,9 @@
 //   k_g_refine   fixed-order reduction of the partial sums, 3x3 Jacobi eigen-solve
 #include <math.h>
 
+#include <algorithm>
+#include <mutex>
+
 #include "fec.h"
 #include "fec_ground.h"
 #include "fec_internal.cuh"
@@ -465,18 +468,22 @@ fec_status_t fec_ground_remove(const float* points, int64_t n, const int32_t* tr
     const int64_t tiles = g_tiles(n);
     if (H > 0) k_g_planes<<<(H + 127) / 128, 128, 0, st>>>(points, n, triplets, H, cos_max_tilt, w.planes, w.valid, w.cnt);
     if (H > 0 && n > 0) {
-        static int sms = 0, bps = 0;
-        static size_t smem_set = 0;
+        // per-device: SM count and the opt-in shared-memory size already granted to k_g_count
+        static int sms_of[64] = {};
+        static size_t smem_of[64] = {};
+        static std::mutex mu;
+        int dev = 0, sms = 0, bps = 0;
+        cudaGetDevice(&dev);
         const size_t smem = (size_t)H * (2 * sizeof(float4) + sizeof(unsigned));
-        if (sms == 0) {
-            int d = 0;
-            cudaGetDevice(&d);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
-        }
-        if (smem > 48 * 1024 && smem_set < smem) {
-            cudaError_t e = cudaFuncSetAttribute(k_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return g_fail("cudaFuncSetAttribute(k_g_count)", e);
-            smem_set = smem;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (sms_of[dev & 63] == 0) cudaDeviceGetAttribute(&sms_of[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+            sms = sms_of[dev & 63];
+            if (smem > 48 * 1024 && smem_of[dev & 63] < smem) {
+                cudaError_t e = cudaFuncSetAttribute(k_g_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return g_fail("cudaFuncSetAttribute(k_g_count)", e);
+                smem_of[dev & 63] = smem;
+            }
         }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_g_count, 256, smem);
         const int64_t need_blocks = (n + 256 * kCountPts - 1) / (256 * kCountPts);

@@ -75,11 +75,10 @@ __global__ void k_relabel(const int* parent, const int* val, const int* size, co
 __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
                               unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, Grid g, uint2* cw);
-__global__ void k_cpopc(const uint2* cw, int64_t words, uint32_t* cnt);
+
 __global__ void k_cscan(uint2* cw, int64_t words, uint32_t* clin, uint32_t* count, u64* cocc, u64* ccoord, Grid g,
                         Meta* meta, unsigned long long* state, unsigned int* counter);
-__global__ void k_clist(uint2* cw, int64_t words, const uint32_t* wpos, uint32_t* clin, uint32_t* count, u64* cocc,
-                        u64* ccoord, Grid g, Meta* meta);
+
 __global__ void k_lkey(const float* p, int64_t n, Grid g, uint32_t* key, int* val);
 __global__ void k_smark(const uint32_t* key, int64_t n, uint2* cw);
 __global__ void k_sgather(const float* p, const uint32_t* key, const int* val, int64_t n, Grid g, const uint2* cw,
