@@ -241,6 +241,7 @@ inline unsigned grid_for(int64_t work, int per_block, int cap) {
 struct Core {
     Layout L;
     Grid g;
+    int node_stats = 0;        // single-GPU tail: dense points' totals accumulated per component node
     const int* val = nullptr;  // local input index of each sorted position
     int launches = 0;
     int passes = 0;
@@ -482,10 +483,12 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         mark(3, st);
         if (key_sort)
             k_dparent<<<grid_for(dense_max(n) * 32, 256, cap * 8), 256, 0, st>>>(L.spts, L.cstart, L.dlist, L.ncomp,
-                                                                                L.cmask, g, (int)n, L.parent, L.meta);
+                                                                                L.cmask, g, (int)n, L.parent, L.meta,
+                                                                                L.sidx, L.size, L.minidx,
+                                                                                C.node_stats, n);
         else
             k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
-                                         L.size, L.minidx, L.sidx);
+                                         L.size, L.minidx, L.sidx, L.meta, C.node_stats);
         ++launches;
         mark(4, st);
         // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
@@ -613,6 +616,7 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     }
     if (ws_bytes < carve(nullptr, n).total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
     Core C;
+    C.node_stats = 1;
     rc = run_core(pts, n, d, t2, ws, st, C, B);
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
@@ -622,8 +626,17 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     const unsigned wave = grid_for(n, 256, dev_info().sms * 8);
     k_flatten_if<<<wave, 256, 0, st>>>(L.parent, n, L.meta);
     mark(8, st);
-    k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta);
+    const int dense = C.g.dense;
+    k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, dense);
     k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
+    if (dense) {
+        // few sparse cells: totals per component node, then the sparse points (node_accumulate)
+        k_node_stats<<<grid_for(8 * dense_max(n), 256, dev_info().sms * 8), 256, 0, st>>>(
+            L.parent, L.ncomp, L.size, L.minidx, (int)n, L.meta, n);
+        k_sparse_stats<<<grid_for(dense_max(n), 256, dev_info().sms * 8), 256, 0, st>>>(
+            L.parent, L.cstart, L.slist, C.val, L.size, L.minidx, L.meta, n);
+        C.launches += 2;
+    }
     mark(9, st);
     k_rootlab<<<wave, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
     k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(

@@ -754,6 +754,29 @@ __global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ 
     }
 }
 
+// Node-level statistics (single-GPU tail of clouds with few sparse cells):
+// points of dense cells add their count and minimum input index to their component node's own
+// accumulators while parents are assigned; k_node_stats later moves each node's totals to its
+// root, so the tail never walks the dense points.  Warp-aggregated: one atomic per distinct
+// node among the warp's points of this round (key < 0 = not a dense point).
+__device__ __forceinline__ void node_accumulate(int key, int si, int* __restrict__ size, int* __restrict__ minidx) {
+    const int lane = threadIdx.x & 31;
+    const bool ok = key >= 0;
+    unsigned todo = __ballot_sync(0xffffffffu, ok);
+    while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const int k = __shfl_sync(0xffffffffu, key, leader);
+        const bool mem = ok && key == k;
+        const unsigned peers = __ballot_sync(0xffffffffu, mem);
+        const int mn = __reduce_min_sync(0xffffffffu, mem ? si : 0x7fffffff);
+        if (lane == leader) {
+            atomicAdd(size + k, __popc(peers));
+            atomicMin(minidx + k, mn);
+        }
+        todo &= ~peers;
+    }
+}
+
 // Sorted-order initialisation (coalesced): points of sparse cells are their own parents,
 // points of dense cells hang under their component's node; accumulators; input index.
 __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, Grid g,
@@ -761,8 +784,9 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                                               const int* __restrict__ crec, const int* __restrict__ ncomp,
                                               const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
                                               int* __restrict__ size, int* __restrict__ minidx,
-                                              int* __restrict__ sidx) {
+                                              int* __restrict__ sidx, const Meta* __restrict__ meta, int node_stats) {
     const int64_t groups = (n + 3) / 4;
+    const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;  // warp-uniform
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b4 = 4 * gi;
         float4 v[4];
@@ -795,6 +819,10 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                 size[b4 + j] = 0;
                 minidx[b4 + j] = 0x7fffffff;
             }
+        if (nstats) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) node_accumulate(b4 + j < n && par[j] >= nbase ? par[j] : -1, si[j], size, minidx);
+        }
         if (b4 + 4 <= n) {
             *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
             *reinterpret_cast<int4*>(sidx + b4) = make_int4(si[0], si[1], si[2], si[3]);
@@ -814,24 +842,33 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
 __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts, const uint32_t* __restrict__ cstart,
                                                 const int* __restrict__ dlist, const int* __restrict__ ncomp,
                                                 const u64* __restrict__ cmask, Grid g, int nbase,
-                                                int* __restrict__ parent, const Meta* __restrict__ meta) {
+                                                int* __restrict__ parent, const Meta* __restrict__ meta,
+                                                const int* __restrict__ sidx, int* __restrict__ size,
+                                                int* __restrict__ minidx, int node_stats, int64_t n) {
     const int lane = threadIdx.x & 31;
     const int nd = meta->ndense;
+    const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nd; r += warps) {
         const int cid = __ldg(dlist + r);
         const int k = __ldg(ncomp + r);
         const int a0 = (int)__ldg(cstart + cid), a1 = (int)__ldg(cstart + cid + 1);
-        for (int s = a0 + lane; s < a1; s += 32) {
-            int cc = 0;
-            if (k > 1) {
-                const float4 v = __ldg(spts + s);
-                uint32_t lin;
-                int q;
-                dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lin, q);
-                while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
+        for (int s0 = a0; s0 < a1; s0 += 32) {  // warp-uniform trip count
+            const int s = s0 + lane;
+            int key = -1;
+            if (s < a1) {
+                int cc = 0;
+                if (k > 1) {
+                    const float4 v = __ldg(spts + s);
+                    uint32_t lin;
+                    int q;
+                    dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lin, q);
+                    while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
+                }
+                key = nbase + 8 * r + cc;
+                parent[s] = key;
             }
-            parent[s] = nbase + 8 * r + cc;
+            if (nstats) node_accumulate(key, s < a1 ? __ldg(sidx + s) : 0x7fffffff, size, minidx);
         }
     }
 }
@@ -1314,6 +1351,56 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
     union_sparse_body<false>(spts, cw, ccoord, cstart, nullptr, g, parent, meta, n);
 }
+// Node-level tail (see node_accumulate): every used component node finds its root, is
+// flattened onto it, and adds its own totals to the root's; then the points of sparse cells
+// (the compact list of k_slist) find their roots, are flattened and counted one by one.
+// Only for dense-grid clouds with few sparse cells; the others run k_flat_stats / k_stats.
+__global__ void __launch_bounds__(256) k_node_stats(int* __restrict__ parent, const int* __restrict__ ncomp,
+                                                   int* __restrict__ size, int* __restrict__ minidx, int nbase,
+                                                   Meta* __restrict__ meta, int64_t n) {
+    if (4 * (int64_t)meta->cells > n) return;
+    const int64_t nn = 8 * (int64_t)meta->ndense;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
+        if ((int)(t & 7) >= __ldg(ncomp + (t >> 3))) continue;  // unused component slot
+        const int node = nbase + (int)t;
+        int curr = ld_parent(parent, node), next;
+        if (curr == node) {  // a root keeps its own totals
+            if (meta->instrument) atomicAdd(&meta->components, 1ull);
+            continue;
+        }
+        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        st_parent(parent, node, curr);
+        const int c = size[node];
+        if (c) {
+            atomicAdd(size + curr, c);
+            atomicMin(minidx + curr, minidx[node]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sparse_stats(int* __restrict__ parent, const uint32_t* __restrict__ cstart,
+                                                     const int* __restrict__ slist, const int* __restrict__ sidx,
+                                                     int* __restrict__ size, int* __restrict__ minidx,
+                                                     Meta* __restrict__ meta, int64_t n) {
+    if (4 * (int64_t)meta->cells > n) return;
+    const int ns = meta->nsparse;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += gridDim.x * blockDim.x) {
+        const int P = __ldg(slist + e);
+        const int a0 = (int)__ldg(cstart + P), a1 = (int)__ldg(cstart + P + 1);
+        for (int s = a0; s < a1; ++s) {
+            int curr = ld_parent(parent, s), next;
+            if (curr != s) {
+                while (curr < (next = ld_parent(parent, curr))) curr = next;
+                st_parent(parent, s, curr);
+            } else if (meta->instrument) {
+                atomicAdd(&meta->components, 1ull);
+            }
+            atomicAdd(size + curr, 1);
+            atomicMin(minidx + curr, __ldg(sidx + s));
+        }
+    }
+}
+
 // LOCAL clouds have few sparse cells (C4: 73k of 358k cells, 0.8% of the points), so the
 // kernel is a few short waves whose time is the dependent-load chain per cell.  16 lanes per
 // sparse cell P (<= 6 points): lane l tests P's own pair l (15 pairs), the ballot gives P's

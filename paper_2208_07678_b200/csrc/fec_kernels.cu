@@ -645,8 +645,9 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
 // mode in k_init_uf).
 __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                                    int* __restrict__ size, int* __restrict__ minidx,
-                                                   Meta* __restrict__ meta) {
+                                                   Meta* __restrict__ meta, int node_tail) {
     if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_flatten_if + k_stats
+    if (node_tail) return;                     // dense grid: k_node_stats + k_sparse_stats
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
     for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
     __syncthreads();
@@ -763,6 +764,9 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (r[j] < 0) continue;
+            // a point of a dense cell points at its component node, which k_node_stats (or
+            // the flattening walks) pointed at the root; roots point at themselves
+            if (r[j] >= n) r[j] = __ldg(parent + r[j]);
             int lab;
             if (folded) {
                 lab = __ldg(minidx + r[j]);

@@ -65,7 +65,7 @@ __global__ void k_init_uf(const u64* ex, const int* gstart, int64_t n, int* pare
 __global__ void k_scan_union(const float4* spts, Grid g, Tables T, int* parent, Meta* meta);
 __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx);
 __global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
-__global__ void k_flat_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta);
+__global__ void k_flat_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta, int node_tail);
 __global__ void k_stats(const int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta, int only_sparse);
 __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
                           long long max_size, const Meta* meta);
@@ -109,9 +109,13 @@ __global__ void k_dcomps(Grid g, const u64* cocc, const u64* ccoord, int* ncomp,
                          uint32_t* oflags, DenseCtx C);
 __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, const uint32_t* cstart,
                         const int* crec, const int* ncomp, const u64* cmask, int nbase, int* parent, int* size,
-                        int* minidx, int* sidx);
+                        int* minidx, int* sidx, const Meta* meta, int node_stats);
 __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int* dlist, const int* ncomp,
-                          const u64* cmask, Grid g, int nbase, int* parent, const Meta* meta);
+                          const u64* cmask, Grid g, int nbase, int* parent, const Meta* meta, const int* sidx,
+                          int* size, int* minidx, int node_stats, int64_t n);
+__global__ void k_node_stats(int* parent, const int* ncomp, int* size, int* minidx, int nbase, Meta* meta, int64_t n);
+__global__ void k_sparse_stats(int* parent, const uint32_t* cstart, const int* slist, const int* sidx, int* size,
+                               int* minidx, Meta* meta, int64_t n);
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart, Grid g,
                                int* parent, Meta* meta, int64_t n);
 __global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
