@@ -820,8 +820,30 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                 minidx[b4 + j] = 0x7fffffff;
             }
         if (nstats) {
+            // the thread's 4 consecutive positions mostly share one node: runs first, then the
+            // first run of every lane aggregated over the warp by a labelled partition
+            int key0 = -1, cnt0 = 0, min0 = 0x7fffffff;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) node_accumulate(b4 + j < n && par[j] >= nbase ? par[j] : -1, si[j], size, minidx);
+            for (int j = 0; j < 4; ++j) {
+                const int key = b4 + j < n && par[j] >= nbase ? par[j] : -1;
+                if (key < 0) continue;
+                if (key0 < 0 || key == key0) {
+                    key0 = key;
+                    ++cnt0;
+                    min0 = min(min0, si[j]);
+                } else {  // a second node inside the thread's 4 points (cell or component edge)
+                    atomicAdd(size + key, 1);
+                    atomicMin(minidx + key, si[j]);
+                }
+            }
+            // lanes past the end left the grid-stride loop: aggregate over the ones still here
+            const unsigned peers = __match_any_sync(__activemask(), key0);
+            const int tot = __reduce_add_sync(peers, cnt0);
+            const int mn = __reduce_min_sync(peers, min0);
+            if (key0 >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) {
+                atomicAdd(size + key0, tot);
+                atomicMin(minidx + key0, mn);
+            }
         }
         if (b4 + 4 <= n) {
             *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
