@@ -1220,21 +1220,20 @@ __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ nco
 }
 
 // Sparse cells.  The grid is one resident wave; each warp grid-strides over chunks of
-// 128 consecutive cells (so the wave sweeps the sorted order upwards), compacts the
+// SP_CHUNK consecutive cells (so the wave sweeps the sorted order upwards), compacts the
 // chunk's nonempty sparse cells into a per-warp list and gives every lane a real cell.
 // Loops are warp-uniform with a reconvergence point per neighbour (SIMT efficiency).
 constexpr int SP_CHUNK = 32;
 
-// LOCAL (clouds with few sparse cells, e.g. LiDAR maps): a neighbour point is united once
-// per local component of P it touches (P's own pairs give 3-bit local labels) instead of
-// once per pred-true pair; sparse-dominated clouds (occupied cells > n/4, ~1-2 points per
-// cell) run the plain form.  Both are launched; the one not chosen returns at once.
-template <bool LOCAL>
+// Sparse-dominated clouds (occupied cells > n/4, ~1-2 points per cell): lane per sparse
+// cell, its own pairs and every sparse forward neighbour's points (dense neighbours are
+// handled by k_dense_link).  Clouds with few sparse cells use k_union_sparse_local instead;
+// both are launched and the one not chosen returns at once.
 __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spts, const uint2* __restrict__ cw,
                                                   const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
-                                                  const int* __restrict__ slist, const Grid& g,
-                                                  int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
-    if ((4 * (int64_t)meta->cells > n) == LOCAL) return;
+                                                  const Grid& g, int* __restrict__ parent, Meta* __restrict__ meta,
+                                                  int64_t n) {
+    if (4 * (int64_t)meta->cells <= n) return;
     const uint32_t cells = (uint32_t)meta->cells;  // occupied cells (compact ids)
     __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
     unsigned long long n_tests = 0;
@@ -1243,26 +1242,19 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     uint32_t* list = lists[threadIdx.x >> 5];
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t nitems = LOCAL ? (uint32_t)meta->nsparse : cells;
-    for (uint32_t base = warp * SP_CHUNK; base < nitems; base += nwarps * SP_CHUNK) {
+    for (uint32_t base = warp * SP_CHUNK; base < cells; base += nwarps * SP_CHUNK) {
         int total = 0;
-        if constexpr (LOCAL) {
-            // consecutive entries of the sparse-cell list (k_slist)
-            if (base + lane < nitems) list[lane] = (uint32_t)__ldg(slist + base + lane);
-            total = (int)min((uint32_t)SP_CHUNK, nitems - base);
-        } else {
 #pragma unroll
-            for (int j = 0; j < SP_CHUNK / 32; ++j) {
-                const uint32_t P = base + j * 32 + lane;
-                bool act = false;
-                if (P < cells) {
-                    const int cnt = (int)__ldg(cstart + P + 1) - (int)__ldg(cstart + P);
-                    act = cnt > 0 && cnt <= SPARSE_MAX;
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, act);
-                if (act) list[total + __popc(m & ((1u << lane) - 1u))] = P;
-                total += __popc(m);
+        for (int j = 0; j < SP_CHUNK / 32; ++j) {
+            const uint32_t P = base + j * 32 + lane;
+            bool act = false;
+            if (P < cells) {
+                const int cnt = (int)__ldg(cstart + P + 1) - (int)__ldg(cstart + P);
+                act = cnt > 0 && cnt <= SPARSE_MAX;
             }
+            const unsigned m = __ballot_sync(0xffffffffu, act);
+            if (act) list[total + __popc(m & ((1u << lane) - 1u))] = P;
+            total += __popc(m);
         }
         __syncwarp();
         for (int e0 = 0; e0 < total; e0 += 32) {
@@ -1271,30 +1263,11 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
             const uint32_t P = v ? list[e] : 0u;
             const int ps = v ? (int)__ldg(cstart + P) : 0;
             const int pe = v ? (int)__ldg(cstart + P + 1) : 0;
-            // P's own pairs; lab = 3-bit local component label (its min local index) per point,
-            // so a neighbour point needs one union per local component it touches, not one
-            // per pred-true pair
-            uint32_t lab = 0;
-            if constexpr (LOCAL)
-                for (int i = 0; i < pe - ps; ++i) lab |= (uint32_t)i << (3 * i);
             for (int s = ps; s < pe; ++s) {
                 const float4 a = __ldg(spts + s);
                 for (int t = s + 1; t < pe; ++t) {
                     ++n_tests;
-                    if (pred(a, __ldg(spts + t), t2)) {
-                        if constexpr (LOCAL) {
-                            const uint32_t ls = (lab >> (3 * (s - ps))) & 7u, lt = (lab >> (3 * (t - ps))) & 7u;
-                            if (ls != lt) {
-                                uf_unite(parent, s, t);
-                                const uint32_t lo = ls < lt ? ls : lt, hi = ls < lt ? lt : ls;
-                                for (int i = 0; i < pe - ps; ++i)
-                                    if (((lab >> (3 * i)) & 7u) == hi)
-                                        lab = (lab & ~(7u << (3 * i))) | (lo << (3 * i));
-                            }
-                        } else {
-                            uf_unite(parent, s, t);
-                        }
-                    }
+                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
                 }
             }
             __syncwarp();
@@ -1310,27 +1283,11 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
                     qe = (int)__ldg(cstart + qc + 1);
                     if (qe - qs > SPARSE_MAX) qe = qs;  // dense neighbours are handled by k_dense_link
                 }
-                if constexpr (LOCAL) {
+                for (int s = ps; s < pe && qe > qs; ++s) {
+                    const float4 a = __ldg(spts + s);
                     for (int t = qs; t < qe; ++t) {
-                        const float4 b = __ldg(spts + t);
-                        uint32_t touched = 0;  // local components of P within d of t
-                        for (int s = ps; s < pe; ++s) {
-                            ++n_tests;
-                            if (pred(__ldg(spts + s), b, t2)) touched |= 1u << ((lab >> (3 * (s - ps))) & 7u);
-                        }
-                        while (touched) {
-                            const int l = __ffs(touched) - 1;
-                            touched &= touched - 1;
-                            uf_unite(parent, ps + l, t);
-                        }
-                    }
-                } else {
-                    for (int s = ps; s < pe && qe > qs; ++s) {
-                        const float4 a = __ldg(spts + s);
-                        for (int t = qs; t < qe; ++t) {
-                            ++n_tests;
-                            if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-                        }
+                        ++n_tests;
+                        if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
                     }
                 }
                 __syncwarp();
@@ -1371,7 +1328,7 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                                                      const u64* __restrict__ ccoord,
                                                      const uint32_t* __restrict__ cstart, Grid g,
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
-    union_sparse_body<false>(spts, cw, ccoord, cstart, nullptr, g, parent, meta, n);
+    union_sparse_body(spts, cw, ccoord, cstart, g, parent, meta, n);
 }
 // Node-level tail (see node_accumulate): every used component node finds its root, is
 // flattened onto it, and adds its own totals to the root's; then the points of sparse cells
