@@ -101,6 +101,18 @@ fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th,
                               int64_t min_size, int64_t max_size, int32_t* labels_host,
                               void* workspace, size_t workspace_bytes, void* stream);
 
+/* Pipelined form of fec_cluster_host for a stream of clouds: the same host->device copy,
+ * clustering and device->host copy are enqueued on `stream`, but the call returns once the
+ * clustering is enqueued (it still waits for the bbox pass, like every call) instead of after
+ * the labels have arrived: labels_host is valid after `stream` completes.  With PINNED host
+ * buffers and two streams (each with its own workspace and host buffers), consecutive calls
+ * overlap one cloud's device->host copy and tail kernels with the next cloud's host->device
+ * copy (PCIe is full duplex).  The host buffers must stay alive until the stream completes.
+ * Errors: as fec_cluster_host. */
+fec_status_t fec_cluster_host_async(const float* points_host, int64_t n, float d_th,
+                                    int64_t min_size, int64_t max_size, int32_t* labels_host,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fills *out with the statistics of this thread's last call whose status was FEC_OK.
  * Counters that need a device read-back (components, pair_tests, group_pairs) are
  * gathered only when fec_set_instrumentation(1) was set before that call. */

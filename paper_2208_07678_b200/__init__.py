@@ -27,7 +27,7 @@ OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_
 
 # every symbol include/fec.h, include/fec_ground.h and include/fec_metrics.h declare
 EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
-           "fec_cluster_host", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
+           "fec_cluster_host", "fec_cluster_host_async", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
            "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap",
@@ -95,6 +95,8 @@ def lib():
         L.fec_cluster.argtypes = [vp, i64, f32, i64, i64, vp]
         L.fec_cluster_host.restype = ctypes.c_int32
         L.fec_cluster_host.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
+        L.fec_cluster_host_async.restype = ctypes.c_int32
+        L.fec_cluster_host_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
         L.fec_get_stats.restype = ctypes.c_int32
         L.fec_get_stats.argtypes = [ctypes.POINTER(FecStats)]
         L.fec_set_instrumentation.restype = None
@@ -213,10 +215,12 @@ def cluster(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=N
 
 
 def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
-                 workspace=None, stream=None, device=None):
+                 workspace=None, stream=None, device=None, sync: bool = True):
     """End-to-end form: host float32 [n, 3] in (numpy or CPU tensor; pinned memory gives
     asynchronous copies), host int32 [n] labels out.  The host<->device copies run inside
-    the C ABI call (fec_cluster_host)."""
+    the C ABI call (fec_cluster_host).  sync=False (fec_cluster_host_async) returns once the
+    work is enqueued on `stream`: `out` is valid after the stream completes, and the caller
+    keeps `points`, `out` and `workspace` alive until then (pipelining over two streams)."""
     torch = _torch()
     if isinstance(points, torch.Tensor):
         if points.is_cuda:
@@ -238,9 +242,10 @@ def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, 
     if n and (workspace is None or workspace.numel() < nb):
         workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    _check(lib().fec_cluster_host(ptr if n else None, n, _f32(d_th), int(min_size), int(max_size),
-                                  out_ptr if n else None, workspace.data_ptr() if n else None,
-                                  workspace.numel() if n else 0, st.cuda_stream))
+    fn = lib().fec_cluster_host if sync else lib().fec_cluster_host_async
+    _check(fn(ptr if n else None, n, _f32(d_th), int(min_size), int(max_size),
+              out_ptr if n else None, workspace.data_ptr() if n else None,
+              workspace.numel() if n else 0, st.cuda_stream))
     del keep
     return out
 

@@ -741,8 +741,26 @@ fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min
     return rc;
 }
 
+static fec_status_t cluster_host_impl(const float* points_host, int64_t n, float d_th, int64_t min_size,
+                                      int64_t max_size, int32_t* labels_host, void* workspace,
+                                      size_t workspace_bytes, void* stream, bool sync);
+
 fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th, int64_t min_size, int64_t max_size,
                               int32_t* labels_host, void* workspace, size_t workspace_bytes, void* stream) {
+    return cluster_host_impl(points_host, n, d_th, min_size, max_size, labels_host, workspace, workspace_bytes,
+                             stream, true);
+}
+
+fec_status_t fec_cluster_host_async(const float* points_host, int64_t n, float d_th, int64_t min_size,
+                                    int64_t max_size, int32_t* labels_host, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    return cluster_host_impl(points_host, n, d_th, min_size, max_size, labels_host, workspace, workspace_bytes,
+                             stream, false);
+}
+
+static fec_status_t cluster_host_impl(const float* points_host, int64_t n, float d_th, int64_t min_size,
+                                      int64_t max_size, int32_t* labels_host, void* workspace,
+                                      size_t workspace_bytes, void* stream, bool sync) {
     float t2;
     fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
     if (rc != FEC_OK) return rc;
@@ -757,7 +775,7 @@ fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th, i
     FEC_CUDA(cudaMemcpyAsync(dpts, points_host, (size_t)12 * n, cudaMemcpyHostToDevice, st));
     rc = run(dpts, n, d_th, min_size, max_size, dlab, workspace, main_b, st);
     if (rc == FEC_OK) FEC_CUDA(cudaMemcpyAsync(labels_host, dlab, (size_t)4 * n, cudaMemcpyDeviceToHost, st));
-    FEC_CUDA(cudaStreamSynchronize(st));
+    if (sync || rc != FEC_OK) FEC_CUDA(cudaStreamSynchronize(st));
     return rc;
 }
 

@@ -150,6 +150,23 @@ def test_host_api_equals_device_api(fec):
     assert_same(host2, dev, "pinned host vs device")
 
 
+def test_async_host_api_pipelined_over_two_streams(fec):
+    """fec_cluster_host_async: six different clouds in flight over two streams (each with its
+    own workspace and pinned buffers); every cloud's labels equal the oracle's."""
+    clouds = [synth.make_config("C2").points] + [synth.random_cloud(s, n=30_000 + 777 * s)[0] for s in range(5)]
+    ds = [0.35] + [float(synth.random_cloud(s, n=10)[1]) for s in range(5)]
+    sts = [torch.cuda.Stream() for _ in range(2)]
+    nmax = max(len(c) for c in clouds)
+    ws = [torch.empty(fec.workspace_bytes_host(nmax), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    pins = [torch.from_numpy(c).pin_memory() for c in clouds]
+    outs = [torch.empty(len(c), dtype=torch.int32).pin_memory() for c in clouds]
+    for k, c in enumerate(clouds):
+        fec.cluster_host(pins[k], ds[k], 2, 10**6, out=outs[k], workspace=ws[k % 2], stream=sts[k % 2], sync=False)
+    torch.cuda.synchronize()
+    for k, c in enumerate(clouds):
+        assert_same(outs[k].numpy(), oracle.fec(c, ds[k], 2, 10**6), f"async cloud {k}")
+
+
 def test_deterministic_repeats(fec):
     w = synth.make_config("C5", scale=0.01)
     first = run_gpu(fec, w.points, w.d_th)
