@@ -2,6 +2,7 @@
 #include <float.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -270,7 +271,7 @@ int cell_scan(const Layout& L, int64_t W, const Grid& g, cudaStream_t st) {
     unsigned int* counter = reinterpret_cast<unsigned int*>(L.dscan);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(L.dscan + 64);
     cudaMemsetAsync(L.dscan, 0, 256 + (size_t)nb * 8, st);
-    k_cscan<<<(unsigned)nb, 256, 0, st>>>(L.cw, W, L.clin, L.cstart, L.cocc, L.ccoord, g, L.meta, state, counter);
+    pdl(k_cscan, (unsigned)nb, 256, 0, st)(L.cw, W, L.clin, L.cstart, L.cocc, L.ccoord, g, L.meta, state, counter);
     return 1;
 }
 
@@ -291,9 +292,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const float near = (float)(2.0 * (double)d * (1.0 + std::ldexp(1.0, -16)));
     float* bbh = nullptr;  // batch: per-cloud bboxes on the host
     if (!B) {
-        k_bbox_partial<<<bb_blocks, 256, 0, st>>>(pts, n, vec4, L.part, &L.meta->nonfinite, near,
+        pdl(k_bbox_partial, bb_blocks, 256, 0, st)(pts, n, vec4, L.part, &L.meta->nonfinite, near,
                                                   &L.meta->near_pairs);
-        k_bbox_final<<<1, 256, 0, st>>>(L.part, (int)bb_blocks, L.meta);
+        pdl(k_bbox_final, 1, 256, 0, st)(L.part, (int)bb_blocks, L.meta);
         launches += 2;
         FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
     } else {
@@ -308,7 +309,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         bbh = static_cast<float*>(g_pinned_batch);
         FEC_CUDA(cudaMemcpyAsync(B->off_dev, B->off_host, (size_t)(B->nclouds + 1) * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, st));
-        k_bbox_clouds<<<B->nclouds, 256, 0, st>>>(pts, B->off_dev, B->bb_dev, &L.meta->nonfinite, near,
+        pdl(k_bbox_clouds, B->nclouds, 256, 0, st)(pts, B->off_dev, B->bb_dev, &L.meta->nonfinite, near,
                                                   &L.meta->near_pairs);
         ++launches;
         FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
@@ -430,20 +431,20 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         if (!key_sort) {
             // a2: occupancy bitmap -> compact cell ids; counts per cell -> slots, fine occupancy
             mark(1, st);
-            k_cmark<<<ew, 256, 0, st>>>(pts, n, g, L.cw);
+            pdl(k_cmark, ew, 256, 0, st)(pts, n, g, L.cw);
             launches += 1 + cell_scan(L, W, g, st);
             const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
-            k_dcount2<<<wt, 256, 0, st>>>(pts, n, g, L.cw, L.cstart, L.cocc);
+            pdl(k_dcount2, wt, 256, 0, st)(pts, n, g, L.cw, L.cstart, L.cocc);
             // a3: counting sort = scan (over the occupied cells only) + cursor scatter
             mark(2, st);
             launches += 2 + exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
-            k_ccount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.slot, L.meta);
-            k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
+            pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta);
+            pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos);
             launches += 2 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
-            k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
-            k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
+            pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+            pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
                                                                       L.dcoord, L.oflag, dctx);
-            k_dscatter2<<<wt, 256, 0, st>>>(pts, n, g, L.cw, L.slot, L.spts);  // slot = per-cell cursors here
+            pdl(k_dscatter2, wt, 256, 0, st)(pts, n, g, L.cw, L.slot, L.spts);  // slot = per-cell cursors here
             launches += 3;
         } else {
             // a2: linear cell keys, LSD radix sort over their significant bits
@@ -451,30 +452,30 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
             uint32_t* kin = reinterpret_cast<uint32_t*>(L.skey0);
             uint32_t* kout = reinterpret_cast<uint32_t*>(L.skey1);
             int *vin = L.sval0, *vout = L.sval1;
-            k_lkey<<<ew4, 256, 0, st>>>(pts, n, g, kin, vin);
+            pdl(k_lkey, ew4, 256, 0, st)(pts, n, g, kin, vin);
             ++launches;
             const int lbits = std::max(1, ceil_log2(cells_total));
             passes = (lbits + 7) / 8;
             const int tiles = (int)((n + RS_TILE - 1) / RS_TILE);
             for (int pp = 0; pp < passes; ++pp) {
-                k_radix_hist32<<<tiles, RS_THREADS, 0, st>>>(kin, n, 8 * pp, L.scounts, tiles);
+                pdl(k_radix_hist32, tiles, RS_THREADS, 0, st)(kin, n, 8 * pp, L.scounts, tiles);
                 launches += exclusive_scan<uint32_t>(L.scounts, L.scounts, (int64_t)256 * tiles, L.dscan, st);
-                k_radix_scatter32l<<<tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
+                pdl(k_radix_scatter32l, tiles, RS_THREADS, 0, st)(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
                 launches += 2;
                 std::swap(kin, kout);
                 std::swap(vin, vout);
             }
             // a3: cells = runs of equal keys -> compact ids, starts, fine occupancy; gather points
             mark(2, st);
-            k_smark<<<ew, 256, 0, st>>>(kin, n, L.cw);
+            pdl(k_smark, ew, 256, 0, st)(kin, n, L.cw);
             launches += 1 + cell_scan(L, W, g, st);
-            k_sgather<<<ew4, 256, 0, st>>>(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.parent, L.sidx,
+            pdl(k_sgather, ew4, 256, 0, st)(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.parent, L.sidx,
                                            L.size, L.minidx, L.meta);
-            k_scount<<<ew, 256, 0, st>>>(L.cstart, L.dbits, L.meta);
-            k_dbits_popc<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos);
+            pdl(k_scount, ew, 256, 0, st)(L.cstart, L.dbits, L.meta);
+            pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos);
             launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
-            k_dbits_list<<<wb, 256, 0, st>>>(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
-            k_dcomps<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
+            pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+            pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
                                                                       L.dcoord, L.oflag, dctx);
             launches += 2;
         }
@@ -482,35 +483,35 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         // path wrote parents/indices in k_sgather and only re-parents points of dense cells
         mark(3, st);
         if (key_sort)
-            k_dparent<<<grid_for(dense_max(n) * 32, 256, cap * 8), 256, 0, st>>>(L.spts, L.cstart, L.dlist, L.ncomp,
+            pdl(k_dparent, grid_for(dense_max(n) * 32, 256, cap * 8), 256, 0, st)(L.spts, L.cstart, L.dlist, L.ncomp,
                                                                                 L.cmask, g, (int)n, L.parent, L.meta,
                                                                                 L.sidx, L.size, L.minidx,
                                                                                 C.node_stats, n);
         else
-            k_dinit<<<ew4, 256, 0, st>>>(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
+            pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
                                          L.size, L.minidx, L.sidx, L.meta, C.node_stats);
         ++launches;
         mark(4, st);
         // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
         // queued uncertain pairs
         mark(5, st);
-        k_union_sparse<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart, g,
+        pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart, g,
                                                                          L.parent, L.meta, n);
-        k_slist<<<grid_for(n, 256, cap * 4), 256, 0, st>>>(L.cstart, L.slist, L.meta, n);
-        k_union_sparse_local<<<di.sms * di.sparse_blocks_per_sm, 256, 0, st>>>(L.spts, L.cw, L.ccoord, L.cstart,
+        pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(L.cstart, L.slist, L.meta, n);
+        pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart,
                                                                                L.slist, g, L.parent, L.meta, n);
         mark(6, st);
         const unsigned lx = grid_for(dense_max(n), 256, cap);
-        k_dense_link<<<dim3(lx, 3), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
-        k_dense_link<<<dim3(lx, 24), 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 3);
+        pdl(k_dense_link, dim3(lx, 3), 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
+        pdl(k_dense_link, dim3(lx, 24), 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 3);
         // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
-        k_dense_overflow<<<di.sms, 256, 0, st>>>(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
-        k_flatten_nodes<<<grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st>>>(L.parent, (int)n, L.meta);
-        k_dense_filter<<<grid_for(L.item_cap, 256, cap * 4), 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
-        k_dense_items<<<di.sms * 8, 256, 0, st>>>(g, dctx, L.items2, L.slices2, L.idone);
+        pdl(k_dense_overflow, di.sms, 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
+        pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta);
+        pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(g, dctx, L.items2, L.slices2, L.idone);
+        pdl(k_dense_items, di.sms * 8, 256, 0, st)(g, dctx, L.items2, L.slices2, L.idone);
         launches += 9;
         if (g_instrument) {
-            k_dense_count<<<grid_for(dense_max(n), 256, cap), 256, 0, st>>>(L.ncomp, L.dlist, L.cstart, dctx);
+            pdl(k_dense_count, grid_for(dense_max(n), 256, cap), 256, 0, st)(L.ncomp, L.dlist, L.cstart, dctx);
             ++launches;
         }
         mark(7, st);
@@ -518,7 +519,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     } else {
         // ---- a2: keys ----------------------------------------------------------------------
         mark(1, st);
-        k_keys<<<ew, 256, 0, st>>>(pts, n, g, L.keyA, L.valA);
+        pdl(k_keys, ew, 256, 0, st)(pts, n, g, L.keyA, L.valA);
         ++launches;
         mark(2, st);
         // ---- a3: LSD radix sort over the significant key bits -------------------------------
@@ -527,9 +528,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         int *vin = L.valA, *vout = L.valB;
         for (int p = 0; p < passes; ++p) {
             const int shift = 8 * p;
-            k_radix_hist<<<L.num_tiles, RS_THREADS, 0, st>>>(kin, n, shift, L.counts, L.num_tiles);
+            pdl(k_radix_hist, L.num_tiles, RS_THREADS, 0, st)(kin, n, shift, L.counts, L.num_tiles);
             launches += exclusive_scan<uint32_t>(L.counts, L.counts, (int64_t)256 * L.num_tiles, L.scan32, st);
-            k_radix_scatter<<<L.num_tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, L.counts,
+            pdl(k_radix_scatter, L.num_tiles, RS_THREADS, 0, st)(kin, vin, kout, vout, n, shift, L.counts,
                                                                 L.num_tiles);
             launches += 2;
             std::swap(kin, kout);
@@ -539,20 +540,20 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         val = vin;
         // ---- a4: gather ----------------------------------------------------------------------
         mark(3, st);
-        k_gather<<<ew, 256, 0, st>>>(pts, val, n, L.spts);
+        pdl(k_gather, ew, 256, 0, st)(pts, val, n, L.spts);
         ++launches;
         mark(4, st);
         // ---- a5: group / cell tables -----------------------------------------------------------
-        k_heads<<<grid_for(n + 1, 256, cap * 4), 256, 0, st>>>(key, n, L.flags);
+        pdl(k_heads, grid_for(n + 1, 256, cap * 4), 256, 0, st)(key, n, L.flags);
         launches += 1 + exclusive_scan<u64>(L.flags, L.flags, n + 1, L.scan64, st);
         FEC_CUDA(cudaMemsetAsync(L.T.hkey, 0xFF, (size_t)hc * 8, st));
-        k_fill_tables<<<ew, 256, 0, st>>>(key, L.flags, n, g, L.T, L.meta);
-        k_init_uf<<<ew, 256, 0, st>>>(L.flags, L.T.gstart, n, L.parent, L.size, L.minidx);
+        pdl(k_fill_tables, ew, 256, 0, st)(key, L.flags, n, g, L.T, L.meta);
+        pdl(k_init_uf, ew, 256, 0, st)(L.flags, L.T.gstart, n, L.parent, L.size, L.minidx);
         launches += 2;
         mark(5, st);
         mark(6, st);
         // ---- a6+a7: neighbour scan + union (persistent warps, dynamic cell counter) -----------
-        k_scan_union<<<di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st>>>(L.spts, g, L.T, L.parent, L.meta);
+        pdl(k_scan_union, di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st)(L.spts, g, L.T, L.parent, L.meta);
         ++launches;
         mark(7, st);
     }
@@ -624,22 +625,22 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     // ---- a8+a9 fused (flatten + stats), a10 -----------------------------------------------------
     // one of each pair below returns at once (device-side choice)
     const unsigned wave = grid_for(n, 256, dev_info().sms * 8);
-    k_flatten_if<<<wave, 256, 0, st>>>(L.parent, n, L.meta);
+    pdl(k_flatten_if, wave, 256, 0, st)(L.parent, n, L.meta);
     mark(8, st);
     const int dense = C.g.dense;
-    k_flat_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, dense);
-    k_stats<<<ew, 256, 0, st>>>(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
+    pdl(k_flat_stats, ew, 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, dense);
+    pdl(k_stats, ew, 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
     if (dense) {
         // few sparse cells: totals per component node, then the sparse points (node_accumulate)
-        k_node_stats<<<grid_for(8 * dense_max(n), 256, dev_info().sms * 8), 256, 0, st>>>(
+        pdl(k_node_stats, grid_for(8 * dense_max(n), 256, dev_info().sms * 8), 256, 0, st)(
             L.parent, L.ncomp, L.size, L.minidx, (int)n, L.meta, n);
-        k_sparse_stats<<<grid_for(dense_max(n), 256, dev_info().sms * 8), 256, 0, st>>>(
+        pdl(k_sparse_stats, grid_for(dense_max(n), 256, dev_info().sms * 8), 256, 0, st)(
             L.parent, L.cstart, L.slist, C.val, L.size, L.minidx, L.meta, n);
         C.launches += 2;
     }
     mark(9, st);
-    k_rootlab<<<wave, 256, 0, st>>>(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
-    k_relabel<<<grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
+    pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
+    pdl(k_relabel, grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st)(
         L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
         B ? B->off_dev : nullptr, B ? B->nclouds : 0);
     C.launches += 5;
@@ -827,14 +828,14 @@ fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n_local, 256, dev_info().sms * 8 * 4);
-    k_flatten<<<ew, 256, 0, st>>>(L.parent, n_local, L.size, L.minidx);
+    pdl(k_flatten, ew, 256, 0, st)(L.parent, n_local, L.size, L.minidx);
     mark(8, st);
     ++C.launches;
     FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)nodes_max(n_local) * 4, st));
-    k_slab_stats<<<ew, 256, 0, st>>>(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
+    pdl(k_slab_stats, ew, 256, 0, st)(L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx,
                                      S.ckey, L.meta);
     mark(9, st);
-    k_slab_pack<<<grid_for(nodes_max(n_local), 256, dev_info().sms * 8 * 4), 256, 0, st>>>(
+    pdl(k_slab_pack, grid_for(nodes_max(n_local), 256, dev_info().sms * 8 * 4), 256, 0, st)(
         L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx, S.ckey, records, (int)rec_cap,
         L.meta);
     C.launches += 2;
@@ -867,22 +868,22 @@ fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t r
     const unsigned mask = (unsigned)(hc - 1);
     const int64_t words = fec_slab_record_words(ss.rec_cap);
     const int cap = dev_info().sms * 8 * 4;
-    k_merge_init<<<grid_for(hc, 256, cap), 256, 0, st>>>(S.hkey, S.hpar, S.gsize, S.gmin, hc);
+    pdl(k_merge_init, grid_for(hc, 256, cap), 256, 0, st)(S.hkey, S.hpar, S.gsize, S.gmin, hc);
     const int64_t total = (int64_t)world * ss.rec_cap;
     if (total > 0) {
-        k_merge_link<<<grid_for(total, 256, cap), 256, 0, st>>>(all_records, world, words, (int)ss.rec_cap, S.hkey,
+        pdl(k_merge_link, grid_for(total, 256, cap), 256, 0, st)(all_records, world, words, (int)ss.rec_cap, S.hkey,
                                                                 mask, S.hpar);
-        k_merge_stats<<<grid_for(total, 256, cap), 256, 0, st>>>(all_records, world, words, (int)ss.rec_cap, S.hkey,
+        pdl(k_merge_stats, grid_for(total, 256, cap), 256, 0, st)(all_records, world, words, (int)ss.rec_cap, S.hkey,
                                                                  mask, S.hpar, S.gsize, S.gmin);
     }
     if (ss.n_local > 0) {
         const Layout L = carve(static_cast<char*>(workspace), ss.n_local);
         const int* val = reinterpret_cast<const int*>(static_cast<const char*>(workspace) + ss.val_off);
         if (ss.rec_cap > 0)
-            k_merge_resolve<<<grid_for(ss.rec_cap, 256, cap), 256, 0, st>>>(all_records + rank * words, (int)ss.rec_cap,
+            pdl(k_merge_resolve, grid_for(ss.rec_cap, 256, cap), 256, 0, st)(all_records + rank * words, (int)ss.rec_cap,
                                                                             S.hkey, mask, S.hpar, S.gsize, S.gmin,
                                                                             L.size, L.minidx);
-        k_slab_relabel<<<grid_for(ss.n_local, 256, cap), 256, 0, st>>>(L.parent, val, L.size, L.minidx, ss.n_local,
+        pdl(k_slab_relabel, grid_for(ss.n_local, 256, cap), 256, 0, st)(L.parent, val, L.size, L.minidx, ss.n_local,
                                                                        (int)ss.n_owned, (long long)min_size,
                                                                        (long long)max_size, labels_owned);
     }
@@ -979,6 +980,13 @@ const char* fec_last_error(void) { return g_err.c_str(); }
 // the other C-ABI translation units (fec_ground.cu) report through the same thread-local slot
 void fec::set_last_error(const std::string& msg) { g_err = msg; }
 bool fec::timing_enabled() { return g_timing != 0; }
+bool fec::pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FEC_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 extern "C" {
 
@@ -992,7 +1000,7 @@ fec_status_t fec_debug_pred(const float* a, const float* b, int64_t m, float d_t
     if (m <= 0) return FEC_OK;
     if (!is_device_ptr(a) || !is_device_ptr(b) || !is_device_ptr(out)) { g_err = "device pointers required"; return FEC_ERR_INVALID_ARGUMENT; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    k_debug_pred<<<grid_for(m, 256, 1024), 256, 0, st>>>(a, b, m, t2, out, d2_out);
+    pdl(k_debug_pred, grid_for(m, 256, 1024), 256, 0, st)(a, b, m, t2, out, d2_out);
     FEC_CUDA(cudaGetLastError());
     FEC_CUDA(cudaStreamSynchronize(st));
     return FEC_OK;

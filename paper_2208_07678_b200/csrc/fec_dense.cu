@@ -160,6 +160,7 @@ __device__ __forceinline__ int bin_slot(int* keys, uint32_t key, int* used, int*
 
 __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__ p, int64_t n, Grid g,
                                                        uint2* __restrict__ cw) {
+    pdl_prologue();
     __shared__ int keys[kBinSlots];
     __shared__ uint32_t bits[kBinSlots];
     __shared__ int used[kBinTile];
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, in
                                                      u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
                                                      Meta* __restrict__ meta, unsigned long long* __restrict__ state,
                                                      unsigned int* __restrict__ counter) {
+    pdl_prologue();
     __shared__ uint32_t s[CS_TILE];
     __shared__ uint32_t wsum[CS_THREADS / kWarp];
     __shared__ unsigned int tile_sh;
@@ -353,6 +355,7 @@ __device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int
 __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, Grid g,
                                                 const uint2* __restrict__ cw, uint32_t* __restrict__ count,
                                                 u64* __restrict__ cocc) {
+    pdl_prologue();
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
     __shared__ int used_all[256 / kWarp][kWTile];
@@ -426,6 +429,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
 __global__ void __launch_bounds__(256) k_dscatter2(const float* __restrict__ p, int64_t n, Grid g,
                                                   const uint2* __restrict__ cw, uint32_t* __restrict__ cursor,
                                                   float4* __restrict__ spts) {
+    pdl_prologue();
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots];
     __shared__ int used_all[256 / kWarp][kWTile];
@@ -483,6 +487,7 @@ __global__ void __launch_bounds__(256) k_dscatter2(const float* __restrict__ p, 
 // Dense bits of the occupied cells from the cell starts; also the scatter cursors.
 __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
                                                uint32_t* __restrict__ cursor, const Meta* __restrict__ meta) {
+    pdl_prologue();
     const int64_t U = meta->cells;
     const int64_t ur = (U + 31) & ~int64_t(31);
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
@@ -503,6 +508,7 @@ __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cst
 // digit passes), cells are the runs of equal keys, and points are gathered into cell order.
 __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64_t n, Grid g, uint32_t* __restrict__ key,
                                              int* __restrict__ val) {
+    pdl_prologue();
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -531,6 +537,7 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
 
 // Occupancy bits of the sorted keys' distinct values (heads only; a warp's heads share words).
 __global__ void __launch_bounds__(256) k_smark(const uint32_t* __restrict__ key, int64_t n, uint2* __restrict__ cw) {
+    pdl_prologue();
     const int64_t nr = (n + 31) & ~int64_t(31);
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += (int64_t)gridDim.x * blockDim.x) {
         const bool ok = s < n;
@@ -553,6 +560,7 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
                                                 int* __restrict__ parent, int* __restrict__ sidx,
                                                 int* __restrict__ size, int* __restrict__ minidx,
                                                 const Meta* __restrict__ meta) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) cstart[meta->cells] = (uint32_t)n;
     // round j: positions s0 + j*256 + threadIdx.x (a warp holds 32 consecutive positions, so
@@ -607,6 +615,7 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
 // so a warp fills one bitmap word with a plain store).
 __global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
                                                const Meta* __restrict__ meta) {
+    pdl_prologue();
     const int64_t U = meta->cells;
     const int64_t ur = (U + 31) & ~int64_t(31);
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
@@ -619,6 +628,7 @@ __global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cst
 // ---- dense records: compact ids of the dense cells in ascending order -----------------------
 __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
                                                    uint32_t* __restrict__ wcount) {
+    pdl_prologue();
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
         wcount[w] = w < words ? (uint32_t)__popc(__ldg(dbits + w)) : 0u;
 }
@@ -626,6 +636,7 @@ __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__
 __global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__ dbits, int64_t words,
                                                    const uint32_t* __restrict__ wpos, int* __restrict__ dlist,
                                                    int* __restrict__ crec, Meta* __restrict__ meta) {
+    pdl_prologue();
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
         if (w == words) { meta->ndense = (int)wpos[words]; continue; }
         uint32_t bits = __ldg(dbits + w);
@@ -732,6 +743,7 @@ __global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ 
                                                int* __restrict__ ncomp,
                                                int* __restrict__ size, int* __restrict__ minidx,
                                                u64* __restrict__ dcoord, uint32_t* __restrict__ oflags, DenseCtx C) {
+    pdl_prologue();
     const int nd = C.meta->ndense;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
         const int cid = __ldg(C.dlist + r);
@@ -785,6 +797,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                                               const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
                                               int* __restrict__ size, int* __restrict__ minidx,
                                               int* __restrict__ sidx, const Meta* __restrict__ meta, int node_stats) {
+    pdl_prologue();
     const int64_t groups = (n + 3) / 4;
     const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;  // warp-uniform
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -867,6 +880,7 @@ __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts
                                                 int* __restrict__ parent, const Meta* __restrict__ meta,
                                                 const int* __restrict__ sidx, int* __restrict__ size,
                                                 int* __restrict__ minidx, int node_stats, int64_t n) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int nd = meta->ndense;
     const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;
@@ -996,6 +1010,7 @@ __device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, con
 __global__ void __launch_bounds__(256) k_dense_link(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
                                                    const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
                                                    uint32_t* __restrict__ oflags, DenseCtx C, int k0) {
+    pdl_prologue();
     const int nd = C.meta->ndense;
     const int k = k0 + blockIdx.y;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x)
@@ -1007,6 +1022,7 @@ __global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __r
                                                        const int* __restrict__ crec, const int* __restrict__ ncomp,
                                                        const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
                                                        DenseCtx C) {
+    pdl_prologue();
     const int nd = C.meta->ndense;
     if (C.meta->nitems <= C.item_cap) return;  // nothing overflowed
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
@@ -1028,6 +1044,7 @@ constexpr int kMaxSlices = 128;
 
 __global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* __restrict__ items2,
                                                      int4* __restrict__ slices2, int* __restrict__ idone) {
+    pdl_prologue();
     const int ni = min(C.meta->nitems, C.item_cap);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
         const int4 it = C.items[e];  // queued before every certain union was done: re-check
@@ -1058,6 +1075,7 @@ __global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* 
 
 // Component nodes -> their roots (shortens the finds of the uncertain pass).
 __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta) {
+    pdl_prologue();
     const int64_t nn = 8 * (int64_t)meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
         const int s = nbase + (int)t;
@@ -1075,6 +1093,7 @@ constexpr int kAPer = 4;
 
 __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const int4* __restrict__ items2,
                                                     const int4* __restrict__ slices2, int* __restrict__ idone) {
+    pdl_prologue();
     __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
     float4* abuf = abuf_all[threadIdx.x >> 5];
@@ -1201,6 +1220,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
 // k_stats) and the number of dense points.
 __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ ncomp, const int* __restrict__ dlist,
                                                     const uint32_t* __restrict__ cstart, DenseCtx C) {
+    pdl_prologue();
     const int nd = C.meta->ndense;
     unsigned long long roots = 0, pts = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
@@ -1305,6 +1325,7 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
 // real sparse cell and all of them run in one wave.
 __global__ void __launch_bounds__(256) k_slist(const uint32_t* __restrict__ cstart, int* __restrict__ slist,
                                               Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_union_sparse walks the cells itself
     const int64_t U = meta->cells;
     const int64_t ur = (U + 31) & ~int64_t(31);
@@ -1328,6 +1349,7 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
                                                      const u64* __restrict__ ccoord,
                                                      const uint32_t* __restrict__ cstart, Grid g,
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
     union_sparse_body(spts, cw, ccoord, cstart, g, parent, meta, n);
 }
 // Node-level tail (see node_accumulate): every used component node finds its root, is
@@ -1337,6 +1359,7 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
 __global__ void __launch_bounds__(256) k_node_stats(int* __restrict__ parent, const int* __restrict__ ncomp,
                                                    int* __restrict__ size, int* __restrict__ minidx, int nbase,
                                                    Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;
     const int64_t nn = 8 * (int64_t)meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
@@ -1361,6 +1384,7 @@ __global__ void __launch_bounds__(256) k_sparse_stats(int* __restrict__ parent, 
                                                      const int* __restrict__ slist, const int* __restrict__ sidx,
                                                      int* __restrict__ size, int* __restrict__ minidx,
                                                      Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;
     const int ns = meta->nsparse;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += gridDim.x * blockDim.x) {
@@ -1396,6 +1420,7 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
                                                            const int* __restrict__ slist, Grid g,
                                                            int* __restrict__ parent, Meta* __restrict__ meta,
                                                            int64_t n) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;
     const uint32_t nitems = (uint32_t)meta->nsparse;
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;

@@ -58,6 +58,7 @@ GroundWs g_carve(char* base, int64_t n, int32_t H) {
 __global__ void k_g_planes(const float* __restrict__ p, int64_t n, const int32_t* __restrict__ tri, int H,
                            double cos_tilt, float4* __restrict__ planes, int* __restrict__ valid,
                            unsigned* __restrict__ cnt) {
+    pdl_prologue();
     const int h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= H) return;
     cnt[h] = 0u;
@@ -119,6 +120,7 @@ __device__ __forceinline__ void g_count_le(unsigned& v, float r, float t) {
 __global__ void __launch_bounds__(256, 4) k_g_count(const float* __restrict__ p, int64_t n,
                                                  const float4* __restrict__ planes, int H, float t,
                                                  unsigned* __restrict__ cnt) {
+    pdl_prologue();
     extern __shared__ float4 g_smem[];
     ulonglong2* sp = reinterpret_cast<ulonglong2*>(g_smem);  // [H][2]: (nx,nx | ny,ny), (nz,nz | off,off)
     unsigned* sc = reinterpret_cast<unsigned*>(g_smem + 2 * H);
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(1024) k_g_best(const float4* __restrict__ plan
                                                  const unsigned* __restrict__ cnt, int H, int64_t n,
                                                  int64_t min_inliers, int64_t* __restrict__ counts,
                                                  fec_ground_result_t* __restrict__ res) {
+    pdl_prologue();
     __shared__ u64 sbest[32];
     __shared__ int snv[32];
     u64 best = 0;
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(256) k_g_flags(const float* __restrict__ p, in
                                                  const int32_t* __restrict__ tri,
                                                  const fec_ground_result_t* __restrict__ res, float t,
                                                  uint32_t* __restrict__ tcount, double* __restrict__ part) {
+    pdl_prologue();
     __shared__ double shd[8];
     __shared__ uint32_t shu[8];
     const int best = res->best;
@@ -287,6 +291,7 @@ __global__ void __launch_bounds__(256) k_g_compact(const float* __restrict__ p, 
                                                    const fec_ground_result_t* __restrict__ res, float t,
                                                    const uint32_t* __restrict__ tscan, float* __restrict__ kp,
                                                    int32_t* __restrict__ kidx) {
+    pdl_prologue();
     __shared__ uint32_t wsum[8];
     const float4 pl = make_float4(res->plane[0], res->plane[1], res->plane[2], res->plane[3]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -358,6 +363,7 @@ __device__ void jacobi3(double A[3][3], double V[3][3]) {
 __global__ void __launch_bounds__(256) k_g_refine(const float* __restrict__ p, const int32_t* __restrict__ tri,
                                                   const double* __restrict__ part, int64_t tiles,
                                                   fec_ground_result_t* __restrict__ res) {
+    pdl_prologue();
     __shared__ double sh[256][9];
     __shared__ double S[9];
     const int best = res->best;
@@ -410,12 +416,14 @@ __global__ void __launch_bounds__(256) k_g_refine(const float* __restrict__ p, c
 }
 
 __global__ void k_g_fill(int32_t* __restrict__ lab, int64_t n) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         lab[i] = -2;
 }
 
 __global__ void k_g_expand(const int32_t* __restrict__ kidx, const int32_t* __restrict__ klab,
                            const fec_ground_result_t* __restrict__ res, int32_t* __restrict__ lab) {
+    pdl_prologue();
     const int64_t nk = res->n_keep;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nk; j += (int64_t)gridDim.x * blockDim.x) {
         const int32_t l = klab[j];

@@ -6,8 +6,49 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace fec {
+
+// ---- programmatic dependent launch (sm_90+) ---------------------------------------------
+// Every kernel of the library starts with pdl_prologue(): wait until the previous kernel of
+// the stream has completed and its writes are visible, then let the next kernel launch.
+// Launched through pdl() (below), consecutive kernels of one stream overlap their launch
+// latency and block rampup with the tail of the previous kernel; launched with <<<>>> the
+// wait returns at once.  Dependencies are unchanged: no kernel reads anything before its wait.
+__device__ __forceinline__ void pdl_prologue() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+bool pdl_enabled();  // FEC_PDL=0 in the environment turns it off (A/B measurements)
+
+template <typename... KArgs>
+struct PdlLaunch {
+    void (*k)(KArgs...);
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    template <typename... Args>
+    cudaError_t operator()(Args&&... args) {
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 1 : 0;
+        return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+    }
+};
+template <typename... KArgs>
+inline PdlLaunch<KArgs...> pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st) {
+    PdlLaunch<KArgs...> l;
+    l.k = k;
+    l.cfg = cudaLaunchConfig_t{};
+    l.cfg.gridDim = grid;
+    l.cfg.blockDim = block;
+    l.cfg.dynamicSmemBytes = smem;
+    l.cfg.stream = st;
+    l.attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    l.attr[0].val.programmaticStreamSerializationAllowed = 1;
+    return l;
+}
 
 void set_last_error(const std::string& msg);  // fec_last_error()'s thread-local slot
 bool timing_enabled();                         // fec_set_timing()

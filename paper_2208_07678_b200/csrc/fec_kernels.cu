@@ -23,6 +23,7 @@ __device__ __forceinline__ void bb_acc(float v, float& mn, float& mx, int& bad) 
 __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ p, int64_t n, int vec4,
                                                      float* __restrict__ part, int* __restrict__ nonfinite,
                                                      float near, unsigned long long* __restrict__ near_pairs) {
+    pdl_prologue();
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     int bad = 0;
     unsigned nearc = 0;
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ 
 
 __global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ part, int nblocks,
                                                    Meta* __restrict__ meta) {
+    pdl_prologue();
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
 #pragma unroll
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ pa
 __global__ void __launch_bounds__(256) k_bbox_clouds(const float* __restrict__ p, const int64_t* __restrict__ off,
                                                     float* __restrict__ bb, int* __restrict__ nonfinite, float near,
                                                     unsigned long long* __restrict__ near_pairs) {
+    pdl_prologue();
     const int c = blockIdx.x;
     const int64_t a = off[c], b = off[c + 1];
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
@@ -159,6 +162,7 @@ __global__ void __launch_bounds__(256) k_bbox_clouds(const float* __restrict__ p
 // =====================================================================================
 __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ p, int64_t n, Grid g,
                                              u64* __restrict__ key, int* __restrict__ val) {
+    pdl_prologue();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t sx = sub_coord(__ldg(p + 3 * i), g.lo[0], g.inv_h);
         uint32_t sy = sub_coord(__ldg(p + 3 * i + 1), g.lo[1], g.inv_h);
@@ -250,12 +254,14 @@ __device__ __forceinline__ void radix_scatter(const K* __restrict__ kin, const i
 
 __global__ void __launch_bounds__(RS_THREADS) k_radix_hist(const u64* __restrict__ key, int64_t n, int shift,
                                                           uint32_t* __restrict__ counts, int num_tiles) {
+    pdl_prologue();
     radix_hist<u64>(key, n, shift, counts, num_tiles);
 }
 __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter(const u64* __restrict__ kin, const int* __restrict__ vin,
                                                              u64* __restrict__ kout, int* __restrict__ vout,
                                                              int64_t n, int shift, const uint32_t* __restrict__ offs,
                                                              int num_tiles) {
+    pdl_prologue();
     radix_scatter<u64>(kin, vin, kout, vout, n, shift, offs, num_tiles);
 }
 // 32-bit keys (linear cell ids of the dense grid's key-sort path).  The scatter first sorts
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32l(const uint32_t*
                                                                 uint32_t* __restrict__ kout, int* __restrict__ vout,
                                                                 int64_t n, int shift, const uint32_t* __restrict__ offs,
                                                                 int num_tiles) {
+    pdl_prologue();
     __shared__ uint32_t wcnt[RS_THREADS / kWarp][256];
     __shared__ uint32_t goff[256], tstart[256];
     __shared__ uint32_t sk[RS_TILE];
@@ -351,12 +358,14 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32l(const uint32_t*
 
 __global__ void __launch_bounds__(RS_THREADS) k_radix_hist32(const uint32_t* __restrict__ key, int64_t n, int shift,
                                                             uint32_t* __restrict__ counts, int num_tiles) {
+    pdl_prologue();
     radix_hist<uint32_t>(key, n, shift, counts, num_tiles);
 }
 __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32(const uint32_t* __restrict__ kin,
                                                                const int* __restrict__ vin, uint32_t* __restrict__ kout,
                                                                int* __restrict__ vout, int64_t n, int shift,
                                                                const uint32_t* __restrict__ offs, int num_tiles) {
+    pdl_prologue();
     radix_scatter<uint32_t>(kin, vin, kout, vout, n, shift, offs, num_tiles);
 }
 
@@ -365,6 +374,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_scatter32(const uint32_t* 
 // =====================================================================================
 __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ p, const int* __restrict__ val, int64_t n,
                                                float4* __restrict__ spts) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         int i = val[s];
         spts[s] = make_float4(__ldg(p + 3 * (int64_t)i), __ldg(p + 3 * (int64_t)i + 1), __ldg(p + 3 * (int64_t)i + 2),
@@ -377,6 +387,7 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ p, con
 // =====================================================================================
 // flags[s] = groupHead | cellHead << 32 ; flags[n] = 0 (so the exclusive scan yields totals)
 __global__ void __launch_bounds__(256) k_heads(const u64* __restrict__ key, int64_t n, u64* __restrict__ flags) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= n; s += (int64_t)gridDim.x * blockDim.x) {
         u64 f = 0;
         if (s < n) {
@@ -410,6 +421,7 @@ __device__ __forceinline__ void decode_cell(u64 key, const Grid& g, uint32_t& cx
 
 __global__ void __launch_bounds__(256) k_fill_tables(const u64* __restrict__ key, const u64* __restrict__ ex, int64_t n,
                                                     Grid g, Tables T, Meta* __restrict__ meta) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const u64 e0 = ex[s], e1 = ex[s + 1];
         const u64 d = e1 - e0;
@@ -453,6 +465,7 @@ __global__ void __launch_bounds__(256) k_fill_tables(const u64* __restrict__ key
 __global__ void __launch_bounds__(256) k_init_uf(const u64* __restrict__ ex, const int* __restrict__ gstart, int64_t n,
                                                 int* __restrict__ parent, int* __restrict__ size,
                                                 int* __restrict__ minidx) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const int gidx = (int)(uint32_t)ex[s + 1] - 1;
         parent[s] = gstart[gidx + 1] - 1;
@@ -482,6 +495,7 @@ constexpr int kCellChunk = 8;  // cells taken per atomic on the dynamic work cou
 // order, groups = octants of the cell.
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_union(const float4* __restrict__ spts, Grid g, Tables T,
                                                            int* __restrict__ parent, Meta* __restrict__ meta) {
+    pdl_prologue();
     __shared__ PairSmem sm[SCAN_THREADS / kWarp];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     PairSmem& S = sm[w];
@@ -549,6 +563,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_union(const float4* __res
 // Also initialises the accumulators of root points (component nodes get theirs in k_dcomps).
 __global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64_t n, int* __restrict__ size,
                                                 int* __restrict__ minidx) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         int curr = ld_parent(parent, (int)s), next;
         if (curr == (int)s) {
@@ -571,6 +586,7 @@ constexpr int HH_SLOTS = 256;
 __global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                               int* __restrict__ size, int* __restrict__ minidx,
                                               Meta* __restrict__ meta, int only_sparse) {
+    pdl_prologue();
     if (only_sparse && 4 * (int64_t)meta->cells <= n) return;
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
     for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
@@ -629,6 +645,7 @@ __global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, c
 // Sparse-dominated clouds (many small components, deep forests: occupied cells > n/4)
 // flatten in a separate pass first; k_flat_stats's walks are then one load each.
 __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, int64_t n, const Meta* __restrict__ meta) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells <= n) return;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         int curr = ld_parent(parent, (int)s), next;
@@ -646,6 +663,7 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
 __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                                    int* __restrict__ size, int* __restrict__ minidx,
                                                    Meta* __restrict__ meta, int node_tail) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_flatten_if + k_stats
     if (node_tail) return;                     // dense grid: k_node_stats + k_sparse_stats
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
@@ -730,6 +748,7 @@ __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, co
 __global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent, const int* __restrict__ size,
                                                 int* __restrict__ minidx, int64_t n, long long min_size,
                                                 long long max_size, const Meta* __restrict__ meta) {
+    pdl_prologue();
     if (4 * (int64_t)meta->cells <= n) return;
     const int64_t nodes = n + 8 * (int64_t)meta->ndense;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nodes; r += (int64_t)gridDim.x * blockDim.x) {
@@ -744,6 +763,7 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
                                                 int64_t n, long long min_size, long long max_size,
                                                 int* __restrict__ labels, const Meta* __restrict__ meta,
                                                 const int64_t* __restrict__ boff, int nclouds) {
+    pdl_prologue();
     const bool folded = 4 * (int64_t)meta->cells > n;  // k_rootlab ran
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -794,6 +814,7 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
 // =====================================================================================
 __global__ void k_debug_pred(const float* __restrict__ a, const float* __restrict__ b, int64_t m, float t2,
                              uint8_t* __restrict__ out, float* __restrict__ d2out) {
+    pdl_prologue();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         float4 pa = make_float4(a[3 * i], a[3 * i + 1], a[3 * i + 2], 0.f);
         float4 pb = make_float4(b[3 * i], b[3 * i + 1], b[3 * i + 2], 0.f);

@@ -72,6 +72,7 @@ ApWs ap_carve(char* base, int64_t n) {
 }
 
 __global__ void k_ap_clear(ApWs w, int64_t n) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
         w.sizeP[i] = 0u;
         w.sizeG[i] = 0u;
@@ -83,6 +84,7 @@ __global__ void k_ap_clear(ApWs w, int64_t n) {
 
 __global__ void k_ap_keys(const int32_t* __restrict__ pred, const int32_t* __restrict__ gt, int64_t n, int B,
                           ApWs w) {
+    pdl_prologue();
     int valid = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + 1; i += (int64_t)gridDim.x * blockDim.x) {
         u64 key = ~0ull;
@@ -106,6 +108,7 @@ __global__ void k_ap_keys(const int32_t* __restrict__ pred, const int32_t* __res
 
 // run heads over the sorted keys (invalid keys sort last and start no run)
 __global__ void k_ap_heads(const u64* __restrict__ key, int64_t m, uint32_t* __restrict__ flag) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t f = 0u;
         if (i < m) {
@@ -118,6 +121,7 @@ __global__ void k_ap_heads(const u64* __restrict__ key, int64_t m, uint32_t* __r
 
 __global__ void k_ap_runs(const u64* __restrict__ key, int64_t m, const uint32_t* __restrict__ flag,
                           const uint32_t* __restrict__ pos, ApWs w) {
+    pdl_prologue();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         if (flag[i]) {
             w.rkey[pos[i]] = key[i];
@@ -132,6 +136,7 @@ __global__ void k_ap_runs(const u64* __restrict__ key, int64_t m, const uint32_t
 
 // one entry per predicted cluster (its first row), sort key (n - |P|) << B | P; the rest ~0
 __global__ void k_ap_pkeys(int64_t n, int B, ApWs w, u64* __restrict__ pk, int* __restrict__ pv) {
+    pdl_prologue();
     const int runs = w.meta[1];
     const u64 gmask = (1ull << B) - 1ull;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n + 1; r += (int64_t)gridDim.x * blockDim.x) {
@@ -155,6 +160,7 @@ __global__ void k_ap_pkeys(int64_t n, int B, ApWs w, u64* __restrict__ pk, int* 
 // greedy matching of M3 takes exactly these (nothing a cluster prefers is consumed before
 // its turn), so TP/FP follow in parallel; otherwise k_ap_greedy replays M3 in order.
 __global__ void k_ap_prefs(int64_t n, int B, double thr, ApWs w) {
+    pdl_prologue();
     const int runs = w.meta[1];
     const u64 gmask = (1ull << B) - 1ull;
     int np = 0, tp = 0, fp = 0, ng = 0;
@@ -198,6 +204,7 @@ __global__ void k_ap_prefs(int64_t n, int B, double thr, ApWs w) {
 // sorted keys, the lanes scan a cluster's rows and a warp argmax picks the unmatched best.
 __global__ void k_ap_greedy(int64_t n, int B, double thr, const u64* __restrict__ pk, const int* __restrict__ pv,
                             ApWs w, fec_ap_result_t* __restrict__ res) {
+    pdl_prologue();
     if (blockIdx.x != 0) return;
     const int lane = threadIdx.x & 31;
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);

@@ -13,6 +13,7 @@ constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 template <typename T>
 __global__ void __launch_bounds__(SC_THREADS) k_scan_tile(const T* __restrict__ in, T* __restrict__ out,
                                                          int64_t n, T* __restrict__ sums, const int* ndev) {
+    pdl_prologue();
     __shared__ T s[SC_TILE];
     __shared__ T wsum[SC_THREADS / kWarp];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_tile(const T* __restrict__ 
 template <typename T>
 __global__ void __launch_bounds__(SC_THREADS) k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__ sums,
                                                         const int* ndev) {
+    pdl_prologue();
     if (ndev) n = min(n, (int64_t)*ndev);
     const int64_t base = (int64_t)blockIdx.x * SC_TILE;
     if (base >= n) return;
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_lb(const uint32_t* __restri
                                                        int64_t n, const int* ndev,
                                                        unsigned long long* __restrict__ state,
                                                        unsigned int* __restrict__ counter) {
+    pdl_prologue();
     __shared__ uint32_t s[SC_TILE];
     __shared__ uint32_t wsum[SC_THREADS / kWarp];
     __shared__ unsigned int tile_sh;
@@ -187,11 +190,11 @@ int exclusive_scan_dn(const T* in, T* out, int64_t n, const int* ndev, T* scratc
     if (n <= 0) return 0;
     int launches = 1;
     int64_t nb = (n + SC_TILE - 1) / SC_TILE;
-    k_scan_tile<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, scratch, ndev);
+    pdl(k_scan_tile<T>, (unsigned)nb, SC_THREADS, 0, st)(in, out, n, scratch, ndev);
     if (nb > 1) {
         T* next = scratch + ((nb + 63) / 64) * 64 + 64;
         launches += exclusive_scan_dn<T>(scratch, scratch, nb, nullptr, next, st);
-        k_scan_add<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(out, n, scratch, ndev);
+        pdl(k_scan_add<T>, (unsigned)nb, SC_THREADS, 0, st)(out, n, scratch, ndev);
         ++launches;
     }
     return launches;
@@ -210,11 +213,11 @@ int scan_recursive(const T* in, T* out, int64_t n, const int* ndev, T* scratch, 
     if (n <= 0) return 0;
     int launches = 1;
     int64_t nb = (n + SC_TILE - 1) / SC_TILE;
-    k_scan_tile<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, scratch, ndev);
+    pdl(k_scan_tile<T>, (unsigned)nb, SC_THREADS, 0, st)(in, out, n, scratch, ndev);
     if (nb > 1) {
         T* next = scratch + ((nb + 63) / 64) * 64 + 64;
         launches += scan_recursive<T>(scratch, scratch, nb, nullptr, next, st);
-        k_scan_add<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(out, n, scratch, ndev);
+        pdl(k_scan_add<T>, (unsigned)nb, SC_THREADS, 0, st)(out, n, scratch, ndev);
         ++launches;
     }
     return launches;
@@ -231,7 +234,7 @@ int exclusive_scan_dn<uint32_t>(const uint32_t* in, uint32_t* out, int64_t n, co
     unsigned int* counter = reinterpret_cast<unsigned int*>(scratch);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(scratch + 64);
     cudaMemsetAsync(scratch, 0, 256 + (size_t)nb * 8, st);
-    k_scan_lb<<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, ndev, state, counter);
+    pdl(k_scan_lb, (unsigned)nb, SC_THREADS, 0, st)(in, out, n, ndev, state, counter);
     return 2;
 }
 template <>

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) k_slab_stats(const int* __restrict__ pare
                                                    int n_first, int* __restrict__ size,
                                                    int* __restrict__ minidx, int* __restrict__ ckey,
                                                    Meta* __restrict__ meta) {
+    pdl_prologue();
     __shared__ int hkey[SL_SLOTS], hcnt[SL_SLOTS], hmin[SL_SLOTS], hbk[SL_SLOTS];
     for (int k = threadIdx.x; k < SL_SLOTS; k += blockDim.x) {
         hkey[k] = -1;
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(256) k_slab_pack(const int* __restrict__ paren
                                                   int n_first, const int* __restrict__ size,
                                                   const int* __restrict__ minidx, const int* __restrict__ ckey,
                                                   int* __restrict__ rec, int rec_cap, const Meta* __restrict__ meta) {
+    pdl_prologue();
     int* P = rec + SLAB_HDR;
     int* Cr = rec + slab_c_off(rec_cap);
     const int64_t nodes = n + 8 * (int64_t)meta->ndense;
@@ -173,6 +175,7 @@ __device__ __forceinline__ int mh_lookup(const int* hkey, unsigned mask, int key
 
 __global__ void __launch_bounds__(256) k_merge_init(int* __restrict__ hkey, int* __restrict__ hpar,
                                                    int* __restrict__ gsize, int* __restrict__ gmin, int64_t hc) {
+    pdl_prologue();
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < hc; k += (int64_t)gridDim.x * blockDim.x) {
         hkey[k] = -1;
         hpar[k] = (int)k;
@@ -185,6 +188,7 @@ __global__ void __launch_bounds__(256) k_merge_init(int* __restrict__ hkey, int*
 __global__ void __launch_bounds__(256) k_merge_link(const int* __restrict__ all, int world, int64_t words,
                                                    int rec_cap, int* __restrict__ hkey, unsigned mask,
                                                    int* __restrict__ hpar) {
+    pdl_prologue();
     const int64_t total = (int64_t)world * rec_cap;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int rk = (int)(t / rec_cap), j = (int)(t % rec_cap);
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(256) k_merge_stats(const int* __restrict__ all
                                                     int rec_cap, const int* __restrict__ hkey, unsigned mask,
                                                     int* __restrict__ hpar, int* __restrict__ gsize,
                                                     int* __restrict__ gmin) {
+    pdl_prologue();
     const int64_t total = (int64_t)world * rec_cap;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int rk = (int)(t / rec_cap), j = (int)(t % rec_cap);
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(256) k_merge_resolve(const int* __restrict__ o
                                                       int* __restrict__ hpar, const int* __restrict__ gsize,
                                                       const int* __restrict__ gmin, int* __restrict__ size,
                                                       int* __restrict__ minidx) {
+    pdl_prologue();
     const int nc = __ldg(own + 1);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += gridDim.x * blockDim.x) {
         const int4 c = reinterpret_cast<const int4*>(own + slab_c_off(rec_cap))[j];
@@ -234,6 +240,7 @@ __global__ void __launch_bounds__(256) k_slab_relabel(const int* __restrict__ pa
                                                      const int* __restrict__ size, const int* __restrict__ minidx,
                                                      int64_t n, int n_owned, long long min_size,
                                                      long long max_size, int* __restrict__ labels) {
+    pdl_prologue();
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const int i = __ldg(val + s);
         if (i >= n_owned) continue;
