@@ -474,7 +474,7 @@ fec_status_t fec_ground_remove(const float* points, int64_t n, const int32_t* tr
     GroundWs w = g_carve(static_cast<char*>(workspace), n, n_hyp);
     const int H = n_hyp;
     const int64_t tiles = g_tiles(n);
-    if (H > 0) k_g_planes<<<(H + 127) / 128, 128, 0, st>>>(points, n, triplets, H, cos_max_tilt, w.planes, w.valid, w.cnt);
+    if (H > 0) pdl(k_g_planes, (H + 127) / 128, 128, 0, st)(points, n, triplets, H, cos_max_tilt, w.planes, w.valid, w.cnt);
     if (H > 0 && n > 0) {
         // per-device: SM count and the opt-in shared-memory size already granted to k_g_count
         static int sms_of[64] = {};
@@ -504,18 +504,18 @@ fec_status_t fec_ground_remove(const float* points, int64_t n, const int32_t* tr
             }
             cudaEventRecord(g_gev.e0, st);
         }
-        k_g_count<<<(unsigned)grid, 256, smem, st>>>(points, n, w.planes, H, threshold, w.cnt);
+        pdl(k_g_count, (unsigned)grid, 256, smem, st)(points, n, w.planes, H, threshold, w.cnt);
         if (timed) {
             cudaEventRecord(g_gev.e1, st);
             g_gev.recorded = true;
         }
     }
-    k_g_best<<<1, 1024, 0, st>>>(w.planes, w.valid, w.cnt, H, n, min_inliers, counts, result);
+    pdl(k_g_best, 1, 1024, 0, st)(w.planes, w.valid, w.cnt, H, n, min_inliers, counts, result);
     if (n > 0) {
-        k_g_flags<<<(unsigned)tiles, 256, 0, st>>>(points, n, triplets, result, threshold, w.tcount, w.part);
+        pdl(k_g_flags, (unsigned)tiles, 256, 0, st)(points, n, triplets, result, threshold, w.tcount, w.part);
         exclusive_scan<uint32_t>(w.tcount, w.tscan, tiles, w.scratch, st);
-        k_g_compact<<<(unsigned)tiles, 256, 0, st>>>(points, n, result, threshold, w.tscan, keep_points, keep_idx);
-        k_g_refine<<<1, 256, 0, st>>>(points, triplets, w.part, tiles, result);
+        pdl(k_g_compact, (unsigned)tiles, 256, 0, st)(points, n, result, threshold, w.tscan, keep_points, keep_idx);
+        pdl(k_g_refine, 1, 256, 0, st)(points, triplets, w.part, tiles, result);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return g_fail("fec_ground_remove launch", e);
@@ -540,8 +540,8 @@ fec_status_t fec_ground_expand_labels(const int32_t* keep_idx, const int32_t* ke
     if (!keep_idx || !keep_labels || !result || !labels_out) { set_last_error("null pointer"); return FEC_ERR_INVALID_ARGUMENT; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    k_g_fill<<<g, 256, 0, st>>>(labels_out, n);
-    k_g_expand<<<g, 256, 0, st>>>(keep_idx, keep_labels, result, labels_out);
+    pdl(k_g_fill, g, 256, 0, st)(labels_out, n);
+    pdl(k_g_expand, g, 256, 0, st)(keep_idx, keep_labels, result, labels_out);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return g_fail("fec_ground_expand_labels launch", e);
     return FEC_OK;

@@ -283,9 +283,9 @@ int ap_sort(u64*& kin, u64*& kout, int*& vin, int*& vout, int64_t m, int bits, c
     const int passes = (bits + 7) / 8;
     for (int p = 0; p < passes; ++p) {
         const int shift = 8 * p;
-        k_radix_hist<<<w.num_tiles, RS_THREADS, 0, st>>>(kin, m, shift, w.counts, w.num_tiles);
+        pdl(k_radix_hist, w.num_tiles, RS_THREADS, 0, st)(kin, m, shift, w.counts, w.num_tiles);
         launches += exclusive_scan<uint32_t>(w.counts, w.counts, (int64_t)256 * w.num_tiles, w.scan32, st);
-        k_radix_scatter<<<w.num_tiles, RS_THREADS, 0, st>>>(kin, vin, kout, vout, m, shift, w.counts, w.num_tiles);
+        pdl(k_radix_scatter, w.num_tiles, RS_THREADS, 0, st)(kin, vin, kout, vout, m, shift, w.counts, w.num_tiles);
         launches += 2;
         std::swap(kin, kout);
         std::swap(vin, vout);
@@ -318,23 +318,23 @@ fec_status_t fec_average_precision(const int32_t* pred, const int32_t* gt, int64
     const int B = ap_bits(n);
     const int64_t m = n + 1;  // one extra (invalid) key keeps every buffer non-empty
     const unsigned g = (unsigned)std::min<int64_t>((m + 255) / 256, 148 * 16);
-    k_ap_clear<<<g, 256, 0, st>>>(w, n);
-    k_ap_keys<<<g, 256, 0, st>>>(pred, gt, n, B, w);
+    pdl(k_ap_clear, g, 256, 0, st)(w, n);
+    pdl(k_ap_keys, g, 256, 0, st)(pred, gt, n, B, w);
     u64 *kin = w.keyA, *kout = w.keyB;
     int *vin = w.valA, *vout = w.valB;
     ap_sort(kin, kout, vin, vout, m, 2 * B, w, st);
-    k_ap_heads<<<g, 256, 0, st>>>(kin, m, w.flag);
+    pdl(k_ap_heads, g, 256, 0, st)(kin, m, w.flag);
     exclusive_scan<uint32_t>(w.flag, w.pos, m + 1, w.scratch, st);
-    k_ap_runs<<<g, 256, 0, st>>>(kin, m, w.flag, w.pos, w);
+    pdl(k_ap_runs, g, 256, 0, st)(kin, m, w.flag, w.pos, w);
     // predicted clusters: keys into the buffers the pair sort no longer needs
     u64* pk = kout;
     int* pv = vout;
-    k_ap_pkeys<<<g, 256, 0, st>>>(n, B, w, pk, pv);
+    pdl(k_ap_pkeys, g, 256, 0, st)(n, B, w, pk, pv);
     u64* pk2 = kin;
     int* pv2 = vin;
     ap_sort(pk, pk2, pv, pv2, m, 2 * B, w, st);
-    k_ap_prefs<<<g, 256, 0, st>>>(n, B, threshold, w);
-    k_ap_greedy<<<1, 32, 0, st>>>(n, B, threshold, pk, pv, w, result);
+    pdl(k_ap_prefs, g, 256, 0, st)(n, B, threshold, w);
+    pdl(k_ap_greedy, 1, 32, 0, st)(n, B, threshold, pk, pv, w, result);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_last_error(std::string("fec_average_precision launch: ") + cudaGetErrorString(e));
