@@ -1,6 +1,7 @@
 // C ABI (include/fec.h) and host orchestration of the FEC sm_100a pipeline.
 #include <float.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -19,6 +20,8 @@ thread_local fec_stats_t g_stats;
 thread_local bool g_stats_valid = false;
 thread_local int g_instrument = 0;
 thread_local Meta* g_pinned_meta = nullptr;
+thread_local HostBBox* g_host_bbox = nullptr;  // mapped pinned memory (k_bbox_final writes it)
+thread_local int g_bbox_seq = 0;
 thread_local int g_timing = 0;
 thread_local int g_grid_mode = 0;
 thread_local int64_t g_item_cap = 0;  // test hook: cap on the queued uncertain pairs (0 = default)
@@ -294,9 +297,24 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     if (!B) {
         pdl(k_bbox_partial, bb_blocks, 256, 0, st)(pts, n, vec4, L.part, &L.meta->nonfinite, near,
                                                   &L.meta->near_pairs);
-        pdl(k_bbox_final, 1, 256, 0, st)(L.part, (int)bb_blocks, L.meta);
+        if (!g_host_bbox) FEC_CUDA(cudaHostAlloc(&g_host_bbox, sizeof(HostBBox), cudaHostAllocMapped));
+        const int seq = ++g_bbox_seq;
+        pdl(k_bbox_final, 1, 256, 0, st)(L.part, (int)bb_blocks, L.meta, g_host_bbox, seq);
         launches += 2;
-        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+        FEC_CUDA(cudaGetLastError());
+        // wait for the record (no stream synchronisation, no copy); if the stream drains
+        // without it, a launch failed: the synchronisation reports the error
+        volatile int* vs = &g_host_bbox->seq;
+        for (int spins = 0; *vs != seq; ++spins) {
+            if ((spins & 1023) == 1023 && cudaStreamQuery(st) != cudaErrorNotReady && *vs != seq) {
+                FEC_CUDA(cudaStreamSynchronize(st));
+                if (*vs != seq) { g_err = "bbox record missing"; return FEC_ERR_CUDA; }
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (int k = 0; k < 6; ++k) g_pinned_meta->bbox[k] = g_host_bbox->bbox[k];
+        g_pinned_meta->nonfinite = g_host_bbox->nonfinite;
+        g_pinned_meta->near_pairs = g_host_bbox->near_pairs;
     } else {
         const size_t need = (size_t)B->nclouds * (6 * sizeof(float) + 3 * sizeof(double) + sizeof(int32_t)) + 64;
         if (g_pinned_batch_bytes < need) {
@@ -315,7 +333,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
         FEC_CUDA(cudaMemcpyAsync(bbh, B->bb_dev, (size_t)B->nclouds * 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
     }
-    FEC_CUDA(cudaStreamSynchronize(st));
+    if (B) FEC_CUDA(cudaStreamSynchronize(st));
     const Meta hm = *g_pinned_meta;
     if (hm.nonfinite) { g_err = "non-finite coordinate"; return FEC_ERR_NONFINITE; }
 

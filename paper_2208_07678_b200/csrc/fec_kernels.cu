@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_bbox_partial(const float* __restrict__ 
 }
 
 __global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ part, int nblocks,
-                                                   Meta* __restrict__ meta) {
+                                                   Meta* __restrict__ meta, HostBBox* hb, int seq) {
     pdl_prologue();
     float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
@@ -106,6 +106,16 @@ __global__ void __launch_bounds__(256) k_bbox_final(const float* __restrict__ pa
         for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
             v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
         meta->bbox[threadIdx.x] = v;
+        if (hb) hb->bbox[threadIdx.x] = v;
+    }
+    if (hb) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            hb->nonfinite = meta->nonfinite;
+            hb->near_pairs = meta->near_pairs;
+            __threadfence_system();
+            *reinterpret_cast<volatile int*>(&hb->seq) = seq;
+        }
     }
 }
 

@@ -48,7 +48,18 @@ struct Tables {
 
 __global__ void k_bbox_partial(const float* p, int64_t n, int vec4, float* part, int* nonfinite, float near,
                                unsigned long long* near_pairs);
-__global__ void k_bbox_final(const float* part, int nblocks, Meta* meta);
+// What the host needs after a1, written by k_bbox_final straight into mapped pinned host
+// memory; `seq` last (after a system-scope fence), so the host can spin on it instead of
+// copying Meta back and synchronising the stream.
+struct HostBBox {
+    float bbox[6];
+    int nonfinite;
+    int pad;
+    unsigned long long near_pairs;
+    int seq;
+    int pad2;
+};
+__global__ void k_bbox_final(const float* part, int nblocks, Meta* meta, HostBBox* hb, int seq);
 __global__ void k_keys(const float* p, int64_t n, Grid g, u64* key, int* val);
 __global__ void k_radix_hist(const u64* key, int64_t n, int shift, uint32_t* counts, int num_tiles);
 __global__ void k_radix_scatter(const u64* kin, const int* vin, u64* kout, int* vout, int64_t n, int shift,
