@@ -1387,19 +1387,39 @@ __global__ void __launch_bounds__(256) k_sparse_stats(int* __restrict__ parent, 
     pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;
     const int ns = meta->nsparse;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += gridDim.x * blockDim.x) {
-        const int P = __ldg(slist + e);
-        const int a0 = (int)__ldg(cstart + P), a1 = (int)__ldg(cstart + P + 1);
-        for (int s = a0; s < a1; ++s) {
-            int curr = ld_parent(parent, s), next;
-            if (curr != s) {
-                while (curr < (next = ld_parent(parent, curr))) curr = next;
-                st_parent(parent, s, curr);
-            } else if (meta->instrument) {
-                atomicAdd(&meta->components, 1ull);
+    const int lane = threadIdx.x & 31;
+    // lane per sparse cell, the cells' points in lock-step rounds (<= SPARSE_MAX), and the
+    // counts aggregated per distinct root over the warp (hot roots: one atomic per warp)
+    const int nr = (ns + 31) & ~31;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nr; e += gridDim.x * blockDim.x) {
+        int a0 = 0, a1 = 0;
+        if (e < ns) {
+            const int P = __ldg(slist + e);
+            a0 = (int)__ldg(cstart + P);
+            a1 = (int)__ldg(cstart + P + 1);
+        }
+        for (int j = 0; j < SPARSE_MAX; ++j) {
+            const int s = a0 + j;
+            int curr = -1, v = 0x7fffffff;
+            if (s < a1) {
+                curr = ld_parent(parent, s);
+                int next;
+                if (curr != s) {
+                    while (curr < (next = ld_parent(parent, curr))) curr = next;
+                    st_parent(parent, s, curr);
+                } else if (meta->instrument) {
+                    atomicAdd(&meta->components, 1ull);
+                }
+                v = __ldg(sidx + s);
             }
-            atomicAdd(size + curr, 1);
-            atomicMin(minidx + curr, __ldg(sidx + s));
+            const unsigned peers = __match_any_sync(0xffffffffu, curr);
+            const int cnt = __popc(peers);
+            const int mn = __reduce_min_sync(peers, v);
+            if (curr >= 0 && lane == __ffs(peers) - 1) {
+                atomicAdd(size + curr, cnt);
+                atomicMin(minidx + curr, mn);
+            }
+            if (!__any_sync(0xffffffffu, a0 + j + 1 < a1)) break;
         }
     }
 }
