@@ -1362,20 +1362,32 @@ __global__ void __launch_bounds__(256) k_node_stats(int* __restrict__ parent, co
     pdl_prologue();
     if (4 * (int64_t)meta->cells > n) return;
     const int64_t nn = 8 * (int64_t)meta->ndense;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
-        if ((int)(t & 7) >= __ldg(ncomp + (t >> 3))) continue;  // unused component slot
-        const int node = nbase + (int)t;
-        int curr = ld_parent(parent, node), next;
-        if (curr == node) {  // a root keeps its own totals
-            if (meta->instrument) atomicAdd(&meta->components, 1ull);
-            continue;
+    const int64_t nr = (nn + 31) & ~int64_t(31);  // whole warps stay in the loop
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (int64_t)gridDim.x * blockDim.x) {
+        int root = -1, c = 0, m = 0x7fffffff;
+        if (t < nn && (int)(t & 7) < __ldg(ncomp + (t >> 3))) {  // a used component slot
+            const int node = nbase + (int)t;
+            int curr = ld_parent(parent, node), next;
+            if (curr == node) {  // a root keeps its own totals
+                if (meta->instrument) atomicAdd(&meta->components, 1ull);
+            } else {
+                while (curr < (next = ld_parent(parent, curr))) curr = next;
+                st_parent(parent, node, curr);
+                c = size[node];
+                if (c) {
+                    root = curr;
+                    m = minidx[node];
+                }
+            }
         }
-        while (curr < (next = ld_parent(parent, curr))) curr = next;
-        st_parent(parent, node, curr);
-        const int c = size[node];
-        if (c) {
-            atomicAdd(size + curr, c);
-            atomicMin(minidx + curr, minidx[node]);
+        // nodes of one big component share a root: one atomic per distinct root per warp
+        const unsigned peers = __match_any_sync(0xffffffffu, root);
+        const int tot = __reduce_add_sync(peers, c);
+        const int mn = __reduce_min_sync(peers, m);
+        if (root >= 0 && lane == __ffs(peers) - 1) {
+            atomicAdd(size + root, tot);
+            atomicMin(minidx + root, mn);
         }
     }
 }
