@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, in
                                                      unsigned int* __restrict__ counter) {
     pdl_prologue();
     __shared__ uint32_t s[CS_TILE];
+    __shared__ uint32_t sbits[CS_TILE];  // the tile's words, for the emission (no reload)
     __shared__ uint32_t wsum[CS_THREADS / kWarp];
     __shared__ unsigned int tile_sh;
     __shared__ uint32_t prefix_sh;
@@ -231,7 +232,9 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, in
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
         const int64_t i = base + k * CS_THREADS + tid;
-        s[k * CS_THREADS + tid] = i < words ? (uint32_t)__popc(cw[i].x) : 0u;
+        const uint32_t b = i < words ? cw[i].x : 0u;
+        sbits[k * CS_THREADS + tid] = b;
+        s[k * CS_THREADS + tid] = (uint32_t)__popc(b);
     }
     __syncthreads();
     uint32_t loc[CS_ITEMS];
@@ -303,8 +306,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, in
     }
     for (int c = 0; c < CS_ITEMS; ++c) {
         const int li = w * (CS_ITEMS * kWarp) + c * kWarp + lane;
-        const int64_t i = base + li;
-        const uint32_t bits = i < words ? cw[i].x : 0u;
+        const uint32_t bits = sbits[li];
         unsigned m = __ballot_sync(0xffffffffu, bits != 0u);
         while (m) {
             const int j = __ffs(m) - 1;
