@@ -297,7 +297,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     if (!B) {
         pdl(k_bbox_partial, bb_blocks, 256, 0, st)(pts, n, vec4, L.part, &L.meta->nonfinite, near,
                                                   &L.meta->near_pairs);
-        if (!g_host_bbox) FEC_CUDA(cudaHostAlloc(&g_host_bbox, sizeof(HostBBox), cudaHostAllocMapped));
+        if (!g_host_bbox) FEC_CUDA(cudaHostAlloc(&g_host_bbox, sizeof(HostBBox), cudaHostAllocMapped | cudaHostAllocPortable));
         const int seq = ++g_bbox_seq;
         pdl(k_bbox_final, 1, 256, 0, st)(L.part, (int)bb_blocks, L.meta, g_host_bbox, seq);
         launches += 2;
