@@ -646,22 +646,16 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     pdl(k_flatten_if, wave, 256, 0, st)(L.parent, n, L.meta);
     mark(8, st);
     const int dense = C.g.dense;
-    pdl(k_flat_stats, ew, 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, dense);
-    pdl(k_stats, ew, 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, 1);
-    if (dense) {
-        // few sparse cells: totals per component node, then the sparse points (node_accumulate)
-        pdl(k_node_stats, grid_for(8 * dense_max(n), 256, dev_info().sms * 8), 256, 0, st)(
-            L.parent, L.ncomp, L.size, L.minidx, (int)n, L.meta, n);
-        pdl(k_sparse_stats, grid_for(dense_max(n), 256, dev_info().sms * 8), 256, 0, st)(
-            L.parent, L.cstart, L.slist, C.val, L.size, L.minidx, L.meta, n);
-        C.launches += 2;
-    }
+    // a9 in one launch (k_stats / node tail / k_flat_stats, chosen on the device)
+    // (at least two blocks: the node tail splits the grid in halves)
+    pdl(k_tail_stats, std::max(ew, 2u), 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, dense, L.ncomp,
+                                                   L.cstart, L.slist);
     mark(9, st);
     pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
     pdl(k_relabel, grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st)(
         L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
         B ? B->off_dev : nullptr, B ? B->nclouds : 0);
-    C.launches += 5;
+    C.launches += 4;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
     return finish_stats(C, n, st);

@@ -1358,85 +1358,9 @@ __global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__
 // flattened onto it, and adds its own totals to the root's; then the points of sparse cells
 // (the compact list of k_slist) find their roots, are flattened and counted one by one.
 // Only for dense-grid clouds with few sparse cells; the others run k_flat_stats / k_stats.
-__global__ void __launch_bounds__(256) k_node_stats(int* __restrict__ parent, const int* __restrict__ ncomp,
-                                                   int* __restrict__ size, int* __restrict__ minidx, int nbase,
-                                                   Meta* __restrict__ meta, int64_t n) {
-    pdl_prologue();
-    if (4 * (int64_t)meta->cells > n) return;
-    const int64_t nn = 8 * (int64_t)meta->ndense;
-    const int64_t nr = (nn + 31) & ~int64_t(31);  // whole warps stay in the loop
-    const int lane = threadIdx.x & 31;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (int64_t)gridDim.x * blockDim.x) {
-        int root = -1, c = 0, m = 0x7fffffff;
-        if (t < nn && (int)(t & 7) < __ldg(ncomp + (t >> 3))) {  // a used component slot
-            const int node = nbase + (int)t;
-            int curr = ld_parent(parent, node), next;
-            if (curr == node) {  // a root keeps its own totals
-                if (meta->instrument) atomicAdd(&meta->components, 1ull);
-            } else {
-                while (curr < (next = ld_parent(parent, curr))) curr = next;
-                st_parent(parent, node, curr);
-                c = size[node];
-                if (c) {
-                    root = curr;
-                    m = minidx[node];
-                }
-            }
-        }
-        // nodes of one big component share a root: one atomic per distinct root per warp
-        const unsigned peers = __match_any_sync(0xffffffffu, root);
-        const int tot = __reduce_add_sync(peers, c);
-        const int mn = __reduce_min_sync(peers, m);
-        if (root >= 0 && lane == __ffs(peers) - 1) {
-            atomicAdd(size + root, tot);
-            atomicMin(minidx + root, mn);
-        }
-    }
-}
 
-__global__ void __launch_bounds__(256) k_sparse_stats(int* __restrict__ parent, const uint32_t* __restrict__ cstart,
-                                                     const int* __restrict__ slist, const int* __restrict__ sidx,
-                                                     int* __restrict__ size, int* __restrict__ minidx,
-                                                     Meta* __restrict__ meta, int64_t n) {
-    pdl_prologue();
-    if (4 * (int64_t)meta->cells > n) return;
-    const int ns = meta->nsparse;
-    const int lane = threadIdx.x & 31;
-    // lane per sparse cell, the cells' points in lock-step rounds (<= SPARSE_MAX), and the
-    // counts aggregated per distinct root over the warp (hot roots: one atomic per warp)
-    const int nr = (ns + 31) & ~31;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nr; e += gridDim.x * blockDim.x) {
-        int a0 = 0, a1 = 0;
-        if (e < ns) {
-            const int P = __ldg(slist + e);
-            a0 = (int)__ldg(cstart + P);
-            a1 = (int)__ldg(cstart + P + 1);
-        }
-        for (int j = 0; j < SPARSE_MAX; ++j) {
-            const int s = a0 + j;
-            int curr = -1, v = 0x7fffffff;
-            if (s < a1) {
-                curr = ld_parent(parent, s);
-                int next;
-                if (curr != s) {
-                    while (curr < (next = ld_parent(parent, curr))) curr = next;
-                    st_parent(parent, s, curr);
-                } else if (meta->instrument) {
-                    atomicAdd(&meta->components, 1ull);
-                }
-                v = __ldg(sidx + s);
-            }
-            const unsigned peers = __match_any_sync(0xffffffffu, curr);
-            const int cnt = __popc(peers);
-            const int mn = __reduce_min_sync(peers, v);
-            if (curr >= 0 && lane == __ffs(peers) - 1) {
-                atomicAdd(size + curr, cnt);
-                atomicMin(minidx + curr, mn);
-            }
-            if (!__any_sync(0xffffffffu, a0 + j + 1 < a1)) break;
-        }
-    }
-}
+
+
 
 // LOCAL clouds have few sparse cells (C4: 73k of 358k cells, 0.8% of the points), so the
 // kernel is a few short waves whose time is the dependent-load chain per cell.  16 lanes per

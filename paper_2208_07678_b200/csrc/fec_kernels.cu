@@ -593,18 +593,17 @@ __global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64
 constexpr int HH_SLOTS = 256;
 // `only_sparse`: run only for sparse-dominated clouds (occupied cells > n/4; the forest was
 // flattened by k_flatten_if), where per-lane aggregation of this form is the faster one.
-__global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+__device__ __forceinline__ void stats_body(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                               int* __restrict__ size, int* __restrict__ minidx,
-                                              Meta* __restrict__ meta, int only_sparse) {
-    pdl_prologue();
+                                              Meta* __restrict__ meta, int only_sparse, int bid, int nblk) {
     if (only_sparse && 4 * (int64_t)meta->cells <= n) return;
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
     for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     unsigned long long roots = 0;
-    const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
-    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int64_t chunk = ((n + nblk - 1) / nblk + 255) / 256 * 256;
+    const int64_t b0 = (int64_t)bid * chunk, b1 = min(n, b0 + chunk);
     for (int64_t s0 = b0; s0 < b1; s0 += blockDim.x) {
         const int64_t s = s0 + threadIdx.x;
         const bool ok = s < b1;
@@ -651,6 +650,12 @@ __global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, c
         if (lane == 0 && roots) atomicAdd(&meta->components, roots);
     }
 }
+__global__ void __launch_bounds__(256) k_stats(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+                                              int* __restrict__ size, int* __restrict__ minidx,
+                                              Meta* __restrict__ meta, int only_sparse) {
+    pdl_prologue();
+    stats_body(parent, val, n, size, minidx, meta, only_sparse, blockIdx.x, gridDim.x);
+}
 
 // Sparse-dominated clouds (many small components, deep forests: occupied cells > n/4)
 // flatten in a separate pass first; k_flat_stats's walks are then one load each.
@@ -670,10 +675,9 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
 // aggregated per warp and per block as in k_stats.  Roots' accumulators were initialised
 // earlier (points of sparse cells in k_dinit / k_sgather, component nodes in k_dcomps, hashed
 // mode in k_init_uf).
-__global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+__device__ __forceinline__ void flat_stats_body(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                                    int* __restrict__ size, int* __restrict__ minidx,
-                                                   Meta* __restrict__ meta, int node_tail) {
-    pdl_prologue();
+                                                   Meta* __restrict__ meta, int node_tail, int bid, int nblk) {
     if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_flatten_if + k_stats
     if (node_tail) return;                     // dense grid: k_node_stats + k_sparse_stats
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
@@ -682,8 +686,8 @@ __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, co
     const int lane = threadIdx.x & 31;
     unsigned long long roots = 0;
     const int64_t per = 4 * (int64_t)blockDim.x;
-    const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + per - 1) / per * per;
-    const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int64_t chunk = ((n + nblk - 1) / nblk + per - 1) / per * per;
+    const int64_t b0 = (int64_t)bid * chunk, b1 = min(n, b0 + chunk);
     for (int64_t s0 = b0; s0 < b1; s0 += per) {
         // round j covers positions s0 + j*blockDim + threadIdx.x: a warp holds 32 consecutive
         // positions per round (equal roots meet in one aggregation step); the 4 rounds' loads
@@ -750,6 +754,129 @@ __global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, co
     if (meta->instrument) {
         for (int o = 16; o > 0; o >>= 1) roots += __shfl_xor_sync(0xffffffffu, roots, o);
         if (lane == 0 && roots) atomicAdd(&meta->components, roots);
+    }
+}
+__global__ void __launch_bounds__(256) k_flat_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+                                                   int* __restrict__ size, int* __restrict__ minidx,
+                                                   Meta* __restrict__ meta, int node_tail) {
+    pdl_prologue();
+    flat_stats_body(parent, val, n, size, minidx, meta, node_tail, blockIdx.x, gridDim.x);
+}
+
+
+// ---- single-GPU tail, one launch for the stats of every mode ----------------------------
+__device__ __forceinline__ void node_stats_body(int* __restrict__ parent, const int* __restrict__ ncomp,
+                                                   int* __restrict__ size, int* __restrict__ minidx, int nbase,
+                                                   Meta* __restrict__ meta, int64_t n, int bid, int nblk) {
+    if (4 * (int64_t)meta->cells > n) return;
+    const int64_t nn = 8 * (int64_t)meta->ndense;
+    const int64_t nr = (nn + 31) & ~int64_t(31);  // whole warps stay in the loop
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (int64_t)bid * blockDim.x + threadIdx.x; t < nr; t += (int64_t)nblk * blockDim.x) {
+        int root = -1, c = 0, m = 0x7fffffff;
+        if (t < nn && (int)(t & 7) < __ldg(ncomp + (t >> 3))) {  // a used component slot
+            const int node = nbase + (int)t;
+            int curr = ld_parent(parent, node), next;
+            if (curr == node) {  // a root keeps its own totals
+                if (meta->instrument) atomicAdd(&meta->components, 1ull);
+            } else {
+                while (curr < (next = ld_parent(parent, curr))) curr = next;
+                st_parent(parent, node, curr);
+                c = size[node];
+                if (c) {
+                    root = curr;
+                    m = minidx[node];
+                }
+            }
+        }
+        // nodes of one big component share a root: one atomic per distinct root per warp
+        const unsigned peers = __match_any_sync(0xffffffffu, root);
+        const int tot = __reduce_add_sync(peers, c);
+        const int mn = __reduce_min_sync(peers, m);
+        if (root >= 0 && lane == __ffs(peers) - 1) {
+            atomicAdd(size + root, tot);
+            atomicMin(minidx + root, mn);
+        }
+    }
+}
+
+__device__ __forceinline__ void sparse_stats_body(int* __restrict__ parent, const uint32_t* __restrict__ cstart,
+                                                     const int* __restrict__ slist, const int* __restrict__ sidx,
+                                                     int* __restrict__ size, int* __restrict__ minidx,
+                                                     Meta* __restrict__ meta, int64_t n, int bid, int nblk) {
+    if (4 * (int64_t)meta->cells > n) return;
+    const int ns = meta->nsparse;
+    const int lane = threadIdx.x & 31;
+    // lane per sparse cell, the cells' points in lock-step rounds (<= SPARSE_MAX), and the
+    // counts aggregated per distinct root over the warp (hot roots: one atomic per warp)
+    const int nr = (ns + 31) & ~31;
+    for (int e = bid * blockDim.x + threadIdx.x; e < nr; e += nblk * blockDim.x) {
+        int a0 = 0, a1 = 0;
+        if (e < ns) {
+            const int P = __ldg(slist + e);
+            a0 = (int)__ldg(cstart + P);
+            a1 = (int)__ldg(cstart + P + 1);
+        }
+        for (int j = 0; j < SPARSE_MAX; ++j) {
+            const int s = a0 + j;
+            int curr = -1, v = 0x7fffffff;
+            if (s < a1) {
+                curr = ld_parent(parent, s);
+                int next;
+                if (curr != s) {
+                    while (curr < (next = ld_parent(parent, curr))) curr = next;
+                    st_parent(parent, s, curr);
+                } else if (meta->instrument) {
+                    atomicAdd(&meta->components, 1ull);
+                }
+                v = __ldg(sidx + s);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, curr);
+            const int cnt = __popc(peers);
+            const int mn = __reduce_min_sync(peers, v);
+            if (curr >= 0 && lane == __ffs(peers) - 1) {
+                atomicAdd(size + curr, cnt);
+                atomicMin(minidx + curr, mn);
+            }
+            if (!__any_sync(0xffffffffu, a0 + j + 1 < a1)) break;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_node_stats(int* __restrict__ parent, const int* __restrict__ ncomp,
+                                                   int* __restrict__ size, int* __restrict__ minidx, int nbase,
+                                                   Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
+    node_stats_body(parent, ncomp, size, minidx, nbase, meta, n, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(256) k_sparse_stats(int* __restrict__ parent, const uint32_t* __restrict__ cstart,
+                                                     const int* __restrict__ slist, const int* __restrict__ sidx,
+                                                     int* __restrict__ size, int* __restrict__ minidx,
+                                                     Meta* __restrict__ meta, int64_t n) {
+    pdl_prologue();
+    sparse_stats_body(parent, cstart, slist, sidx, size, minidx, meta, n, blockIdx.x, gridDim.x);
+}
+
+// The component statistics of the single-GPU tail in one launch (the variant is a device-side
+// choice): sparse-dominated clouds -> k_stats's body; dense grid with few sparse cells -> the
+// node tail (first half of the blocks: component nodes, second half: points of sparse cells;
+// independent: they only add into roots); otherwise (hashed mode) -> k_flat_stats's body.
+__global__ void __launch_bounds__(256) k_tail_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
+                                                   int* __restrict__ size, int* __restrict__ minidx,
+                                                   Meta* __restrict__ meta, int dense, const int* __restrict__ ncomp,
+                                                   const uint32_t* __restrict__ cstart, const int* __restrict__ slist) {
+    pdl_prologue();
+    if (4 * (int64_t)meta->cells > n) {
+        stats_body(parent, val, n, size, minidx, meta, 1, blockIdx.x, gridDim.x);
+    } else if (dense) {
+        const int half = (int)(gridDim.x >> 1);  // >= 1: the host launches >= 2 blocks
+        if ((int)blockIdx.x < half)
+            node_stats_body(parent, ncomp, size, minidx, (int)n, meta, n, blockIdx.x, half);
+        else
+            sparse_stats_body(parent, cstart, slist, val, size, minidx, meta, n, blockIdx.x - half, gridDim.x - half);
+    } else {
+        flat_stats_body(parent, val, n, size, minidx, meta, 0, blockIdx.x, gridDim.x);
     }
 }
 

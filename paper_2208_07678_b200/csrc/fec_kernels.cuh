@@ -124,6 +124,8 @@ __global__ void k_dinit(const float4* spts, int64_t n, Grid g, const uint2* cw, 
 __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int* dlist, const int* ncomp,
                           const u64* cmask, Grid g, int nbase, int* parent, const Meta* meta, const int* sidx,
                           int* size, int* minidx, int node_stats, int64_t n);
+__global__ void k_tail_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta, int dense,
+                             const int* ncomp, const uint32_t* cstart, const int* slist);
 __global__ void k_node_stats(int* parent, const int* ncomp, int* size, int* minidx, int nbase, Meta* meta, int64_t n);
 __global__ void k_sparse_stats(int* parent, const uint32_t* cstart, const int* slist, const int* sidx, int* size,
                                int* minidx, Meta* meta, int64_t n);
