@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--check", action="store_true", help="also verify the labels bit-exactly (untimed)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay one captured CUDA graph per step (auto: clouds of <= 2^20 points, whose "
+                         "step is launch-bound); the call is fec_cluster_ws_async either way")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even at N=1 (testing)")
     ap.add_argument("--grid-mode", default="auto", choices=["auto", "hashed", "keysort", "countsort"],
                     help="testing: force a binning mode")
@@ -135,12 +138,15 @@ class ClockSampler:
 
 
 STAGE_KERNELS = {
-    "a2_bin_keys": "k_cmark, k_cscan, k_dcount2 (count path) / k_lkey + radix (key path)",
-    "a3_sort": "k_scan_lb, k_ccount, k_dbits_*, k_dcomps, k_dscatter2 (count path) / k_smark .. k_scount",
-    "a4_gather_init": "k_dinit / k_dparent",
+    "a1_bbox_validate": "k_bbox (its last block plans the grid on the device), k_zero",
+    "a2_bin_keys": "k_lkey + k_onesweep x passes (key path)",
+    "a3_sort": "k_cmark / k_smark, k_cscan, k_dcount2 + k_scan_lb + k_ccount / k_sgather + k_scount, k_dbits_*, "
+               "k_dcomps",
+    "a4_gather_init": "k_dscatter (count path: scatter + sorted-order init) / k_dparent (key path)",
     "a6a7_scan_union": "k_union_sparse(_local), k_slist, k_dense_link x2, k_dense_overflow, k_flatten_nodes, "
                        "k_dense_filter, k_dense_items",
-    "a9_stats": "k_node_stats + k_sparse_stats / k_flat_stats / k_stats",
+    "a8_flatten": "k_flatten_if",
+    "a9_stats": "k_tail_stats",
     "a10_relabel": "k_rootlab, k_relabel",
 }
 
@@ -153,48 +159,35 @@ def roofline_stages(stages: dict) -> dict:
 
 
 def algorithmic_bytes(stage: str, n: int, st: dict) -> float:
-    """Bytes each stage must move: n points, C grid cells (dense mode),
-    md points in dense cells, G groups / U cells and P radix passes (hashed mode)."""
-    if st["dense_table"]:
-        C = float(np.prod(st["dims"]))          # grid cells (occupancy bitmap: 1 bit each)
-        U = float(max(st.get("cells", 0), 0))  # occupied cells
-        nd = float(max(st.get("dense_cells", 0), 0))
-        md = float(max(st.get("dense_points", 0), 0))
-        ns = n - md                             # points of sparse cells
-        model = {
-            "a1_bbox_validate": 12.0 * n,
-            # occupancy bitmap + word bases (C/8 B, ~9 touches), cell lists (28 B/cell), two
-            # reads of xyz, per-cell counts + fine masks
-            "a2_bin_keys": 24.0 * n + 1.125 * C + 44.0 * U,
-            # scan counts, cursors, dense records + components (~180 B/cell), xyz -> float4
-            "a3_sort": 24.0 * U + 180.0 * nd + 12.0 * n + 16.0 * n,
-            "a4_gather_init": 16.0 * n + 8.0 * n + 8.0 * ns,      # float4 -> parent, idx (+ root accumulators)
-            "a5_tables": 0.0,
-            "a6a7_union_sparse": 24.0 * ns + 8.0 * U,             # sparse points + parents, cell starts
-            "a6a7_union_dense": 128.0 * nd,                       # component masks + node parents
-            # SURVEY §8(d) B_model for the neighbour scan + union-find (a6+a7): 28 B per point
-            # (float4 read 16 + parent init / hook 12), over the two union stages together
-            "a6a7_scan_union": 28.0 * n,
-            "a8_flatten": 8.0 * n if 4 * U > n else 0.0,          # separate flatten (sparse-dominated only)
-            # node tail (few sparse cells): sparse points + 8 node slots per dense cell
-            "a9_stats": (12.0 * ns + 64.0 * nd) if 4 * U <= n else 12.0 * n,
-            "a10_relabel": 12.0 * n,                              # parent + index -> label
-        }
-    else:
-        G, U, P = st["groups"], st["cells"], st["radix_passes"]
-        model = {
-            "a1_bbox_validate": 12.0 * n,
-            "a2_bin_keys": 12.0 * n + 12.0 * n,
-            "a3_sort": P * (8.0 * n + 24.0 * n),
-            "a4_gather_init": 4.0 * n + 12.0 * n + 16.0 * n,
-            "a5_tables": 72.0 * n + 5.0 * G + 16.0 * U,
-            "a6a7_union_sparse": 0.0,
-            "a6a7_union_dense": 16.0 * n + 8.0 * n + 5.0 * G + 12.0 * U,
-            "a6a7_scan_union": 28.0 * n,
-            "a8_flatten": 8.0 * n,
-            "a9_stats": 8.0 * n,
-            "a10_relabel": 20.0 * n,
-        }
+    """Bytes each stage must move: n points, C grid cells (bitmap index; hash
+    mode: table slots), U occupied cells, nd dense cells, md points in dense cells, P key-sort
+    passes (0 on the counting path)."""
+    C = float(np.prod(st["dims"])) if st["dense_table"] == 1 else 4.0 * n
+    U = float(max(st.get("cells", 0), 0))  # occupied cells
+    nd = float(max(st.get("dense_cells", 0), 0))
+    md = float(max(st.get("dense_points", 0), 0))
+    P = float(max(st.get("radix_passes", 0), 0))
+    ns = n - md                             # points of sparse cells
+    key = P > 0
+    model = {
+        "a1_bbox_validate": 12.0 * n,
+        # key path: read xyz, write key + index (+ histograms), then per pass read + write 8 B
+        "a2_bin_keys": (12.0 * n + 8.0 * n + 16.0 * n * P) if key else 0.0,
+        # bitmap (C/8 B, ~9 touches), cell lists (28 B/cell), xyz reads, counts + fine masks,
+        # scan, dense records + components (~180 B/dense cell); key path: keys instead of xyz
+        "a3_sort": (8.0 * n + 1.125 * C + 44.0 * U + 24.0 * U + 180.0 * nd + 12.0 * n + 16.0 * n) if key else
+                   (24.0 * n + 1.125 * C + 44.0 * U + 24.0 * U + 180.0 * nd),
+        # count path: xyz -> float4 scatter, float4 -> parent, idx (+ root accumulators)
+        "a4_gather_init": (8.0 * md) if key else (12.0 * n + 16.0 * n + 16.0 * n + 8.0 * n + 8.0 * ns),
+        "a5_tables": 0.0,
+        # SURVEY §8(d) B_model for the neighbour scan + union-find (a6+a7): 28 B per point
+        # (float4 read 16 + parent init / hook 12), over the two union stages together
+        "a6a7_scan_union": 28.0 * n,
+        "a8_flatten": 8.0 * n if 4 * U > n else 0.0,          # separate flatten (sparse-dominated only)
+        # node tail (few sparse cells): sparse points + 8 node slots per dense cell
+        "a9_stats": (12.0 * ns + 64.0 * nd) if 4 * U <= n else 12.0 * n,
+        "a10_relabel": 12.0 * n,                              # parent + index -> label
+    }
     return model[stage]
 
 
@@ -245,12 +238,13 @@ def run_reference(args, rank, world):
     pts, desc = make_workload(args.config, args.scale, limit)
     n = pts.shape[0]
     times = []
-    for k in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle.fec(pts, d, mn, mx)
-        dt = time.perf_counter() - t0
-        if k >= args.warmup:
-            times.append(dt)
+    with pinned_core():
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oracle.fec(pts, d, mn, mx)
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                times.append(dt)
     mean = float(np.mean(times))
     value = n / mean / 1e6
     line = {
@@ -259,21 +253,54 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.config], "n_points_per_step": n, "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": 1, "kind": "oracle",
+                         "sample": desc + "; pinned to core 0", **host_cpu()},
         "e2e": {"value": value, "unit": "Mpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def host_cpu() -> dict:
+    """The GPU box's host CPU (SURVEY §8(d) "Oracle timing": model, nproc, the pinned core)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+class pinned_core:
+    """Runs the enclosed code on core 0 only (taskset -c 0 equivalent), then restores."""
+
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {0})
+        except (AttributeError, OSError):
+            self.prev = None
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
 
 
 def cpu_baseline(name: str, scale: float):
     import oracle
     d, mn, mx = synth.CONFIGS[name]
     pts, desc = make_workload(name, scale, CPU_SAMPLE[name])
-    t0 = time.perf_counter()
-    oracle.fec(pts, d, mn, mx)
-    dt = time.perf_counter() - t0
+    with pinned_core():
+        t0 = time.perf_counter()
+        oracle.fec(pts, d, mn, mx)
+        dt = time.perf_counter() - t0
     return {"value": pts.shape[0] / dt / 1e6, "unit": "Mpoints/s", "cores": 1, "kind": "oracle",
-            "sample": f"{desc}; {dt:.1f} s single-threaded"}
+            "sample": f"{desc}; {dt:.1f} s single-threaded, pinned to core 0", **host_cpu()}
 
 
 def run_slab(args, rank: int, world: int, local: int):
@@ -470,7 +497,7 @@ def run_batch(args, local: int):
     e0.record(stream)
     for _ in range(max(1, args.steps // 3)):
         for k in range(len(scans)):
-            fec.cluster(xs[k], d_th, mn, mx, out=out[offs[k]:offs[k + 1]], workspace=wss)
+            fec.cluster(xs[k], d_th, mn, mx, out=out[offs[k]:offs[k + 1]], workspace=wss, check=False)
     e1.record(stream)
     torch.cuda.synchronize()
     ms_seq = e0.elapsed_time(e1) / max(1, args.steps // 3)
@@ -723,7 +750,8 @@ def main():
 
     # one instrumented, untimed call: sizes for the byte model + launch count
     fec.set_instrumentation(True)
-    fec.cluster(x, d_th, mn, mx, out=out, workspace=ws)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    fec.cluster(x, d_th, mn, mx, out=out, workspace=ws, status=status)
     torch.cuda.synchronize()
     st = fec.stats()
     fec.set_instrumentation(False)
@@ -736,8 +764,27 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
+    def call():
+        fec.cluster(x, d_th, mn, mx, out=out, workspace=ws, status=status, check=False)
+
+    use_graph = args.graph == "on" or (args.graph == "auto" and n <= (1 << 20))
+    step = call
+    if use_graph:
+        # the whole call has no host round trip (the grid is planned on the device), so one
+        # captured graph replays the complete step: launch-bound small clouds are timed
+        # without the host's per-launch cost
+        graph = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            call()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cs):
+            call()
+        torch.cuda.synchronize()
+        step = graph.replay
     for _ in range(args.warmup):
-        fec.cluster(x, d_th, mn, mx, out=out, workspace=ws)
+        step()
     torch.cuda.synchronize()
     barrier()
 
@@ -748,16 +795,17 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
-            fec.cluster(x, d_th, mn, mx, out=out, workspace=ws)
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    fec.raise_status(status)  # the device status of the timed calls (read after the timed region)
     # per-stage times (library events at the stage boundaries) in a second pass of the same
     # steps: the events split the stream, so they are kept out of the timed loop
     fec.set_timing(True)
     for _ in range(args.steps):
-        fec.cluster(x, d_th, mn, mx, out=out, workspace=ws)
+        fec.cluster(x, d_th, mn, mx, out=out, workspace=ws, status=status, check=False)
         for k, v in fec.stage_times().items():
             stage_sum[k] = stage_sum.get(k, 0.0) + v
     fec.set_timing(False)
@@ -836,6 +884,8 @@ def main():
             "config": {"workload": WORKLOAD_TEXT[args.config] + ("" if args.scale == 1.0 else f" (scale {args.scale})"),
                        "n_points": n, "d_th": d_th, "min_size": mn, "max_size": mx,
                        "parallelism": "single",
+                       "timing": ("one captured CUDA graph of the call replayed per step" if use_graph else
+                                  "one fec_cluster_ws_async call per step, enqueued from Python"),
                        "l2": f"no flush: inputs ({12 * n / 1e6:.0f} MB) and working set "
                              f"({fec.workspace_bytes(n) / 1e9:.1f} GB) exceed the 126 MB L2"
                              if 12 * n > 126e6 else "small input: L2-resident (latency-bound)",

@@ -78,17 +78,42 @@ typedef struct {
  * not depend on the coordinates).  Returns 0 for n <= 0. */
 size_t fec_workspace_bytes(int64_t n);
 
-/* Enqueue the whole path on `stream` (cudaStream_t; NULL = legacy default stream) using
- * caller-provided workspace.  Host-synchronises once, after the bbox/validation kernel,
- * to size the grid; returns after the remaining kernels are enqueued (they complete
- * in stream order; labels_out is valid once the stream reaches that point).
- * n == 0 returns FEC_OK without launching anything. */
+/* ---- Asynchronous forms: no host round trip ------------------------------
+ *
+ * The whole path is enqueued on `stream` (cudaStream_t; NULL = legacy default stream) and the
+ * call returns at once: the grid (origin, dims, bitmap vs hashed cell index, counting vs key
+ * sort) is planned ON THE DEVICE by the validation kernel (a1) and read there by every later
+ * kernel, so nothing waits for the host and the call can be captured in a CUDA graph
+ * (stream capture; replays recompute everything from the current contents of `points`).
+ *
+ * status_dev (optional, may be NULL): a device (or mapped host) int32 that receives, in stream
+ * order, FEC_OK or what the device found: FEC_ERR_NONFINITE (a coordinate is NaN/inf, reading
+ * A12) or FEC_ERR_GRID_RANGE (reading A14).  After such an error every later kernel returns at
+ * once and labels_out is left untouched.  The return value covers only what the host can see
+ * before enqueueing: argument errors (FEC_ERR_INVALID_ARGUMENT, nothing enqueued), allocation
+ * failure (FEC_ERR_OUT_OF_MEMORY) and launch errors (FEC_ERR_CUDA).  n == 0 returns FEC_OK,
+ * enqueues nothing and does not write *status_dev.
+ *
+ * fec_cluster_async: the signature of SURVEY §8(b); the workspace (fec_workspace_bytes(n)) is
+ * taken stream-ordered from the device's default memory pool (cudaMallocAsync / cudaFreeAsync
+ * on `stream`; under capture these become graph allocation nodes).
+ * fec_cluster_ws_async: the same with a caller-provided workspace of at least
+ * fec_workspace_bytes(n) bytes (kept alive until the stream has passed the call). */
+fec_status_t fec_cluster_async(const float* points, int64_t n, float d_th, int64_t min_size,
+                               int64_t max_size, int32_t* labels_out, void* stream, int32_t* status_dev);
+fec_status_t fec_cluster_ws_async(const float* points, int64_t n, float d_th, int64_t min_size,
+                                  int64_t max_size, int32_t* labels_out, void* workspace,
+                                  size_t workspace_bytes, void* stream, int32_t* status_dev);
+
+/* Synchronous form with a caller-provided workspace: fec_cluster_ws_async, then waits for
+ * `stream` and returns the device status (FEC_ERR_NONFINITE / FEC_ERR_GRID_RANGE included). */
 fec_status_t fec_cluster_ws(const float* points, int64_t n, float d_th, int64_t min_size,
                             int64_t max_size, int32_t* labels_out, void* workspace,
                             size_t workspace_bytes, void* stream);
 
-/* Synchronous convenience form: allocates the workspace itself (stream-ordered
- * cudaMallocAsync on the legacy default stream), runs, synchronises, frees. */
+/* Synchronous convenience form (the north-star signature): fec_cluster_async on the legacy
+ * default stream with its own workspace, then waits and returns the device status.  Returns
+ * FEC_ERR_OUT_OF_MEMORY if the workspace cannot be allocated. */
 fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min_size,
                          int64_t max_size, int32_t* labels_out);
 
@@ -102,16 +127,17 @@ fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th,
                               void* workspace, size_t workspace_bytes, void* stream);
 
 /* Pipelined form of fec_cluster_host for a stream of clouds: the same host->device copy,
- * clustering and device->host copy are enqueued on `stream`, but the call returns once the
- * clustering is enqueued (it still waits for the bbox pass, like every call) instead of after
- * the labels have arrived: labels_host is valid after `stream` completes.  With PINNED host
+ * clustering and device->host copy are enqueued on `stream` and the call returns at once
+ * (no host round trip): labels_host is valid after `stream` completes, and status_dev
+ * (optional device / mapped int32, as fec_cluster_async) receives the device status.  With PINNED host
  * buffers and two streams (each with its own workspace and host buffers), consecutive calls
  * overlap one cloud's device->host copy and tail kernels with the next cloud's host->device
  * copy (PCIe is full duplex).  The host buffers must stay alive until the stream completes.
  * Errors: as fec_cluster_host. */
 fec_status_t fec_cluster_host_async(const float* points_host, int64_t n, float d_th,
                                     int64_t min_size, int64_t max_size, int32_t* labels_host,
-                                    void* workspace, size_t workspace_bytes, void* stream);
+                                    void* workspace, size_t workspace_bytes, void* stream,
+                                    int32_t* status_dev);
 
 /* Fills *out with the statistics of this thread's last call whose status was FEC_OK.
  * Counters that need a device read-back (components, pair_tests, group_pairs) are
@@ -132,8 +158,13 @@ void fec_set_grid_mode(int mode);
  * place by one thread each; labels are identical either way. */
 void fec_set_item_cap(int64_t cap);
 
+/* Test hook (thread-local): the self-allocating calls (fec_cluster, fec_cluster_async) ask the
+ * allocator for `bytes` more than they need; a huge value makes the allocation really fail,
+ * exercising the FEC_ERR_OUT_OF_MEMORY path.  0 (default) = off. */
+void fec_debug_alloc_extra(size_t bytes);
+
 /* Per-stage device timing.  With fec_set_timing(1), each call records CUDA events on its
- * stream at the stage boundaries (a1 validate+bbox incl. the host sync, a2 keys, a3 sort,
+ * stream at the stage boundaries (a1 validate+bbox+plan, a2 keys, a3 sort,
  * a4 gather, a5 tables, a6+a7 scan+union, a8 flatten, a9 stats, a10 relabel).
  * fec_get_stage_times() waits for the last event of this thread's last call and writes up
  * to max_stages durations in milliseconds; it returns the number of stages (or <0). */
@@ -199,14 +230,15 @@ int64_t fec_slab_record_words(int64_t rec_cap);
  * both calls; it carries the local forest from the first call to the second). */
 size_t fec_slab_workspace_bytes(int64_t n_local, int32_t world, int64_t rec_cap);
 
-/* Step 1 (device pointers; enqueued on `stream`, one host sync after the bbox kernel like
- * fec_cluster_ws).  Writes the rank's record buffer `records` (fec_slab_record_words(rec_cap)
- * words) and fills *state.  Errors: as fec_cluster_ws, plus FEC_ERR_INVALID_ARGUMENT for
+/* Step 1 (device pointers; enqueued on `stream` with no host synchronisation, like
+ * fec_cluster_ws_async; status_dev (optional) receives the device status; after an error the
+ * records stay empty and fec_slab_merge leaves labels_owned untouched).  Writes the rank's
+ * record buffer `records` (fec_slab_record_words(rec_cap) words) and fills *state.  Errors: as fec_cluster_ws, plus FEC_ERR_INVALID_ARGUMENT for
  * n_first/n_owned/n_local out of order or rec_cap too small.  n_local == 0 is valid (the
  * header is zeroed, nothing else is launched). */
 fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_local, int64_t n_owned,
                             int64_t n_first, float d_th, int32_t* records, int64_t rec_cap, void* workspace,
-                            size_t workspace_bytes, fec_slab_state_t* state, void* stream);
+                            size_t workspace_bytes, fec_slab_state_t* state, void* stream, int32_t* status_dev);
 
 /* Step 3.  all_records: world * fec_slab_record_words(rec_cap) int32 (device), the gathered
  * buffers in rank order.  labels_owned: int32[n_owned] (device), in local order.  The

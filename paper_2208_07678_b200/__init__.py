@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 __all__ = ["average_precision", "ap_workspace_bytes", "remove_ground", "expand_labels", "cluster_nonground", "ground_result", "ground_workspace_bytes",
-           "cluster", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
+           "cluster", "cluster_async", "raise_status", "cluster_host", "cluster_batch", "batch_workspace_bytes", "slab_local", "slab_merge", "slab_record_words",
            "slab_workspace_bytes", "SlabState", "workspace_bytes", "workspace_bytes_host", "stats",
            "set_instrumentation", "set_timing", "stage_times", "FecError", "lib", "LIB_PATH", "debug_pred", "EXPORTS"]
 
@@ -26,7 +26,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfec.so")
 OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_CUDA = 0, -1, -2, -3, -4, -5
 
 # every symbol include/fec.h, include/fec_ground.h and include/fec_metrics.h declare
-EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_workspace_bytes_host",
+EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_cluster_async", "fec_cluster_ws_async",
+           "fec_debug_alloc_extra", "fec_workspace_bytes_host",
            "fec_cluster_host", "fec_cluster_host_async", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
@@ -93,10 +94,16 @@ def lib():
         L.fec_cluster_ws.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
         L.fec_cluster.restype = ctypes.c_int32
         L.fec_cluster.argtypes = [vp, i64, f32, i64, i64, vp]
+        L.fec_cluster_async.restype = ctypes.c_int32
+        L.fec_cluster_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, vp]
+        L.fec_cluster_ws_async.restype = ctypes.c_int32
+        L.fec_cluster_ws_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp, vp]
+        L.fec_debug_alloc_extra.restype = None
+        L.fec_debug_alloc_extra.argtypes = [sz]
         L.fec_cluster_host.restype = ctypes.c_int32
         L.fec_cluster_host.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
         L.fec_cluster_host_async.restype = ctypes.c_int32
-        L.fec_cluster_host_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp]
+        L.fec_cluster_host_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp, vp]
         L.fec_get_stats.restype = ctypes.c_int32
         L.fec_get_stats.argtypes = [ctypes.POINTER(FecStats)]
         L.fec_set_instrumentation.restype = None
@@ -133,7 +140,7 @@ def lib():
         L.fec_slab_workspace_bytes.restype = sz
         L.fec_slab_workspace_bytes.argtypes = [i64, ctypes.c_int32, i64]
         L.fec_slab_local.restype = ctypes.c_int32
-        L.fec_slab_local.argtypes = [vp, vp, i64, i64, i64, f32, vp, i64, vp, sz, ctypes.POINTER(SlabState), vp]
+        L.fec_slab_local.argtypes = [vp, vp, i64, i64, i64, f32, vp, i64, vp, sz, ctypes.POINTER(SlabState), vp, vp]
         L.fec_slab_merge.restype = ctypes.c_int32
         L.fec_slab_merge.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, i64, i64, vp, vp, sz,
                                      ctypes.POINTER(SlabState), vp]
@@ -186,20 +193,58 @@ def _f32(d_th: float) -> float:
     return float(np.float32(d_th))
 
 
+def _stream_for(dev, stream):
+    """(stream, foreign): the stream to enqueue on and whether it differs from the current one."""
+    torch = _torch()
+    cur = torch.cuda.current_stream(dev)
+    st = stream if stream is not None else cur
+    return st, st.cuda_stream != cur.cuda_stream
+
+
+def _enter(st, foreign):
+    """Before enqueueing on a foreign stream: order it after the current stream's pending work
+    (the input tensors, and the allocations made below, were produced there)."""
+    if foreign:
+        st.wait_stream(_torch().cuda.current_stream(st.device))
+
+
+def _keep(st, foreign, *tensors):
+    """After enqueueing on a foreign stream: tensors allocated on the current stream must not be
+    recycled by the caching allocator while `st` still uses them."""
+    if foreign:
+        for t in tensors:
+            if t is not None and hasattr(t, "record_stream") and t.is_cuda:
+                t.record_stream(st)
+
+
+def raise_status(status) -> None:
+    """Raise FecError if a device status word (int32 CUDA tensor, filled by an async call) holds
+    an error.  One device->host read (synchronises with the stream that wrote it)."""
+    code = int(status.item())
+    if code != OK:
+        raise FecError(code, {ERR_NONFINITE: "non-finite coordinate (reading A12)",
+                              ERR_GRID_RANGE: "bbox extent / cell >= 2^20 on an axis (reading A14)"}.get(
+                                  code, "device-side error"))
+
+
 def cluster(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
-            workspace=None, stream=None):
+            workspace=None, stream=None, status=None, check: bool = True):
     """Labels of `points` (CUDA float32 tensor [n, 3], contiguous) on the current device.
 
     Returns an int32 CUDA tensor [n]: min input index of the point's component, or -1
     when the component size is outside [min_size, max_size].  Enqueued on PyTorch's
-    current stream (or `stream`); the result is ready in stream order."""
+    current stream (or `stream`) through fec_cluster_ws_async: no host round trip, so the
+    call can be captured in a CUDA graph.  `status` (int32 CUDA tensor [1], optional)
+    receives the device status; with check=True (default) it is read back after the call
+    (one synchronisation) and an error raises FecError."""
     torch = _torch()
     if not (isinstance(points, torch.Tensor) and points.is_cuda):
         raise TypeError("points must be a CUDA tensor (use cluster_host for host arrays)")
     if points.dtype != torch.float32 or points.dim() != 2 or points.shape[1] != 3:
         raise TypeError("points must be float32 [n, 3]")
-    points = points.contiguous()
-    n = points.shape[0]
+    st, foreign = _stream_for(points.device, stream)
+    points_c = points.contiguous()
+    n = points_c.shape[0]
     if out is None:
         out = torch.empty(n, dtype=torch.int32, device=points.device)
     if n == 0:
@@ -208,19 +253,41 @@ def cluster(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=N
     nb = workspace_bytes(n)
     if workspace is None or workspace.numel() < nb:
         workspace = torch.empty(nb, dtype=torch.uint8, device=points.device)
-    st = stream if stream is not None else torch.cuda.current_stream(points.device)
-    _check(lib().fec_cluster_ws(points.data_ptr(), n, _f32(d_th), int(min_size), int(max_size),
-                                out.data_ptr(), workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=points.device)
+    _enter(st, foreign)
+    _check(lib().fec_cluster_ws_async(points_c.data_ptr(), n, _f32(d_th), int(min_size), int(max_size),
+                                      out.data_ptr(), workspace.data_ptr(), workspace.numel(), st.cuda_stream,
+                                      status.data_ptr()))
+    _keep(st, foreign, points_c, out, workspace, status)
+    if check:
+        st.synchronize()
+        raise_status(status)
+    return out
+
+
+def cluster_async(points, d_th: float, min_size: int, max_size: int, out, status, stream=None):
+    """fec_cluster_async (SURVEY §8(b)'s signature): the library takes its workspace from the
+    device's stream-ordered memory pool; nothing is synchronised; `status` (int32 CUDA [1])
+    receives the device status.  Graph-capturable."""
+    torch = _torch()
+    st, foreign = _stream_for(points.device, stream)
+    n = points.shape[0]
+    _enter(st, foreign)
+    _check(lib().fec_cluster_async(points.data_ptr() if n else None, n, _f32(d_th), int(min_size), int(max_size),
+                                   out.data_ptr() if n else None, st.cuda_stream, status.data_ptr()))
+    _keep(st, foreign, points, out, status)
     return out
 
 
 def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, out=None,
-                 workspace=None, stream=None, device=None, sync: bool = True):
+                 workspace=None, stream=None, device=None, sync: bool = True, status=None):
     """End-to-end form: host float32 [n, 3] in (numpy or CPU tensor; pinned memory gives
     asynchronous copies), host int32 [n] labels out.  The host<->device copies run inside
     the C ABI call (fec_cluster_host).  sync=False (fec_cluster_host_async) returns once the
     work is enqueued on `stream`: `out` is valid after the stream completes, and the caller
-    keeps `points`, `out` and `workspace` alive until then (pipelining over two streams)."""
+    keeps `points`, `out` and `workspace` alive until then (pipelining over two streams);
+    `status` (int32 CUDA [1], optional) then receives the device status."""
     torch = _torch()
     if isinstance(points, torch.Tensor):
         if points.is_cuda:
@@ -241,11 +308,17 @@ def cluster_host(points, d_th: float, min_size: int = 1, max_size: int = 2**62, 
     nb = workspace_bytes_host(n)
     if n and (workspace is None or workspace.numel() < nb):
         workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    fn = lib().fec_cluster_host if sync else lib().fec_cluster_host_async
-    _check(fn(ptr if n else None, n, _f32(d_th), int(min_size), int(max_size),
-              out_ptr if n else None, workspace.data_ptr() if n else None,
-              workspace.numel() if n else 0, st.cuda_stream))
+    st, foreign = _stream_for(dev, stream)
+    _enter(st, foreign)
+    args = (ptr if n else None, n, _f32(d_th), int(min_size), int(max_size), out_ptr if n else None,
+            workspace.data_ptr() if n else None, workspace.numel() if n else 0, st.cuda_stream)
+    if sync:
+        _check(lib().fec_cluster_host(*args))
+    else:
+        if status is None and n:
+            status = torch.empty(1, dtype=torch.int32, device=dev)
+        _check(lib().fec_cluster_host_async(*args, status.data_ptr() if n else None))
+        _keep(st, foreign, workspace, status)
     del keep
     return out
 
@@ -274,9 +347,11 @@ def cluster_batch(points, offsets, d_th: float, min_size: int = 1, max_size: int
     nb = max(batch_workspace_bytes(n, nc), 1)
     if workspace is None or workspace.numel() < nb:
         workspace = torch.empty(nb, dtype=torch.uint8, device=points.device)
-    st = stream if stream is not None else torch.cuda.current_stream(points.device)
+    st, foreign = _stream_for(points.device, stream)
+    _enter(st, foreign)
     _check(lib().fec_cluster_batch_ws(_ptr(points), off.ctypes.data, nc, _f32(d_th), int(min_size), int(max_size),
                                       _ptr(out), workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    _keep(st, foreign, points, out, workspace)
     return out
 
 
@@ -328,11 +403,13 @@ def remove_ground(points, triplets, threshold: float = 0.2, max_tilt_deg: float 
         raise FecError(ERR_INVALID_ARGUMENT, "bad sizes for fec_ground_remove")
     if workspace is None or workspace.numel() < nb:
         workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st, foreign = _stream_for(dev, stream)
+    _enter(st, foreign)
     _check(lib().fec_ground_remove(_ptr(points) if n else None, n, _ptr(triplets) if H else None, H,
                                    float(np.float32(threshold)), float(cos_max_tilt), int(min_inliers),
                                    _ptr(kp), _ptr(ki), _ptr(cnt) if cnt is not None else None, _ptr(res),
                                    workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    _keep(st, foreign, points, triplets, kp, ki, res, cnt, workspace)
     return kp, ki, res, cnt
 
 
@@ -350,9 +427,11 @@ def expand_labels(keep_idx, keep_labels, result_buf, n: int, out=None, stream=No
     dev = keep_idx.device
     if out is None:
         out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st, foreign = _stream_for(dev, stream)
+    _enter(st, foreign)
     _check(lib().fec_ground_expand_labels(_ptr(keep_idx), _ptr(keep_labels), _ptr(result_buf), int(n), _ptr(out),
                                           st.cuda_stream))
+    _keep(st, foreign, keep_idx, keep_labels, result_buf, out)
     return out[:n]
 
 
@@ -396,11 +475,15 @@ def average_precision(pred, gt, threshold: float = 0.75, workspace=None, stream=
         workspace = torch.empty(nb, dtype=torch.uint8, device=dev)
     if result is None:
         result = torch.empty(AP_RESULT_BYTES, dtype=torch.uint8, device=dev)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    st, foreign = _stream_for(dev, stream)
+    _enter(st, foreign)
     _check(lib().fec_average_precision(_ptr(pred), _ptr(gt), n, float(threshold), result.data_ptr(),
                                        workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    _keep(st, foreign, pred, gt, workspace, result)
     if not read:
         return result
+    if foreign:  # the read below runs on the current stream: order it after the kernels on `st`
+        torch.cuda.current_stream(dev).wait_stream(st)
     r = ApResult.from_buffer_copy(bytes(result.cpu().numpy().tobytes()))
     return {"tp": r.tp, "fp": r.fp, "n_pred": r.n_pred, "n_gt": r.n_gt, "ap": r.ap, "status": r.status}
 
@@ -418,8 +501,15 @@ def stats() -> dict:
 
 
 def set_grid_mode(mode: int):
-    """0 = automatic, 1 = always the hashed (Morton radix-sort) mode.  Testing aid."""
+    """Testing aid: 0 = automatic, 1 = hashed cell index (open-addressing table of occupied
+    cells) always, 2 = key sort (bitmap index), 3 = counting sort (bitmap index)."""
     lib().fec_set_grid_mode(int(mode))
+
+
+def debug_alloc_extra(nbytes: int):
+    """Testing aid: self-allocating calls ask for `nbytes` more (a huge value forces
+    FEC_ERR_OUT_OF_MEMORY); 0 turns it off."""
+    lib().fec_debug_alloc_extra(int(nbytes))
 
 
 def set_item_cap(cap: int):
@@ -466,7 +556,7 @@ def _ptr(t):
 
 
 def slab_local(points, gidx, n_owned: int, n_first: int, d_th: float, records, rec_cap: int, workspace,
-               stream=None) -> SlabState:
+               stream=None, status=None) -> SlabState:
     """Step 1 on this rank: cluster owned ∪ halo (CUDA float32 [n_local, 3], local order
     first-layer | other owned | halo) and pack boundary records into `records` (CUDA int32
     [slab_record_words(rec_cap)]).  Returns the state slab_merge needs."""
@@ -477,11 +567,13 @@ def slab_local(points, gidx, n_owned: int, n_first: int, d_th: float, records, r
         raise TypeError("gidx and records must be CUDA int32 tensors")
     points = points.contiguous()
     n_local = points.shape[0]
-    st = stream if stream is not None else torch.cuda.current_stream(records.device)
+    st, foreign = _stream_for(records.device, stream)
+    _enter(st, foreign)
     state = SlabState()
     _check(lib().fec_slab_local(_ptr(points), _ptr(gidx), n_local, int(n_owned), int(n_first), _f32(d_th),
                                 records.data_ptr(), int(rec_cap), workspace.data_ptr(), workspace.numel(),
-                                ctypes.byref(state), st.cuda_stream))
+                                ctypes.byref(state), st.cuda_stream, _ptr(status)))
+    _keep(st, foreign, points, gidx, records, workspace, status)
     return state
 
 
@@ -490,7 +582,8 @@ def slab_merge(all_records, world: int, rank: int, min_size: int, max_size: int,
     """Step 3 on this rank: replicated boundary union-find over the gathered records, then
     the global labels (min global index, or -1) of the rank's owned points."""
     torch = _torch()
-    st = stream if stream is not None else torch.cuda.current_stream(all_records.device)
+    st, foreign = _stream_for(all_records.device, stream)
+    _enter(st, foreign)
     _check(lib().fec_slab_merge(all_records.data_ptr(), int(world), int(rank), int(min_size), int(max_size),
                                 _ptr(labels_owned), workspace.data_ptr(), workspace.numel(), ctypes.byref(state),
                                 st.cuda_stream))

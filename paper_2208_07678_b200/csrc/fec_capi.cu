@@ -19,18 +19,59 @@ thread_local std::string g_err;
 thread_local fec_stats_t g_stats;
 thread_local bool g_stats_valid = false;
 thread_local int g_instrument = 0;
-thread_local Meta* g_pinned_meta = nullptr;
-thread_local HostBBox* g_host_bbox = nullptr;  // mapped pinned memory (k_bbox_final writes it)
-thread_local int g_bbox_seq = 0;
 thread_local int g_timing = 0;
 thread_local int g_grid_mode = 0;
-thread_local int64_t g_item_cap = 0;  // test hook: cap on the queued uncertain pairs (0 = default)
+thread_local int64_t g_item_cap = 0;     // test hook: cap on the queued uncertain pairs (0 = default)
+thread_local size_t g_alloc_extra = 0;   // test hook: extra bytes asked of the allocator (forced OOM)
+struct Snapshot {                        // instrumented calls: Meta + Grid copied back (pinned)
+    Meta meta;
+    Grid grid;
+};
+thread_local Snapshot* g_snap = nullptr;
+thread_local int32_t* g_status_host = nullptr;  // mapped pinned status word of the synchronous calls
+thread_local Meta* g_pinned_meta = nullptr;     // batch mode: the per-cloud pass's Meta
+thread_local void* g_pinned_batch = nullptr;
+thread_local size_t g_pinned_batch_bytes = 0;
+thread_local cudaEvent_t g_batch_copied = nullptr;  // batch mode: the pinned buffer's last H2D copy
+
+// A high-priority side stream per device (thread-local) for latency-bound kernels that can run
+// concurrently with bandwidth-bound ones of the same call (fork/join through events: also
+// captured into a graph when the caller's stream is being captured).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+thread_local SideStream g_side[64];
+thread_local int g_side_off = -1;  // FEC_SIDE_STREAM=0 turns the fork off (A/B measurements)
+fec_status_t side_stream(SideStream** out) {
+    if (g_side_off < 0) {
+        const char* e = std::getenv("FEC_SIDE_STREAM");
+        g_side_off = (e && e[0] == '0') ? 1 : 0;
+    }
+    *out = nullptr;
+    if (g_side_off) return FEC_OK;
+    int d = 0;
+    cudaGetDevice(&d);
+    SideStream& ss = g_side[d & 63];
+    if (!ss.s) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+            g_err = "side stream creation failed";
+            return FEC_ERR_CUDA;
+        }
+    }
+    *out = &ss;
+    return FEC_OK;
+}
 
 constexpr int kStages = 10;
 const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",       "a3_sort",
                                           "a4_gather_init",   "a5_tables",    "a6a7_union_sparse",
                                           "a6a7_union_dense", "a8_flatten",        "a9_stats",
-                                          "a10_relabel"};  // single-GPU path: a8 = separate flatten (sparse-dominated clouds only), a9 = k_flat_stats
+                                          "a10_relabel"};  // a8 = flatten (sparse-dominated clouds), a9 = k_tail_stats
 struct StageEvents {
     cudaEvent_t ev[kStages + 1] = {};
     bool created = false;
@@ -50,6 +91,7 @@ inline void mark(int i, cudaStream_t st) {
 }
 
 constexpr int kMaxBBoxBlocks = 148 * 8;
+constexpr int64_t kSmallN = int64_t(1) << 17;  // below: the counting path only (no key-sort launches)
 
 fec_status_t fail_cuda(cudaError_t e, const char* where) {
     g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -60,12 +102,15 @@ fec_status_t fail_cuda(cudaError_t e, const char* where) {
         cudaError_t e_ = (call);                         \
         if (e_ != cudaSuccess) return fail_cuda(e_, #call); \
     } while (0)
+#define FEC_CUDA_RC(call)                                \
+    do {                                                 \
+        fec_status_t r_ = (call);                        \
+        if (r_ != FEC_OK) return r_;                     \
+    } while (0)
 
 struct DevInfo {
     int sms = 0;
-    int scan_blocks_per_sm = 0;
     int sparse_blocks_per_sm = 0;
-    int wfix_blocks_per_sm = 0;
 };
 DevInfo dev_info() {
     static DevInfo cache[64];
@@ -73,63 +118,67 @@ DevInfo dev_info() {
     cudaGetDevice(&d);
     DevInfo& di = cache[d & 63];
     if (di.sms == 0) {
-        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_scan_union, SCAN_THREADS, 0);
-        di.scan_blocks_per_sm = b > 0 ? b : 1;
+        int sms = 0, b = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_union_sparse, 256, 0);
         di.sparse_blocks_per_sm = b > 0 ? b : 1;
+        di.sms = sms > 0 ? sms : 148;
     }
     return di;
 }
 
-// dense-grid mode needs 1/4 B per grid cell (occupancy bitmap + word bases + scan)
+// bitmap mode needs 1/4 B per grid cell (occupancy bits + word bases)
 int64_t dense_cap(int64_t n) { return 32 * n + (int64_t(1) << 26); }
 int64_t dense_max(int64_t n) { return n / (SPARSE_MAX + 1) + 16; }
 int64_t nodes_max(int64_t n) { return n + 8 * dense_max(n); }
-int64_t hash_cap(int64_t n) {
+int64_t hash_slots(int64_t n) {  // hash mode: a power of two >= 2n (load factor <= 1/2)
     int64_t c = 1024;
     while (c < 2 * n) c <<= 1;
     return c;
 }
+constexpr int CS_TILE_WORDS = 2048;  // k_cscan tile (fec_dense.cu)
 
-// Workspace = common part + max(radix/hash-mode part, dense-grid-mode part).
+// One linear carve of the workspace (fec_workspace_bytes = its total).
 struct Layout {
-    // common
     Meta* meta;
+    Grid* grid;
     float* part;
     float4* spts;
-    int *parent, *size, *minidx;
-    // radix / hash mode
-    u64 *keyA, *keyB;
-    int *valA, *valB;
-    u64* flags;
-    u64* scan64;
-    uint32_t* counts;
-    uint32_t* scan32;
-    Tables T;
-    int num_tiles;
-    // dense-grid mode (per-cell tables indexed by compact id of the occupied cells)
-    uint2* cw;          // [W+1] occupancy bitmap words {bits, occupied cells before the word}
-    uint32_t* clin;     // [n]   linear cell id of each compact id
+    int *parent, *size, *minidx;   // union-find nodes: n points + 8 per dense cell
+    // arena zeroed by k_zero every call: counters, look-back states, histograms, dense bits
+    uint32_t* arena;
+    int64_t arena_words;
+    unsigned int* ctr;             // [0] k_cscan, [1] scan A, [2] scan B, [4..7] onesweep passes
+    unsigned long long* cs_state;  // k_cscan look-back
+    unsigned long long* sa_state;  // cell starts scan
+    unsigned long long* sb_state;  // dense-bits popcount scan
+    uint32_t* ghist;               // onesweep: [4][256] digit histograms
+    uint32_t* dbits;               // [n/32+2] bitmap of dense compact ids
+    int64_t cs_tiles;              // k_cscan tiles (worst case over both cell-index modes)
+    uint2* cw;                     // occupancy words {bits, occupied cells before the word}
+    u64* hkey;                     // hash mode: packed cell coordinates per slot
+    int64_t slots;
+    uint32_t* clin;     // [n]   cell handle of each compact id
     uint32_t* cstart;   // [n+1] counts, then exclusive prefix (cell start)
     int* crec;          // [n]   dense record id of a dense cell
-    uint32_t* dscan;    // scan scratch
-    uint32_t* slot;     // [n]
-    int* sidx;          // [n] input index of each sorted position
+    uint32_t* slot;     // [n]   per-cell scatter cursors
+    int* sidx;          // [n]   input index of each sorted position
     int* dlist;         // dense record -> compact cell id
-    uint32_t* dbits;    // [n/32+2] bitmap of dense compact ids
-    uint32_t* dwpos;    // [n/32+2] popcount prefix of the bitmap words
+    uint32_t* dwpos;    // [n/32+2] popcount prefix of the dense bits
     u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
+    int* cmin;          // [n]   counting path: smallest input index in each occupied cell
     u64* ccoord;        // [n]   cell coordinates of each occupied cell, 21 bits each
-    int* slist;         // [n]   compact ids of the sparse cells (clouds with few of them)
+    int* slist;         // [n]   compact ids of the sparse cells
     int* ncomp;         // per dense record: certain-connected components (<= 8)
-    u64* dcoord;        // per dense record: cell coordinates, 21 bits each
+    u64* dcoord;        // per dense record: cell coordinates
     uint32_t* oflag;    // per dense record: slots whose pairs overflowed the queue
     u64* cmask;         // per dense record: 8 component masks
+    uint4* litems;            // dense link items (k_dcomps -> k_dense_link), aliasing the sort buffers
+    int lhalf;                // capacity of each of the two item lists
     uint32_t *skey0, *skey1;  // key-sort path: linear cell keys (double buffer)
     int *sval0, *sval1;       // key-sort path: input indices (double buffer)
-    uint32_t* scounts;        // key-sort path: digit counts per tile
+    uint32_t* os_state;       // onesweep look-back: 2 x tiles x 256
+    int64_t os_tiles;
     int4* items;        // queued component pairs (not certain, possibly within reach)
     int4* items2;       // those still apart after all certain unions (split into slices)
     int4* slices2;      // (slice, slices, queued pair) of each items2 entry
@@ -142,65 +191,64 @@ Layout carve(char* base, int64_t n) {
     Layout L{};
     Carver cv{base, 0, 0};
     L.meta = cv.take<Meta>(1);
+    L.grid = cv.take<Grid>(1);
     L.part = cv.take<float>(6 * kMaxBBoxBlocks);
     L.spts = cv.take<float4>(n);
-    // union-find nodes: the n points, then (dense-grid mode) 8 component nodes per dense cell
     L.parent = cv.take<int>(nodes_max(n));
     L.size = cv.take<int>(nodes_max(n));
     L.minidx = cv.take<int>(nodes_max(n));
-    const size_t common = (cv.off + 255) & ~size_t(255);
-    // radix / hash mode
-    Carver a{base, common, 0};
-    L.keyA = a.take<u64>(n);
-    L.keyB = a.take<u64>(n);
-    L.valA = a.take<int>(n);
-    L.valB = a.take<int>(n);
-    L.flags = a.take<u64>(n + 1);
-    L.scan64 = a.take<u64>(scan_scratch_elems(n + 1));
-    L.num_tiles = (int)((n + RS_TILE - 1) / RS_TILE);
-    L.counts = a.take<uint32_t>((size_t)256 * L.num_tiles);
-    L.scan32 = a.take<uint32_t>(scan_scratch_elems((int64_t)256 * L.num_tiles));
-    L.T.gstart = a.take<int>(n + 1);
-    L.T.goct = a.take<uint8_t>(n);
-    L.T.cell_gstart = a.take<int>(n + 1);
-    L.T.cell_pc = a.take<u64>(n);
-    const int64_t hc = hash_cap(n);
-    L.T.hkey = a.take<u64>(hc);
-    L.T.hval = a.take<int>(hc);
-    L.T.dense = nullptr;
-    // dense-grid mode
-    const int64_t dc = dense_cap(n);
-    const int64_t W = dc / 32 + 1;
-    Carver b{base, common, 0};
-    L.cw = b.take<uint2>(W + 1);
-    L.clin = b.take<uint32_t>(n);
-    L.cstart = b.take<uint32_t>(n + 1);
-    L.crec = b.take<int>(n);
-    L.dscan = b.take<uint32_t>(
-        scan_scratch_elems(std::max<int64_t>(std::max<int64_t>(W + 2, n + 1), 256 * ((n + RS_TILE - 1) / RS_TILE))));
-    L.slot = b.take<uint32_t>(n);
-    L.sidx = b.take<int>(n);
-    L.dlist = b.take<int>(dense_max(n));
-    L.dbits = b.take<uint32_t>(n / 32 + 2);
-    L.dwpos = b.take<uint32_t>(n / 32 + 2);
-    L.cocc = b.take<u64>(n);
-    L.skey0 = b.take<uint32_t>(n);
-    L.skey1 = b.take<uint32_t>(n);
-    L.sval0 = b.take<int>(n);
-    L.sval1 = b.take<int>(n);
-    L.scounts = b.take<uint32_t>((size_t)256 * ((n + RS_TILE - 1) / RS_TILE));
-    L.ccoord = b.take<u64>(n);
-    L.slist = b.take<int>(n);
-    L.ncomp = b.take<int>(dense_max(n));
-    L.dcoord = b.take<u64>(dense_max(n));
-    L.oflag = b.take<uint32_t>(dense_max(n));
-    L.cmask = b.take<u64>((size_t)8 * dense_max(n));
+    L.slots = hash_slots(n);
+    const int64_t w_max = std::max<int64_t>((dense_cap(n) + 31) / 32, L.slots / 32);
+    L.cs_tiles = (w_max + 1 + CS_TILE_WORDS - 1) / CS_TILE_WORDS;
+    const int64_t dwords = n / 32 + 2;
+    // arena (u32 words, each part 256-B aligned)
+    Carver ar{base, 0, 0};
+    ar.off = (cv.off + 255) & ~size_t(255);
+    const size_t a0 = ar.off;
+    L.arena = reinterpret_cast<uint32_t*>(base + a0);
+    L.ctr = ar.take<unsigned int>(64);
+    L.cs_state = ar.take<unsigned long long>(L.cs_tiles + 32);
+    L.sa_state = ar.take<unsigned long long>(scan_lb_tiles(n + 1) + 32);
+    L.sb_state = ar.take<unsigned long long>(scan_lb_tiles(dwords + 1) + 32);
+    L.ghist = ar.take<uint32_t>(4 * 256);
+    L.dbits = ar.take<uint32_t>(dwords + 1);
+    ar.off = (ar.off + 255) & ~size_t(255);
+    L.arena_words = (int64_t)((ar.off - a0) / 4);
+    cv.off = ar.off;
+    L.cw = cv.take<uint2>(w_max + 4);
+    L.hkey = cv.take<u64>(L.slots);
+    L.clin = cv.take<uint32_t>(n);
+    L.cstart = cv.take<uint32_t>(n + 1);
+    L.crec = cv.take<int>(n);
+    L.slot = cv.take<uint32_t>(n);
+    L.sidx = cv.take<int>(n);
+    L.dlist = cv.take<int>(dense_max(n));
+    L.dwpos = cv.take<uint32_t>(dwords + 1);
+    L.cocc = cv.take<u64>(n);
+    L.cmin = cv.take<int>(n);
+    L.ccoord = cv.take<u64>(n);
+    L.slist = cv.take<int>(n);
+    L.ncomp = cv.take<int>(dense_max(n));
+    L.dcoord = cv.take<u64>(dense_max(n));
+    L.oflag = cv.take<uint32_t>(dense_max(n));
+    L.cmask = cv.take<u64>((size_t)8 * dense_max(n));
+    // key-sort buffers; after binning the same bytes hold the dense link items (2 x n/2 uint4)
+    const int64_t n64 = (n + 63) & ~int64_t(63);  // each buffer 256-B aligned (vector stores)
+    char* sortbuf = cv.take<char>((size_t)16 * n64 + 1024);
+    L.skey0 = reinterpret_cast<uint32_t*>(sortbuf);
+    L.skey1 = L.skey0 + n64;
+    L.sval0 = reinterpret_cast<int*>(L.skey1 + n64);
+    L.sval1 = L.sval0 + n64;
+    L.litems = reinterpret_cast<uint4*>(sortbuf);
+    L.lhalf = (int)std::min<int64_t>(n64 / 2, INT32_MAX / 2);
+    L.os_tiles = (n + RS_TILE - 1) / RS_TILE;
+    L.os_state = cv.take<uint32_t>((size_t)2 * L.os_tiles * 256);
     L.item_cap = (int)std::min<int64_t>(n / 8 + 65536, INT32_MAX / 2);
-    L.items = b.take<int4>(L.item_cap);
-    L.items2 = b.take<int4>(2 * (size_t)L.item_cap);
-    L.slices2 = b.take<int4>(2 * (size_t)L.item_cap);
-    L.idone = b.take<int>(L.item_cap);
-    L.total = std::max(a.off, b.off) + 256;
+    L.items = cv.take<int4>(L.item_cap);
+    L.items2 = cv.take<int4>(2 * (size_t)L.item_cap);
+    L.slices2 = cv.take<int4>(2 * (size_t)L.item_cap);
+    L.idone = cv.take<int>(L.item_cap);
+    L.total = cv.off + 256;
     return L;
 }
 
@@ -219,8 +267,14 @@ int ceil_log2(int64_t v) {
     return b;
 }
 
+// Largest n whose union-find node ids (n points + 8 per possible dense cell) fit in int32.
+constexpr int64_t kMaxN = (int64_t)INT32_MAX / 8 * 7 - 1024;
+
 fec_status_t check_args(int64_t n, float d, int64_t mn, int64_t mx, float* t2_out) {
-    if (n < 0 || n > INT32_MAX) { g_err = "n out of range [0, INT32_MAX]"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (n < 0 || n > kMaxN || (n > 0 && nodes_max(n) >= (int64_t)INT32_MAX)) {
+        g_err = "n out of range [0, " + std::to_string(kMaxN) + "] (int32 union-find node ids)";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
     if (!(d > 0.0f) || !std::isfinite(d)) { g_err = "d_th must be finite and > 0"; return FEC_ERR_INVALID_ARGUMENT; }
     volatile float dv = d;
     const float t2 = dv * dv;  // one fp32 rounding (reading A3)
@@ -240,15 +294,40 @@ inline unsigned grid_for(int64_t work, int per_block, int cap) {
     return (unsigned)b;
 }
 
-// State of a call after a1..a8 (flattened forest over sorted positions), shared by the
-// single-GPU tail (a9, a10) and the slab tail (owned-only stats + boundary records).
+const char* device_status_text(int32_t s) {
+    switch (s) {
+        case FEC_ERR_NONFINITE: return "non-finite coordinate (reading A12)";
+        case FEC_ERR_GRID_RANGE: return "bbox extent / cell >= 2^20 on an axis (reading A14)";
+        default: return "device-side error";
+    }
+}
+
+fec_status_t ensure_status_word() {
+    if (!g_status_host) {
+        FEC_CUDA(cudaHostAlloc(&g_status_host, sizeof(int32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+        *g_status_host = 0;
+    }
+    return FEC_OK;
+}
+
+// Synchronous forms: wait for the stream, then report what the device found.
+fec_status_t wait_status(cudaStream_t st, const int32_t* status_host) {
+    FEC_CUDA(cudaStreamSynchronize(st));
+    const int32_t s = *reinterpret_cast<const volatile int32_t*>(status_host);
+    if (s != FEC_OK) {
+        g_err = device_status_text(s);
+        return s;
+    }
+    return FEC_OK;
+}
+
+// State of a call after a1..a8 (forest over sorted positions), shared by the single-GPU tail
+// (a9, a10) and the slab tail (owned-only stats + boundary records).
 struct Core {
     Layout L;
-    Grid g;
     int node_stats = 0;        // single-GPU tail: dense points' totals accumulated per component node
     const int* val = nullptr;  // local input index of each sorted position
     int launches = 0;
-    int passes = 0;
 };
 
 // Batch mode (fec_cluster_batch_ws): clouds [off[c], off[c+1]) clustered independently in one
@@ -261,162 +340,66 @@ struct BatchArgs {
     double* blo_dev = nullptr;
     int32_t* bz_dev = nullptr;
 };
-constexpr fec_status_t kNeedPerCloud = 1;  // internal: the combined grid does not fit, run clouds one by one
+constexpr fec_status_t kNeedPerCloud = 1;  // internal: the stacked grid cannot be indexed, run clouds one by one
 
-thread_local void* g_pinned_batch = nullptr;
-thread_local size_t g_pinned_batch_bytes = 0;
-
-// a1..a8 on n > 0 points (arguments already checked, pointers validated).
-// word bases + compact cell list in one single-pass look-back kernel (k_cscan); the look-back
-// state lives in the scan scratch (counter in the first 256 B)
-int cell_scan(const Layout& L, int64_t W, const Grid& g, cudaStream_t st) {
-    const int64_t nb = (W + 1 + 2047) / 2048;
-    unsigned int* counter = reinterpret_cast<unsigned int*>(L.dscan);
-    unsigned long long* state = reinterpret_cast<unsigned long long*>(L.dscan + 64);
-    cudaMemsetAsync(L.dscan, 0, 256 + (size_t)nb * 8, st);
-    pdl(k_cscan, (unsigned)nb, 256, 0, st)(L.cw, W, L.clin, L.cstart, L.cocc, L.ccoord, g, L.meta, state, counter);
-    return 1;
-}
-
-fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C,
-                      const BatchArgs* B = nullptr) {
-    Layout& L = C.L;
-    L = carve(static_cast<char*>(ws), n);
-    int launches = 0;
-    if (!g_pinned_meta) FEC_CUDA(cudaMallocHost(&g_pinned_meta, sizeof(Meta)));
-    const DevInfo di = dev_info();
-    const int cap = di.sms * 8;
-
-    // ---- a1: validate + bbox, then the only host synchronisation ----------------------
-    mark(0, st);
-    FEC_CUDA(cudaMemsetAsync(L.meta, 0, sizeof(Meta), st));
-    const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
-    const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
-    const float near = (float)(2.0 * (double)d * (1.0 + std::ldexp(1.0, -16)));
-    float* bbh = nullptr;  // batch: per-cloud bboxes on the host
-    if (!B) {
-        pdl(k_bbox_partial, bb_blocks, 256, 0, st)(pts, n, vec4, L.part, &L.meta->nonfinite, near,
-                                                  &L.meta->near_pairs);
-        if (!g_host_bbox) FEC_CUDA(cudaHostAlloc(&g_host_bbox, sizeof(HostBBox), cudaHostAllocMapped | cudaHostAllocPortable));
-        const int seq = ++g_bbox_seq;
-        pdl(k_bbox_final, 1, 256, 0, st)(L.part, (int)bb_blocks, L.meta, g_host_bbox, seq);
-        launches += 2;
-        FEC_CUDA(cudaGetLastError());
-        // wait for the record (no stream synchronisation, no copy); if the stream drains
-        // without it, a launch failed: the synchronisation reports the error
-        volatile int* vs = &g_host_bbox->seq;
-        for (int spins = 0; *vs != seq; ++spins) {
-            if ((spins & 1023) == 1023 && cudaStreamQuery(st) != cudaErrorNotReady && *vs != seq) {
-                FEC_CUDA(cudaStreamSynchronize(st));
-                if (*vs != seq) { g_err = "bbox record missing"; return FEC_ERR_CUDA; }
-            }
-        }
-        std::atomic_thread_fence(std::memory_order_acquire);
-        for (int k = 0; k < 6; ++k) g_pinned_meta->bbox[k] = g_host_bbox->bbox[k];
-        g_pinned_meta->nonfinite = g_host_bbox->nonfinite;
-        g_pinned_meta->near_pairs = g_host_bbox->near_pairs;
-    } else {
-        const size_t need = (size_t)B->nclouds * (6 * sizeof(float) + 3 * sizeof(double) + sizeof(int32_t)) + 64;
-        if (g_pinned_batch_bytes < need) {
-            if (g_pinned_batch) cudaFreeHost(g_pinned_batch);
-            g_pinned_batch = nullptr;
-            g_pinned_batch_bytes = 0;
-            FEC_CUDA(cudaMallocHost(&g_pinned_batch, need));
-            g_pinned_batch_bytes = need;
-        }
-        bbh = static_cast<float*>(g_pinned_batch);
-        FEC_CUDA(cudaMemcpyAsync(B->off_dev, B->off_host, (size_t)(B->nclouds + 1) * sizeof(int64_t),
-                                 cudaMemcpyHostToDevice, st));
-        pdl(k_bbox_clouds, B->nclouds, 256, 0, st)(pts, B->off_dev, B->bb_dev, &L.meta->nonfinite, near,
-                                                  &L.meta->near_pairs);
-        ++launches;
-        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
-        FEC_CUDA(cudaMemcpyAsync(bbh, B->bb_dev, (size_t)B->nclouds * 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
+// Batch mode: per-cloud bboxes on the device, then the grid planned on the HOST (the clouds'
+// origins and z offsets) and uploaded; one host synchronisation.
+fec_status_t plan_batch(const float* pts, int64_t n, const Grid& g0, const Layout& L, const BatchArgs* B,
+                        float near, int vec4, cudaStream_t st, bool& key_sort) {
+    const size_t need = (size_t)B->nclouds * (6 * sizeof(float) + 3 * sizeof(double) + sizeof(int32_t)) + 64;
+    if (!g_batch_copied) FEC_CUDA(cudaEventCreateWithFlags(&g_batch_copied, cudaEventDisableTiming));
+    if (g_pinned_batch) FEC_CUDA(cudaEventSynchronize(g_batch_copied));  // the previous call's H2D copies are done
+    if (g_pinned_batch_bytes < need) {
+        if (g_pinned_batch) cudaFreeHost(g_pinned_batch);
+        g_pinned_batch = nullptr;
+        g_pinned_batch_bytes = 0;
+        FEC_CUDA(cudaMallocHost(&g_pinned_batch, need));
+        g_pinned_batch_bytes = need;
     }
-    if (B) FEC_CUDA(cudaStreamSynchronize(st));
+    if (!g_pinned_meta) FEC_CUDA(cudaMallocHost(&g_pinned_meta, sizeof(Meta)));
+    float* bbh = static_cast<float*>(g_pinned_batch);
+    FEC_CUDA(cudaMemcpyAsync(B->off_dev, B->off_host, (size_t)(B->nclouds + 1) * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st));
+    pdl(k_bbox_clouds, B->nclouds, 256, 0, st)(pts, B->off_dev, B->bb_dev, &L.meta->nonfinite, near,
+                                              &L.meta->near_pairs);
+    FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    FEC_CUDA(cudaMemcpyAsync(bbh, B->bb_dev, (size_t)B->nclouds * 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
+    FEC_CUDA(cudaStreamSynchronize(st));
     const Meta hm = *g_pinned_meta;
     if (hm.nonfinite) { g_err = "non-finite coordinate"; return FEC_ERR_NONFINITE; }
-
-    // ---- grid parameters (reading A6): cell c = d(1+2^-16), sub-cell h = c/2 -----------
-    Grid g{};
-    const double c = (double)d * (1.0 + std::ldexp(1.0, -16));
-    g.h = c * 0.5;
-    g.inv_h = 1.0 / g.h;
-    g.inv_q = 2.0 * g.inv_h;
-    int64_t cells_total = 1;
-    int key_bits = 3;
-    if (!B) {
+    // each cloud: its own origin and cell dims; stacked along z with one empty layer between
+    double* blo = reinterpret_cast<double*>(static_cast<char*>(g_pinned_batch) +
+                                            ((size_t)B->nclouds * 6 * sizeof(float) + 7) / 8 * 8);
+    int32_t* bz = reinterpret_cast<int32_t*>(blo + 3 * B->nclouds);
+    int64_t gx = 1, gy = 1, gz = 0;
+    for (int cidx = 0; cidx < B->nclouds; ++cidx) {
+        const float* bb = bbh + 6 * cidx;
+        bz[cidx] = (int32_t)gz;
+        if (B->off_host[cidx + 1] == B->off_host[cidx]) {
+            blo[3 * cidx] = blo[3 * cidx + 1] = blo[3 * cidx + 2] = 0.0;
+            continue;
+        }
+        int64_t dm[3];
         for (int a = 0; a < 3; ++a) {
-            g.lo[a] = (double)hm.bbox[a];
-            // the same double operations as sub_coord() on the device
-            const double smax = std::floor(((double)hm.bbox[3 + a] - g.lo[a]) * g.inv_h);
-            if (!(smax < 2097152.0)) { g_err = "bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
-            g.dims[a] = (int32_t)(((int64_t)smax >> 1) + 1);
+            blo[3 * cidx + a] = (double)bb[a];
+            const double smax = std::floor(((double)bb[3 + a] - (double)bb[a]) * g0.inv_h);
+            if (!(smax < 2097152.0)) { g_err = "a cloud's bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
+            dm[a] = ((int64_t)smax >> 1) + 1;
         }
-    } else {
-        // each cloud: its own origin and cell dims; stacked along z with one empty layer between
-        double* blo = reinterpret_cast<double*>(static_cast<char*>(g_pinned_batch) +
-                                                ((size_t)B->nclouds * 6 * sizeof(float) + 7) / 8 * 8);
-        int32_t* bz = reinterpret_cast<int32_t*>(blo + 3 * B->nclouds);
-        int64_t gx = 1, gy = 1, gz = 0;
-        for (int cidx = 0; cidx < B->nclouds; ++cidx) {
-            const float* bb = bbh + 6 * cidx;
-            bz[cidx] = (int32_t)gz;
-            if (B->off_host[cidx + 1] == B->off_host[cidx]) {
-                blo[3 * cidx] = blo[3 * cidx + 1] = blo[3 * cidx + 2] = 0.0;
-                continue;
-            }
-            int64_t dm[3];
-            for (int a = 0; a < 3; ++a) {
-                blo[3 * cidx + a] = (double)bb[a];
-                const double smax = std::floor(((double)bb[3 + a] - (double)bb[a]) * g.inv_h);
-                if (!(smax < 2097152.0)) { g_err = "a cloud's bbox extent / cell >= 2^20 (reading A14)"; return FEC_ERR_GRID_RANGE; }
-                dm[a] = ((int64_t)smax >> 1) + 1;
-            }
-            gx = std::max(gx, dm[0]);
-            gy = std::max(gy, dm[1]);
-            gz += dm[2] + 1;
-        }
-        if (gz < 1) gz = 1;
-        if (g_grid_mode == 1 || gx * gy * gz > dense_cap(n) || gx * gy * gz >= (int64_t)0xfffffff0ll || gz >= (1 << 20))
-            return kNeedPerCloud;
-        FEC_CUDA(cudaMemcpyAsync(B->blo_dev, blo, (size_t)B->nclouds * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-        FEC_CUDA(cudaMemcpyAsync(B->bz_dev, bz, (size_t)B->nclouds * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-        g.lo[0] = g.lo[1] = g.lo[2] = 0.0;
-        g.dims[0] = (int32_t)gx;
-        g.dims[1] = (int32_t)gy;
-        g.dims[2] = (int32_t)gz;
-        g.batch = 1;
-        g.nclouds = B->nclouds;
-        g.boff = B->off_dev;
-        g.blo = B->blo_dev;
-        g.bz = B->bz_dev;
+        gx = std::max(gx, dm[0]);
+        gy = std::max(gy, dm[1]);
+        gz += dm[2] + 1;
     }
-    for (int a = 0; a < 3; ++a) {
-        g.bits[a] = ceil_log2(g.dims[a]);
-        key_bits += g.bits[a];
-        cells_total *= g.dims[a];
-    }
-    g.key_bits = key_bits;
-    g.t2 = t2;
-    const int64_t hc = hash_cap(n);
-    g.hash_mask = (u64)(hc - 1);
-    g.dense = (g_grid_mode != 1 && cells_total <= dense_cap(n) && cells_total < (int64_t)0xfffffff0ll) ? 1 : 0;
-    int passes = 0;
-    FEC_CUDA(cudaMemsetAsync(&L.meta->instrument, 0, sizeof(int), st));
-    if (g_instrument) {
-        static const int one = 1;
-        FEC_CUDA(cudaMemcpyAsync(&L.meta->instrument, &one, sizeof(int), cudaMemcpyHostToDevice, st));
-    }
-    const unsigned ew = grid_for(n, 256, cap * 4);
-    const unsigned ew4 = grid_for((n + 3) / 4, 256, cap * 4);  // kernels taking 4 points per thread
-    const int* val = nullptr;
-    DenseCtx dctx{};
-    bool key_sort = false;
-
-    if (g.dense) {
-        FEC_CUDA(ensure_subcell_tables());
-        // smallest dimension fastest in the linear cell id (L2 locality of the slow axis)
+    if (gz < 1) gz = 1;
+    if (gz >= (1 << 21)) return kNeedPerCloud;  // packed cell coordinates hold 21 bits per axis
+    Grid g = g0;
+    g.dims[0] = (int32_t)gx;
+    g.dims[1] = (int32_t)gy;
+    g.dims[2] = (int32_t)gz;
+    const int64_t cells = gx * gy * gz;
+    g.cells_total = cells;
+    g.hashed = (g_grid_mode == 1 || cells > dense_cap(n) || cells >= (int64_t)0xfffffff0ll) ? 1 : 0;
+    if (!g.hashed) {
         int perm[3] = {0, 1, 2};
         for (int i = 0; i < 3; ++i)
             for (int j = i + 1; j < 3; ++j)
@@ -427,197 +410,267 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         g.stride[perm[2]] = (uint32_t)g.dims[perm[0]] * (uint32_t)g.dims[perm[1]];
         g.sdiv[0] = g.stride[perm[2]];
         g.sdiv[1] = g.stride[perm[1]];
-        // dense cells get certain-connected components of their fine occupancy (component nodes)
-        dctx.spts = L.spts;
-        dctx.cstart = L.cstart;
-        dctx.dlist = L.dlist;
-        dctx.clin = L.clin;
-        dctx.cmask = L.cmask;
-        dctx.parent = L.parent;
-        dctx.items = L.items;
-        dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
-        dctx.nbase = (int)n;
-        dctx.meta = L.meta;
-        const int64_t W = (cells_total + 31) / 32;
-        const int64_t dwords = n / 32 + 1;
-        const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
-        // input order: spatially coherent (LiDAR scan order) -> counting sort; shuffled -> key sort
-        const double pairs = 3.0 * (double)(n / 4);
-        key_sort = g_grid_mode == 2 || (g_grid_mode != 3 && !(vec4 && (double)hm.near_pairs >= 0.5 * pairs));
-        FEC_CUDA(cudaMemsetAsync(L.cw, 0, (size_t)(W + 1) * sizeof(uint2), st));
-        FEC_CUDA(cudaMemsetAsync(L.dbits, 0, (size_t)(dwords + 1) * 4, st));
-        if (!key_sort) {
-            // a2: occupancy bitmap -> compact cell ids; counts per cell -> slots, fine occupancy
-            mark(1, st);
-            pdl(k_cmark, ew, 256, 0, st)(pts, n, g, L.cw);
-            launches += 1 + cell_scan(L, W, g, st);
-            const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
-            pdl(k_dcount2, wt, 256, 0, st)(pts, n, g, L.cw, L.cstart, L.cocc);
-            // a3: counting sort = scan (over the occupied cells only) + cursor scatter
-            mark(2, st);
-            launches += 2 + exclusive_scan_dn<uint32_t>(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.dscan, st);
-            pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta);
-            pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos);
-            launches += 2 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
-            pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
-            pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
-                                                                      L.dcoord, L.oflag, dctx);
-            pdl(k_dscatter2, wt, 256, 0, st)(pts, n, g, L.cw, L.slot, L.spts);  // slot = per-cell cursors here
-            launches += 3;
-        } else {
-            // a2: linear cell keys, LSD radix sort over their significant bits
-            mark(1, st);
-            uint32_t* kin = reinterpret_cast<uint32_t*>(L.skey0);
-            uint32_t* kout = reinterpret_cast<uint32_t*>(L.skey1);
-            int *vin = L.sval0, *vout = L.sval1;
-            pdl(k_lkey, ew4, 256, 0, st)(pts, n, g, kin, vin);
-            ++launches;
-            const int lbits = std::max(1, ceil_log2(cells_total));
-            passes = (lbits + 7) / 8;
-            const int tiles = (int)((n + RS_TILE - 1) / RS_TILE);
-            for (int pp = 0; pp < passes; ++pp) {
-                pdl(k_radix_hist32, tiles, RS_THREADS, 0, st)(kin, n, 8 * pp, L.scounts, tiles);
-                launches += exclusive_scan<uint32_t>(L.scounts, L.scounts, (int64_t)256 * tiles, L.dscan, st);
-                pdl(k_radix_scatter32l, tiles, RS_THREADS, 0, st)(kin, vin, kout, vout, n, 8 * pp, L.scounts, tiles);
-                launches += 2;
-                std::swap(kin, kout);
-                std::swap(vin, vout);
-            }
-            // a3: cells = runs of equal keys -> compact ids, starts, fine occupancy; gather points
-            mark(2, st);
-            pdl(k_smark, ew, 256, 0, st)(kin, n, L.cw);
-            launches += 1 + cell_scan(L, W, g, st);
-            pdl(k_sgather, ew4, 256, 0, st)(pts, kin, vin, n, g, L.cw, L.spts, L.cstart, L.cocc, L.parent, L.sidx,
-                                           L.size, L.minidx, L.meta);
-            pdl(k_scount, ew, 256, 0, st)(L.cstart, L.dbits, L.meta);
-            pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos);
-            launches += 4 + exclusive_scan<uint32_t>(L.dwpos, L.dwpos, dwords + 1, L.dscan, st);
-            pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
-            pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(g, L.cocc, L.ccoord, L.ncomp, L.size, L.minidx,
-                                                                      L.dcoord, L.oflag, dctx);
-            launches += 2;
-        }
-        // a4: sorted-order init (parents: self, or the point's component node); the key-sort
-        // path wrote parents/indices in k_sgather and only re-parents points of dense cells
-        mark(3, st);
-        if (key_sort)
-            pdl(k_dparent, grid_for(dense_max(n) * 32, 256, cap * 8), 256, 0, st)(L.spts, L.cstart, L.dlist, L.ncomp,
-                                                                                L.cmask, g, (int)n, L.parent, L.meta,
-                                                                                L.sidx, L.size, L.minidx,
-                                                                                C.node_stats, n);
-        else
-            pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, g, L.cw, L.cstart, L.crec, L.ncomp, L.cmask, (int)n, L.parent,
-                                         L.size, L.minidx, L.sidx, L.meta, C.node_stats);
-        ++launches;
-        mark(4, st);
-        // a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
-        // queued uncertain pairs
-        mark(5, st);
-        pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart, g,
-                                                                         L.parent, L.meta, n);
-        pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(L.cstart, L.slist, L.meta, n);
-        pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart,
-                                                                               L.slist, g, L.parent, L.meta, n);
-        mark(6, st);
-        const unsigned lx = grid_for(dense_max(n), 256, cap);
-        pdl(k_dense_link, dim3(lx, 3), 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 0);
-        pdl(k_dense_link, dim3(lx, 24), 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx, 3);
-        // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
-        pdl(k_dense_overflow, di.sms, 256, 0, st)(g, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
-        pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta);
-        pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(g, dctx, L.items2, L.slices2, L.idone);
-        pdl(k_dense_items, di.sms * 8, 256, 0, st)(g, dctx, L.items2, L.slices2, L.idone);
-        launches += 9;
-        if (g_instrument) {
-            pdl(k_dense_count, grid_for(dense_max(n), 256, cap), 256, 0, st)(L.ncomp, L.dlist, L.cstart, dctx);
-            ++launches;
-        }
-        mark(7, st);
-        val = L.sidx;
+        g.words = (cells + 31) / 32;
+        g.key_bits = std::max(1, ceil_log2(cells));
     } else {
-        // ---- a2: keys ----------------------------------------------------------------------
-        mark(1, st);
-        pdl(k_keys, ew, 256, 0, st)(pts, n, g, L.keyA, L.valA);
-        ++launches;
-        mark(2, st);
-        // ---- a3: LSD radix sort over the significant key bits -------------------------------
-        passes = (key_bits + 7) / 8;
-        u64 *kin = L.keyA, *kout = L.keyB;
-        int *vin = L.valA, *vout = L.valB;
-        for (int p = 0; p < passes; ++p) {
-            const int shift = 8 * p;
-            pdl(k_radix_hist, L.num_tiles, RS_THREADS, 0, st)(kin, n, shift, L.counts, L.num_tiles);
-            launches += exclusive_scan<uint32_t>(L.counts, L.counts, (int64_t)256 * L.num_tiles, L.scan32, st);
-            pdl(k_radix_scatter, L.num_tiles, RS_THREADS, 0, st)(kin, vin, kout, vout, n, shift, L.counts,
-                                                                L.num_tiles);
-            launches += 2;
-            std::swap(kin, kout);
-            std::swap(vin, vout);
-        }
-        const u64* key = kin;
-        val = vin;
-        // ---- a4: gather ----------------------------------------------------------------------
-        mark(3, st);
-        pdl(k_gather, ew, 256, 0, st)(pts, val, n, L.spts);
-        ++launches;
-        mark(4, st);
-        // ---- a5: group / cell tables -----------------------------------------------------------
-        pdl(k_heads, grid_for(n + 1, 256, cap * 4), 256, 0, st)(key, n, L.flags);
-        launches += 1 + exclusive_scan<u64>(L.flags, L.flags, n + 1, L.scan64, st);
-        FEC_CUDA(cudaMemsetAsync(L.T.hkey, 0xFF, (size_t)hc * 8, st));
-        pdl(k_fill_tables, ew, 256, 0, st)(key, L.flags, n, g, L.T, L.meta);
-        pdl(k_init_uf, ew, 256, 0, st)(L.flags, L.T.gstart, n, L.parent, L.size, L.minidx);
-        launches += 2;
-        mark(5, st);
-        mark(6, st);
-        // ---- a6+a7: neighbour scan + union (persistent warps, dynamic cell counter) -----------
-        pdl(k_scan_union, di.sms * di.scan_blocks_per_sm, SCAN_THREADS, 0, st)(L.spts, g, L.T, L.parent, L.meta);
-        ++launches;
-        mark(7, st);
+        g.words = ((int64_t)g.hmask + 1) / 32;
     }
-
-    C.g = g;
-    C.val = val;
-    C.launches = launches;
-    C.passes = passes;
+    const double pairs = 3.0 * (double)(n / 4);
+    const bool coherent = vec4 && (double)hm.near_pairs >= 0.5 * pairs;
+    key_sort = !g.hashed && (g_grid_mode == 2 || (g_grid_mode != 3 && !coherent));
+    g.key_sort = key_sort ? 1 : 0;
+    g.passes = key_sort ? (g.key_bits + 7) / 8 : 0;
+    g.batch = 1;
+    g.nclouds = B->nclouds;
+    g.boff = B->off_dev;
+    g.blo = B->blo_dev;
+    g.bz = B->bz_dev;
+    FEC_CUDA(cudaMemcpyAsync(B->blo_dev, blo, (size_t)B->nclouds * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    FEC_CUDA(cudaMemcpyAsync(B->bz_dev, bz, (size_t)B->nclouds * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    FEC_CUDA(cudaMemcpyAsync(L.grid, &g, sizeof(Grid), cudaMemcpyHostToDevice, st));  // pageable: staged now
+    static const int one = 1;
+    if (g_instrument) FEC_CUDA(cudaMemcpyAsync(&L.meta->instrument, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    FEC_CUDA(cudaEventRecord(g_batch_copied, st));
     return FEC_OK;
 }
 
-// Fills g_stats after a successful call (instrumented counters need one read-back).
+// a1..a8 on n > 0 points (arguments already checked, pointers validated).  No host
+// synchronisation (single cloud): a1's last block plans the grid on the device and every
+// later kernel reads it there; kernels of a path the plan did not choose return at once.
+fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, cudaStream_t st, Core& C,
+                      const BatchArgs* B = nullptr, int32_t* status_dev = nullptr) {
+    Layout& L = C.L;
+    L = carve(static_cast<char*>(ws), n);
+    int launches = 0;
+    const DevInfo di = dev_info();
+    const int cap = di.sms * 8;
+    FEC_CUDA(ensure_subcell_tables());
+
+    // ---- a1: validate + bbox + device-side plan ---------------------------------------------
+    mark(0, st);
+    FEC_CUDA(cudaMemsetAsync(L.meta, 0, sizeof(Meta), st));
+    const int vec4 = (reinterpret_cast<uintptr_t>(pts) & 15u) == 0;
+    const unsigned bb_blocks = grid_for(n, 256 * 4, std::min(cap, kMaxBBoxBlocks));
+    const float near = (float)(2.0 * (double)d * (1.0 + std::ldexp(1.0, -16)));
+    Grid g0{};
+    const double c = (double)d * (1.0 + std::ldexp(1.0, -16));  // reading A6: cell edge
+    g0.h = c * 0.5;
+    g0.inv_h = 1.0 / g0.h;
+    g0.inv_q = 2.0 * g0.inv_h;
+    g0.t2 = t2;
+    g0.hmask = (uint32_t)(L.slots - 1);
+    g0.hkey = L.hkey;
+    bool key_path = g_grid_mode == 2 || (g_grid_mode == 0 && n > kSmallN);
+    if (!B) {
+        PlanArgs a{};
+        a.g0 = g0;
+        a.n = n;
+        a.dense_cap = dense_cap(n);
+        a.grid_mode = g_grid_mode;
+        a.key_path = key_path ? 1 : 0;
+        a.vec4 = vec4;
+        a.instrument = g_instrument;
+        a.near = near;
+        a.status_dev = status_dev;
+        pdl(k_bbox, bb_blocks, 256, 0, st)(pts, a, L.part, L.meta, L.grid);
+        ++launches;
+    } else {
+        bool ks = false;
+        fec_status_t rc = plan_batch(pts, n, g0, L, B, near, vec4, st, ks);
+        if (rc != FEC_OK) return rc;
+        key_path = ks;
+        ++launches;
+    }
+    const Grid* gp = L.grid;
+    const int* gstatus = &L.grid->status;
+    const int* gkeysort = &L.grid->key_sort;
+    pdl(k_zero, di.sms * 4, 256, 0, st)(gp, L.cw, L.hkey, L.slots, L.arena, L.arena_words);
+    ++launches;
+
+    const unsigned ew = grid_for(n, 256, cap * 4);
+    const unsigned ew4 = grid_for((n + 3) / 4, 256, cap * 4);  // kernels taking 4 points per thread
+    const int64_t dwords = n / 32 + 1;
+    const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
+    const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
+    const unsigned cs_blocks = (unsigned)std::min<int64_t>(L.cs_tiles, di.sms * 8);
+    DenseCtx dctx{};
+    dctx.spts = L.spts;
+    dctx.cstart = L.cstart;
+    dctx.dlist = L.dlist;
+    dctx.clin = L.clin;
+    dctx.cmask = L.cmask;
+    dctx.parent = L.parent;
+    dctx.items = L.items;
+    dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
+    dctx.nbase = (int)n;
+    dctx.meta = L.meta;
+    // single cloud: the counting path is always enqueued (hash mode has no key sort); batch
+    // mode planned on the host enqueues only the chosen path
+    const bool count_path = !B || !key_path;
+
+    // ---- a2/a3: binning (counting sort for coherent input, key sort for shuffled input) -------
+    mark(1, st);
+    if (key_path) {
+        pdl(k_lkey, grid_for((n + 3) / 4, 256, di.sms * 4), 256, 0, st)(pts, n, gp, L.skey0, L.sval0, L.ghist, L.os_state, L.os_tiles * 256);
+        ++launches;
+        for (int pass = 0; pass < 4; ++pass) {  // passes beyond the planned count return at once
+            pdl(k_onesweep, (unsigned)std::min<int64_t>(L.os_tiles, di.sms * 2), RS_THREADS, 0, st)(gp, pass, L.skey0, L.sval0, L.skey1, L.sval1, n,
+                                                                    L.ghist, L.os_state, L.os_tiles, L.ctr + 4);
+            ++launches;
+        }
+    }
+    mark(2, st);
+    if (count_path) {
+        pdl(k_cmark, ew, 256, 0, st)(pts, n, gp, L.cw);
+        ++launches;
+    }
+    if (key_path) {
+        pdl(k_smark, grid_for(n, 256, di.sms * 4), 256, 0, st)(L.skey0, L.skey1, n, L.cw, gp);
+        ++launches;
+    }
+    pdl(k_cscan, cs_blocks, 256, 0, st)(L.cw, L.clin, L.cstart, L.cocc, L.cmin, L.ccoord, gp, L.meta, L.cs_state,
+                                        L.ctr + 0);
+    ++launches;
+    if (count_path) {
+        pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin);
+        launches += 1 + exclusive_scan_lb(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.sa_state, L.ctr + 1, cap,
+                                          gstatus, gkeysort, st);
+        pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta, gp, L.crec);
+        ++launches;
+    }
+    if (key_path) {
+        pdl(k_sgather, grid_for((n + 3) / 4, 256, di.sms * 8), 256, 0, st)(pts, L.skey0, L.sval0, L.skey1, L.sval1, n, gp, L.cw, L.spts, L.cstart, L.cocc,
+                                       L.parent, L.sidx, L.size, L.minidx, L.meta);
+        pdl(k_scount, grid_for(n, 256, di.sms * 4), 256, 0, st)(L.cstart, L.dbits, L.meta, gp, L.crec);
+        launches += 2;
+    }
+    // dense records: compact ids of the dense cells, their components and nodes
+    pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.meta);
+    launches += 1 + exclusive_scan_lb(L.dwpos, L.dwpos, dwords + 1, nullptr, L.sb_state, L.ctr + 2, cap, gstatus,
+                                      nullptr, st);
+    pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+    pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(gp, L.cw, L.crec, L.cocc, L.ccoord, L.ncomp, L.size,
+                                                              L.minidx, L.dcoord, L.oflag, dctx, L.litems, L.lhalf,
+                                                              L.cmin, L.sidx, C.node_stats);
+    launches += 2;
+    // the dense-dense certain unions need no point: they run on the side stream while the
+    // points are scattered and initialised
+    SideStream* side = nullptr;
+    FEC_CUDA_RC(side_stream(&side));
+    if (side) {
+        FEC_CUDA(cudaEventRecord(side->fork, st));
+        FEC_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+        pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, side->s)(
+            gp, L.crec, L.ncomp, L.oflag, dctx, L.litems, L.lhalf, 1);
+        FEC_CUDA(cudaEventRecord(side->join, side->s));
+        ++launches;
+    }
+    // ---- a4: sorted-order init (counting path: scatter + init; key path: dense re-parenting)
+    mark(3, st);
+    if (count_path) {
+        // slot = per-cell cursors here
+        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts);
+        pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, gp, L.cw, L.crec, L.cmask, (int)n, L.parent, L.size, L.minidx,
+                                     L.sidx);
+        ++launches;
+        ++launches;
+    }
+    // both paths: points of dense cells under their component nodes + node statistics
+    pdl(k_dparent, grid_for(dense_max(n) * 32, 256, di.sms * 8), 256, 0, st)(L.spts, L.cstart, L.dlist, L.ncomp,
+                                                                        L.cmask, gp, (int)n, L.parent, L.meta,
+                                                                        L.sidx, L.size, L.minidx, C.node_stats, n);
+    ++launches;
+    mark(4, st);
+    // ---- a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
+    // queued uncertain pairs
+    mark(5, st);
+    const int local_only = n <= kSmallN ? 1 : 0;
+    if (!local_only)
+        pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart, gp,
+                                                                         L.parent, L.meta, n, local_only);
+    // sparse-sparse pairs: items listed by k_slist (in the dead fine-occupancy buffer), one thread
+    // each; the per-cell kernel runs only if the list overflowed
+    uint2* sitems = reinterpret_cast<uint2*>(L.cocc);
+    const int scap = (int)std::min<int64_t>(n, INT32_MAX);
+    pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(gp, L.cw, L.ccoord, L.cstart, L.slist, L.meta, n, local_only,
+                                                       sitems, scap);
+    pdl(k_sparse_pairs, grid_for(n, 256, cap * 2), 256, 0, st)(L.spts, L.cstart, gp, L.parent, L.meta, n, local_only,
+                                                              sitems, scap);
+    pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart,
+                                                                           L.slist, gp, L.parent, L.meta, n,
+                                                                           local_only);
+    ++launches;
+    mark(6, st);
+    // thread per listed item (k_dcomps): the sparse neighbours and own pairs here, the forward
+    // dense pairs on the side stream (forked after k_dcomps); the fallback runs only if a list
+    // overflowed
+    pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, st)(gp, L.crec, L.ncomp, L.oflag, dctx,
+                                                                            L.litems, L.lhalf, side ? 2 : 3);
+    if (side) FEC_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+    pdl(k_dense_link_all, di.sms * 2, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
+    // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
+    pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
+    pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta);
+    pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(dctx, L.items2, L.slices2, L.idone);
+    pdl(k_dense_items, di.sms * 8, 256, 0, st)(gp, dctx, L.items2, L.slices2, L.idone);
+    launches += local_only ? 8 : 9;
+    if (g_instrument) {
+        pdl(k_dense_count, grid_for(dense_max(n), 256, cap), 256, 0, st)(L.ncomp, L.dlist, L.cstart, dctx);
+        ++launches;
+    }
+    mark(7, st);
+    C.val = L.sidx;
+    C.launches = launches;
+    return FEC_OK;
+}
+
+// Fills g_stats after an enqueued call.  Fields planned on the device (grid, cells, ...) need
+// a read-back, done only for instrumented calls (which therefore synchronise); otherwise -1.
 fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
-    const Grid& g = C.g;
     const Layout& L = C.L;
-    const int launches = C.launches;
-    const int passes = C.passes;
-    const int key_bits = g.key_bits;
     std::memset(&g_stats, 0, sizeof(g_stats));
     g_stats.n = n;
     g_stats.cells = g_stats.groups = g_stats.components = g_stats.pair_tests = g_stats.group_pairs = -1;
     g_stats.dense_cells = g_stats.dense_points = g_stats.dense_tests = -1;
-    g_stats.key_bits = key_bits;
-    g_stats.radix_passes = passes;
-    g_stats.dense_table = g.dense;
-    for (int a = 0; a < 3; ++a) g_stats.dims[a] = g.dims[a];
-    g_stats.launches = launches;
+    g_stats.key_bits = -1;
+    g_stats.radix_passes = -1;
+    g_stats.dense_table = -1;
+    for (int a = 0; a < 3; ++a) g_stats.dims[a] = -1;
+    g_stats.launches = C.launches;
     if (g_instrument) {
-        FEC_CUDA(cudaMemcpyAsync(g_pinned_meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+        if (!g_snap) FEC_CUDA(cudaMallocHost(&g_snap, sizeof(Snapshot)));
+        FEC_CUDA(cudaMemcpyAsync(&g_snap->meta, L.meta, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+        FEC_CUDA(cudaMemcpyAsync(&g_snap->grid, L.grid, sizeof(Grid), cudaMemcpyDeviceToHost, st));
         FEC_CUDA(cudaStreamSynchronize(st));
-        g_stats.cells = g_pinned_meta->cells;
-        g_stats.groups = g.dense ? -1 : g_pinned_meta->groups;
-        g_stats.dense_cells = g.dense ? g_pinned_meta->ndense : -1;
-        g_stats.dense_points = g.dense ? (int64_t)g_pinned_meta->dense_points : -1;
-        g_stats.components = (int64_t)g_pinned_meta->components;
-        g_stats.pair_tests = (int64_t)(g_pinned_meta->pair_tests + g_pinned_meta->dense_tests);
-        g_stats.dense_tests = g.dense ? (int64_t)g_pinned_meta->dense_tests : -1;
-        g_stats.group_pairs = g.dense ? (int64_t)g_pinned_meta->nitems2 : (int64_t)g_pinned_meta->group_pairs;
-        if (g_pinned_meta->internal_error) { g_err = "internal invariant failed (component bound)"; return FEC_ERR_CUDA; }
+        const Meta& m = g_snap->meta;
+        const Grid& g = g_snap->grid;
+        if (m.status != FEC_OK) {  // nothing to report (the caller sees the status)
+            g_stats_valid = true;
+            return FEC_OK;
+        }
+        g_stats.key_bits = g.key_bits;
+        g_stats.radix_passes = g.passes;
+        g_stats.dense_table = g.hashed ? 0 : 1;
+        for (int a = 0; a < 3; ++a) g_stats.dims[a] = g.dims[a];
+        g_stats.cells = m.cells;
+        g_stats.groups = -1;
+        g_stats.dense_cells = m.ndense;
+        g_stats.dense_points = (int64_t)m.dense_points;
+        g_stats.components = (int64_t)m.components;
+        g_stats.pair_tests = (int64_t)(m.pair_tests + m.dense_tests);
+        g_stats.dense_tests = (int64_t)m.dense_tests;
+        g_stats.group_pairs = (int64_t)m.nitems2;
+        if (m.internal_error) { g_err = "internal invariant failed (component bound)"; return FEC_ERR_CUDA; }
     }
     g_stats_valid = true;
     return FEC_OK;
 }
 
+// Validates and enqueues the whole path (a1..a10).  No host synchronisation for a single cloud
+// (status_dev receives what the device finds); batch mode synchronises once after its bboxes.
 fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t max_size, int32_t* labels,
-                 void* ws, size_t ws_bytes, cudaStream_t st, const BatchArgs* B = nullptr) {
+                 void* ws, size_t ws_bytes, cudaStream_t st, const BatchArgs* B = nullptr,
+                 int32_t* status_dev = nullptr, bool ws_own = false) {
     g_stats_valid = false;
     g_ev.recorded = false;
     float t2 = 0.f;
@@ -629,30 +682,30 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
         return FEC_OK;
     }
     if (!pts || !labels || !ws) { g_err = "null pointer"; return FEC_ERR_INVALID_ARGUMENT; }
-    if (!is_device_ptr(pts) || !is_device_ptr(labels) || !is_device_ptr(ws)) {
+    // (a workspace the library just took from the stream-ordered pool is not queried: under
+    // graph capture it is not mapped yet)
+    if (!is_device_ptr(pts) || !is_device_ptr(labels) || (!ws_own && !is_device_ptr(ws))) {
         g_err = "points, labels_out and workspace must be device pointers";
         return FEC_ERR_INVALID_ARGUMENT;
     }
     if (ws_bytes < carve(nullptr, n).total) { g_err = "workspace too small (see fec_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
     Core C;
     C.node_stats = 1;
-    rc = run_core(pts, n, d, t2, ws, st, C, B);
+    rc = run_core(pts, n, d, t2, ws, st, C, B, status_dev);
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
-    const unsigned ew = grid_for(n, 256, dev_info().sms * 8 * 4);
-    // ---- a8+a9 fused (flatten + stats), a10 -----------------------------------------------------
-    // one of each pair below returns at once (device-side choice)
-    const unsigned wave = grid_for(n, 256, dev_info().sms * 8);
+    const int cap = dev_info().sms * 8;
+    const unsigned ew = grid_for(n, 256, cap * 4);
+    // ---- a8 (sparse-dominated clouds only), a9 (one launch, variant chosen on the device), a10
+    const unsigned wave = grid_for(n, 256, cap);
     pdl(k_flatten_if, wave, 256, 0, st)(L.parent, n, L.meta);
     mark(8, st);
-    const int dense = C.g.dense;
-    // a9 in one launch (k_stats / node tail / k_flat_stats, chosen on the device)
     // (at least two blocks: the node tail splits the grid in halves)
-    pdl(k_tail_stats, std::max(ew, 2u), 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, dense, L.ncomp,
+    pdl(k_tail_stats, std::max(ew, 2u), 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, L.ncomp,
                                                    L.cstart, L.slist);
     mark(9, st);
     pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
-    pdl(k_relabel, grid_for((n + 3) / 4, 256, dev_info().sms * 8 * 4), 256, 0, st)(
+    pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(
         L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
         B ? B->off_dev : nullptr, B ? B->nclouds : 0);
     C.launches += 4;
@@ -661,6 +714,19 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     return finish_stats(C, n, st);
 }
 
+// Stream-ordered workspace for the self-allocating calls (the device's default memory pool;
+// capturable: a graph gets allocation / free nodes).
+fec_status_t alloc_ws(void** ws, size_t bytes, cudaStream_t st) {
+    *ws = nullptr;
+    cudaError_t e = cudaMallocAsync(ws, bytes + g_alloc_extra, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *ws = nullptr;
+        g_err = std::string("cudaMallocAsync(") + std::to_string(bytes + g_alloc_extra) + " B): " + cudaGetErrorString(e);
+        return FEC_ERR_OUT_OF_MEMORY;
+    }
+    return FEC_OK;
+}
 
 // ---- slab (multi-GPU) path ----------------------------------------------------------------
 constexpr int64_t kSlabMagic = 0x46454353'4c414231ll;  // "FECSLAB1"
@@ -718,19 +784,48 @@ BatchArgs batch_carve(char* base, int64_t n, int32_t nclouds, const int64_t* off
 extern "C" {
 
 size_t fec_workspace_bytes(int64_t n) {
-    if (n <= 0) return 0;
+    if (n <= 0 || n > kMaxN) return 0;
     return carve(nullptr, n).total;
 }
 
 size_t fec_workspace_bytes_host(int64_t n) {
-    if (n <= 0) return 0;
+    if (n <= 0 || n > kMaxN) return 0;
     return fec_workspace_bytes(n) + ((size_t)12 * n + 256) + ((size_t)4 * n + 256);
+}
+
+fec_status_t fec_cluster_ws_async(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
+                                  int32_t* labels_out, void* workspace, size_t workspace_bytes, void* stream,
+                                  int32_t* status_dev) {
+    return run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes,
+               static_cast<cudaStream_t>(stream), nullptr, status_dev);
 }
 
 fec_status_t fec_cluster_ws(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
                             int32_t* labels_out, void* workspace, size_t workspace_bytes, void* stream) {
-    return run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes,
-               static_cast<cudaStream_t>(stream));
+    float t2;
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK || n == 0) return run(points, n, d_th, min_size, max_size, labels_out, workspace, 0, 0);
+    rc = ensure_status_word();
+    if (rc != FEC_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    rc = run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes, st, nullptr, g_status_host);
+    if (rc != FEC_OK || n == 0) return rc;
+    return wait_status(st, g_status_host);
+}
+
+fec_status_t fec_cluster_async(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
+                               int32_t* labels_out, void* stream, int32_t* status_dev) {
+    float t2;
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK || n == 0) return run(points, n, d_th, min_size, max_size, labels_out, nullptr, 0, 0);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t b = fec_workspace_bytes(n);
+    void* ws = nullptr;
+    rc = alloc_ws(&ws, b, st);
+    if (rc != FEC_OK) return rc;
+    rc = run(points, n, d_th, min_size, max_size, labels_out, ws, b, st, nullptr, status_dev, true);
+    cudaFreeAsync(ws, st);  // stream-ordered: after the last kernel of the call
+    return rc;
 }
 
 fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min_size, int64_t max_size,
@@ -738,42 +833,38 @@ fec_status_t fec_cluster(const float* points, int64_t n, float d_th, int64_t min
     float t2;
     fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
     if (rc != FEC_OK || n == 0) return run(points, n, d_th, min_size, max_size, labels_out, nullptr, 0, 0);
-    const size_t b = fec_workspace_bytes(n);
-    void* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, b, 0);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        g_err = std::string("cudaMallocAsync: ") + cudaGetErrorString(e);
-        return FEC_ERR_OUT_OF_MEMORY;
-    }
-    rc = run(points, n, d_th, min_size, max_size, labels_out, ws, b, 0);
-    cudaError_t e2 = cudaStreamSynchronize(0);
-    cudaFreeAsync(ws, 0);
-    cudaStreamSynchronize(0);
-    if (rc == FEC_OK && e2 != cudaSuccess) return fail_cuda(e2, "fec_cluster sync");
-    return rc;
+    rc = ensure_status_word();
+    if (rc != FEC_OK) return rc;
+    rc = fec_cluster_async(points, n, d_th, min_size, max_size, labels_out, nullptr, g_status_host);
+    if (rc != FEC_OK || n == 0) return rc;
+    return wait_status(nullptr, g_status_host);
 }
 
 static fec_status_t cluster_host_impl(const float* points_host, int64_t n, float d_th, int64_t min_size,
                                       int64_t max_size, int32_t* labels_host, void* workspace,
-                                      size_t workspace_bytes, void* stream, bool sync);
+                                      size_t workspace_bytes, void* stream, bool sync, int32_t* status_dev);
 
 fec_status_t fec_cluster_host(const float* points_host, int64_t n, float d_th, int64_t min_size, int64_t max_size,
                               int32_t* labels_host, void* workspace, size_t workspace_bytes, void* stream) {
+    float t2;
+    fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
+    if (rc != FEC_OK || n == 0) return run(nullptr, n, d_th, min_size, max_size, nullptr, nullptr, 0, 0);
+    rc = ensure_status_word();
+    if (rc != FEC_OK) return rc;
     return cluster_host_impl(points_host, n, d_th, min_size, max_size, labels_host, workspace, workspace_bytes,
-                             stream, true);
+                             stream, true, g_status_host);
 }
 
 fec_status_t fec_cluster_host_async(const float* points_host, int64_t n, float d_th, int64_t min_size,
                                     int64_t max_size, int32_t* labels_host, void* workspace,
-                                    size_t workspace_bytes, void* stream) {
+                                    size_t workspace_bytes, void* stream, int32_t* status_dev) {
     return cluster_host_impl(points_host, n, d_th, min_size, max_size, labels_host, workspace, workspace_bytes,
-                             stream, false);
+                             stream, false, status_dev);
 }
 
 static fec_status_t cluster_host_impl(const float* points_host, int64_t n, float d_th, int64_t min_size,
                                       int64_t max_size, int32_t* labels_host, void* workspace,
-                                      size_t workspace_bytes, void* stream, bool sync) {
+                                      size_t workspace_bytes, void* stream, bool sync, int32_t* status_dev) {
     float t2;
     fec_status_t rc = check_args(n, d_th, min_size, max_size, &t2);
     if (rc != FEC_OK) return rc;
@@ -786,10 +877,11 @@ static fec_status_t cluster_host_impl(const float* points_host, int64_t n, float
     float* dpts = reinterpret_cast<float*>(base + ((main_b + 255) & ~size_t(255)));
     int32_t* dlab = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dpts) + (((size_t)12 * n + 255) & ~size_t(255)));
     FEC_CUDA(cudaMemcpyAsync(dpts, points_host, (size_t)12 * n, cudaMemcpyHostToDevice, st));
-    rc = run(dpts, n, d_th, min_size, max_size, dlab, workspace, main_b, st);
+    rc = run(dpts, n, d_th, min_size, max_size, dlab, workspace, main_b, st, nullptr, status_dev);
     if (rc == FEC_OK) FEC_CUDA(cudaMemcpyAsync(labels_host, dlab, (size_t)4 * n, cudaMemcpyDeviceToHost, st));
-    if (sync || rc != FEC_OK) FEC_CUDA(cudaStreamSynchronize(st));
-    return rc;
+    if (rc != FEC_OK) return rc;
+    if (sync) return wait_status(st, status_dev);
+    return FEC_OK;
 }
 
 
@@ -802,7 +894,7 @@ size_t fec_slab_workspace_bytes(int64_t n_local, int32_t world, int64_t rec_cap)
 
 fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_local, int64_t n_owned,
                             int64_t n_first, float d_th, int32_t* records, int64_t rec_cap, void* workspace,
-                            size_t workspace_bytes, fec_slab_state_t* state, void* stream) {
+                            size_t workspace_bytes, fec_slab_state_t* state, void* stream, int32_t* status_dev) {
     g_stats_valid = false;
     g_ev.recorded = false;
     float t2 = 0.f;
@@ -836,11 +928,11 @@ fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_
         return FEC_OK;
     }
     Core C;
-    rc = run_core(points, n_local, d_th, t2, workspace, st, C);
+    rc = run_core(points, n_local, d_th, t2, workspace, st, C, nullptr, status_dev);
     if (rc != FEC_OK) return rc;
     const Layout& L = C.L;
     const unsigned ew = grid_for(n_local, 256, dev_info().sms * 8 * 4);
-    pdl(k_flatten, ew, 256, 0, st)(L.parent, n_local, L.size, L.minidx);
+    pdl(k_flatten, ew, 256, 0, st)(L.parent, n_local, L.size, L.minidx, L.meta);
     mark(8, st);
     ++C.launches;
     FEC_CUDA(cudaMemsetAsync(S.ckey, 0xFF, (size_t)nodes_max(n_local) * 4, st));
@@ -897,7 +989,7 @@ fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t r
                                                                             L.size, L.minidx);
         pdl(k_slab_relabel, grid_for(ss.n_local, 256, cap), 256, 0, st)(L.parent, val, L.size, L.minidx, ss.n_local,
                                                                        (int)ss.n_owned, (long long)min_size,
-                                                                       (long long)max_size, labels_owned);
+                                                                       (long long)max_size, labels_owned, L.meta);
     }
     FEC_CUDA(cudaGetLastError());
     return FEC_OK;
@@ -935,11 +1027,15 @@ fec_status_t fec_cluster_batch_ws(const float* points, const int64_t* offsets, i
     const BatchArgs B = batch_carve(static_cast<char*>(workspace), n, nclouds, offsets);
     rc = run(points, n, d_th, min_size, max_size, labels_out, workspace, workspace_bytes, st, &B);
     if (rc != kNeedPerCloud) return rc;
+    rc = ensure_status_word();
+    if (rc != FEC_OK) return rc;
     // the stacked grid does not fit the dense mode: cluster the clouds one after another
     for (int32_t c = 0; c < nclouds; ++c) {
         const int64_t a = offsets[c], nc = offsets[c + 1] - offsets[c];
         if (nc == 0) continue;
-        rc = run(points + 3 * a, nc, d_th, min_size, max_size, labels_out + a, workspace, workspace_bytes, st);
+        rc = run(points + 3 * a, nc, d_th, min_size, max_size, labels_out + a, workspace, workspace_bytes, st, nullptr,
+                 g_status_host);
+        if (rc == FEC_OK) rc = wait_status(st, g_status_host);
         if (rc != FEC_OK) return rc;
     }
     return FEC_OK;
@@ -959,6 +1055,8 @@ void fec_set_timing(int enable) { g_timing = enable ? 1 : 0; }
 void fec_set_grid_mode(int mode) { g_grid_mode = mode; }
 
 void fec_set_item_cap(int64_t cap) { g_item_cap = cap > 0 ? cap : 0; }
+
+void fec_debug_alloc_extra(size_t bytes) { g_alloc_extra = bytes; }
 
 int32_t fec_get_stage_times(float* ms_out, int32_t max_stages) {
     if (!g_ev.recorded) { g_err = "no timed call on this thread (fec_set_timing(1) first)"; return -1; }

@@ -12,12 +12,28 @@
 // DESIGN.md §4 describes why every edge of the graph of Eq. 1 is covered exactly.
 #include "fec_internal.cuh"
 #include "fec_kernels.cuh"
-#include "fec_pairs.cuh"
 #include "fec_subcell.cuh"
 
 namespace fec {
 
-__device__ SubcellTables d_sc;  // filled once per device (fec_capi.cu)
+__device__ SubcellTables d_sc = sc_make_tables();  // compile-time constant (fec_subcell.cuh)
+
+// The 13 forward neighbour offsets: (dz>0) or (dz==0 and dy>0) or (dz==0, dy==0, dx>0).
+// With same-cell pairs, every unordered pair of adjacent cells is visited exactly once.
+__constant__ signed char c_fwd[13][3] = {
+    {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},  {1, 1, 0},  {-1, -1, 1}, {0, -1, 1}, {1, -1, 1},
+    {-1, 0, 1}, {0, 0, 1},  {1, 0, 1},  {-1, 1, 1}, {0, 1, 1},   {1, 1, 1}};
+
+// Neighbour slots of the dense-cell kernels: 0-2 forward faces, 3-12 forward edges and corners,
+// 13-25 backward; slot 26 (not in the table) = a record's own component pairs.
+__constant__ signed char c_slot[26][3] = {
+    {1, 0, 0},   {0, 1, 0},   {0, 0, 1},                                         // forward faces
+    {-1, 1, 0},  {1, 1, 0},   {0, -1, 1}, {-1, 0, 1}, {1, 0, 1}, {0, 1, 1},      // forward edges
+    {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1}, {1, 1, 1},                             // forward corners
+    {-1, 0, 0},  {0, -1, 0},  {0, 0, -1},                                        // backward ...
+    {1, -1, 0},  {-1, -1, 0}, {0, 1, -1}, {1, 0, -1}, {-1, 0, -1}, {0, -1, -1},
+    {1, 1, -1},  {-1, 1, -1}, {1, -1, -1}, {-1, -1, -1}};
+
 
 // Batched clouds (fec_cluster_batch_ws): the cloud holding input index i (binary search over
 // the cloud offsets, a small L1-resident array).
@@ -36,8 +52,7 @@ __device__ __forceinline__ int cloud_of(const Grid& g, int64_t i) {
 // mode each cloud uses its own origin and is shifted by a whole number of cells along z,
 // with an empty cell layer between clouds, so no cell neighbourhood spans two clouds.
 // `i` is the point's input index.
-__device__ __forceinline__ void dense_cell_of(float x, float y, float z, int64_t i, const Grid& g, uint32_t& lin,
-                                              int& q) {
+__device__ __forceinline__ void fine_of(float x, float y, float z, int64_t i, const Grid& g, uint32_t f[3]) {
     double l0 = g.lo[0], l1 = g.lo[1], l2 = g.lo[2];
     uint32_t zoff = 0;
     if (g.batch) {
@@ -47,14 +62,66 @@ __device__ __forceinline__ void dense_cell_of(float x, float y, float z, int64_t
         l2 = __ldg(g.blo + 3 * c + 2);
         zoff = 4u * (uint32_t)__ldg(g.bz + c);
     }
-    const uint32_t fx = sub_coord(x, l0, g.inv_q);
-    const uint32_t fy = sub_coord(y, l1, g.inv_q);
-    const uint32_t fz = sub_coord(z, l2, g.inv_q) + zoff;
-    q = (int)((fx & 3u) | ((fy & 3u) << 2) | ((fz & 3u) << 4));
-    lin = (fx >> 2) * g.stride[0] + (fy >> 2) * g.stride[1] + (fz >> 2) * g.stride[2];
+    f[0] = sub_coord(x, l0, g.inv_q);
+    f[1] = sub_coord(y, l1, g.inv_q);
+    f[2] = sub_coord(z, l2, g.inv_q) + zoff;
+}
+__device__ __forceinline__ int fine_index(const uint32_t f[3]) {
+    return (int)((f[0] & 3u) | ((f[1] & 3u) << 2) | ((f[2] & 3u) << 4));
+}
+// Fine sub-cell index (bit of the cell's 4x4x4 mask) of a point.
+__device__ __forceinline__ int q_of(float x, float y, float z, int64_t i, const Grid& g) {
+    uint32_t f[3];
+    fine_of(x, y, z, i, g, f);
+    return fine_index(f);
+}
+
+// ---- cell handles ---------------------------------------------------------------------------
+// Bitmap mode (the grid holds <= 32n + 2^26 cells): handle = linear cell id, an index into an
+// occupancy bitmap over the whole grid.  Hash mode (sparse, huge bounding boxes): handle = the
+// slot of the cell's packed coordinates in an open-addressing table (linear probing, >= 2n
+// slots), filled by k_cmark; the occupancy bitmap then runs over the table's slots.  Either
+// way the compact id of an occupied cell is the rank of its handle's bit (cid_of), so every
+// kernel after binning is the same for both.
+__device__ __forceinline__ uint32_t hash_find(const Grid& g, u64 pc) {  // ~0u: absent
+    uint32_t h = (uint32_t)hash_cell(pc) & g.hmask;
+    while (true) {
+        const u64 k = __ldg(g.hkey + h);  // read-only after k_cmark
+        if (k == pc) return h;
+        if (k == ~0ull) return 0xffffffffu;
+        h = (h + 1) & g.hmask;
+    }
+}
+// k_cmark (hash mode): slot of pc, inserting it if absent.
+__device__ __forceinline__ uint32_t hash_insert(const Grid& g, u64 pc) {
+    uint32_t h = (uint32_t)hash_cell(pc) & g.hmask;
+    while (true) {
+        u64 k = *reinterpret_cast<volatile u64*>(g.hkey + h);
+        if (k == ~0ull) k = atomicCAS(g.hkey + h, ~0ull, pc);
+        if (k == ~0ull || k == pc) return h;
+        h = (h + 1) & g.hmask;
+    }
+}
+__device__ __forceinline__ uint32_t cell_handle(const Grid& g, uint32_t cx, uint32_t cy, uint32_t cz) {
+    if (g.hashed) return hash_find(g, pack_cell(cx, cy, cz));
+    return cx * g.stride[0] + cy * g.stride[1] + cz * g.stride[2];
+}
+__device__ __forceinline__ void dense_cell_of(float x, float y, float z, int64_t i, const Grid& g, uint32_t& lin,
+                                              int& q) {
+    uint32_t f[3];
+    fine_of(x, y, z, i, g, f);
+    q = fine_index(f);
+    lin = cell_handle(g, f[0] >> 2, f[1] >> 2, f[2] >> 2);
 }
 
 __device__ __forceinline__ void dense_decode(uint32_t lin, const Grid& g, int c[3]) {
+    if (g.hashed) {
+        const u64 pc = __ldg(g.hkey + lin);
+        c[0] = (int)(pc & 0x1fffff);
+        c[1] = (int)((pc >> 21) & 0x1fffff);
+        c[2] = (int)(pc >> 42);
+        return;
+    }
     // slow axis = perm[2] (stride sdiv[0]), middle = perm[1] (stride sdiv[1]), fast = perm[0]
     const uint32_t q2 = lin / g.sdiv[0];
     lin -= q2 * g.sdiv[0];
@@ -65,11 +132,12 @@ __device__ __forceinline__ void dense_decode(uint32_t lin, const Grid& g, int c[
     c[2] = (int)(g.perm[2] == 2 ? q2 : (g.perm[1] == 2 ? q1 : q0));
 }
 
+// Handle of the cell at c + (dx, dy, dz); false if it is outside the grid or (hash mode) empty.
 __device__ __forceinline__ bool dense_neighbor(const Grid& g, const int c[3], int dx, int dy, int dz, uint32_t& lin) {
     const int x = c[0] + dx, y = c[1] + dy, z = c[2] + dz;
     if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) return false;
-    lin = (uint32_t)x * g.stride[0] + (uint32_t)y * g.stride[1] + (uint32_t)z * g.stride[2];
-    return true;
+    lin = cell_handle(g, (uint32_t)x, (uint32_t)y, (uint32_t)z);
+    return lin != 0xffffffffu;
 }
 
 // Four consecutive input points per thread: three 16-byte loads when `points` is 16-byte
@@ -131,6 +199,27 @@ __device__ __forceinline__ int cid_lookup(const uint2* __restrict__ cw, uint32_t
     return (v.x & b) ? (int)(v.y + (uint32_t)__popc(v.x & (b - 1u))) : -1;
 }
 
+// ---- scratch initialisation (device-sized) -------------------------------------------------
+// The occupancy words (their count is planned on the device), the hash table (hash mode: all
+// slots empty) and the host-sized arena of look-back states, counters and dense-cell bits.
+__global__ void __launch_bounds__(256) k_zero(const Grid* __restrict__ gp, uint2* __restrict__ cw,
+                                             u64* __restrict__ hkey, int64_t slots, uint32_t* __restrict__ arena,
+                                             int64_t arena_words) {
+    pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nw2 = (g.words + 2) / 2;  // words + 1 uint2 entries, as uint4 pairs (256-B aligned)
+    uint4* c4 = reinterpret_cast<uint4*>(cw);
+    for (int64_t i = t0; i < nw2; i += stride) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (g.hashed) {
+        ulonglong2* h2 = reinterpret_cast<ulonglong2*>(hkey);
+        for (int64_t i = t0; i < slots / 2; i += stride) h2[i] = make_ulonglong2(~0ull, ~0ull);
+    }
+    for (int64_t i = t0; i < arena_words; i += stride) arena[i] = 0u;
+}
+
 // ---- a2: occupancy bitmap ------------------------------------------------------------------
 // Binning kernels aggregate per block through a small shared-memory hash table (keys = bitmap
 // word or compact cell id): one global atomic per distinct key per tile of kBinTile points.
@@ -158,9 +247,11 @@ __device__ __forceinline__ int bin_slot(int* keys, uint32_t key, int* used, int*
     }
 }
 
-__global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__ p, int64_t n, Grid g,
-                                                       uint2* __restrict__ cw) {
+__global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__ p, int64_t n,
+                                                       const Grid* __restrict__ gp, uint2* __restrict__ cw) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || g.key_sort) return;
     __shared__ int keys[kBinSlots];
     __shared__ uint32_t bits[kBinSlots];
     __shared__ int used[kBinTile];
@@ -175,12 +266,20 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
         load_pts4(p, n, b4, vec, P);
         // runs of this thread's points in the same bitmap word take one table update
         uint32_t word = 0xffffffffu, wbits = 0u;
+        u64 prev_pc = ~0ull;
+        uint32_t lin = 0;
 #pragma unroll
         for (int j = 0; j < kBinIpt; ++j) {
             if (b4 + j < n) {
-                uint32_t lin;
-                int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
+                uint32_t f[3];
+                fine_of(P.x[j], P.y[j], P.z[j], b4 + j, g, f);
+                if (g.hashed) {  // insert the cell (consecutive points of one cell: one probe)
+                    const u64 pc = pack_cell(f[0] >> 2, f[1] >> 2, f[2] >> 2);
+                    if (pc != prev_pc) lin = hash_insert(g, pc);
+                    prev_pc = pc;
+                } else {
+                    lin = (f[0] >> 2) * g.stride[0] + (f[1] >> 2) * g.stride[1] + (f[2] >> 2) * g.stride[2];
+                }
                 if ((lin >> 5) != word) {
                     if (wbits) atomicOr(bits + bin_slot(keys, word, used, &nused), wbits);
                     word = lin >> 5;
@@ -211,22 +310,30 @@ __global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__
 // lanes.  One pass over the bitmap, one launch (+ the state memset).
 constexpr int CS_THREADS = 256, CS_ITEMS = 8, CS_TILE = CS_THREADS * CS_ITEMS;
 
-__global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, int64_t words,
-                                                     uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
-                                                     u64* __restrict__ cocc, u64* __restrict__ ccoord, Grid g,
+__global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, uint32_t* __restrict__ clin,
+                                                     uint32_t* __restrict__ count, u64* __restrict__ cocc,
+                                                     int* __restrict__ cmin,
+                                                     u64* __restrict__ ccoord, const Grid* __restrict__ gp,
                                                      Meta* __restrict__ meta, unsigned long long* __restrict__ state,
                                                      unsigned int* __restrict__ counter) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
     __shared__ uint32_t s[CS_TILE];
     __shared__ uint32_t sbits[CS_TILE];  // the tile's words, for the emission (no reload)
     __shared__ uint32_t wsum[CS_THREADS / kWarp];
     __shared__ unsigned int tile_sh;
     __shared__ uint32_t prefix_sh;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t words = g.words;
+    const int64_t n = words + 1;  // the extra element yields U = the total
+    // persistent blocks take tiles in order from the counter (a tile only ever waits on
+    // earlier tiles, which blocks already running hold)
+    while (true) {
+    __syncthreads();
     if (tid == 0) tile_sh = atomicAdd(counter, 1u);
     __syncthreads();
     const unsigned tile = tile_sh;
-    const int64_t n = words + 1;  // the extra element yields U = the total
     const int64_t base = (int64_t)tile * CS_TILE;
     if (base >= n) return;
 #pragma unroll
@@ -322,9 +429,11 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, in
                 ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
                 count[r] = 0u;
                 cocc[r] = 0ull;
+                cmin[r] = 0x7fffffff;
             }
         }
     }
+    }  // tiles
 }
 
 // ---- a2: per-cell counts, slot[i] = rank of point i inside its cell, fine occupancy ------
@@ -353,21 +462,25 @@ __device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int
 
 // Counting without return values: per warp-tile cell counts and fine-occupancy bits are added
 // to the cell's counters fire-and-forget (no dependent round trip); slots are assigned later
-// by k_dscatter2 against per-cell cursors.
-__global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, Grid g,
+// by k_dscatter against per-cell cursors.
+__global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
                                                 const uint2* __restrict__ cw, uint32_t* __restrict__ count,
-                                                u64* __restrict__ cocc) {
+                                                u64* __restrict__ cocc, int* __restrict__ cmin) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || g.key_sort) return;
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
+    __shared__ int mn_all[256 / kWarp][kWSlots];
     __shared__ int used_all[256 / kWarp][kWTile];
     __shared__ int nused_all[256 / kWarp];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int* keys = keys_all[wid];
     uint32_t *cnt = cnt_all[wid], *olo = olo_all[wid], *ohi = ohi_all[wid];
+    int* mn = mn_all[wid];
     int* used = used_all[wid];
     int* nused = nused_all + wid;
-    for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; }
+    for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; olo[k] = 0u; ohi[k] = 0u; mn[k] = 0x7fffffff; }
     if (lane == 0) *nused = 0;
     __syncwarp();
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
@@ -377,7 +490,9 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
         // runs of this thread's points in one cell take one table update
+        // (a run's first point has its smallest input index)
         uint32_t rc = 0xffffffffu, rn = 0u;
+        int rfirst = 0;
         u64 rb = 0ull;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -390,12 +505,14 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
                     if (rn) {
                         const int h = wbin_slot(keys, rc, used, nused);
                         atomicAdd(cnt + h, rn);
+                        atomicMin(mn + h, rfirst);
                         if ((uint32_t)rb) atomicOr(olo + h, (uint32_t)rb);
                         if ((uint32_t)(rb >> 32)) atomicOr(ohi + h, (uint32_t)(rb >> 32));
                     }
                     rc = cid;
                     rn = 0u;
                     rb = 0ull;
+                    rfirst = (int)(b4 + j);
                 }
                 ++rn;
                 rb |= 1ull << q;
@@ -404,6 +521,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         if (rn) {
             const int h = wbin_slot(keys, rc, used, nused);
             atomicAdd(cnt + h, rn);
+            atomicMin(mn + h, rfirst);
             if ((uint32_t)rb) atomicOr(olo + h, (uint32_t)rb);
             if ((uint32_t)(rb >> 32)) atomicOr(ohi + h, (uint32_t)(rb >> 32));
         }
@@ -414,10 +532,12 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
             const int cid = keys[k];
             atomicAdd(count + cid, cnt[k]);
             atomicOr(cocc + cid, ((u64)ohi[k] << 32) | (u64)olo[k]);
+            atomicMin(cmin + cid, mn[k]);
             keys[k] = -1;
             cnt[k] = 0u;
             olo[k] = 0u;
             ohi[k] = 0u;
+            mn[k] = 0x7fffffff;
         }
         __syncwarp();
         if (lane == 0) *nused = 0;
@@ -425,13 +545,18 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
     }
 }
 
-// Scatter into cell order: per warp-tile, one atomicAdd on the cell's cursor (initialised to
-// the cell start) per distinct cell gives the tile's base; ranks inside the tile come from
-// the warp's shared-memory table.
-__global__ void __launch_bounds__(256) k_dscatter2(const float* __restrict__ p, int64_t n, Grid g,
-                                                  const uint2* __restrict__ cw, uint32_t* __restrict__ cursor,
-                                                  float4* __restrict__ spts) {
+// Counting path, a3: scatter into cell order.  Per warp tile (128 consecutive input points), a
+// shared-memory table of the tile's distinct cells gives each point its rank among the tile's
+// points of its cell; one atomicAdd per distinct cell on the cell's cursor (initialised to the
+// cell start) gives the tile's base inside the cell.  Only the float4 (x, y, z, idx) is written
+// here: the scattered store is the expensive part, and k_dinit derives everything else from
+// the sorted float4s with coalesced accesses.
+__global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n,
+                                                 const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                                 uint32_t* __restrict__ cursor, float4* __restrict__ spts) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || g.key_sort) return;
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots];
     __shared__ int used_all[256 / kWarp][kWTile];
@@ -486,10 +611,71 @@ __global__ void __launch_bounds__(256) k_dscatter2(const float* __restrict__ p, 
     }
 }
 
+// Counting path, a4: sorted-order initialisation (coalesced, 4 positions per thread): the
+// point's cell from its coordinates, the cell's record word (crec: -1 for a sparse cell) gives
+// the parent -- itself for a point of a sparse cell (accumulators reset), else its certain-
+// connected component's node -- and the input index goes to sidx.  (Node statistics come from
+// k_dcomps / k_dparent: no atomics here.)
+__global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, const Grid* __restrict__ gp,
+                                              const uint2* __restrict__ cw, const int* __restrict__ crec,
+                                              const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
+                                              int* __restrict__ size, int* __restrict__ minidx,
+                                              int* __restrict__ sidx) {
+    pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || g.key_sort) return;
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b4 = 4 * gi;
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = b4 + j < n ? __ldg(spts + b4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        int par[4], si[4], rv[4], q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            par[j] = (int)(b4 + j);
+            si[j] = __float_as_int(v[j].w);
+            rv[j] = -1;
+            q[j] = 0;
+            if (b4 + j >= n) continue;
+            uint32_t lin;
+            dense_cell_of(v[j].x, v[j].y, v[j].z, si[j], g, lin, q[j]);
+            rv[j] = __ldg(crec + cid_of(cw, lin));  // -1 sparse, else record << 3 | (components - 1)
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (b4 + j >= n) continue;
+            if (rv[j] < 0) {  // a point of a sparse cell: a possible root
+                size[b4 + j] = 0;
+                minidx[b4 + j] = 0x7fffffff;
+            } else {
+                const int r = rv[j] >> 3, kc = (rv[j] & 7) + 1;
+                int c = 0;
+                if (kc > 1)
+                    while (c < kc - 1 && !((__ldg(cmask + 8 * r + c) >> q[j]) & 1ull)) ++c;
+                par[j] = nbase + 8 * r + c;
+            }
+        }
+        if (b4 + 4 <= n) {
+            *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
+            *reinterpret_cast<int4*>(sidx + b4) = make_int4(si[0], si[1], si[2], si[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (b4 + j < n) {
+                    parent[b4 + j] = par[j];
+                    sidx[b4 + j] = si[j];
+                }
+        }
+    }
+}
+
 // Dense bits of the occupied cells from the cell starts; also the scatter cursors.
 __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
-                                               uint32_t* __restrict__ cursor, const Meta* __restrict__ meta) {
+                                               uint32_t* __restrict__ cursor, const Meta* __restrict__ meta,
+                                               const Grid* __restrict__ gp, int* __restrict__ crec) {
     pdl_prologue();
+    if (gp->status || gp->key_sort) return;
     const int64_t U = meta->cells;
     const int64_t ur = (U + 31) & ~int64_t(31);
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
@@ -498,6 +684,7 @@ __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cst
             const uint32_t c0 = __ldg(cstart + u);
             dense = __ldg(cstart + u + 1) - c0 > (uint32_t)SPARSE_MAX;
             cursor[u] = c0;
+            if (!dense) crec[u] = -1;  // dense cells get their record word in k_dcomps
         }
         const unsigned m = __ballot_sync(0xffffffffu, dense);
         if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
@@ -508,9 +695,21 @@ __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cst
 // For inputs without spatial coherence (C1, C5) the counting sort's per-point atomics and
 // scatter hit random DRAM sectors; instead the linear cell ids are radix-sorted (coalesced
 // digit passes), cells are the runs of equal keys, and points are gathered into cell order.
-__global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64_t n, Grid g, uint32_t* __restrict__ key,
-                                             int* __restrict__ val) {
+// Also the onesweep sort's digit histograms of all passes (ghist[pass][digit], block-
+// aggregated in shared memory) and the zeroed look-back state of its first pass.
+__global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
+                                             uint32_t* __restrict__ key, int* __restrict__ val,
+                                             uint32_t* __restrict__ ghist, uint32_t* __restrict__ state0,
+                                             int64_t state_words) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || !g.key_sort) return;
+    __shared__ uint32_t h[4][256];
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < state_words; k += (int64_t)gridDim.x * blockDim.x)
+        state0[k] = 0u;
+    __syncthreads();
+    const int passes = g.passes;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -521,7 +720,10 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             int q;
-            if (b4 + j < n) dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, k[j], q);
+            if (b4 + j < n) {
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, k[j], q);
+                for (int ps = 0; ps < passes; ++ps) atomicAdd(&h[ps][(k[j] >> (8 * ps)) & 255u], 1u);
+            }
         }
         if (b4 + 4 <= n) {
             *reinterpret_cast<uint4*>(key + b4) = make_uint4(k[0], k[1], k[2], k[3]);
@@ -535,11 +737,19 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
                 }
         }
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) {
+        const uint32_t c = (&h[0][0])[k];
+        if (c) atomicAdd(ghist + k, c);
+    }
 }
 
 // Occupancy bits of the sorted keys' distinct values (heads only; a warp's heads share words).
-__global__ void __launch_bounds__(256) k_smark(const uint32_t* __restrict__ key, int64_t n, uint2* __restrict__ cw) {
+__global__ void __launch_bounds__(256) k_smark(const uint32_t* __restrict__ key0, const uint32_t* __restrict__ key1,
+                                              int64_t n, uint2* __restrict__ cw, const Grid* __restrict__ gp) {
     pdl_prologue();
+    if (gp->status || !gp->key_sort) return;
+    const uint32_t* __restrict__ key = (gp->passes & 1) ? key1 : key0;  // the sort's output buffer
     const int64_t nr = (n + 31) & ~int64_t(31);
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += (int64_t)gridDim.x * blockDim.x) {
         const bool ok = s < n;
@@ -555,14 +765,19 @@ __global__ void __launch_bounds__(256) k_smark(const uint32_t* __restrict__ key,
 // Points into cell order (random 12-byte gathers, coalesced float4 stores), cell starts at
 // the run heads, fine occupancy OR-ed per run (segmented within the warp, one atomic per run
 // piece).
-__global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, const uint32_t* __restrict__ key,
-                                                const int* __restrict__ val, int64_t n, Grid g,
-                                                const uint2* __restrict__ cw, float4* __restrict__ spts,
-                                                uint32_t* __restrict__ cstart, u64* __restrict__ cocc,
-                                                int* __restrict__ parent, int* __restrict__ sidx,
-                                                int* __restrict__ size, int* __restrict__ minidx,
-                                                const Meta* __restrict__ meta) {
+__global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, const uint32_t* __restrict__ key0,
+                                                const int* __restrict__ val0, const uint32_t* __restrict__ key1,
+                                                const int* __restrict__ val1, int64_t n,
+                                                const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                                float4* __restrict__ spts, uint32_t* __restrict__ cstart,
+                                                u64* __restrict__ cocc, int* __restrict__ parent,
+                                                int* __restrict__ sidx, int* __restrict__ size,
+                                                int* __restrict__ minidx, const Meta* __restrict__ meta) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || !g.key_sort) return;
+    const uint32_t* __restrict__ key = (g.passes & 1) ? key1 : key0;  // the sort's output buffers
+    const int* __restrict__ val = (g.passes & 1) ? val1 : val0;
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) cstart[meta->cells] = (uint32_t)n;
     // round j: positions s0 + j*256 + threadIdx.x (a warp holds 32 consecutive positions, so
@@ -591,9 +806,7 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
             u64 bit = 0;
             const uint32_t prev = __shfl_up_sync(0xffffffffu, k[j], 1);  // all lanes take part
             if (ok) {
-                uint32_t lin;
-                int q;
-                dense_cell_of(x[j], y[j], z[j], vi[j], g, lin, q);
+                const int q = q_of(x[j], y[j], z[j], vi[j], g);
                 cid = cid_of(cw, k[j]);
                 bit = 1ull << q;
                 spts[s] = make_float4(x[j], y[j], z[j], __int_as_float(vi[j]));
@@ -616,12 +829,15 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
 // Dense bits of the occupied cells from the run lengths (lanes = consecutive compact ids,
 // so a warp fills one bitmap word with a plain store).
 __global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
-                                               const Meta* __restrict__ meta) {
+                                               const Meta* __restrict__ meta, const Grid* __restrict__ gp,
+                                               int* __restrict__ crec) {
     pdl_prologue();
+    if (gp->status || !gp->key_sort) return;
     const int64_t U = meta->cells;
     const int64_t ur = (U + 31) & ~int64_t(31);
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
         const bool dense = u < U && __ldg(cstart + u + 1) - __ldg(cstart + u) > (uint32_t)SPARSE_MAX;
+        if (u < U && !dense) crec[u] = -1;  // dense cells get their record word in k_dcomps
         const unsigned m = __ballot_sync(0xffffffffu, dense);
         if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
     }
@@ -629,8 +845,9 @@ __global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cst
 
 // ---- dense records: compact ids of the dense cells in ascending order -----------------------
 __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
-                                                   uint32_t* __restrict__ wcount) {
+                                                   uint32_t* __restrict__ wcount, const Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
         wcount[w] = w < words ? (uint32_t)__popc(__ldg(dbits + w)) : 0u;
 }
@@ -639,6 +856,7 @@ __global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__
                                                    const uint32_t* __restrict__ wpos, int* __restrict__ dlist,
                                                    int* __restrict__ crec, Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
         if (w == words) { meta->ndense = (int)wpos[words]; continue; }
         uint32_t bits = __ldg(dbits + w);
@@ -662,6 +880,15 @@ __device__ __forceinline__ int cell_slot_of(const Grid& g, uint32_t lin_p, uint3
     dense_decode(lin_p, g, a);
     dense_decode(lin_q, g, b);
     return sc_slot(b[0] - a[0], b[1] - a[1], b[2] - a[2]);
+}
+// Neighbour slot of the cell holding point v relative to cell lin_p, and v's fine index.
+__device__ __forceinline__ int point_slot_of(const Grid& g, uint32_t lin_p, float4 v, int& qv) {
+    int a[3];
+    dense_decode(lin_p, g, a);
+    uint32_t f[3];
+    fine_of(v.x, v.y, v.z, __float_as_int(v.w), g, f);
+    qv = fine_index(f);
+    return sc_slot((int)(f[0] >> 2) - a[0], (int)(f[1] >> 2) - a[1], (int)(f[2] >> 2) - a[2]);
 }
 
 __device__ __forceinline__ u64 reach_of(const u64 m, int slot) {
@@ -697,24 +924,18 @@ __device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, 
         nb = it.z;
         b0 = it.z;
         b1 = it.z + 1;
-        uint32_t lq;
         int qq;
-        const float4 v = C.spts[it.z];
-        dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lq, qq);
-        slot = cell_slot_of(g, lp, lq);
+        slot = point_slot_of(g, lp, C.spts[it.z], qq);
     }
     const int a0 = (int)__ldg(C.cstart + cp), a1 = (int)__ldg(C.cstart + cp + 1);
     for (int i = a0; i < a1; ++i) {
         const float4 pa = C.spts[i];
-        uint32_t l;
-        int qa;
-        dense_cell_of(pa.x, pa.y, pa.z, __float_as_int(pa.w), g, l, qa);
+        const int qa = q_of(pa.x, pa.y, pa.z, __float_as_int(pa.w), g);
         if (!((ma >> qa) & 1ull)) continue;
         const u64 reach = d_sc.U[slot][qa];
         for (int j = b0; j < b1; ++j) {
             const float4 pb = C.spts[j];
-            int qb;
-            dense_cell_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g, l, qb);
+            const int qb = q_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g);
             if (it.w >= 0 && !(((mb & reach) >> qb) & 1ull)) continue;
             if (pred(pa, pb, t2)) {
                 uf_unite(C.parent, na, nb);
@@ -740,174 +961,218 @@ __device__ __forceinline__ bool queue_item(const DenseCtx& C, int4 it) {
     return true;
 }
 
-// ---- dense records: components of the fine occupancy, node init, in-cell uncertain pairs --
-__global__ void __launch_bounds__(256) k_dcomps(Grid g, const u64* __restrict__ cocc, const u64* __restrict__ ccoord,
-                                               int* __restrict__ ncomp,
-                                               int* __restrict__ size, int* __restrict__ minidx,
-                                               u64* __restrict__ dcoord, uint32_t* __restrict__ oflags, DenseCtx C) {
+// ---- dense records: components of the fine occupancy, node init, and the link items --------
+// Thread per dense record: its certain-connected components (at most 8 union-find nodes), then
+// its 26 neighbour cells (13 bitmap lookups in flight at a time) give the record's items for
+// k_dense_link: every forward dense neighbour ("DD" list) and every sparse neighbour in either
+// direction, plus slot 26 = its own component pairs when it has several ("DS" list).  Absent
+// and backward-dense neighbours produce nothing, so the link kernel's threads all have work.
+// Items are block-aggregated (one atomic per list per block) into two halves of `litems`; if a
+// half overflows, meta->list_overflow makes k_dense_link_all redo every (record, slot).
+__global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                               int* __restrict__ crec,
+                                               const u64* __restrict__ cocc, const u64* __restrict__ ccoord,
+                                               int* __restrict__ ncomp, int* __restrict__ size,
+                                               int* __restrict__ minidx, u64* __restrict__ dcoord,
+                                               uint32_t* __restrict__ oflags, DenseCtx C, uint4* __restrict__ litems,
+                                               int lhalf, const int* __restrict__ cmin, const int* __restrict__ sidx,
+                                               int node_stats) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
+    // node-level statistics of single-component records come from their cell: the count is
+    // the cell's size and the minimum input index was taken while counting (counting path;
+    // the key path's stable sort puts it first in the cell)
+    const bool nstats = node_stats && 4 * (int64_t)C.meta->cells <= (int64_t)C.nbase;
+    __shared__ signed char soff[26][3];
+    __shared__ int wsum[256 / kWarp][2];
+    __shared__ int bbase[2];
+    if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nd = C.meta->ndense;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
-        const int cid = __ldg(C.dlist + r);
-        const u64 occ = __ldg(cocc + cid);
-        dcoord[r] = __ldg(ccoord + cid);
-        oflags[r] = 0u;
-        u64 comp[kMaxComp];
-        u64 rest;
-        const int k = sc_components(occ, comp, rest);
-        if (rest) atomicOr(&C.meta->internal_error, 1);  // impossible by the 8-component bound
-        ncomp[r] = k;
+    for (int r0 = blockIdx.x * blockDim.x; r0 < nd; r0 += gridDim.x * blockDim.x) {  // block-uniform
+        const int r = r0 + threadIdx.x;
+        const bool v = r < nd;
+        int kp = 0, cid = 0;
+        int c[3] = {0, 0, 0};
+        if (v) {
+            cid = __ldg(C.dlist + r);
+            const u64 occ = __ldg(cocc + cid);
+            const u64 pc = __ldg(ccoord + cid);
+            dcoord[r] = pc;
+            c[0] = (int)(pc & 0x1fffff);
+            c[1] = (int)((pc >> 21) & 0x1fffff);
+            c[2] = (int)(pc >> 42);
+            oflags[r] = 0u;
+            u64 comp[kMaxComp];
+            u64 rest;
+            kp = sc_components(occ, comp, rest);
+            if (rest) atomicOr(&C.meta->internal_error, 1);  // impossible by the 8-component bound
+            ncomp[r] = kp;
+            crec[cid] = (r << 3) | (kp - 1);  // the cell's record word (k_dscatter, k_dense_link)
 #pragma unroll
-        for (int j = 0; j < kMaxComp; ++j) {
-            const int node = C.nbase + 8 * r + j;
-            C.parent[node] = node;
-            size[node] = 0;
-            minidx[node] = 0x7fffffff;
-            C.cmask[8 * r + j] = j < k ? comp[j] : 0ull;
-        }
-    }
-}
-
-// Node-level statistics (single-GPU tail of clouds with few sparse cells):
-// points of dense cells add their count and minimum input index to their component node's own
-// accumulators while parents are assigned; k_node_stats later moves each node's totals to its
-// root, so the tail never walks the dense points.  Warp-aggregated: one atomic per distinct
-// node among the warp's points of this round (key < 0 = not a dense point).
-__device__ __forceinline__ void node_accumulate(int key, int si, int* __restrict__ size, int* __restrict__ minidx) {
-    const int lane = threadIdx.x & 31;
-    const bool ok = key >= 0;
-    unsigned todo = __ballot_sync(0xffffffffu, ok);
-    while (todo) {
-        const int leader = __ffs(todo) - 1;
-        const int k = __shfl_sync(0xffffffffu, key, leader);
-        const bool mem = ok && key == k;
-        const unsigned peers = __ballot_sync(0xffffffffu, mem);
-        const int mn = __reduce_min_sync(0xffffffffu, mem ? si : 0x7fffffff);
-        if (lane == leader) {
-            atomicAdd(size + k, __popc(peers));
-            atomicMin(minidx + k, mn);
-        }
-        todo &= ~peers;
-    }
-}
-
-// Sorted-order initialisation (coalesced): points of sparse cells are their own parents,
-// points of dense cells hang under their component's node; accumulators; input index.
-__global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, int64_t n, Grid g,
-                                              const uint2* __restrict__ cw, const uint32_t* __restrict__ cstart,
-                                              const int* __restrict__ crec, const int* __restrict__ ncomp,
-                                              const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
-                                              int* __restrict__ size, int* __restrict__ minidx,
-                                              int* __restrict__ sidx, const Meta* __restrict__ meta, int node_stats) {
-    pdl_prologue();
-    const int64_t groups = (n + 3) / 4;
-    const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;  // warp-uniform
-    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b4 = 4 * gi;
-        float4 v[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = b4 + j < n ? __ldg(spts + b4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-        int par[4], si[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            par[j] = (int)(b4 + j);
-            si[j] = __float_as_int(v[j].w);
-            if (b4 + j >= n) continue;
-            uint32_t lin;
-            int q;
-            dense_cell_of(v[j].x, v[j].y, v[j].z, __float_as_int(v[j].w), g, lin, q);
-            const uint32_t cid = cid_of(cw, lin);
-            if (__ldg(cstart + cid + 1) - __ldg(cstart + cid) > (uint32_t)SPARSE_MAX) {
-                const int r = __ldg(crec + cid);
-                const int k = __ldg(ncomp + r);
-                int c = 0;
-                if (k > 1)
-                    while (c < k - 1 && !((__ldg(cmask + 8 * r + c) >> q) & 1ull)) ++c;
-                par[j] = nbase + 8 * r + c;
+            for (int j = 0; j < kMaxComp; ++j) {
+                const int node = C.nbase + 8 * r + j;
+                C.parent[node] = node;
+                size[node] = 0;
+                minidx[node] = 0x7fffffff;
+                C.cmask[8 * r + j] = j < kp ? comp[j] : 0ull;
+            }
+            if (kp == 1 && nstats) {
+                const int a0 = (int)__ldg(C.cstart + cid);
+                size[C.nbase + 8 * r] = (int)__ldg(C.cstart + cid + 1) - a0;
+                minidx[C.nbase + 8 * r] = g.key_sort ? __ldg(sidx + a0) : __ldg(cmin + cid);
             }
         }
-        // accumulators of the possible root points (points of sparse cells); points of dense
-        // cells hang under component nodes and never become roots
+        // neighbour slots that need work
+        uint32_t mdd = 0u, mds = 0u;
+#pragma unroll 1
+        for (int k0 = 0; k0 < 26; k0 += 13) {
+            int cq[13];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (b4 + j < n && par[j] == (int)(b4 + j)) {
-                size[b4 + j] = 0;
-                minidx[b4 + j] = 0x7fffffff;
+            for (int j = 0; j < 13; ++j) {
+                uint32_t lq;
+                cq[j] = (v && dense_neighbor(g, c, soff[k0 + j][0], soff[k0 + j][1], soff[k0 + j][2], lq))
+                            ? cid_lookup(cw, lq) : -1;
             }
-        if (nstats) {
-            // the thread's 4 consecutive positions mostly share one node: runs first, then the
-            // first run of every lane aggregated over the warp by a labelled partition
-            int key0 = -1, cnt0 = 0, min0 = 0x7fffffff;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int key = b4 + j < n && par[j] >= nbase ? par[j] : -1;
-                if (key < 0) continue;
-                if (key0 < 0 || key == key0) {
-                    key0 = key;
-                    ++cnt0;
-                    min0 = min(min0, si[j]);
-                } else {  // a second node inside the thread's 4 points (cell or component edge)
-                    atomicAdd(size + key, 1);
-                    atomicMin(minidx + key, si[j]);
+            for (int j = 0; j < 13; ++j) {
+                if (cq[j] < 0) continue;
+                const uint32_t cnt = __ldg(C.cstart + cq[j] + 1) - __ldg(C.cstart + cq[j]);
+                if (cnt <= (uint32_t)SPARSE_MAX) mds |= 1u << (k0 + j);
+                else if (k0 + j < 13) mdd |= 1u << (k0 + j);
+            }
+        }
+        if (v && kp > 1) mds |= 1u << 26;
+        // block-aggregated reservation in the two lists
+        const int cdd = __popc(mdd), cds = __popc(mds);
+        int xdd = cdd, xds = cds;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ydd = __shfl_up_sync(0xffffffffu, xdd, o), yds = __shfl_up_sync(0xffffffffu, xds, o);
+            if (lane >= o) {
+                xdd += ydd;
+                xds += yds;
+            }
+        }
+        if (lane == 31) {
+            wsum[w][0] = xdd;
+            wsum[w][1] = xds;
+        }
+        __syncthreads();
+        if (threadIdx.x < 2) {
+            int tot = 0;
+            for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) {
+                const int t = wsum[ww][threadIdx.x];
+                wsum[ww][threadIdx.x] = tot;
+                tot += t;
+            }
+            bbase[threadIdx.x] = tot ? atomicAdd(threadIdx.x == 0 ? &C.meta->ndd : &C.meta->nds, tot) : 0;
+            if (tot && bbase[threadIdx.x] + tot > lhalf) atomicOr(&C.meta->list_overflow, 1);
+        }
+        __syncthreads();
+        int pdd = bbase[0] + wsum[w][0] + xdd - cdd, pds = bbase[1] + wsum[w][1] + xds - cds;
+        if (pdd + cdd <= lhalf && pds + cds <= lhalf) {
+            uint32_t m = mdd;
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                uint32_t lq;
+                dense_neighbor(g, c, soff[k][0], soff[k][1], soff[k][2], lq);
+                litems[pdd++] = make_uint4((uint32_t)r, (uint32_t)k, (uint32_t)cid_of(cw, lq), 0u);
+            }
+            m = mds;
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                uint32_t cq = 0u;
+                if (k < 26) {
+                    uint32_t lq;
+                    dense_neighbor(g, c, soff[k][0], soff[k][1], soff[k][2], lq);
+                    cq = cid_of(cw, lq);
                 }
-            }
-            // lanes past the end left the grid-stride loop: aggregate over the ones still here
-            const unsigned peers = __match_any_sync(__activemask(), key0);
-            const int tot = __reduce_add_sync(peers, cnt0);
-            const int mn = __reduce_min_sync(peers, min0);
-            if (key0 >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) {
-                atomicAdd(size + key0, tot);
-                atomicMin(minidx + key0, mn);
+                litems[lhalf + pds++] = make_uint4((uint32_t)r, (uint32_t)k, cq, 0u);
             }
         }
-        if (b4 + 4 <= n) {
-            *reinterpret_cast<int4*>(parent + b4) = make_int4(par[0], par[1], par[2], par[3]);
-            *reinterpret_cast<int4*>(sidx + b4) = make_int4(si[0], si[1], si[2], si[3]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (b4 + j < n) {
-                    parent[b4 + j] = par[j];
-                    sidx[b4 + j] = si[j];
-                }
-        }
+        __syncthreads();  // wsum / bbase are reused
     }
 }
 
-// Key-sort path: points of dense cells hang under their component nodes (warp per dense
-// record; the cell's points are contiguous).  k_sgather made every point its own parent.
+// Warp per dense record (the cell's points are contiguous in sorted order).  Key path: every
+// point of the cell hangs under its component's node (coalesced parent writes; k_sgather made
+// every point its own parent).  Both paths: records with several components get their nodes'
+// counts and minimum input indices (reduced in registers and stored once: the warp owns the
+// record's nodes); single-component records got theirs in k_dcomps, and on the counting path
+// k_dscatter already wrote the parents.
 __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts, const uint32_t* __restrict__ cstart,
                                                 const int* __restrict__ dlist, const int* __restrict__ ncomp,
-                                                const u64* __restrict__ cmask, Grid g, int nbase,
-                                                int* __restrict__ parent, const Meta* __restrict__ meta,
+                                                const u64* __restrict__ cmask, const Grid* __restrict__ gp,
+                                                int nbase, int* __restrict__ parent, const Meta* __restrict__ meta,
                                                 const int* __restrict__ sidx, int* __restrict__ size,
                                                 int* __restrict__ minidx, int node_stats, int64_t n) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
     const int lane = threadIdx.x & 31;
     const int nd = meta->ndense;
     const bool nstats = node_stats && 4 * (int64_t)meta->cells <= n;
     const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nd; r += warps) {
+    // 32 records per warp iteration: the lanes read their records' component counts and the warp
+    // then walks only the records with work (counting path: those with several components)
+    for (int rb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; rb < nd; rb += warps * 32) {
+    const int kl = rb + lane < nd ? __ldg(ncomp + rb + lane) : 0;
+    unsigned todo = __ballot_sync(0xffffffffu, kl > 1 || (kl > 0 && g.key_sort));
+    while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int r = rb + j;
+        const int k = __shfl_sync(0xffffffffu, kl, j);
         const int cid = __ldg(dlist + r);
-        const int k = __ldg(ncomp + r);
         const int a0 = (int)__ldg(cstart + cid), a1 = (int)__ldg(cstart + cid + 1);
+        const int node0 = nbase + 8 * r;
+        if (k == 1) {  // key path, one component: every point under node 0 (stats: k_dcomps)
+            for (int s = a0 + lane; s < a1; s += 32) parent[s] = node0;
+            continue;
+        }
+        // several components: each point's component from its fine sub-cell; the warp owns the
+        // record's nodes, so their totals are reduced in registers and stored once (no atomics)
+        int accn[kMaxComp], accm[kMaxComp];
+#pragma unroll
+        for (int c = 0; c < kMaxComp; ++c) {
+            accn[c] = 0;
+            accm[c] = 0x7fffffff;
+        }
         for (int s0 = a0; s0 < a1; s0 += 32) {  // warp-uniform trip count
             const int s = s0 + lane;
-            int key = -1;
+            int cc = -1, v = 0x7fffffff;
             if (s < a1) {
-                int cc = 0;
-                if (k > 1) {
-                    const float4 v = __ldg(spts + s);
-                    uint32_t lin;
-                    int q;
-                    dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lin, q);
-                    while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
-                }
-                key = nbase + 8 * r + cc;
-                parent[s] = key;
+                const float4 pt = __ldg(spts + s);
+                const int q = q_of(pt.x, pt.y, pt.z, __float_as_int(pt.w), g);
+                cc = 0;
+                while (cc < k - 1 && !((__ldg(cmask + 8 * r + cc) >> q) & 1ull)) ++cc;
+                if (g.key_sort) parent[s] = node0 + cc;  // (counting path: k_dscatter wrote it)
+                v = __float_as_int(pt.w);
             }
-            if (nstats) node_accumulate(key, s < a1 ? __ldg(sidx + s) : 0x7fffffff, size, minidx);
+            if (nstats) {
+#pragma unroll
+                for (int c = 0; c < kMaxComp; ++c) {
+                    if (c >= k) break;
+                    const bool m = cc == c;
+                    accn[c] += __popc(__ballot_sync(0xffffffffu, m));
+                    accm[c] = min(accm[c], __reduce_min_sync(0xffffffffu, m ? v : 0x7fffffff));
+                }
+            }
         }
+        if (nstats && lane == 0) {
+#pragma unroll
+            for (int c = 0; c < kMaxComp; ++c) {
+                if (c >= k) break;
+                size[node0 + c] = accn[c];
+                minidx[node0 + c] = accm[c];
+            }
+        }
+    }
     }
 }
 
@@ -927,19 +1192,13 @@ __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts
 // `serial` (overflow path): such pairs are tested in place by this thread instead.
 // Slot order: 0-2 forward faces, 3-12 forward edges and corners, 13-25 backward, 26 = P's own
 // components.
-__constant__ signed char c_slot[26][3] = {
-    {1, 0, 0},   {0, 1, 0},   {0, 0, 1},                                         // forward faces
-    {-1, 1, 0},  {1, 1, 0},   {0, -1, 1}, {-1, 0, 1}, {1, 0, 1}, {0, 1, 1},      // forward edges
-    {-1, -1, 1}, {1, -1, 1},  {-1, 1, 1}, {1, 1, 1},                             // forward corners
-    {-1, 0, 0},  {0, -1, 0},  {0, 0, -1},                                        // backward ...
-    {1, -1, 0},  {-1, -1, 0}, {0, 1, -1}, {1, 0, -1}, {-1, 0, -1}, {0, -1, -1},
-    {1, 1, -1},  {-1, 1, -1}, {1, -1, -1}, {-1, -1, -1}};
 
+// The work of one (dense record r, neighbour slot k) item whose neighbour cell cq (compact id,
+// occupied) is already known; k == 26 is the record's own component pairs (cq unused).
 template <bool serial>
-__device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, const uint2* __restrict__ cw,
+__device__ __forceinline__ void dense_link_pair(int r, int k, int ox, int oy, int oz, int cq, const Grid& g,
                                                 const int* __restrict__ crec, const int* __restrict__ ncomp,
-                                                const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
-                                                const DenseCtx& C) {
+                                                uint32_t* __restrict__ oflags, const DenseCtx& C) {
     const int kp = __ldg(ncomp + r);
     const u64* mp = C.cmask + 8 * r;
     bool overflow = false;
@@ -953,18 +1212,12 @@ __device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, con
                 else overflow |= !queue_item(C, make_int4(r, i, r, j));
             }
     } else {
-        const u64 pc = __ldg(dcoord + r);
-        const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
-        const int ox = c_slot[k][0], oy = c_slot[k][1], oz = c_slot[k][2];
-        uint32_t lq;
-        const int cq = dense_neighbor(g, c, ox, oy, oz, lq) ? cid_lookup(cw, lq) : -1;
-        if (cq < 0) return;
         const int q0 = (int)__ldg(C.cstart + cq), q1 = (int)__ldg(C.cstart + cq + 1);
         const int slot = sc_slot(ox, oy, oz);
         if (q1 - q0 > SPARSE_MAX) {
             if (k >= 13) return;  // backward dense pairs belong to the other cell
-            const int rq = __ldg(crec + cq);
-            const int kq = __ldg(ncomp + rq);
+            const int cw_q = __ldg(crec + cq);  // record << 3 | (components - 1)
+            const int rq = cw_q >> 3, kq = (cw_q & 7) + 1;
             for (int x = 0; x < kp; ++x) {
                 const u64 mx = mp[x];
                 const u64 dc = sc_certain_across(d_sc, mx, slot);
@@ -986,9 +1239,7 @@ __device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, con
             const int opp = 26 - slot;
             for (int t = q0; t < q1; ++t) {
                 const float4 v = C.spts[t];
-                uint32_t l;
-                int qb;
-                dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, l, qb);
+                const int qb = q_of(v.x, v.y, v.z, __float_as_int(v.w), g);
                 const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
                 for (int x = 0; x < kp; ++x) {
                     const u64 mx = mp[x];
@@ -1006,25 +1257,87 @@ __device__ __forceinline__ void dense_link_item(int r, int k, const Grid& g, con
     if (overflow) atomicOr(oflags + r, 1u << k);
 }
 
-// Slots [k0, k0 + gridDim.y) of every record (blockIdx.y = slot: a warp shares its slot).
-// Launched for the face slots first, then the rest: by then most non-certain pairs of
-// edge/corner neighbours are already connected through faces and are not queued.
-__global__ void __launch_bounds__(256) k_dense_link(Grid g, const uint2* __restrict__ cw, const int* __restrict__ crec,
-                                                   const int* __restrict__ ncomp, const u64* __restrict__ dcoord,
-                                                   uint32_t* __restrict__ oflags, DenseCtx C, int k0) {
+// Overflow path: the same item with the neighbour looked up here.
+__device__ __forceinline__ void dense_link_serial(int r, int k, const Grid& g, const uint2* __restrict__ cw,
+                                                  const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                                  const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
+                                                  const DenseCtx& C) {
+    int ox = 0, oy = 0, oz = 0, cq = 0;
+    if (k != 26) {
+        const u64 pc = __ldg(dcoord + r);
+        const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
+        ox = c_slot[k][0];
+        oy = c_slot[k][1];
+        oz = c_slot[k][2];
+        uint32_t lq;
+        cq = dense_neighbor(g, c, ox, oy, oz, lq) ? cid_lookup(cw, lq) : -1;
+        if (cq < 0) return;
+    }
+    dense_link_pair<true>(r, k, ox, oy, oz, cq, g, crec, ncomp, oflags, C);
+}
+
+// a6+a7 for dense cells: one thread per listed item (k_dcomps), the forward dense pairs first,
+// then the sparse neighbours and own pairs.  Certain component pairs are united at once;
+// non-certain pairs within reach whose nodes are still apart are queued (k_dense_filter
+// re-checks them after every certain union).
+// `which`: 1 = the forward dense pairs only (they touch no point: this launch may run on a side
+// stream concurrently with the scatter of the points), 2 = the sparse neighbours and own pairs
+// only, 3 = both lists.
+__global__ void __launch_bounds__(256, 4) k_dense_link(const Grid* __restrict__ gp, const int* __restrict__ crec,
+                                                   const int* __restrict__ ncomp, uint32_t* __restrict__ oflags,
+                                                   DenseCtx C, const uint4* __restrict__ litems, int lhalf, int which) {
     pdl_prologue();
-    const int nd = C.meta->ndense;
-    const int k = k0 + blockIdx.y;
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x)
-        dense_link_item<false>(r, k, g, cw, crec, ncomp, dcoord, oflags, C);
+    FEC_LOAD_GRID(gp);
+    if (g.status || C.meta->list_overflow) return;
+    __shared__ signed char soff[26][3];
+    if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
+    __syncthreads();
+    const int ndd = (which & 1) ? min(C.meta->ndd, lhalf) : 0, nds = (which & 2) ? min(C.meta->nds, lhalf) : 0;
+    const int tot = ndd + nds;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+        const uint4 it = __ldg(litems + (i < ndd ? i : lhalf + (i - ndd)));
+        const int k = (int)it.y;
+        const int ox = k < 26 ? soff[k][0] : 0, oy = k < 26 ? soff[k][1] : 0, oz = k < 26 ? soff[k][2] : 0;
+        dense_link_pair<false>((int)it.x, k, ox, oy, oz, (int)it.z, g, crec, ncomp, oflags, C);
+    }
+}
+
+// Fallback when the item lists overflowed (never on the configs measured): every (record,
+// slot) is processed by its own thread, looking its neighbour up itself.  Unions are
+// idempotent and queued duplicates are filtered, so items already handled do no harm.
+__global__ void __launch_bounds__(256) k_dense_link_all(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                                       const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                                       const u64* __restrict__ dcoord,
+                                                       uint32_t* __restrict__ oflags, DenseCtx C) {
+    pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || !C.meta->list_overflow) return;
+    const int64_t total = 27 * (int64_t)C.meta->ndense;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(t / 27), k = (int)(t % 27);
+        int ox = 0, oy = 0, oz = 0, cq = 0;
+        if (k != 26) {
+            const u64 pc = __ldg(dcoord + r);
+            const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
+            ox = c_slot[k][0];
+            oy = c_slot[k][1];
+            oz = c_slot[k][2];
+            uint32_t lq;
+            cq = dense_neighbor(g, c, ox, oy, oz, lq) ? cid_lookup(cw, lq) : -1;
+            if (cq < 0) continue;
+        }
+        dense_link_pair<false>(r, k, ox, oy, oz, cq, g, crec, ncomp, oflags, C);
+    }
 }
 
 // Queue overflow: the marked slots' pairs are tested in place (one thread per record).
-__global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __restrict__ cw,
+__global__ void __launch_bounds__(256) k_dense_overflow(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                        const int* __restrict__ crec, const int* __restrict__ ncomp,
                                                        const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
                                                        DenseCtx C) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
     const int nd = C.meta->ndense;
     if (C.meta->nitems <= C.item_cap) return;  // nothing overflowed
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
@@ -1032,7 +1345,7 @@ __global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __r
         while (f) {
             const int k = __ffs(f) - 1;
             f &= f - 1;
-            dense_link_item<true>(r, k, g, cw, crec, ncomp, dcoord, oflags, C);
+            dense_link_serial(r, k, g, cw, crec, ncomp, dcoord, oflags, C);
         }
     }
 }
@@ -1044,9 +1357,10 @@ __global__ void __launch_bounds__(256) k_dense_overflow(Grid g, const uint2* __r
 constexpr int kSliceWork = 4096;   // cell-size product per slice
 constexpr int kMaxSlices = 128;
 
-__global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* __restrict__ items2,
+__global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restrict__ items2,
                                                      int4* __restrict__ slices2, int* __restrict__ idone) {
     pdl_prologue();
+    if (C.meta->status) return;
     const int ni = min(C.meta->nitems, C.item_cap);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
         const int4 it = C.items[e];  // queued before every certain union was done: re-check
@@ -1078,6 +1392,7 @@ __global__ void __launch_bounds__(256) k_dense_filter(Grid g, DenseCtx C, int4* 
 // Component nodes -> their roots (shortens the finds of the uncertain pass).
 __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;
     const int64_t nn = 8 * (int64_t)meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
         const int s = nbase + (int)t;
@@ -1093,9 +1408,12 @@ __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent,
 // batches); B's points stream through the warp 32 at a time and are broadcast by shuffle.
 constexpr int kAPer = 4;
 
-__global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const int4* __restrict__ items2,
+__global__ void __launch_bounds__(256) k_dense_items(const Grid* __restrict__ gp, DenseCtx C,
+                                                    const int4* __restrict__ items2,
                                                     const int4* __restrict__ slices2, int* __restrict__ idone) {
     pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status) return;
     __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
     float4* abuf = abuf_all[threadIdx.x >> 5];
@@ -1133,11 +1451,8 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
         } else {
             b0 = it.z;
             b1 = it.z + 1;
-            const float4 v = C.spts[it.z];
-            uint32_t lq;
             int qb;
-            dense_cell_of(v.x, v.y, v.z, __float_as_int(v.w), g, lq, qb);
-            slot = cell_slot_of(g, lp, lq);
+            slot = point_slot_of(g, lp, C.spts[it.z], qb);
             fb = ~0ull;
             fa = d_sc.U[26 - slot][qb] & ma;
         }
@@ -1158,9 +1473,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
                 float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (i < a1) {
                     p = C.spts[i];
-                    uint32_t l;
-                    int qa;
-                    dense_cell_of(p.x, p.y, p.z, __float_as_int(p.w), g, l, qa);
+                    const int qa = q_of(p.x, p.y, p.z, __float_as_int(p.w), g);
                     v = (fa >> qa) & 1ull;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, v);
@@ -1184,9 +1497,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
                 bool vb = false;
                 if (j < b1) {
                     pb = C.spts[j];
-                    uint32_t l;
-                    int qb;
-                    dense_cell_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g, l, qb);
+                    const int qb = q_of(pb.x, pb.y, pb.z, __float_as_int(pb.w), g);
                     vb = (fb >> qb) & 1ull;
                 }
                 unsigned mb = __ballot_sync(0xffffffffu, vb);
@@ -1223,6 +1534,7 @@ __global__ void __launch_bounds__(256) k_dense_items(Grid g, DenseCtx C, const i
 __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ ncomp, const int* __restrict__ dlist,
                                                     const uint32_t* __restrict__ cstart, DenseCtx C) {
     pdl_prologue();
+    if (C.meta->status) return;
     const int nd = C.meta->ndense;
     unsigned long long roots = 0, pts = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
@@ -1254,8 +1566,8 @@ constexpr int SP_CHUNK = 32;
 __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spts, const uint2* __restrict__ cw,
                                                   const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
                                                   const Grid& g, int* __restrict__ parent, Meta* __restrict__ meta,
-                                                  int64_t n) {
-    if (4 * (int64_t)meta->cells <= n) return;
+                                                  int64_t n, int local_only) {
+    if (g.status || local_only || 4 * (int64_t)meta->cells <= n) return;
     const uint32_t cells = (uint32_t)meta->cells;  // occupied cells (compact ids)
     __shared__ uint32_t lists[256 / kWarp][SP_CHUNK];
     unsigned long long n_tests = 0;
@@ -1323,36 +1635,140 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     }
 }
 
-// LOCAL clouds: the sparse cells in one compact list, so every lane of the union kernel owns a
-// real sparse cell and all of them run in one wave.
-__global__ void __launch_bounds__(256) k_slist(const uint32_t* __restrict__ cstart, int* __restrict__ slist,
-                                              Meta* __restrict__ meta, int64_t n) {
+// LOCAL clouds (and small clouds): the sparse cells in one compact list, and the work items of
+// the sparse-sparse pairs: one per sparse cell with >= 2 points (its own pairs) and one per
+// (sparse cell, occupied sparse forward neighbour).  Thread per occupied cell; the 13 neighbour
+// lookups are issued together; items are block-aggregated (one atomic per block).  If the item
+// list would overflow, meta->sp_overflow hands the sparse cells to k_union_sparse_local.
+__global__ void __launch_bounds__(256) k_slist(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                              const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
+                                              int* __restrict__ slist, Meta* __restrict__ meta, int64_t n,
+                                              int local_only, uint2* __restrict__ sitems, int scap) {
     pdl_prologue();
-    if (4 * (int64_t)meta->cells > n) return;  // sparse-dominated: k_union_sparse walks the cells itself
+    FEC_LOAD_GRID(gp);
+    if (g.status || (!local_only && 4 * (int64_t)meta->cells > n)) return;  // sparse-dominated: k_union_sparse
+    __shared__ int wsum[256 / kWarp];
+    __shared__ int bbase;
     const int64_t U = meta->cells;
-    const int64_t ur = (U + 31) & ~int64_t(31);
-    const int lane = threadIdx.x & 31;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
-        bool sp = false;
-        if (u < U) {
-            const uint32_t c = __ldg(cstart + u + 1) - __ldg(cstart + u);
-            sp = c > 0 && c <= (uint32_t)SPARSE_MAX;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x; u0 < U; u0 += stride) {  // block-uniform
+        const int64_t u = u0 + threadIdx.x;
+        int np = 0;
+        if (u < U) np = (int)(__ldg(cstart + u + 1) - __ldg(cstart + u));
+        const bool sp = np > 0 && np <= SPARSE_MAX;
+        // the compact list (warp-aggregated)
+        {
+            const unsigned m = __ballot_sync(0xffffffffu, sp);
+            int base = 0;
+            if (m && lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, sp);
-        if (!m) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
+        // forward sparse neighbours
+        int cq[13];
+        uint32_t fm = 0u;
+        int c[3] = {0, 0, 0};
+        if (sp) {
+            const u64 pc = __ldg(ccoord + u);
+            c[0] = (int)(pc & 0x1fffff);
+            c[1] = (int)((pc >> 21) & 0x1fffff);
+            c[2] = (int)(pc >> 42);
+        }
+#pragma unroll
+        for (int k = 0; k < 13; ++k) {
+            uint32_t lq;
+            cq[k] = (sp && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], lq)) ? cid_lookup(cw, lq) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < 13; ++k)
+            if (cq[k] >= 0 && __ldg(cstart + cq[k] + 1) - __ldg(cstart + cq[k]) <= (uint32_t)SPARSE_MAX) fm |= 1u << k;
+        const int own = (sp && np >= 2) ? 1 : 0;
+        const int cnt = __popc(fm) + own;
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) {
+                const int t = wsum[ww];
+                wsum[ww] = tot;
+                tot += t;
+            }
+            bbase = tot ? atomicAdd(&meta->nspitems, tot) : 0;
+            if (tot && bbase + tot > scap) atomicOr(&meta->sp_overflow, 1);
+        }
+        __syncthreads();
+        int pos = bbase + wsum[w] + x - cnt;
+        if (pos + cnt <= scap) {
+            if (own) sitems[pos++] = make_uint2((uint32_t)u, (uint32_t)u);
+#pragma unroll
+            for (int k = 0; k < 13; ++k)
+                if ((fm >> k) & 1u) sitems[pos++] = make_uint2((uint32_t)u, (uint32_t)cq[k]);
+        }
+        __syncthreads();  // wsum / bbase are reused
     }
 }
 
-__global__ void __launch_bounds__(256) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
-                                                     const u64* __restrict__ ccoord,
-                                                     const uint32_t* __restrict__ cstart, Grid g,
-                                                     int* __restrict__ parent, Meta* __restrict__ meta, int64_t n) {
+// Sparse-sparse pairs, thread per item: (P, P) tests P's own pairs, (P, Q) every point pair of
+// P and its forward neighbour Q (<= 6 x 6), uniting the pred-true ones.
+__global__ void __launch_bounds__(256, 4) k_sparse_pairs(const float4* __restrict__ spts,
+                                                     const uint32_t* __restrict__ cstart, const Grid* __restrict__ gp,
+                                                     int* __restrict__ parent, Meta* __restrict__ meta, int64_t n,
+                                                     int local_only, const uint2* __restrict__ sitems, int scap) {
     pdl_prologue();
-    union_sparse_body(spts, cw, ccoord, cstart, g, parent, meta, n);
+    FEC_LOAD_GRID(gp);
+    if (g.status || meta->sp_overflow || (!local_only && 4 * (int64_t)meta->cells > n)) return;
+    const float t2 = g.t2;
+    const int ni = min(meta->nspitems, scap);
+    unsigned long long n_tests = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
+        const uint2 it = __ldg(sitems + i);
+        const int ps = (int)__ldg(cstart + it.x), pe = (int)__ldg(cstart + it.x + 1);
+        if (it.x == it.y) {
+            for (int s = ps; s < pe; ++s) {
+                const float4 a = __ldg(spts + s);
+                for (int t = s + 1; t < pe; ++t) {
+                    ++n_tests;
+                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
+                }
+            }
+        } else {
+            const int qs = (int)__ldg(cstart + it.y), qe = (int)__ldg(cstart + it.y + 1);
+            float4 b[SPARSE_MAX];
+#pragma unroll
+            for (int j = 0; j < SPARSE_MAX; ++j)
+                if (qs + j < qe) b[j] = __ldg(spts + qs + j);
+            for (int s = ps; s < pe; ++s) {
+                const float4 a = __ldg(spts + s);
+#pragma unroll
+                for (int j = 0; j < SPARSE_MAX; ++j) {
+                    if (qs + j >= qe) break;
+                    ++n_tests;
+                    if (pred(a, b[j], t2)) uf_unite(parent, s, qs + j);
+                }
+            }
+        }
+    }
+    if (meta->instrument) {
+        for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(__activemask(), n_tests, o);
+        if ((threadIdx.x & 31) == 0 && n_tests) atomicAdd(&meta->pair_tests, n_tests);
+    }
+}
+
+__global__ void __launch_bounds__(256, 8) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
+                                                     const u64* __restrict__ ccoord,
+                                                     const uint32_t* __restrict__ cstart, const Grid* __restrict__ gp,
+                                                     int* __restrict__ parent, Meta* __restrict__ meta, int64_t n,
+                                                     int local_only) {
+    pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    union_sparse_body(spts, cw, ccoord, cstart, g, parent, meta, n, local_only);
 }
 // Node-level tail (see node_accumulate): every used component node finds its root, is
 // flattened onto it, and adds its own totals to the root's; then the points of sparse cells
@@ -1375,11 +1791,14 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
                                                            const uint2* __restrict__ cw,
                                                            const u64* __restrict__ ccoord,
                                                            const uint32_t* __restrict__ cstart,
-                                                           const int* __restrict__ slist, Grid g,
+                                                           const int* __restrict__ slist,
+                                                           const Grid* __restrict__ gp,
                                                            int* __restrict__ parent, Meta* __restrict__ meta,
-                                                           int64_t n) {
+                                                           int64_t n, int local_only) {
     pdl_prologue();
-    if (4 * (int64_t)meta->cells > n) return;
+    FEC_LOAD_GRID(gp);
+    // the fallback of k_sparse_pairs: only when its item list overflowed
+    if (g.status || !meta->sp_overflow || (!local_only && 4 * (int64_t)meta->cells > n)) return;
     const uint32_t nitems = (uint32_t)meta->nsparse;
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
     const float t2 = g.t2;
@@ -1467,30 +1886,23 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
 
 namespace fec {
 
+// The device tables are a compile-time constant; this checks once, on the host, that the
+// bit-operation dilation used by the flood fill and the whole-mask shift lists agree with
+// the tables' certain relation (a failed check would be a build defect).
 cudaError_t ensure_subcell_tables() {
-    static std::mutex mu;
-    static bool done[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    std::lock_guard<std::mutex> lock(mu);
-    if (done[dev & 63]) return cudaSuccess;
-    static SubcellTables t;
-    sc_build_tables(t);
-    // the bit-operation dilation used by the flood fill must equal the table's certain
-    // relation inside a cell (slot 13); checked once on the host
-    for (int a = 0; a < 64; ++a)
-        if ((sc_dilate(1ull << a) | (1ull << a)) != (t.T[13][a] | (1ull << a))) return cudaErrorInvalidValue;
-    // so must the whole-mask shift lists across the 26 neighbour slots
-    for (int sl = 0; sl < 27; ++sl) {
-        if (sl == 13) continue;
-        if (t.nsh[sl] < 0) return cudaErrorInvalidValue;
+    static const bool ok = [] {
+        constexpr SubcellTables t = sc_make_tables();
         for (int a = 0; a < 64; ++a)
-            if (sc_certain_across(t, 1ull << a, sl) != t.T[sl][a]) return cudaErrorInvalidValue;
-    }
-    e = cudaMemcpyToSymbol(d_sc, &t, sizeof(t));
-    if (e == cudaSuccess) done[dev & 63] = true;
-    return e;
+            if ((sc_dilate(1ull << a) | (1ull << a)) != (t.T[13][a] | (1ull << a))) return false;
+        for (int sl = 0; sl < 27; ++sl) {
+            if (sl == 13) continue;
+            if (t.nsh[sl] < 0) return false;
+            for (int a = 0; a < 64; ++a)
+                if (sc_certain_across(t, 1ull << a, sl) != t.T[sl][a]) return false;
+        }
+        return true;
+    }();
+    return ok ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 }  // namespace fec

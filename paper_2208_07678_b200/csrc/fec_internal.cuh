@@ -69,22 +69,32 @@ __device__ __forceinline__ float d2_rn(float4 a, float4 b) {
 }
 __device__ __forceinline__ bool pred(float4 a, float4 b, float t2) { return d2_rn(a, b) <= t2; }
 
-// ---- grid geometry (host-computed once per call, passed by value) ---------------------
+// ---- grid geometry -----------------------------------------------------------------------
+// Computed on the DEVICE by the planning block of k_bbox (fec_kernels.cu) from the bbox, or
+// uploaded by the host (batch mode); every kernel of the path reads it from the workspace
+// (load_grid), so no host round trip sits between a1 and the rest of the pipeline.
 struct Grid {
     double lo[3];       // bbox minimum (fp32 values widened)
     double inv_h;       // 1/h (double): sub-cell coordinate = floor((x - lo) * inv_h)
     double h;           // sub-cell edge = c/2, c = d*(1+2^-16)
     double inv_q;       // 2*inv_h (exact): fine sub-cell coordinate = floor((x - lo) * inv_q), edge c/4
     int32_t dims[3];    // cells per axis
-    int32_t bits[3];    // ceil(log2(dims)) per axis (cell-level Morton bits, hash mode)
-    int32_t key_bits;   // 3 + sum(bits): significant bits of the sub-cell Morton key
-    int32_t dense;      // 1: dense cell grid (counting sort), 0: Morton radix sort + hash
-    uint32_t stride[3]; // dense mode: linear cell id = sum_a c[a]*stride[a] (smallest dim fastest)
-    int32_t perm[3];    // dense mode: axes from fastest to slowest
-    uint32_t sdiv[2];   // dense mode: stride[perm[2]], stride[perm[1]] (for decoding)
-    u64 hash_mask;
-    float t2;
-    // batch mode (dense grid only): clouds [boff[c], boff[c+1]) with origins blo[3c..3c+2]
+    int32_t hashed;     // 0: cell handle = linear cell id (occupancy bitmap over the grid)
+                        // 1: cell handle = slot of an open-addressing table of occupied cells
+    uint32_t stride[3]; // bitmap mode: linear cell id = sum_a c[a]*stride[a] (smallest dim fastest)
+    int32_t perm[3];    // bitmap mode: axes from fastest to slowest
+    uint32_t sdiv[2];   // bitmap mode: stride[perm[2]], stride[perm[1]] (for decoding)
+    uint32_t hmask;     // hash mode: slots - 1 (slots a power of two >= 2n)
+    float t2;           // fl32(d*d) (reading A3)
+    int32_t status;     // FEC_OK, or the error found by a1 (every later kernel returns at once)
+    int32_t key_sort;   // 1: the key-sort binning path runs, 0: the counting path
+    int32_t passes;     // key-sort path: 8-bit LSD passes over the linear cell ids
+    int32_t key_bits;   // significant bits of the linear cell id (bitmap mode)
+    int32_t pad0;
+    int64_t words;      // occupancy words: grid cells / 32 (bitmap) or slots / 32 (hash)
+    int64_t cells_total;
+    u64* hkey;          // hash mode: packed cell coordinates of each slot (~0 = empty)
+    // batch mode (fec_cluster_batch_ws): clouds [boff[c], boff[c+1]) with origins blo[3c..3c+2]
     // and z cell offsets bz[c] (device arrays); batch == 0 for a single cloud
     int32_t batch;
     int32_t nclouds;
@@ -93,30 +103,21 @@ struct Grid {
     const int32_t* bz;
 };
 
+// Every kernel stages the device-resident Grid in shared memory after its PDL wait (one
+// thread copies it; all threads then read fields with LDS, which costs no registers: a
+// register copy of the whole struct would live through every loop).  Must be reached by
+// all threads of the block (it synchronises).
+#define FEC_LOAD_GRID(gp)                                       \
+    __shared__ Grid fec_grid_sh_;                               \
+    if (threadIdx.x == 0) fec_grid_sh_ = *(gp);                 \
+    __syncthreads();                                            \
+    const Grid& g = fec_grid_sh_
+
 // Sub-cell coordinate on one axis: floor((x - lo) * inv_h).  Cell = sub >> 1 and the octant
 // bit = sub & 1, so cell and sub-cell always agree.  Monotone in x (DESIGN.md §4.2 shows
 // that pred-true pairs differ by <= 2 sub-cells and <= 1 cell on every axis).
 __device__ __forceinline__ uint32_t sub_coord(float x, double lo, double inv_h) {
     return (uint32_t)floor(__dmul_rn(__dadd_rn((double)x, -lo), inv_h));
-}
-
-// Generalised Morton interleave of cell coordinates with per-axis bit counts: level l takes
-// bit l of x, y, z (each only while l < bits[axis]).  Prefixed (low bits) by the octant.
-__device__ __forceinline__ u64 subcell_key(uint32_t sx, uint32_t sy, uint32_t sz, const Grid& g) {
-    u64 key = (u64)((sx & 1u) | ((sy & 1u) << 1) | ((sz & 1u) << 2));
-    uint32_t c[3] = {sx >> 1, sy >> 1, sz >> 1};
-    int pos = 3;
-    int maxb = max(g.bits[0], max(g.bits[1], g.bits[2]));
-    for (int l = 0; l < maxb; ++l) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            if (l < g.bits[a]) {
-                key |= (u64)((c[a] >> l) & 1u) << pos;
-                ++pos;
-            }
-        }
-    }
-    return key;
 }
 
 __device__ __forceinline__ u64 pack_cell(uint32_t cx, uint32_t cy, uint32_t cz) {
@@ -182,6 +183,11 @@ int exclusive_scan(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st);
 template <typename T>
 int exclusive_scan_dn(const T* in, T* out, int64_t n, const int* ndev, T* scratch, cudaStream_t st);
 size_t scan_scratch_elems(int64_t n);
+// single-pass scan on a look-back state zeroed earlier in the call (no memset node); does
+// nothing when *skip0 or *skip1 (optional device ints) is nonzero
+int exclusive_scan_lb(const uint32_t* in, uint32_t* out, int64_t n, const int* ndev, unsigned long long* state,
+                      unsigned int* counter, int max_blocks, const int* skip0, const int* skip1, cudaStream_t st);
+int64_t scan_lb_tiles(int64_t n);
 
 // ---- workspace carving -----------------------------------------------------------------
 struct Carver {

@@ -90,19 +90,25 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_add(T* __restrict__ out, in
 __global__ void __launch_bounds__(SC_THREADS) k_scan_lb(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                        int64_t n, const int* ndev,
                                                        unsigned long long* __restrict__ state,
-                                                       unsigned int* __restrict__ counter) {
+                                                       unsigned int* __restrict__ counter, const int* skip0,
+                                                       const int* skip1) {
     pdl_prologue();
+    if ((skip0 && *skip0) || (skip1 && *skip1)) return;  // device-side choice: this scan is not needed
     __shared__ uint32_t s[SC_TILE];
     __shared__ uint32_t wsum[SC_THREADS / kWarp];
     __shared__ unsigned int tile_sh;
     __shared__ uint32_t prefix_sh;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (ndev) n = min(n, (int64_t)*ndev);
+    // persistent blocks take tiles in order from the counter until past the end (every
+    // later tile is past the end too, so nobody looks back at those)
+    while (true) {
+    __syncthreads();
     if (tid == 0) tile_sh = atomicAdd(counter, 1u);
     __syncthreads();
     const unsigned tile = tile_sh;
-    if (ndev) n = min(n, (int64_t)*ndev);
     const int64_t base = (int64_t)tile * SC_TILE;
-    if (base >= n) return;  // every later tile is past the end too: nobody looks back at this one
+    if (base >= n) return;
 #pragma unroll
     for (int k = 0; k < SC_ITEMS; ++k) {
         int64_t i = base + k * SC_THREADS + tid;
@@ -170,6 +176,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_lb(const uint32_t* __restri
         int64_t i = base + k * SC_THREADS + tid;
         if (i < n) out[i] = s[k * SC_THREADS + tid];
     }
+    }  // tiles
 }
 
 size_t scan_scratch_elems(int64_t n) {
@@ -234,9 +241,22 @@ int exclusive_scan_dn<uint32_t>(const uint32_t* in, uint32_t* out, int64_t n, co
     unsigned int* counter = reinterpret_cast<unsigned int*>(scratch);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(scratch + 64);
     cudaMemsetAsync(scratch, 0, 256 + (size_t)nb * 8, st);
-    pdl(k_scan_lb, (unsigned)nb, SC_THREADS, 0, st)(in, out, n, ndev, state, counter);
+    pdl(k_scan_lb, (unsigned)nb, SC_THREADS, 0, st)(in, out, n, ndev, state, counter, nullptr, nullptr);
     return 2;
 }
+// Single-pass scan whose look-back state (nb x 8 B) and counter were zeroed earlier in the call
+// (k_zero): no memset node; a persistent grid of at most `max_blocks` blocks.
+// skip0 / skip1 (optional device ints): the scan does nothing when either is nonzero.
+int exclusive_scan_lb(const uint32_t* in, uint32_t* out, int64_t n, const int* ndev, unsigned long long* state,
+                      unsigned int* counter, int max_blocks, const int* skip0, const int* skip1, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const int64_t nb = (n + SC_TILE - 1) / SC_TILE;
+    const unsigned blocks = (unsigned)(nb < max_blocks ? nb : max_blocks);
+    pdl(k_scan_lb, blocks, SC_THREADS, 0, st)(in, out, n, ndev, state, counter, skip0, skip1);
+    return 1;
+}
+int64_t scan_lb_tiles(int64_t n) { return (n + SC_TILE - 1) / SC_TILE; }
+
 template <>
 int exclusive_scan<uint32_t>(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* scratch, cudaStream_t st) {
     return exclusive_scan_dn<uint32_t>(in, out, n, nullptr, scratch, st);

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256) k_slab_stats(const int* __restrict__ pare
                                                    int* __restrict__ minidx, int* __restrict__ ckey,
                                                    Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;  // a1 rejected the input
     __shared__ int hkey[SL_SLOTS], hcnt[SL_SLOTS], hmin[SL_SLOTS], hbk[SL_SLOTS];
     for (int k = threadIdx.x; k < SL_SLOTS; k += blockDim.x) {
         hkey[k] = -1;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(256) k_slab_pack(const int* __restrict__ paren
                                                   const int* __restrict__ minidx, const int* __restrict__ ckey,
                                                   int* __restrict__ rec, int rec_cap, const Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;  // header stays zero: no records
     int* P = rec + SLAB_HDR;
     int* Cr = rec + slab_c_off(rec_cap);
     const int64_t nodes = n + 8 * (int64_t)meta->ndense;
@@ -239,8 +241,10 @@ __global__ void __launch_bounds__(256) k_merge_resolve(const int* __restrict__ o
 __global__ void __launch_bounds__(256) k_slab_relabel(const int* __restrict__ parent, const int* __restrict__ val,
                                                      const int* __restrict__ size, const int* __restrict__ minidx,
                                                      int64_t n, int n_owned, long long min_size,
-                                                     long long max_size, int* __restrict__ labels) {
+                                                     long long max_size, int* __restrict__ labels,
+                                                     const Meta* __restrict__ meta) {
     pdl_prologue();
+    if (meta->status) return;  // the local step failed: labels_owned is left untouched
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         const int i = __ldg(val + s);
         if (i >= n_owned) continue;

@@ -20,6 +20,6 @@ __global__ void k_merge_stats(const int* all, int world, int64_t words, int rec_
 __global__ void k_merge_resolve(const int* own, int rec_cap, const int* hkey, unsigned mask, int* hpar,
                                 const int* gsize, const int* gmin, int* size, int* minidx);
 __global__ void k_slab_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
-                               int n_owned, long long min_size, long long max_size, int* labels);
+                               int n_owned, long long min_size, long long max_size, int* labels, const Meta* meta);
 
 }  // namespace fec

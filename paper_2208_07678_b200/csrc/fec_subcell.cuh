@@ -89,8 +89,9 @@ __host__ __device__ __forceinline__ u64s sc_certain_across(const SubcellTables& 
     return r;
 }
 
-// Host-side construction from the arithmetic definition above.
-inline void sc_build_tables(SubcellTables& t) {
+// Construction from the arithmetic definition above (constexpr: the device copy is a
+// compile-time constant, so no upload is needed and the first call may be graph-captured).
+constexpr void sc_build_tables(SubcellTables& t) {
     for (int s = 0; s < 27; ++s) {
         const int ox = s % 3 - 1, oy = (s / 3) % 3 - 1, oz = s / 9 - 1;
         t.F[s] = 0;
@@ -141,6 +142,12 @@ inline void sc_build_tables(SubcellTables& t) {
                     t.shm[s][k] = m;
                 }
     }
+}
+
+constexpr SubcellTables sc_make_tables() {
+    SubcellTables t{};
+    sc_build_tables(t);
+    return t;
 }
 
 }  // namespace fec

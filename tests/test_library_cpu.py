@@ -62,16 +62,38 @@ def _functions(sass):
     return funcs
 
 
+PRED_KERNELS = ("k_union_sparse", "k_union_sparse_local", "k_dense_items", "k_dense_overflow", "k_debug_pred")
+
+
 def test_predicate_kernels_have_no_fma(libpath):
+    """Reading A2: the predicate is fp32 multiplies and adds, each rounded.  Every kernel of
+    the clustering path is checked for FFMA/DFMA (the build uses -fmad=false; the ground-
+    removal kernels k_g_* use fused multiply-adds by reading G3, and the AP kernels k_ap_*
+    contain the correctly rounded fp64 division sequence, made of DFMA), and every kernel
+    that inlines the predicate must show the unfused FMUL + FADD."""
     funcs = _functions(_sass(libpath))
-    checked = 0
+    found = set()
     for name, body in funcs.items():
-        if "k_scan_union" in name or "k_debug_pred" in name:
-            text = "\n".join(body)
-            assert "FFMA" not in text, name
-            assert "FMUL" in text and "FADD" in text, name
-            checked += 1
-    assert checked == 2
+        text = "\n".join(body)
+        if "k_g_" not in name and "k_ap_" not in name:
+            # (HFMA2 with zero operands is the compiler's register move: not an FMA)
+            assert not re.search(r"\b(FFMA2?|DFMA)\b", text), name
+        for k in PRED_KERNELS:
+            if f"{len(k)}{k}E" in name:  # Itanium mangling: length-prefixed name, then the parameters
+                assert "FMUL" in text and "FADD" in text, name
+                found.add(k)
+    assert found == set(PRED_KERNELS), found
+
+
+def test_node_id_guard(libpath):
+    """Union-find node ids are n + 8 * (dense cells) in int32: n beyond the bound is rejected on
+    the host (and its workspace size is 0), before any CUDA call."""
+    L = fec.lib()
+    kmax = (2**31 - 1) // 8 * 7 - 1024
+    assert fec.workspace_bytes(kmax + 1) == 0 and fec.workspace_bytes(kmax) > 0
+    assert L.fec_cluster_ws(None, kmax + 1, 1.0, 1, 4, None, None, 0, None) == fec.ERR_INVALID_ARGUMENT
+    assert b"node ids" in L.fec_last_error()
+    assert L.fec_cluster_async(None, kmax + 1, 1.0, 1, 4, None, None, None) == fec.ERR_INVALID_ARGUMENT
 
 
 def test_workspace_bytes_monotone_and_zero_for_empty(libpath):
