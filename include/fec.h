@@ -46,7 +46,7 @@ extern "C" {
 typedef int32_t fec_status_t;
 
 #define FEC_OK 0
-#define FEC_ERR_INVALID_ARGUMENT (-1) /* n<0 or n>INT32_MAX; d_th not finite > 0 or t2 not a
+#define FEC_ERR_INVALID_ARGUMENT (-1) /* n<0 or n>fec_max_points(); d_th not finite > 0 or t2 not a
                                          finite normal fp32 (reading A13); min>max;
                                          max<1; min<0; null/host pointer where a device
                                          pointer is required; workspace too small */
@@ -249,12 +249,59 @@ fec_status_t fec_slab_merge(const int32_t* all_records, int32_t world, int32_t r
                             int64_t max_size, int32_t* labels_owned, void* workspace, size_t workspace_bytes,
                             const fec_slab_state_t* state, void* stream);
 
+/* ---- Multi-GPU Mode B: index-sharded input -> spatial slabs, on the device
+ *
+ * When each rank starts with an arbitrary shard of the cloud (e.g. an index range) instead of
+ * its slab, the slab decomposition of the path above is computed from device data: the same
+ * rule as the host planner (paper_2208_07678_b200/dist.py plan_slabs): the cut axis is the
+ * longest extent of the global bbox (ties: lowest axis), cell layers along it have edge
+ * c = d_th*(1+2^-16) (reading A6) and are cut into `world` count-balanced slabs.  Per rank, on
+ * `stream`, with one workspace of fec_part_workspace_bytes() bytes kept across the steps:
+ *   1. fec_part_bbox   shard bbox -> bbox_out (device float[8]: min xyz, -max xyz, -nonfinite,
+ *                      0); also zeroes `hist`.  Caller: all-reduce MIN of the 8 floats.
+ *   2. fec_part_hist   histogram of the shard's layers -> hist (device int32[fec_part_max_layers()]).
+ *                      Caller: all-reduce SUM.
+ *   3. fec_part_plan   the cuts -> plan (device int64[4*world + 3]: cuts[world+1], owned[world],
+ *                      first[world], halo[world], rec_cap, status); identical on every rank.
+ *                      status = FEC_ERR_NONFINITE / FEC_ERR_GRID_RANGE if the cloud cannot be cut.
+ *   4. fec_part_pack   with send_pts == NULL: counts[world] (device int64) of the points each rank
+ *                      receives (its owned points, plus the first cell layer of the next slab as
+ *                      its halo); then with the send buffers (sum(counts) points): the points and
+ *                      gidx packed by destination rank.  Caller: all-to-all of counts, then of the
+ *                      points and gidx.
+ *   5. fec_part_order  the received points in the local order of fec_slab_local (first-layer
+ *                      owned | other owned | halo); counts3 (device int64[3]) gives n_first =
+ *                      counts3[0], n_owned = counts3[0] + counts3[1].
+ * Then fec_slab_local / all-gather / fec_slab_merge with rec_cap = plan[4*world + 1].
+ * Device pointers throughout; nothing synchronises the host (the caller reads counts and the
+ * plan for the collectives' sizes). */
+size_t fec_part_workspace_bytes(void);
+int32_t fec_part_max_layers(void);
+fec_status_t fec_part_bbox(const float* points, int64_t m, float* bbox_out, int32_t* hist, void* workspace,
+                           size_t workspace_bytes, void* stream);
+fec_status_t fec_part_hist(const float* points, int64_t m, const float* gbbox, float d_th, int32_t* hist,
+                           void* workspace, size_t workspace_bytes, void* stream);
+fec_status_t fec_part_plan(const int32_t* ghist, int32_t world, int64_t* plan_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+fec_status_t fec_part_pack(const float* points, const int32_t* gidx, int64_t m, const float* gbbox, float d_th,
+                           const int64_t* plan, int32_t world, int64_t* counts, float* send_pts,
+                           int32_t* send_gidx, void* workspace, size_t workspace_bytes, void* stream);
+fec_status_t fec_part_order(const float* recv_pts, const int32_t* recv_gidx, int64_t k, const float* gbbox,
+                            float d_th, const int64_t* plan, int32_t world, int32_t rank, int64_t* counts3,
+                            float* out_pts, int32_t* out_gidx, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* Human-readable status text (static storage) and the last error detail of this thread. */
 const char* fec_status_string(fec_status_t status);
 const char* fec_last_error(void);
 
-/* Library version string, e.g. "fec-b200 0.1 sm_100a". */
+/* Library version string, e.g. "fec-b200 0.2 sm_100a". */
 const char* fec_version(void);
+
+/* The largest n the library accepts: union-find node ids (n points + 8 per dense-record slot,
+ * record capacity rounded up to a power of two) must fit in int32.  Larger n is rejected with
+ * FEC_ERR_INVALID_ARGUMENT before any launch. */
+int64_t fec_max_points(void);
 
 /* Diagnostic: evaluate the device predicate on m point pairs (a[k], b[k]), each [m][3]
  * fp32 device arrays; out[k] = pred (uint8 0/1), d2_out[k] = the fp32 squared distance

@@ -27,13 +27,15 @@ OK, ERR_INVALID_ARGUMENT, ERR_NONFINITE, ERR_GRID_RANGE, ERR_OUT_OF_MEMORY, ERR_
 
 # every symbol include/fec.h, include/fec_ground.h and include/fec_metrics.h declare
 EXPORTS = ("fec_workspace_bytes", "fec_cluster_ws", "fec_cluster", "fec_cluster_async", "fec_cluster_ws_async",
-           "fec_debug_alloc_extra", "fec_workspace_bytes_host",
+           "fec_debug_alloc_extra", "fec_max_points", "fec_workspace_bytes_host",
            "fec_cluster_host", "fec_cluster_host_async", "fec_get_stats", "fec_set_instrumentation", "fec_status_string",
            "fec_last_error", "fec_version", "fec_debug_pred", "fec_set_timing",
            "fec_get_stage_times", "fec_stage_name", "fec_set_grid_mode", "fec_slab_record_words",
            "fec_slab_workspace_bytes", "fec_slab_local", "fec_slab_merge", "fec_set_item_cap",
            "fec_debug_subcell_tables", "fec_debug_subcell_dilate", "fec_debug_subcell_components",
            "fec_batch_workspace_bytes", "fec_cluster_batch_ws",
+           "fec_part_workspace_bytes", "fec_part_max_layers", "fec_part_bbox", "fec_part_hist", "fec_part_plan",
+           "fec_part_pack", "fec_part_order",
            # include/fec_ground.h
            "fec_ground_workspace_bytes", "fec_ground_remove", "fec_ground_expand_labels", "fec_ground_count_ms",
            # include/fec_metrics.h
@@ -98,6 +100,8 @@ def lib():
         L.fec_cluster_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, vp]
         L.fec_cluster_ws_async.restype = ctypes.c_int32
         L.fec_cluster_ws_async.argtypes = [vp, i64, f32, i64, i64, vp, vp, sz, vp, vp]
+        L.fec_max_points.restype = i64
+        L.fec_max_points.argtypes = []
         L.fec_debug_alloc_extra.restype = None
         L.fec_debug_alloc_extra.argtypes = [sz]
         L.fec_cluster_host.restype = ctypes.c_int32
@@ -141,6 +145,20 @@ def lib():
         L.fec_slab_workspace_bytes.argtypes = [i64, ctypes.c_int32, i64]
         L.fec_slab_local.restype = ctypes.c_int32
         L.fec_slab_local.argtypes = [vp, vp, i64, i64, i64, f32, vp, i64, vp, sz, ctypes.POINTER(SlabState), vp, vp]
+        L.fec_part_workspace_bytes.restype = sz
+        L.fec_part_workspace_bytes.argtypes = []
+        L.fec_part_max_layers.restype = ctypes.c_int32
+        L.fec_part_max_layers.argtypes = []
+        L.fec_part_bbox.restype = ctypes.c_int32
+        L.fec_part_bbox.argtypes = [vp, i64, vp, vp, vp, sz, vp]
+        L.fec_part_hist.restype = ctypes.c_int32
+        L.fec_part_hist.argtypes = [vp, i64, vp, f32, vp, vp, sz, vp]
+        L.fec_part_plan.restype = ctypes.c_int32
+        L.fec_part_plan.argtypes = [vp, ctypes.c_int32, vp, vp, sz, vp]
+        L.fec_part_pack.restype = ctypes.c_int32
+        L.fec_part_pack.argtypes = [vp, vp, i64, vp, f32, vp, ctypes.c_int32, vp, vp, vp, vp, sz, vp]
+        L.fec_part_order.restype = ctypes.c_int32
+        L.fec_part_order.argtypes = [vp, vp, i64, vp, f32, vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp, vp, sz, vp]
         L.fec_slab_merge.restype = ctypes.c_int32
         L.fec_slab_merge.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, i64, i64, vp, vp, sz,
                                      ctypes.POINTER(SlabState), vp]

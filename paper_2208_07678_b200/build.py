@@ -13,8 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfec.so")
-SOURCES = ["fec_capi.cu", "fec_kernels.cu", "fec_dense.cu", "fec_sort.cu", "fec_scan_prim.cu", "fec_slab.cu", "fec_ground.cu", "fec_metrics.cu"]
-HEADERS = ["fec_internal.cuh", "fec_kernels.cuh", "fec_slab.cuh", "fec_subcell.cuh"]
+SOURCES = ["fec_capi.cu", "fec_kernels.cu", "fec_dense.cu", "fec_sort.cu", "fec_scan_prim.cu", "fec_slab.cu", "fec_part.cu", "fec_ground.cu", "fec_metrics.cu"]
+HEADERS = ["fec_internal.cuh", "fec_kernels.cuh", "fec_slab.cuh", "fec_subcell.cuh", "fec_part.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [

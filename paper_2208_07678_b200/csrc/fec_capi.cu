@@ -10,6 +10,7 @@
 #include "fec.h"
 #include "fec_kernels.cuh"
 #include "fec_slab.cuh"
+#include "fec_part.cuh"
 
 using namespace fec;
 
@@ -128,9 +129,25 @@ DevInfo dev_info() {
 }
 
 // bitmap mode needs 1/4 B per grid cell (occupancy bits + word bases)
-int64_t dense_cap(int64_t n) { return 32 * n + (int64_t(1) << 26); }
-int64_t dense_max(int64_t n) { return n / (SPARSE_MAX + 1) + 16; }
-int64_t nodes_max(int64_t n) { return n + 8 * dense_max(n); }
+constexpr int64_t dense_cap(int64_t n) { return 32 * n + (int64_t(1) << 26); }
+constexpr int64_t dense_max(int64_t n) { return n / (SPARSE_MAX + 1) + 16; }
+// dense-record capacity rounded to a power of two (the node-id permutation, node_of)
+constexpr int64_t rec_pow2(int64_t n) {
+    int64_t r = 1;
+    while (r < dense_max(n)) r <<= 1;
+    return r;
+}
+constexpr int64_t nodes_max(int64_t n) { return n + 8 * rec_pow2(n); }
+// the largest n whose node ids (nodes_max) fit in int32 (node_of, union-find)
+constexpr int64_t max_points() {
+    int64_t lo = 0, hi = INT32_MAX;
+    while (hi - lo > 1) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (nodes_max(mid) < (int64_t)INT32_MAX) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
 int64_t hash_slots(int64_t n) {  // hash mode: a power of two >= 2n (load factor <= 1/2)
     int64_t c = 1024;
     while (c < 2 * n) c <<= 1;
@@ -267,11 +284,12 @@ int ceil_log2(int64_t v) {
     return b;
 }
 
-// Largest n whose union-find node ids (n points + 8 per possible dense cell) fit in int32.
-constexpr int64_t kMaxN = (int64_t)INT32_MAX / 8 * 7 - 1024;
+// Bound on n: the node ids (n points + 8 per record slot of a power-of-two record capacity)
+// must fit in int32.
+constexpr int64_t kMaxN = max_points();
 
 fec_status_t check_args(int64_t n, float d, int64_t mn, int64_t mx, float* t2_out) {
-    if (n < 0 || n > kMaxN || (n > 0 && nodes_max(n) >= (int64_t)INT32_MAX)) {
+    if (n < 0 || n > kMaxN) {
         g_err = "n out of range [0, " + std::to_string(kMaxN) + "] (int32 union-find node ids)";
         return FEC_ERR_INVALID_ARGUMENT;
     }
@@ -460,6 +478,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     g0.t2 = t2;
     g0.hmask = (uint32_t)(L.slots - 1);
     g0.hkey = L.hkey;
+    g0.rmask = (uint32_t)(rec_pow2(n) - 1);
     bool key_path = g_grid_mode == 2 || (g_grid_mode == 0 && n > kSmallN);
     if (!B) {
         PlanArgs a{};
@@ -503,6 +522,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     dctx.items = L.items;
     dctx.item_cap = g_item_cap > 0 ? (int)std::min<int64_t>(g_item_cap, L.item_cap) : L.item_cap;
     dctx.nbase = (int)n;
+    dctx.rmask = (uint32_t)(rec_pow2(n) - 1);
     dctx.meta = L.meta;
     // single cloud: the counting path is always enqueued (hash mode has no key sort); batch
     // mode planned on the host enqueues only the chosen path
@@ -571,7 +591,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         // slot = per-cell cursors here
         pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts);
         pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, gp, L.cw, L.crec, L.cmask, (int)n, L.parent, L.size, L.minidx,
-                                     L.sidx);
+                                     L.sidx, L.meta, C.node_stats ? 0 : 1);
         ++launches;
         ++launches;
     }
@@ -588,18 +608,11 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     if (!local_only)
         pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart, gp,
                                                                          L.parent, L.meta, n, local_only);
-    // sparse-sparse pairs: items listed by k_slist (in the dead fine-occupancy buffer), one thread
-    // each; the per-cell kernel runs only if the list overflowed
-    uint2* sitems = reinterpret_cast<uint2*>(L.cocc);
-    const int scap = (int)std::min<int64_t>(n, INT32_MAX);
-    pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(gp, L.cw, L.ccoord, L.cstart, L.slist, L.meta, n, local_only,
-                                                       sitems, scap);
-    pdl(k_sparse_pairs, grid_for(n, 256, cap * 2), 256, 0, st)(L.spts, L.cstart, gp, L.parent, L.meta, n, local_only,
-                                                              sitems, scap);
+    pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(L.cstart, L.slist, L.meta, n, local_only, gp,
+                                                       C.node_stats ? 0 : 1, L.parent, L.size, L.minidx);
     pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart,
                                                                            L.slist, gp, L.parent, L.meta, n,
                                                                            local_only);
-    ++launches;
     mark(6, st);
     // thread per listed item (k_dcomps): the sparse neighbours and own pairs here, the forward
     // dense pairs on the side stream (forked after k_dcomps); the fallback runs only if a list
@@ -610,7 +623,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     pdl(k_dense_link_all, di.sms * 2, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
     // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
     pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
-    pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta);
+    pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta,
+                                                                            (uint32_t)(rec_pow2(n) - 1));
     pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(dctx, L.items2, L.slices2, L.idone);
     pdl(k_dense_items, di.sms * 8, 256, 0, st)(gp, dctx, L.items2, L.slices2, L.idone);
     launches += local_only ? 8 : 9;
@@ -702,12 +716,18 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     mark(8, st);
     // (at least two blocks: the node tail splits the grid in halves)
     pdl(k_tail_stats, std::max(ew, 2u), 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, L.ncomp,
-                                                   L.cstart, L.slist);
+                                                   L.cstart, L.slist, (uint32_t)(rec_pow2(n) - 1), L.spts);
     mark(9, st);
-    pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta);
-    pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(
-        L.parent, C.val, L.size, L.minidx, n, (long long)min_size, (long long)max_size, labels, L.meta,
-        B ? B->off_dev : nullptr, B ? B->nclouds : 0);
+    pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta,
+                                     (uint32_t)(rec_pow2(n) - 1), L.cstart, L.slist, L.ncomp, L.dlist, L.crec);
+    // labels: input order for node-tail clouds, sorted order for sparse-dominated ones (one of
+    // the two returns at once)
+    pdl(k_relabel_in, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(pts, n, L.grid, L.cw, L.crec, L.cmask,
+                                                                      L.cstart, L.spts, L.parent, L.minidx, labels,
+                                                                      L.meta);
+    pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(L.parent, C.val, L.minidx, n, labels, L.meta,
+                                                                   B ? B->off_dev : nullptr, B ? B->nclouds : 0);
+    ++C.launches;
     C.launches += 4;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
@@ -779,6 +799,147 @@ BatchArgs batch_carve(char* base, int64_t n, int32_t nclouds, const int64_t* off
     B.bz_dev = cv.take<int32_t>(nclouds);
     return B;
 }
+
+// ---- multi-GPU Mode B: device-side slab partition of index-sharded input (fec_part.cu) -----
+struct PartWs {
+    unsigned* state;            // 8 words: bbox (ordered uint) + non-finite flag
+    int* info;                  // axis, nlayers, status
+    unsigned long long* cnt;    // per destination / category counts (64)
+    unsigned long long* cur;    // cursors (64)
+    long long* cum;             // kPartMaxLayers + 1 prefix counts
+    size_t total;
+};
+PartWs part_carve(char* base) {
+    PartWs W{};
+    Carver cv{base, 0, 0};
+    W.state = cv.take<unsigned>(8);
+    W.info = cv.take<int>(8);
+    W.cnt = cv.take<unsigned long long>(64);
+    W.cur = cv.take<unsigned long long>(64);
+    W.cum = cv.take<long long>((size_t)kPartMaxLayers + 1);
+    W.total = cv.off + 256;
+    return W;
+}
+double part_inv_h(float d) { return 1.0 / ((double)d * (1.0 + std::ldexp(1.0, -16)) * 0.5); }
+fec_status_t part_check(void* ws, size_t bytes, int32_t world) {
+    if (!ws || bytes < part_carve(nullptr).total) { g_err = "workspace missing or too small (see fec_part_workspace_bytes)"; return FEC_ERR_INVALID_ARGUMENT; }
+    if (world < 1 || world > 64) { g_err = "need 1 <= world <= 64"; return FEC_ERR_INVALID_ARGUMENT; }
+    return FEC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t fec_part_workspace_bytes(void) { return part_carve(nullptr).total; }
+int32_t fec_part_max_layers(void) { return kPartMaxLayers; }
+
+fec_status_t fec_part_bbox(const float* points, int64_t m, float* bbox_out, int32_t* hist, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    fec_status_t rc = part_check(workspace, workspace_bytes, 1);
+    if (rc != FEC_OK) return rc;
+    if (m < 0 || (m > 0 && !points) || !bbox_out || !hist) { g_err = "bad arguments"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PartWs W = part_carve(static_cast<char*>(workspace));
+    const int cap = dev_info().sms * 8;
+    pdl(k_part_init, cap, 256, 0, st)(W.state, hist);
+    if (m > 0) pdl(k_part_bbox, grid_for(m, 256, cap), 256, 0, st)(points, m, W.state);
+    pdl(k_part_bbox_out, 1, 32, 0, st)(W.state, bbox_out);
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+fec_status_t fec_part_hist(const float* points, int64_t m, const float* gbbox, float d_th, int32_t* hist,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+    float t2;
+    fec_status_t rc = check_args(0, d_th, 1, 1, &t2);
+    if (rc == FEC_OK) rc = part_check(workspace, workspace_bytes, 1);
+    if (rc != FEC_OK) return rc;
+    if (m < 0 || (m > 0 && !points) || !gbbox || !hist) { g_err = "bad arguments"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PartWs W = part_carve(static_cast<char*>(workspace));
+    pdl(k_part_hist, grid_for(std::max<int64_t>(m, 1), 256, dev_info().sms * 8), 256, 0, st)(points, m, gbbox,
+                                                                                         part_inv_h(d_th), hist,
+                                                                                         W.info);
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+fec_status_t fec_part_plan(const int32_t* ghist, int32_t world, int64_t* plan_out, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+    fec_status_t rc = part_check(workspace, workspace_bytes, world);
+    if (rc != FEC_OK) return rc;
+    if (!ghist || !plan_out) { g_err = "bad arguments"; return FEC_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PartWs W = part_carve(static_cast<char*>(workspace));
+    pdl(k_part_plan, 1, 1024, 0, st)(ghist, W.info, world, W.cum, reinterpret_cast<long long*>(plan_out));
+    pdl(k_part_status, 1, 32, 0, st)(W.info, reinterpret_cast<long long*>(plan_out), world);
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+fec_status_t fec_part_pack(const float* points, const int32_t* gidx, int64_t m, const float* gbbox, float d_th,
+                           const int64_t* plan, int32_t world, int64_t* counts, float* send_pts,
+                           int32_t* send_gidx, void* workspace, size_t workspace_bytes, void* stream) {
+    float t2;
+    fec_status_t rc = check_args(0, d_th, 1, 1, &t2);
+    if (rc == FEC_OK) rc = part_check(workspace, workspace_bytes, world);
+    if (rc != FEC_OK) return rc;
+    if (m < 0 || (m > 0 && (!points || !gidx)) || !gbbox || !plan || !counts || (!send_pts != !send_gidx)) {
+        g_err = "bad arguments";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PartWs W = part_carve(static_cast<char*>(workspace));
+    const unsigned blocks = grid_for(std::max<int64_t>(m, 1), 256, dev_info().sms * 8);
+    auto* c64 = reinterpret_cast<unsigned long long*>(counts);
+    if (!send_pts) {  // count pass
+        FEC_CUDA(cudaMemsetAsync(counts, 0, (size_t)world * 8, st));
+        if (m > 0)
+            pdl(k_part_pack, blocks, 256, 0, st)(points, gidx, m, gbbox, part_inv_h(d_th), W.info,
+                                                reinterpret_cast<const long long*>(plan), world, 0, c64, nullptr,
+                                                nullptr);
+    } else if (m > 0) {  // scatter pass: segments in rank order, sizes from the count pass
+        pdl(k_part_offsets, 1, 32, 0, st)(c64, world, W.cur);
+        pdl(k_part_pack, blocks, 256, 0, st)(points, gidx, m, gbbox, part_inv_h(d_th), W.info,
+                                            reinterpret_cast<const long long*>(plan), world, 1, W.cur, send_pts,
+                                            send_gidx);
+    }
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+fec_status_t fec_part_order(const float* recv_pts, const int32_t* recv_gidx, int64_t k, const float* gbbox,
+                            float d_th, const int64_t* plan, int32_t world, int32_t rank, int64_t* counts3,
+                            float* out_pts, int32_t* out_gidx, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+    float t2;
+    fec_status_t rc = check_args(0, d_th, 1, 1, &t2);
+    if (rc == FEC_OK) rc = part_check(workspace, workspace_bytes, world);
+    if (rc != FEC_OK) return rc;
+    if (rank < 0 || rank >= world || k < 0 || (k > 0 && (!recv_pts || !recv_gidx || !out_pts || !out_gidx)) ||
+        !gbbox || !plan || !counts3) {
+        g_err = "bad arguments";
+        return FEC_ERR_INVALID_ARGUMENT;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PartWs W = part_carve(static_cast<char*>(workspace));
+    auto* c64 = reinterpret_cast<unsigned long long*>(counts3);
+    FEC_CUDA(cudaMemsetAsync(counts3, 0, 3 * 8, st));
+    if (k > 0) {
+        const unsigned blocks = grid_for(k, 256, dev_info().sms * 8);
+        const auto* pl = reinterpret_cast<const long long*>(plan);
+        pdl(k_part_order, blocks, 256, 0, st)(recv_pts, recv_gidx, k, gbbox, part_inv_h(d_th), W.info, pl, world,
+                                             rank, 0, c64, nullptr, nullptr);
+        pdl(k_part_offsets, 1, 32, 0, st)(c64, 3, W.cur);
+        pdl(k_part_order, blocks, 256, 0, st)(recv_pts, recv_gidx, k, gbbox, part_inv_h(d_th), W.info, pl, world,
+                                             rank, 1, W.cur, out_pts, out_gidx);
+    }
+    FEC_CUDA(cudaGetLastError());
+    return FEC_OK;
+}
+
+}  // extern "C"
+namespace {
 }  // namespace
 
 extern "C" {
@@ -941,7 +1102,7 @@ fec_status_t fec_slab_local(const float* points, const int32_t* gidx, int64_t n_
     mark(9, st);
     pdl(k_slab_pack, grid_for(nodes_max(n_local), 256, dev_info().sms * 8 * 4), 256, 0, st)(
         L.parent, C.val, gidx, n_local, (int)n_owned, (int)n_first, L.size, L.minidx, S.ckey, records, (int)rec_cap,
-        L.meta);
+        L.meta, (uint32_t)(rec_pow2(n_local) - 1));
     C.launches += 2;
     mark(10, st);
     FEC_CUDA(cudaGetLastError());
@@ -1100,7 +1261,9 @@ bool fec::pdl_enabled() {
 
 extern "C" {
 
-const char* fec_version(void) { return "fec-b200 0.1 sm_100a"; }
+const char* fec_version(void) { return "fec-b200 0.2 sm_100a"; }
+
+int64_t fec_max_points(void) { return kMaxN; }
 
 fec_status_t fec_debug_pred(const float* a, const float* b, int64_t m, float d_th, uint8_t* out, float* d2_out,
                             void* stream) {

@@ -221,85 +221,56 @@ __global__ void __launch_bounds__(256) k_zero(const Grid* __restrict__ gp, uint2
 }
 
 // ---- a2: occupancy bitmap ------------------------------------------------------------------
-// Binning kernels aggregate per block through a small shared-memory hash table (keys = bitmap
-// word or compact cell id): one global atomic per distinct key per tile of kBinTile points.
-constexpr int kBinThreads = 256;
-constexpr int kBinIpt = 4;
-constexpr int kBinTile = kBinThreads * kBinIpt;
-constexpr int kBinSlots = 2 * kBinTile;
-
-// Insert `key`; a thread that claims a new slot appends it to `used` (so the flush visits only
-// occupied slots).
-__device__ __forceinline__ int bin_slot(int* keys, uint32_t key, int* used, int* nused) {
-    uint32_t h = (key * 2654435761u) & (kBinSlots - 1);
-    while (true) {
-        const int cur = keys[h];
-        if (cur == (int)key) return (int)h;
-        if (cur == -1) {
-            const int old = atomicCAS(keys + h, -1, (int)key);
-            if (old == -1) {
-                used[atomicAdd(nused, 1)] = (int)h;
-                return (int)h;
-            }
-            if (old == (int)key) return (int)h;
-        }
-        h = (h + 1) & (kBinSlots - 1);
-    }
-}
-
-__global__ void __launch_bounds__(kBinThreads) k_cmark(const float* __restrict__ p, int64_t n,
-                                                       const Grid* __restrict__ gp, uint2* __restrict__ cw) {
+// Warp-synchronous aggregation (no shared-memory table): a thread's 4 consecutive points are
+// merged into runs of one bitmap word; each thread's first run then meets the warp's other
+// first runs in one __match_any_sync round, and one lane per distinct word ORs the combined
+// bits into the bitmap (a reduction at L2, nothing waited on).  Later runs of a thread (a word
+// boundary inside its 4 points) go straight to the bitmap.  Spatially coherent input (the
+// counting path) makes the runs long and the distinct words per warp few.
+__global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
+                                              uint2* __restrict__ cw) {
     pdl_prologue();
     FEC_LOAD_GRID(gp);
     if (g.status || g.key_sort) return;
-    __shared__ int keys[kBinSlots];
-    __shared__ uint32_t bits[kBinSlots];
-    __shared__ int used[kBinTile];
-    __shared__ int nused;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
-    for (int k = threadIdx.x; k < kBinSlots; k += kBinThreads) { keys[k] = -1; bits[k] = 0u; }
-    if (threadIdx.x == 0) nused = 0;
-    __syncthreads();
-    for (int64_t t0 = (int64_t)blockIdx.x * kBinTile; t0 < n; t0 += (int64_t)gridDim.x * kBinTile) {
-        const int64_t b4 = t0 + kBinIpt * threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; t0 < n; t0 += nw * 128) {
+        const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
-        // runs of this thread's points in the same bitmap word take one table update
-        uint32_t word = 0xffffffffu, wbits = 0u;
+        uint32_t w0 = 0xffffffffu, bits0 = 0u;  // the thread's first run
+        uint32_t w = 0xffffffffu, bits = 0u;     // the current (later) run
         u64 prev_pc = ~0ull;
         uint32_t lin = 0;
 #pragma unroll
-        for (int j = 0; j < kBinIpt; ++j) {
-            if (b4 + j < n) {
-                uint32_t f[3];
-                fine_of(P.x[j], P.y[j], P.z[j], b4 + j, g, f);
-                if (g.hashed) {  // insert the cell (consecutive points of one cell: one probe)
-                    const u64 pc = pack_cell(f[0] >> 2, f[1] >> 2, f[2] >> 2);
-                    if (pc != prev_pc) lin = hash_insert(g, pc);
-                    prev_pc = pc;
-                } else {
-                    lin = (f[0] >> 2) * g.stride[0] + (f[1] >> 2) * g.stride[1] + (f[2] >> 2) * g.stride[2];
-                }
-                if ((lin >> 5) != word) {
-                    if (wbits) atomicOr(bits + bin_slot(keys, word, used, &nused), wbits);
-                    word = lin >> 5;
-                    wbits = 0u;
-                }
-                wbits |= 1u << (lin & 31u);
+        for (int j = 0; j < 4; ++j) {
+            if (b4 + j >= n) continue;
+            uint32_t f[3];
+            fine_of(P.x[j], P.y[j], P.z[j], b4 + j, g, f);
+            if (g.hashed) {  // insert the cell (consecutive points of one cell: one probe)
+                const u64 pc = pack_cell(f[0] >> 2, f[1] >> 2, f[2] >> 2);
+                if (pc != prev_pc) lin = hash_insert(g, pc);
+                prev_pc = pc;
+            } else {
+                lin = (f[0] >> 2) * g.stride[0] + (f[1] >> 2) * g.stride[1] + (f[2] >> 2) * g.stride[2];
+            }
+            const uint32_t wd = lin >> 5, bit = 1u << (lin & 31u);
+            if (w0 == 0xffffffffu || (wd == w0 && w == 0xffffffffu)) {
+                w0 = wd;
+                bits0 |= bit;
+            } else if (wd == w) {
+                bits |= bit;
+            } else {
+                if (w != 0xffffffffu) atomicOr(reinterpret_cast<unsigned int*>(cw + w), bits);
+                w = wd;
+                bits = bit;
             }
         }
-        if (wbits) atomicOr(bits + bin_slot(keys, word, used, &nused), wbits);
-        __syncthreads();
-        const int nu = nused;
-        for (int e = threadIdx.x; e < nu; e += kBinThreads) {
-            const int k = used[e];
-            atomicOr(reinterpret_cast<unsigned int*>(cw + keys[k]), bits[k]);
-            keys[k] = -1;
-            bits[k] = 0u;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) nused = 0;
-        __syncthreads();
+        if (w != 0xffffffffu) atomicOr(reinterpret_cast<unsigned int*>(cw + w), bits);
+        const unsigned peers = __match_any_sync(0xffffffffu, w0);
+        const uint32_t all = __reduce_or_sync(peers, bits0);
+        if (w0 != 0xffffffffu && lane == __ffs(peers) - 1) atomicOr(reinterpret_cast<unsigned int*>(cw + w0), all);
     }
 }
 
@@ -620,10 +591,14 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                                               const uint2* __restrict__ cw, const int* __restrict__ crec,
                                               const u64* __restrict__ cmask, int nbase, int* __restrict__ parent,
                                               int* __restrict__ size, int* __restrict__ minidx,
-                                              int* __restrict__ sidx) {
+                                              int* __restrict__ sidx, const Meta* __restrict__ meta,
+                                              int all_parents) {
     pdl_prologue();
     FEC_LOAD_GRID(gp);
     if (g.status || g.key_sort) return;
+    // node-tail clouds of the single-GPU path read no sorted-order array of the dense points
+    // (node statistics, k_relabel_in): k_slist initialises the points of sparse cells instead
+    if (!all_parents && 4 * (int64_t)meta->cells <= n) return;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b4 = 4 * gi;
@@ -653,7 +628,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                 int c = 0;
                 if (kc > 1)
                     while (c < kc - 1 && !((__ldg(cmask + 8 * r + c) >> q[j]) & 1ull)) ++c;
-                par[j] = nbase + 8 * r + c;
+                par[j] = node_of(nbase, g.rmask, r, c);
             }
         }
         if (b4 + 4 <= n) {
@@ -908,14 +883,14 @@ __device__ __noinline__ void test_item_serial(const DenseCtx& C, const Grid& g, 
     const int cp = __ldg(C.dlist + it.x);
     const uint32_t lp = __ldg(C.clin + cp);
     const u64 ma = C.cmask[8 * it.x + it.y];
-    const int na = C.nbase + 8 * it.x + it.y;
+    const int na = node_of(C.nbase, C.rmask, it.x, it.y);
     int nb, b0, b1;
     u64 mb;
     int slot;
     if (it.w >= 0) {
         const int cq = __ldg(C.dlist + it.z);
         mb = C.cmask[8 * it.z + it.w];
-        nb = C.nbase + 8 * it.z + it.w;
+        nb = node_of(C.nbase, C.rmask, it.z, it.w);
         b0 = (int)__ldg(C.cstart + cq);
         b1 = (int)__ldg(C.cstart + cq + 1);
         slot = cell_slot_of(g, lp, __ldg(C.clin + cq));
@@ -1013,7 +988,7 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
             crec[cid] = (r << 3) | (kp - 1);  // the cell's record word (k_dscatter, k_dense_link)
 #pragma unroll
             for (int j = 0; j < kMaxComp; ++j) {
-                const int node = C.nbase + 8 * r + j;
+                const int node = node_of(C.nbase, C.rmask, r, j);
                 C.parent[node] = node;
                 size[node] = 0;
                 minidx[node] = 0x7fffffff;
@@ -1021,8 +996,9 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
             }
             if (kp == 1 && nstats) {
                 const int a0 = (int)__ldg(C.cstart + cid);
-                size[C.nbase + 8 * r] = (int)__ldg(C.cstart + cid + 1) - a0;
-                minidx[C.nbase + 8 * r] = g.key_sort ? __ldg(sidx + a0) : __ldg(cmin + cid);
+                const int node0 = node_of(C.nbase, C.rmask, r, 0);
+                size[node0] = (int)__ldg(C.cstart + cid + 1) - a0;
+                minidx[node0] = g.key_sort ? __ldg(sidx + a0) : __ldg(cmin + cid);
             }
         }
         // neighbour slots that need work
@@ -1130,7 +1106,7 @@ __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts
         const int k = __shfl_sync(0xffffffffu, kl, j);
         const int cid = __ldg(dlist + r);
         const int a0 = (int)__ldg(cstart + cid), a1 = (int)__ldg(cstart + cid + 1);
-        const int node0 = nbase + 8 * r;
+        const int node0 = node_of(nbase, g.rmask, r, 0);
         if (k == 1) {  // key path, one component: every point under node 0 (stats: k_dcomps)
             for (int s = a0 + lane; s < a1; s += 32) parent[s] = node0;
             continue;
@@ -1206,7 +1182,7 @@ __device__ __forceinline__ void dense_link_pair(int r, int k, int ox, int oy, in
         // P's own components (never certain-adjacent to each other)
         for (int i = 0; i + 1 < kp; ++i)
             for (int j = i + 1; j < kp; ++j) {
-                const int na = C.nbase + 8 * r + i, nb = C.nbase + 8 * r + j;
+                const int na = node_of(C.nbase, C.rmask, r, i), nb = node_of(C.nbase, C.rmask, r, j);
                 if (uf_find(C.parent, na) == uf_find(C.parent, nb)) continue;
                 if constexpr (serial) test_item_serial(C, g, make_int4(r, i, r, j));
                 else overflow |= !queue_item(C, make_int4(r, i, r, j));
@@ -1222,10 +1198,10 @@ __device__ __forceinline__ void dense_link_pair(int r, int k, int ox, int oy, in
                 const u64 mx = mp[x];
                 const u64 dc = sc_certain_across(d_sc, mx, slot);
                 const bool near_p = (mx & d_sc.F[slot]) != 0;
-                const int na = C.nbase + 8 * r + x;
+                const int na = node_of(C.nbase, C.rmask, r, x);
                 for (int y = 0; y < kq; ++y) {
                     const u64 my = C.cmask[8 * rq + y];
-                    const int nb = C.nbase + 8 * rq + y;
+                    const int nb = node_of(C.nbase, C.rmask, rq, y);
                     if (dc & my) {
                         if constexpr (!serial) uf_unite(C.parent, na, nb);
                     } else if (near_p && (my & d_sc.F[26 - slot]) &&
@@ -1243,7 +1219,7 @@ __device__ __forceinline__ void dense_link_pair(int r, int k, int ox, int oy, in
                 const u64 tc = d_sc.T[opp][qb], tu = d_sc.U[opp][qb];
                 for (int x = 0; x < kp; ++x) {
                     const u64 mx = mp[x];
-                    const int na = C.nbase + 8 * r + x;
+                    const int na = node_of(C.nbase, C.rmask, r, x);
                     if (tc & mx) {
                         if constexpr (!serial) uf_unite(C.parent, t, na);
                     } else if ((tu & mx) && uf_find(C.parent, na) != uf_find(C.parent, t)) {
@@ -1364,8 +1340,8 @@ __global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restri
     const int ni = min(C.meta->nitems, C.item_cap);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
         const int4 it = C.items[e];  // queued before every certain union was done: re-check
-        const int na = C.nbase + 8 * it.x + it.y;
-        const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
+        const int na = node_of(C.nbase, C.rmask, it.x, it.y);
+        const int nb = it.w >= 0 ? node_of(C.nbase, C.rmask, it.z, it.w) : it.z;
         if (uf_find(C.parent, na) == uf_find(C.parent, nb)) continue;
         const int cp = __ldg(C.dlist + it.x);
         const int wa = (int)(__ldg(C.cstart + cp + 1) - __ldg(C.cstart + cp));
@@ -1390,12 +1366,13 @@ __global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restri
 }
 
 // Component nodes -> their roots (shortens the finds of the uncertain pass).
-__global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta) {
+__global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta,
+                                                      uint32_t rmask) {
     pdl_prologue();
     if (meta->status) return;
     const int64_t nn = 8 * (int64_t)meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
-        const int s = nbase + (int)t;
+        const int s = node_of(nbase, rmask, (int)(t >> 3), (int)(t & 7));
         int curr = ld_parent(parent, s), next;
         if (curr == s) continue;
         while (curr < (next = ld_parent(parent, curr))) curr = next;
@@ -1425,8 +1402,8 @@ __global__ void __launch_bounds__(256) k_dense_items(const Grid* __restrict__ gp
         const int4 it = items2[w];
         const int4 sl = slices2[w];
         volatile int* done = idone + sl.z;
-        const int na = C.nbase + 8 * it.x + it.y;
-        const int nb = it.w >= 0 ? C.nbase + 8 * it.z + it.w : it.z;
+        const int na = node_of(C.nbase, C.rmask, it.x, it.y);
+        const int nb = it.w >= 0 ? node_of(C.nbase, C.rmask, it.z, it.w) : it.z;
         int same = 0;
         if (lane == 0) same = *done || uf_find(C.parent, na) == uf_find(C.parent, nb);
         if (__shfl_sync(0xffffffffu, same, 0)) continue;
@@ -1539,7 +1516,7 @@ __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ nco
     unsigned long long roots = 0, pts = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nd; r += gridDim.x * blockDim.x) {
         const int k = ncomp[r];
-        for (int j = 0; j < k; ++j) roots += C.parent[C.nbase + 8 * r + j] == C.nbase + 8 * r + j;
+        for (int j = 0; j < k; ++j) roots += C.parent[node_of(C.nbase, C.rmask, r, j)] == node_of(C.nbase, C.rmask, r, j);
         const int cid = dlist[r];
         pts += cstart[cid + 1] - cstart[cid];
     }
@@ -1635,129 +1612,39 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     }
 }
 
-// LOCAL clouds (and small clouds): the sparse cells in one compact list, and the work items of
-// the sparse-sparse pairs: one per sparse cell with >= 2 points (its own pairs) and one per
-// (sparse cell, occupied sparse forward neighbour).  Thread per occupied cell; the 13 neighbour
-// lookups are issued together; items are block-aggregated (one atomic per block).  If the item
-// list would overflow, meta->sp_overflow hands the sparse cells to k_union_sparse_local.
-__global__ void __launch_bounds__(256) k_slist(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
-                                              const u64* __restrict__ ccoord, const uint32_t* __restrict__ cstart,
-                                              int* __restrict__ slist, Meta* __restrict__ meta, int64_t n,
-                                              int local_only, uint2* __restrict__ sitems, int scap) {
+// LOCAL clouds (and small clouds): the sparse cells in one compact list, so every lane of the
+// union kernel owns a real sparse cell and all of them run in one wave.
+// Also (counting path without k_dinit) the union-find init of the sparse cells' points.
+__global__ void __launch_bounds__(256) k_slist(const uint32_t* __restrict__ cstart, int* __restrict__ slist,
+                                              Meta* __restrict__ meta, int64_t n, int local_only,
+                                              const Grid* __restrict__ gp, int all_parents, int* __restrict__ parent,
+                                              int* __restrict__ size, int* __restrict__ minidx) {
     pdl_prologue();
-    FEC_LOAD_GRID(gp);
-    if (g.status || (!local_only && 4 * (int64_t)meta->cells > n)) return;  // sparse-dominated: k_union_sparse
-    __shared__ int wsum[256 / kWarp];
-    __shared__ int bbase;
+    if (meta->status || (!local_only && 4 * (int64_t)meta->cells > n)) return;  // sparse-dominated: k_union_sparse
+    const bool init = !gp->key_sort && !all_parents && 4 * (int64_t)meta->cells <= n;
     const int64_t U = meta->cells;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t u0 = (int64_t)blockIdx.x * blockDim.x; u0 < U; u0 += stride) {  // block-uniform
-        const int64_t u = u0 + threadIdx.x;
-        int np = 0;
-        if (u < U) np = (int)(__ldg(cstart + u + 1) - __ldg(cstart + u));
-        const bool sp = np > 0 && np <= SPARSE_MAX;
-        // the compact list (warp-aggregated)
-        {
-            const unsigned m = __ballot_sync(0xffffffffu, sp);
-            int base = 0;
-            if (m && lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
+    const int64_t ur = (U + 31) & ~int64_t(31);
+    const int lane = threadIdx.x & 31;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
+        bool sp = false;
+        if (u < U) {
+            const uint32_t c = __ldg(cstart + u + 1) - __ldg(cstart + u);
+            sp = c > 0 && c <= (uint32_t)SPARSE_MAX;
         }
-        // forward sparse neighbours
-        int cq[13];
-        uint32_t fm = 0u;
-        int c[3] = {0, 0, 0};
-        if (sp) {
-            const u64 pc = __ldg(ccoord + u);
-            c[0] = (int)(pc & 0x1fffff);
-            c[1] = (int)((pc >> 21) & 0x1fffff);
-            c[2] = (int)(pc >> 42);
-        }
-#pragma unroll
-        for (int k = 0; k < 13; ++k) {
-            uint32_t lq;
-            cq[k] = (sp && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], lq)) ? cid_lookup(cw, lq) : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < 13; ++k)
-            if (cq[k] >= 0 && __ldg(cstart + cq[k] + 1) - __ldg(cstart + cq[k]) <= (uint32_t)SPARSE_MAX) fm |= 1u << k;
-        const int own = (sp && np >= 2) ? 1 : 0;
-        const int cnt = __popc(fm) + own;
-        int x = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int tot = 0;
-            for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) {
-                const int t = wsum[ww];
-                wsum[ww] = tot;
-                tot += t;
-            }
-            bbase = tot ? atomicAdd(&meta->nspitems, tot) : 0;
-            if (tot && bbase + tot > scap) atomicOr(&meta->sp_overflow, 1);
-        }
-        __syncthreads();
-        int pos = bbase + wsum[w] + x - cnt;
-        if (pos + cnt <= scap) {
-            if (own) sitems[pos++] = make_uint2((uint32_t)u, (uint32_t)u);
-#pragma unroll
-            for (int k = 0; k < 13; ++k)
-                if ((fm >> k) & 1u) sitems[pos++] = make_uint2((uint32_t)u, (uint32_t)cq[k]);
-        }
-        __syncthreads();  // wsum / bbase are reused
-    }
-}
-
-// Sparse-sparse pairs, thread per item: (P, P) tests P's own pairs, (P, Q) every point pair of
-// P and its forward neighbour Q (<= 6 x 6), uniting the pred-true ones.
-__global__ void __launch_bounds__(256, 4) k_sparse_pairs(const float4* __restrict__ spts,
-                                                     const uint32_t* __restrict__ cstart, const Grid* __restrict__ gp,
-                                                     int* __restrict__ parent, Meta* __restrict__ meta, int64_t n,
-                                                     int local_only, const uint2* __restrict__ sitems, int scap) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
-    if (g.status || meta->sp_overflow || (!local_only && 4 * (int64_t)meta->cells > n)) return;
-    const float t2 = g.t2;
-    const int ni = min(meta->nspitems, scap);
-    unsigned long long n_tests = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
-        const uint2 it = __ldg(sitems + i);
-        const int ps = (int)__ldg(cstart + it.x), pe = (int)__ldg(cstart + it.x + 1);
-        if (it.x == it.y) {
-            for (int s = ps; s < pe; ++s) {
-                const float4 a = __ldg(spts + s);
-                for (int t = s + 1; t < pe; ++t) {
-                    ++n_tests;
-                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-                }
-            }
-        } else {
-            const int qs = (int)__ldg(cstart + it.y), qe = (int)__ldg(cstart + it.y + 1);
-            float4 b[SPARSE_MAX];
-#pragma unroll
-            for (int j = 0; j < SPARSE_MAX; ++j)
-                if (qs + j < qe) b[j] = __ldg(spts + qs + j);
-            for (int s = ps; s < pe; ++s) {
-                const float4 a = __ldg(spts + s);
-#pragma unroll
-                for (int j = 0; j < SPARSE_MAX; ++j) {
-                    if (qs + j >= qe) break;
-                    ++n_tests;
-                    if (pred(a, b[j], t2)) uf_unite(parent, s, qs + j);
-                }
+        const unsigned m = __ballot_sync(0xffffffffu, sp);
+        if (!m) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
+        if (sp && init) {
+            const int s0 = (int)__ldg(cstart + u), s1 = (int)__ldg(cstart + u + 1);
+            for (int t = s0; t < s1; ++t) {
+                parent[t] = t;
+                size[t] = 0;
+                minidx[t] = 0x7fffffff;
             }
         }
-    }
-    if (meta->instrument) {
-        for (int o = 16; o > 0; o >>= 1) n_tests += __shfl_xor_sync(__activemask(), n_tests, o);
-        if ((threadIdx.x & 31) == 0 && n_tests) atomicAdd(&meta->pair_tests, n_tests);
     }
 }
 
@@ -1797,8 +1684,7 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
                                                            int64_t n, int local_only) {
     pdl_prologue();
     FEC_LOAD_GRID(gp);
-    // the fallback of k_sparse_pairs: only when its item list overflowed
-    if (g.status || !meta->sp_overflow || (!local_only && 4 * (int64_t)meta->cells > n)) return;
+    if (g.status || (!local_only && 4 * (int64_t)meta->cells > n)) return;
     const uint32_t nitems = (uint32_t)meta->nsparse;
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
     const float t2 = g.t2;
@@ -1877,6 +1763,76 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
         }
     }
     if (meta->instrument && n_tests) atomicAdd(&meta->pair_tests, n_tests);
+}
+
+// a10, second half, clouds with few sparse cells (the node tail): walk the INPUT order, so the
+// labels are written coalesced and no sorted-order array is read.  A point's cell (from its
+// coordinates, the same arithmetic as binning) gives its record word: a point of a dense cell
+// takes the folded label of its component's node (its fine sub-cell picks the component); a point
+// of a sparse cell is found among the cell's <= 6 sorted points (by its index) and takes its
+// root's folded label.  (The sorted-order pass below serves sparse-dominated clouds.)
+__global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p, int64_t n,
+                                                   const Grid* __restrict__ gp, const uint2* __restrict__ cw,
+                                                   const int* __restrict__ crec, const u64* __restrict__ cmask,
+                                                   const uint32_t* __restrict__ cstart,
+                                                   const float4* __restrict__ spts, const int* __restrict__ parent,
+                                                   const int* __restrict__ minidx, int* __restrict__ labels,
+                                                   const Meta* __restrict__ meta) {
+    pdl_prologue();
+    FEC_LOAD_GRID(gp);
+    if (g.status || 4 * (int64_t)meta->cells > n) return;
+    const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    const int64_t groups = (n + 3) / 4;
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b4 = 4 * gi;
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
+        int rv[4], q[4];
+        uint32_t cid[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            rv[j] = 0;
+            q[j] = 0;
+            cid[j] = 0;
+            if (b4 + j >= n) continue;
+            uint32_t lin;
+            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q[j]);
+            cid[j] = cid_of(cw, lin);
+            // -1 sparse cell; <= -2 single-component dense cell: -(label + 3) (k_rootlab);
+            // >= 0 several components: record << 3 | (components - 1)
+            rv[j] = __ldg(crec + cid[j]);
+        }
+        int lab[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            lab[j] = -1;
+            if (b4 + j >= n) continue;
+            if (rv[j] <= -2) {
+                lab[j] = -rv[j] - 3;
+            } else if (rv[j] >= 0) {
+                const int r = rv[j] >> 3, kc = (rv[j] & 7) + 1;
+                int c = 0;
+                if (kc > 1)
+                    while (c < kc - 1 && !((__ldg(cmask + 8 * r + c) >> q[j]) & 1ull)) ++c;
+                lab[j] = __ldg(minidx + node_of((int)n, g.rmask, r, c));
+            } else {
+                const int s0 = (int)__ldg(cstart + cid[j]), s1 = (int)__ldg(cstart + cid[j] + 1);
+                for (int t = s0; t < s1; ++t)
+                    if (__float_as_int(__ldg(spts + t).w) == (int)(b4 + j)) {
+                        lab[j] = __ldg(minidx + __ldg(parent + t));
+                        break;
+                    }
+            }
+            if (g.batch && lab[j] >= 0) lab[j] -= (int)__ldg(g.boff + cloud_of(g, b4 + j));
+        }
+        if (b4 + 4 <= n && (reinterpret_cast<uintptr_t>(labels) & 15u) == 0) {
+            *reinterpret_cast<int4*>(labels + b4) = make_int4(lab[0], lab[1], lab[2], lab[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (b4 + j < n) labels[b4 + j] = lab[j];
+        }
+    }
 }
 
 }  // namespace fec

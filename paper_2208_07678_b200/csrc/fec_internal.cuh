@@ -85,6 +85,7 @@ struct Grid {
     int32_t perm[3];    // bitmap mode: axes from fastest to slowest
     uint32_t sdiv[2];   // bitmap mode: stride[perm[2]], stride[perm[1]] (for decoding)
     uint32_t hmask;     // hash mode: slots - 1 (slots a power of two >= 2n)
+    uint32_t rmask;     // dense records: R - 1 (node ids, fec_kernels.cuh node_of)
     float t2;           // fl32(d*d) (reading A3)
     int32_t status;     // FEC_OK, or the error found by a1 (every later kernel returns at once)
     int32_t key_sort;   // 1: the key-sort binning path runs, 0: the counting path

@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
 // ---- single-GPU tail, one launch for the stats of every mode ----------------------------
 __device__ __forceinline__ void node_stats_body(int* __restrict__ parent, const int* __restrict__ ncomp,
                                                    int* __restrict__ size, int* __restrict__ minidx, int nbase,
-                                                   Meta* __restrict__ meta, int64_t n, int bid, int nblk) {
+                                                   Meta* __restrict__ meta, int64_t n, int bid, int nblk,
+                                                   uint32_t rmask) {
     if (4 * (int64_t)meta->cells > n) return;
     const int64_t nn = 8 * (int64_t)meta->ndense;
     const int64_t nr = (nn + 31) & ~int64_t(31);  // whole warps stay in the loop
@@ -429,7 +430,7 @@ __device__ __forceinline__ void node_stats_body(int* __restrict__ parent, const 
     for (int64_t t = (int64_t)bid * blockDim.x + threadIdx.x; t < nr; t += (int64_t)nblk * blockDim.x) {
         int root = -1, c = 0, m = 0x7fffffff;
         if (t < nn && (int)(t & 7) < __ldg(ncomp + (t >> 3))) {  // a used component slot
-            const int node = nbase + (int)t;
+            const int node = node_of(nbase, rmask, (int)(t >> 3), (int)(t & 7));
             int curr = ld_parent(parent, node), next;
             if (curr == node) {  // a root keeps its own totals
                 if (meta->instrument) atomicAdd(&meta->components, 1ull);
@@ -455,7 +456,7 @@ __device__ __forceinline__ void node_stats_body(int* __restrict__ parent, const 
 }
 
 __device__ __forceinline__ void sparse_stats_body(int* __restrict__ parent, const uint32_t* __restrict__ cstart,
-                                                     const int* __restrict__ slist, const int* __restrict__ sidx,
+                                                     const int* __restrict__ slist, const float4* __restrict__ spts,
                                                      int* __restrict__ size, int* __restrict__ minidx,
                                                      Meta* __restrict__ meta, int64_t n, int bid, int nblk) {
     if (4 * (int64_t)meta->cells > n) return;
@@ -483,7 +484,7 @@ __device__ __forceinline__ void sparse_stats_body(int* __restrict__ parent, cons
                 } else if (meta->instrument) {
                     atomicAdd(&meta->components, 1ull);
                 }
-                v = __ldg(sidx + s);
+                v = __float_as_int(__ldg(spts + s).w);
             }
             const unsigned peers = __match_any_sync(0xffffffffu, curr);
             const int cnt = __popc(peers);
@@ -504,7 +505,8 @@ __device__ __forceinline__ void sparse_stats_body(int* __restrict__ parent, cons
 __global__ void __launch_bounds__(256) k_tail_stats(int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                                    int* __restrict__ size, int* __restrict__ minidx,
                                                    Meta* __restrict__ meta, const int* __restrict__ ncomp,
-                                                   const uint32_t* __restrict__ cstart, const int* __restrict__ slist) {
+                                                   const uint32_t* __restrict__ cstart, const int* __restrict__ slist,
+                                                   uint32_t rmask, const float4* __restrict__ spts) {
     pdl_prologue();
     if (meta->status) return;
     if (4 * (int64_t)meta->cells > n) {
@@ -512,35 +514,78 @@ __global__ void __launch_bounds__(256) k_tail_stats(int* __restrict__ parent, co
     } else {
         const int half = (int)(gridDim.x >> 1);  // >= 1: the host launches >= 2 blocks
         if ((int)blockIdx.x < half)
-            node_stats_body(parent, ncomp, size, minidx, (int)n, meta, n, blockIdx.x, half);
+            node_stats_body(parent, ncomp, size, minidx, (int)n, meta, n, blockIdx.x, half, rmask);
         else
-            sparse_stats_body(parent, cstart, slist, val, size, minidx, meta, n, blockIdx.x - half, gridDim.x - half);
+            sparse_stats_body(parent, cstart, slist, spts, size, minidx, meta, n, blockIdx.x - half, gridDim.x - half);
     }
 }
 
-// Sparse-dominated clouds (many components, roots scattered): fold the filter into the roots
-// (minidx[r] = final label) so k_relabel reads one root word per point instead of two.
+// a10, first half: the size filter folded into the union-find nodes, so k_relabel reads one
+// word per point.  Every root (parent[x] == x) gets minidx[x] = its component's final label
+// (the minimum input index, or -1 outside [min_size, max_size]); every component node that is
+// not a root gets its root's final label (its own partial minimum is no longer needed: the
+// statistics are complete).  The nodes visited: all points and node slots of sparse-dominated
+// clouds; otherwise the node slots and the points of sparse cells (the compact list), since a
+// point of a dense cell hangs under a component node.  A node that reads its root while the
+// root's own thread folds it sees either the minimum or the folded label, which agree unless
+// the size is filtered -- and then both sides write -1.
+// Node-tail clouds: a single-component dense cell's record word (crec, >= 0) is replaced by its
+// final label encoded as -(label + 3) (<= -2; -1 stays "sparse cell"), so k_relabel_in needs one
+// lookup per point of such a cell.
 __global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent, const int* __restrict__ size,
                                                 int* __restrict__ minidx, int64_t n, long long min_size,
-                                                long long max_size, const Meta* __restrict__ meta) {
+                                                long long max_size, const Meta* __restrict__ meta, uint32_t rmask,
+                                                const uint32_t* __restrict__ cstart, const int* __restrict__ slist,
+                                                const int* __restrict__ ncomp, const int* __restrict__ dlist,
+                                                int* __restrict__ crec) {
     pdl_prologue();
-    if (meta->status || 4 * (int64_t)meta->cells <= n) return;
-    const int64_t nodes = n + 8 * (int64_t)meta->ndense;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nodes; r += (int64_t)gridDim.x * blockDim.x) {
-        if (__ldg(parent + r) != (int)r) continue;
-        const long long sz = __ldg(size + r);
-        if (!(sz >= min_size && sz <= max_size)) minidx[r] = -1;
+    if (meta->status) return;
+    const bool sparse_dom = 4 * (int64_t)meta->cells > n;
+    const int64_t nslot = 8 * (int64_t)meta->ndense;
+    const int64_t npts = sparse_dom ? n : (int64_t)meta->nsparse * SPARSE_MAX;  // points, or sparse-cell slots
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < npts + nslot;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x;
+        if (u < npts) {
+            if (sparse_dom) {
+                x = u;
+            } else {  // slot j of sparse cell e
+                const int e = (int)(u / SPARSE_MAX), j = (int)(u % SPARSE_MAX);
+                const int P = __ldg(slist + e);
+                const int s0 = (int)__ldg(cstart + P);
+                if (s0 + j >= (int)__ldg(cstart + P + 1)) continue;
+                x = s0 + j;
+            }
+        } else {
+            x = node_of((int)n, rmask, (int)((u - npts) >> 3), (int)((u - npts) & 7));
+        }
+        const int p = __ldg(parent + x);
+        int lab = 0;
+        if (p == (int)x) {
+            const long long sz = __ldg(size + x);
+            lab = (sz >= min_size && sz <= max_size) ? minidx[x] : -1;
+            if (lab < 0) minidx[x] = -1;
+        } else if (x >= n) {  // a component node under another root (flattened by the tail)
+            const long long sz = __ldg(size + p);
+            lab = (sz >= min_size && sz <= max_size) ? minidx[p] : -1;
+            minidx[x] = lab;
+        }
+        if (!sparse_dom && u >= npts && ((u - npts) & 7) == 0) {  // component 0 of record r
+            const int r = (int)((u - npts) >> 3);
+            if (__ldg(ncomp + r) == 1) crec[__ldg(dlist + r)] = -(lab + 3);
+        }
     }
 }
 
+// a10, second half: labels[input index] = the folded label of the point's parent (its root, or
+// for a point of a dense cell its component node), scattered back to input order.
 __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent, const int* __restrict__ val,
-                                                const int* __restrict__ size, const int* __restrict__ minidx,
-                                                int64_t n, long long min_size, long long max_size,
+                                                const int* __restrict__ minidx, int64_t n,
                                                 int* __restrict__ labels, const Meta* __restrict__ meta,
                                                 const int64_t* __restrict__ boff, int nclouds) {
     pdl_prologue();
-    if (meta->status) return;  // a1 rejected the input: labels_out is left untouched
-    const bool folded = 4 * (int64_t)meta->cells > n;  // k_rootlab ran
+    // (a1 rejected the input: labels_out is left untouched; node-tail clouds: k_relabel_in)
+    if (meta->status || 4 * (int64_t)meta->cells <= n) return;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sb = 4 * gi;
@@ -557,20 +602,14 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
                 v[j] = sb + j < n ? __ldg(val + sb + j) : -1;
             }
         }
+        int lab[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) lab[j] = r[j] >= 0 ? __ldg(minidx + r[j]) : -1;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (r[j] < 0) continue;
-            // a point of a dense cell points at its component node, which k_node_stats (or
-            // the flattening walks) pointed at the root; roots point at themselves
-            if (r[j] >= n) r[j] = __ldg(parent + r[j]);
-            int lab;
-            if (folded) {
-                lab = __ldg(minidx + r[j]);
-            } else {
-                const long long sz = __ldg(size + r[j]);
-                lab = (sz >= min_size && sz <= max_size) ? __ldg(minidx + r[j]) : -1;
-            }
-            if (boff && lab >= 0) {
+            int l = lab[j];
+            if (boff && l >= 0) {
                 // batch mode: index inside the point's own cloud (the component never spans two)
                 int lo = 0, hi = nclouds;
                 while (hi - lo > 1) {
@@ -578,9 +617,9 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
                     if (__ldg(boff + mid) <= (int64_t)v[j]) lo = mid;
                     else hi = mid;
                 }
-                lab -= (int)__ldg(boff + lo);
+                l -= (int)__ldg(boff + lo);
             }
-            labels[v[j]] = lab;
+            labels[v[j]] = l;
         }
     }
 }

@@ -38,8 +38,6 @@ struct Meta {
     int nslices_extra;                // dense-grid mode: extra slices of heavy uncertain pairs
     int ndd, nds;                     // dense link items: forward dense pairs / sparse neighbours + own pairs
     int list_overflow;                // != 0: a link item list overflowed (k_dense_link_all redoes all)
-    int nspitems;                     // sparse-sparse pair items (k_slist -> k_sparse_pairs)
-    int sp_overflow;                  // != 0: that list overflowed (k_union_sparse_local takes over)
 };
 
 // What the host passes to a1 (k_bbox); its last block turns the bbox into the Grid (plan_grid).
@@ -66,10 +64,10 @@ __global__ void k_onesweep(const Grid* gp, int pass, uint32_t* k0, int* v0, uint
 __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx, const Meta* meta);
 __global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
 __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
-                          long long max_size, const Meta* meta);
-__global__ void k_relabel(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
-                          long long min_size, long long max_size, int* labels, const Meta* meta, const int64_t* boff,
-                          int nclouds);
+                          long long max_size, const Meta* meta, uint32_t rmask, const uint32_t* cstart,
+                          const int* slist, const int* ncomp, const int* dlist, int* crec);
+__global__ void k_relabel(const int* parent, const int* val, const int* minidx, int64_t n, int* labels,
+                          const Meta* meta, const int64_t* boff, int nclouds);
 __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
                               unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, const Grid* gp, uint2* cw);
@@ -87,12 +85,20 @@ __global__ void k_dcount2(const float* p, int64_t n, const Grid* gp, const uint2
 __global__ void k_dscatter(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* cursor,
                            float4* spts);
 __global__ void k_dinit(const float4* spts, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
-                        const u64* cmask, int nbase, int* parent, int* size, int* minidx, int* sidx);
+                        const u64* cmask, int nbase, int* parent, int* size, int* minidx, int* sidx, const Meta* meta,
+                        int all_parents);
 __global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta,
                          const Grid* gp, int* crec);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount, const Meta* meta);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
                              Meta* meta);
+// Component node of dense record r, component c (rmask: R - 1 for the record capacity R, a
+// power of two; node ids stay below nbase + 8R).
+__host__ __device__ __forceinline__ int node_of(int nbase, uint32_t rmask, int r, int c) {
+    (void)rmask;
+    return nbase + 8 * r + c;
+}
+
 // Dense-grid mode: what the component kernels share (item = (P record, P component,
 // Q record or point, Q component or -1 for a point)).
 struct DenseCtx {
@@ -104,7 +110,8 @@ struct DenseCtx {
     int* parent;
     int4* items;
     int item_cap;
-    int nbase;          // node id of component k of record r: nbase + 8r + k
+    int nbase;          // node id of component k of record r: node_of(nbase, rmask, r, k)
+    uint32_t rmask;
     Meta* meta;
 };
 __global__ void k_dcomps(const Grid* gp, const uint2* cw, int* crec, const u64* cocc, const u64* ccoord, int* ncomp, int* size,
@@ -114,7 +121,11 @@ __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int*
                           const u64* cmask, const Grid* gp, int nbase, int* parent, const Meta* meta, const int* sidx,
                           int* size, int* minidx, int node_stats, int64_t n);
 __global__ void k_tail_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta,
-                             const int* ncomp, const uint32_t* cstart, const int* slist);
+                             const int* ncomp, const uint32_t* cstart, const int* slist, uint32_t rmask,
+                             const float4* spts);
+__global__ void k_relabel_in(const float* p, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
+                             const u64* cmask, const uint32_t* cstart, const float4* spts, const int* parent,
+                             const int* minidx, int* labels, const Meta* meta);
 // local_only != 0 (small clouds, host-chosen): the sparse cells always go through the compact
 // list and k_union_sparse_local (more parallel per cell), whatever their share of the cells.
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
@@ -122,10 +133,8 @@ __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* c
 __global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
                                      const int* slist, const Grid* gp, int* parent, Meta* meta, int64_t n,
                                      int local_only);
-__global__ void k_slist(const Grid* gp, const uint2* cw, const u64* ccoord, const uint32_t* cstart, int* slist,
-                        Meta* meta, int64_t n, int local_only, uint2* sitems, int scap);
-__global__ void k_sparse_pairs(const float4* spts, const uint32_t* cstart, const Grid* gp, int* parent, Meta* meta,
-                               int64_t n, int local_only, const uint2* sitems, int scap);
+__global__ void k_slist(const uint32_t* cstart, int* slist, Meta* meta, int64_t n, int local_only, const Grid* gp,
+                        int all_parents, int* parent, int* size, int* minidx);
 __global__ void k_dense_link(const Grid* gp, const int* crec, const int* ncomp, uint32_t* oflags, DenseCtx C,
                              const uint4* litems, int lhalf, int which);
 __global__ void k_dense_link_all(const Grid* gp, const uint2* cw, const int* crec, const int* ncomp,
@@ -134,7 +143,7 @@ __global__ void k_dense_overflow(const Grid* gp, const uint2* cw, const int* cre
                                  const u64* dcoord, uint32_t* oflags, DenseCtx C);
 __global__ void k_dense_filter(DenseCtx C, int4* items2, int4* slices2, int* idone);
 __global__ void k_dense_items(const Grid* gp, DenseCtx C, const int4* items2, const int4* slices2, int* idone);
-__global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta);
+__global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta, uint32_t rmask);
 __global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);
 cudaError_t ensure_subcell_tables();  // host: upload the fine sub-cell tables (once per device)
 __global__ void k_debug_pred(const float* a, const float* b, int64_t m, float t2, uint8_t* out, float* d2out);

@@ -116,13 +116,14 @@ __device__ __forceinline__ int warp_append(int* counter, bool want) {
 }
 
 // P records for every boundary point, C records for every boundary-touching local root.
-// Roots are points or (dense-grid mode) component nodes n + 8r + k, so the loop runs over
-// all n + 8 * ndense union-find nodes.
+// Roots are points or component nodes node_of(n, rmask, r, k), so the loop runs over the n
+// points and the 8 node slots of every dense record.
 __global__ void __launch_bounds__(256) k_slab_pack(const int* __restrict__ parent, const int* __restrict__ val,
                                                   const int* __restrict__ gidx, int64_t n, int n_owned,
                                                   int n_first, const int* __restrict__ size,
                                                   const int* __restrict__ minidx, const int* __restrict__ ckey,
-                                                  int* __restrict__ rec, int rec_cap, const Meta* __restrict__ meta) {
+                                                  int* __restrict__ rec, int rec_cap, const Meta* __restrict__ meta,
+                                                  uint32_t rmask) {
     pdl_prologue();
     if (meta->status) return;  // header stays zero: no records
     int* P = rec + SLAB_HDR;
@@ -130,9 +131,10 @@ __global__ void __launch_bounds__(256) k_slab_pack(const int* __restrict__ paren
     const int64_t nodes = n + 8 * (int64_t)meta->ndense;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t nr = (nodes + 31) & ~int64_t(31);  // whole warps stay in the loop
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nr; s += stride) {
-        const bool ok = s < nodes;
-        const bool pt = s < n;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nr; u += stride) {
+        const bool ok = u < nodes;
+        const bool pt = u < n;
+        const int64_t s = (pt || !ok) ? u : node_of((int)n, rmask, (int)((u - n) >> 3), (int)((u - n) & 7));
         const int r = ok ? __ldg(parent + s) : 0;
         const int i = pt ? __ldg(val + s) : 0;
         const bool bnd = pt && (i < n_first || i >= n_owned);

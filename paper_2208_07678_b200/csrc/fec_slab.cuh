@@ -11,7 +11,8 @@ __host__ __device__ __forceinline__ int64_t slab_c_off(int64_t rec_cap) { return
 __global__ void k_slab_stats(const int* parent, const int* val, const int* gidx, int64_t n, int n_owned, int n_first,
                              int* size, int* minidx, int* ckey, Meta* meta);
 __global__ void k_slab_pack(const int* parent, const int* val, const int* gidx, int64_t n, int n_owned, int n_first,
-                            const int* size, const int* minidx, const int* ckey, int* rec, int rec_cap, const Meta* meta);
+                            const int* size, const int* minidx, const int* ckey, int* rec, int rec_cap, const Meta* meta,
+                            uint32_t rmask);
 __global__ void k_merge_init(int* hkey, int* hpar, int* gsize, int* gmin, int64_t hc);
 __global__ void k_merge_link(const int* all, int world, int64_t words, int rec_cap, int* hkey, unsigned mask,
                              int* hpar);

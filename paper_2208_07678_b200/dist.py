@@ -167,3 +167,124 @@ def cluster_sharded(points, gidx, n_owned: int, n_first: int, d_th: float, min_s
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     return SlabRunner(points, gidx, n_owned, n_first, rec_cap, d_th, min_size, max_size, world, rank,
                       group).step()
+
+
+# ---- Mode B: index-sharded input -> spatial slabs on the device ----------
+class DevicePartOps:
+    """The steps of Mode B in libfec.so (fec_part_*, include/fec.h), on one device."""
+
+    def __init__(self, device):
+        import torch
+        from . import lib
+        self.L = lib()
+        self.dev = torch.device(device)
+        self.ws = torch.empty(int(self.L.fec_part_workspace_bytes()), dtype=torch.uint8, device=self.dev)
+        self.nl = int(self.L.fec_part_max_layers())
+
+    def _st(self):
+        import torch
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _chk(self, rc):
+        from . import _check
+        _check(rc)
+
+    @staticmethod
+    def _p(t):
+        return t.data_ptr() if t is not None and t.numel() else None
+
+    def bbox(self, points):
+        import torch
+        out = torch.empty(8, dtype=torch.float32, device=self.dev)
+        self.hist_buf = torch.empty(self.nl, dtype=torch.int32, device=self.dev)
+        self._chk(self.L.fec_part_bbox(self._p(points), points.shape[0], out.data_ptr(), self.hist_buf.data_ptr(),
+                                       self.ws.data_ptr(), self.ws.numel(), self._st()))
+        return out
+
+    def hist(self, points, gbb, d_th):
+        self._chk(self.L.fec_part_hist(self._p(points), points.shape[0], gbb.data_ptr(), _f32(d_th),
+                                       self.hist_buf.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._st()))
+        return self.hist_buf
+
+    def plan(self, ghist, world):
+        import torch
+        plan = torch.empty(4 * world + 3, dtype=torch.int64, device=self.dev)
+        self._chk(self.L.fec_part_plan(ghist.data_ptr(), world, plan.data_ptr(), self.ws.data_ptr(),
+                                       self.ws.numel(), self._st()))
+        return plan
+
+    def count(self, points, gidx, gbb, d_th, plan, world):
+        import torch
+        counts = torch.empty(world, dtype=torch.int64, device=self.dev)
+        self._chk(self.L.fec_part_pack(self._p(points), self._p(gidx), points.shape[0], gbb.data_ptr(), _f32(d_th),
+                                       plan.data_ptr(), world, counts.data_ptr(), None, None, self.ws.data_ptr(),
+                                       self.ws.numel(), self._st()))
+        return counts
+
+    def pack(self, points, gidx, gbb, d_th, plan, world, counts, total):
+        import torch
+        sp = torch.empty((max(total, 1), 3), dtype=torch.float32, device=self.dev)
+        sg = torch.empty(max(total, 1), dtype=torch.int32, device=self.dev)
+        if total:
+            self._chk(self.L.fec_part_pack(self._p(points), self._p(gidx), points.shape[0], gbb.data_ptr(),
+                                           _f32(d_th), plan.data_ptr(), world, counts.data_ptr(), sp.data_ptr(),
+                                           sg.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._st()))
+        return sp[:total], sg[:total]
+
+    def order(self, rpts, rgidx, gbb, d_th, plan, world, rank):
+        import torch
+        k = rpts.shape[0]
+        op = torch.empty((max(k, 1), 3), dtype=torch.float32, device=self.dev)
+        og = torch.empty(max(k, 1), dtype=torch.int32, device=self.dev)
+        c3 = torch.empty(3, dtype=torch.int64, device=self.dev)
+        self._chk(self.L.fec_part_order(self._p(rpts), self._p(rgidx), k, gbb.data_ptr(), _f32(d_th),
+                                        plan.data_ptr(), world, rank, c3.data_ptr(), self._p(op), self._p(og),
+                                        self.ws.data_ptr(), self.ws.numel(), self._st()))
+        return op[:k], og[:k], c3
+
+
+def repartition(points, gidx, d_th: float, group=None, ops=None):
+    """Mode B on this rank: `points` (float32 [m, 3]) / `gidx` (int32 [m]) is an arbitrary shard of
+    the cloud; returns (Shard of this rank's slab in fec_slab_local's order, rec_cap).  Collective
+    over `group`: one all-reduce of the bbox, one of the layer histogram, an all-to-all of the
+    counts and one of the points / indices.  `ops` defaults to the device kernels (DevicePartOps);
+    the split sizes of the all-to-all are the only device->host reads."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if ops is None:
+        ops = DevicePartOps(points.device)
+    bb = ops.bbox(points)
+    if world > 1:
+        dist.all_reduce(bb, op=dist.ReduceOp.MIN, group=group)
+    hist = ops.hist(points, bb, d_th)
+    if world > 1:
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    plan = ops.plan(hist, world)
+    ph = plan.cpu().numpy()
+    status = int(ph[4 * world + 2])
+    if status:
+        from . import FecError
+        raise FecError(status, "Mode B partition: the global cloud cannot be cut (non-finite or extent)")
+    rec_cap = int(ph[4 * world + 1])
+    counts = ops.count(points, gidx, bb, d_th, plan, world)
+    recv_counts = torch.empty_like(counts)
+    if world > 1:
+        dist.all_to_all_single(recv_counts, counts, group=group)
+    else:
+        recv_counts.copy_(counts)
+    sc = counts.cpu().tolist()
+    rc = recv_counts.cpu().tolist()
+    sp, sg = ops.pack(points, gidx, bb, d_th, plan, world, counts, int(sum(sc)))
+    rp = torch.empty((int(sum(rc)), 3), dtype=torch.float32, device=points.device)
+    rg = torch.empty(int(sum(rc)), dtype=torch.int32, device=points.device)
+    if world > 1:
+        dist.all_to_all_single(rp, sp, rc, sc, group=group)
+        dist.all_to_all_single(rg, sg, rc, sc, group=group)
+    else:
+        rp.copy_(sp)
+        rg.copy_(sg)
+    op, og, c3 = ops.order(rp, rg, bb, d_th, plan, world, rank)
+    c = c3.cpu().tolist()
+    return Shard(op, og, int(c[0] + c[1]), int(c[0])), rec_cap

@@ -213,3 +213,181 @@ def test_gloo_world2_exchange():
         assert p.exitcode == 0
     res = dict(q.get(timeout=5) for _ in range(2))
     assert res[0] and res[1]
+
+
+# ---- Mode B (device slab partition of index-sharded input), modelled in numpy ----------------
+MAXL = 1 << 20  # fec_part_max_layers()
+
+
+class NumpyPartOps:
+    """numpy model of the fec_part_* steps (include/fec.h "Multi-GPU Mode B"), on CPU tensors, so
+    dist.repartition's collectives run over gloo.  The layer arithmetic is the planner's:
+    floor((x - lo) * (1/(c/2))) >> 1 in fp64, c = fp32(d)(1 + 2^-16)."""
+
+    def bbox(self, points):
+        import torch
+        p = points.numpy()
+        bad = not np.isfinite(p).all()
+        if p.shape[0]:
+            mn, mx = p.min(0), p.max(0)
+        else:
+            mn = np.full(3, np.finfo(np.float32).max, np.float32)
+            mx = -mn
+        return torch.from_numpy(np.concatenate([mn, -mx, [-1.0 if bad else 0.0, 0.0]]).astype(np.float32))
+
+    @staticmethod
+    def _axis(gbb, d):
+        ext = (-gbb[3:6].astype(np.float64)) - gbb[:3].astype(np.float64)
+        axis = int(np.argmax(ext))
+        lo = np.float64(gbb[axis])
+        inv_h = 1.0 / (fdist.cell_edge(d) * 0.5)
+        nl = (int(np.floor((np.float64(-gbb[3 + axis]) - lo) * inv_h)) >> 1) + 1
+        return axis, lo, inv_h, nl
+
+    def _layers(self, p, gbb, d):
+        axis, lo, inv_h, nl = self._axis(gbb, d)
+        return (np.floor((p[:, axis].astype(np.float64) - lo) * inv_h).astype(np.int64) >> 1), nl
+
+    def hist(self, points, gbb, d):
+        import torch
+        lay, nl = self._layers(points.numpy(), gbb.numpy(), d)
+        return torch.from_numpy(np.bincount(lay, minlength=MAXL)[:MAXL].astype(np.int32))
+
+    def plan(self, ghist, world):
+        import torch
+        hist = ghist.numpy().astype(np.int64)
+        nl = int(np.nonzero(hist)[0].max()) + 1 if hist.any() else 1
+        self._nl = nl
+        cum = np.concatenate([[0], np.cumsum(hist[:nl])])
+        n = int(cum[-1])
+        cuts = np.zeros(world + 1, np.int64)
+        cuts[world] = nl
+        for r in range(1, world):
+            b = int(np.searchsorted(cum, (n * r) // world, side="left"))
+            cuts[r] = min(max(b, int(cuts[r - 1]) + 1), nl)
+        owned = cum[cuts[1:]] - cum[cuts[:-1]]
+        first = np.array([hist[cuts[r]] if (r > 0 and cuts[r] < nl) else 0 for r in range(world)], np.int64)
+        halo = np.array([hist[cuts[r + 1]] if (cuts[r + 1] < nl and cuts[r + 1] > cuts[r]) else 0
+                         for r in range(world)], np.int64)
+        first[owned == 0] = 0
+        halo[owned == 0] = 0
+        rec = int((first + halo).max()) if world > 1 else 0
+        return torch.from_numpy(np.concatenate([cuts, owned, first, halo, [rec, 0]]).astype(np.int64))
+
+    def _dest(self, p, gbb, d, plan, world):
+        lay, _ = self._layers(p, gbb.numpy(), d)
+        pl = plan.numpy()
+        cuts, owned = pl[:world + 1], pl[world + 1:2 * world + 1]
+        r = np.searchsorted(cuts[1:world], lay, side="right")  # last r with cuts[r] <= L
+        halo = (r > 0) & (lay == cuts[np.maximum(r, 0)]) & (owned[np.maximum(r - 1, 0)] > 0)
+        return r, halo
+
+    def count(self, points, gidx, gbb, d, plan, world):
+        import torch
+        r, halo = self._dest(points.numpy(), gbb, d, plan, world)
+        c = np.bincount(r, minlength=world) + np.bincount(r[halo] - 1, minlength=world)
+        return torch.from_numpy(c.astype(np.int64))
+
+    def pack(self, points, gidx, gbb, d, plan, world, counts, total):
+        import torch
+        p, g = points.numpy(), gidx.numpy()
+        r, halo = self._dest(p, gbb, d, plan, world)
+        dst = np.concatenate([r, r[halo] - 1])
+        src = np.concatenate([np.arange(len(p)), np.nonzero(halo)[0]])
+        o = np.argsort(dst, kind="stable")
+        return torch.from_numpy(p[src[o]].copy()), torch.from_numpy(g[src[o]].copy())
+
+    def order(self, rpts, rgidx, gbb, d, plan, world, rank):
+        import torch
+        p, g = rpts.numpy(), rgidx.numpy()
+        lay, _ = self._layers(p, gbb.numpy(), d)
+        cuts = plan.numpy()[:world + 1]
+        cat = np.where(lay >= cuts[rank + 1], 2, np.where((rank > 0) & (lay == cuts[rank]), 0, 1))
+        o = np.argsort(cat, kind="stable")
+        c3 = np.bincount(cat, minlength=3).astype(np.int64)
+        return torch.from_numpy(p[o].copy()), torch.from_numpy(g[o].copy()), torch.from_numpy(c3)
+
+
+def _same_slab(sh_b, sh_a):
+    """Mode B's slab equals the host planner's: same owned / first-layer / halo point sets."""
+    gb = sh_b.gidx.numpy() if hasattr(sh_b.gidx, "numpy") else sh_b.gidx
+    ga = sh_a.gidx
+    return (sh_b.n_owned == sh_a.n_owned and sh_b.n_first == sh_a.n_first and
+            set(gb[:sh_b.n_first].tolist()) == set(ga[:sh_a.n_first].tolist()) and
+            set(gb[sh_b.n_first:sh_b.n_owned].tolist()) == set(ga[sh_a.n_first:sh_a.n_owned].tolist()) and
+            set(gb[sh_b.n_owned:].tolist()) == set(ga[sh_a.n_owned:].tolist()))
+
+
+def _worker_mode_b(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ok = True
+        for pts, d in clouds():
+            n = pts.shape[0]
+            lo, hi = (n * rank) // world, (n * (rank + 1)) // world  # index-range shard
+            sh, rec_cap = fdist.repartition(torch.from_numpy(pts[lo:hi].copy()),
+                                            torch.arange(lo, hi, dtype=torch.int32), d, ops=NumpyPartOps())
+            plan = fdist.plan_slabs(pts, d, world)
+            ok &= rec_cap == plan.rec_cap and _same_slab(sh, fdist.shard(pts, plan, rank))
+            # then the Mode A protocol on the received slab, against the oracle on the whole cloud
+            sh_np = fdist.Shard(sh.points.numpy(), sh.gidx.numpy(), sh.n_owned, sh.n_first)
+            rec = model_local(sh_np, d, rec_cap)
+            state = getattr(model_local, "state", None)
+            allrec = fdist.exchange_records(torch.from_numpy(rec), world).numpy()
+            lab = model_merge(allrec, world, rank, rec_cap, sh_np, state, 1, HUGE)
+            parts = [None] * world
+            dist.all_gather_object(parts, (sh_np.gidx[:sh_np.n_owned], lab))
+            if rank == 0:
+                full = np.full(n, -7, np.int32)
+                for g, l in parts:
+                    full[g] = l
+                ok &= bool(np.array_equal(full, oracle.fec(pts, d, 1, HUGE)))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mode_b_model_matches_planner_single_process():
+    # world 1..5 emulated by hand (the model's collectives are elementwise min / sum / concat)
+    ops = NumpyPartOps()
+    import torch
+    for world in (1, 2, 3, 5):
+        for pts, d in clouds():
+            n = pts.shape[0]
+            shards = [(torch.from_numpy(pts[(n * r) // world:(n * (r + 1)) // world].copy()),
+                       torch.arange((n * r) // world, (n * (r + 1)) // world, dtype=torch.int32)) for r in range(world)]
+            bb = torch.stack([ops.bbox(p) for p, _ in shards]).min(0).values
+            hist = sum(ops.hist(p, bb, d).to(torch.int64) for p, _ in shards).to(torch.int32)
+            plan = ops.plan(hist, world)
+            ref = fdist.plan_slabs(pts, d, world)
+            assert np.array_equal(plan.numpy()[:world + 1][:len(ref.cuts)], ref.cuts)
+            sends = [ops.pack(p, g, bb, d, plan, world, None, 0) for p, g in shards]
+            dests = [ops._dest(p.numpy(), bb, d, plan, world) for p, _ in shards]
+            for r in range(world):
+                rp, rg = [], []
+                for (sp, sg), (dr, halo) in zip(sends, dests):
+                    dst = np.sort(np.concatenate([dr, dr[halo] - 1]), kind="stable")
+                    rp.append(sp.numpy()[dst == r])
+                    rg.append(sg.numpy()[dst == r])
+                op, og, c3 = ops.order(torch.from_numpy(np.concatenate(rp)), torch.from_numpy(np.concatenate(rg)),
+                                       bb, d, plan, world, r)
+                sh = fdist.Shard(op, og, int(c3[0] + c3[1]), int(c3[0]))
+                assert _same_slab(sh, fdist.shard(pts, ref, r)), (world, r)
+
+
+def test_gloo_world2_mode_b():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_mode_b, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res[0] and res[1]

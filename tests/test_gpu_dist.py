@@ -121,3 +121,74 @@ def test_slab_argument_errors(fec):
         fec.slab_merge(allrec, 2, 2, 1, 10, lab, ws, st)  # rank >= world
     with pytest.raises(fec.FecError):
         fec.slab_merge(allrec, 2, 0, 1, 10, lab, ws, fec.SlabState())  # state not filled
+
+
+def run_mode_b_emulated(fec, pts, d, world):
+    """Mode B with the ranks emulated on one GPU: fec_part_* per rank, the collectives replaced
+    by their definitions (min / sum / exchange of the packed segments)."""
+    from paper_2208_07678_b200 import dist as fdist
+    n = pts.shape[0]
+    ranks = []
+    for r in range(world):
+        lo, hi = (n * r) // world, (n * (r + 1)) // world
+        ops = fdist.DevicePartOps("cuda")
+        ranks.append((ops, torch.from_numpy(pts[lo:hi].copy()).cuda(), torch.arange(lo, hi, dtype=torch.int32, device="cuda")))
+    bbs = [ops.bbox(p) for ops, p, _ in ranks]
+    gbb = torch.stack(bbs).min(0).values
+    hists = [ops.hist(p, gbb, d) for ops, p, _ in ranks]
+    ghist = torch.stack([h.to(torch.int64) for h in hists]).sum(0).to(torch.int32)
+    plans = [ops.plan(ghist, world) for ops, _, _ in ranks]
+    for pl in plans[1:]:
+        assert torch.equal(pl, plans[0])
+    rec_cap = int(plans[0][4 * world + 1].item())
+    sends = []
+    for (ops, p, g), pl in zip(ranks, plans):
+        c = ops.count(p, g, gbb, d, pl, world)
+        sp, sg = ops.pack(p, g, gbb, d, pl, world, c, int(c.sum().item()))
+        sends.append((c.cpu().tolist(), sp, sg))
+    out = []
+    for r, ((ops, _, _), pl) in enumerate(zip(ranks, plans)):
+        rp, rg = [], []
+        for c, sp, sg in sends:
+            o = sum(c[:r])
+            rp.append(sp[o:o + c[r]])
+            rg.append(sg[o:o + c[r]])
+        op, og, c3 = ops.order(torch.cat(rp), torch.cat(rg), gbb, d, pl, world, r)
+        c3 = c3.cpu().tolist()
+        out.append(fdist.Shard(op, og, int(c3[0] + c3[1]), int(c3[0])))
+    return out, rec_cap
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_mode_b_partition_equals_planner(fec, world):
+    """The device partition (fec_part_*) gives every rank exactly the host planner's slab (owned,
+    first layer, halo), and Mode A on those slabs equals the oracle on the whole cloud."""
+    from paper_2208_07678_b200 import dist as fdist
+    from test_dist_cpu import clouds, _same_slab
+    cases = list(clouds()) + [(synth.make_config("C2").points, 0.35),
+                              (synth.make_config("C4", scale=0.01).points, 0.25)]
+    for k, (pts, d) in enumerate(cases):
+        shards, rec_cap = run_mode_b_emulated(fec, pts, d, world)
+        plan = fdist.plan_slabs(pts, d, world)
+        assert rec_cap == plan.rec_cap, (k, rec_cap, plan.rec_cap)
+        for r, sh in enumerate(shards):
+            sh_h = fdist.Shard(sh.points.cpu().numpy(), sh.gidx.cpu().numpy(), sh.n_owned, sh.n_first)
+            assert _same_slab(sh_h, fdist.shard(pts, plan, r)), (k, world, r)
+        # Mode A on the device-partitioned slabs
+        words = fec.slab_record_words(rec_cap)
+        states, bufs, wss = [], [], []
+        for sh in shards:
+            ws = torch.empty(fec.slab_workspace_bytes(sh.points.shape[0], world, rec_cap), dtype=torch.uint8,
+                             device="cuda")
+            rec = torch.zeros(words, dtype=torch.int32, device="cuda")
+            states.append(fec.slab_local(sh.points, sh.gidx, sh.n_owned, sh.n_first, d, rec, rec_cap, ws))
+            bufs.append(rec)
+            wss.append(ws)
+        allrec = torch.cat(bufs)
+        labels = np.full(pts.shape[0], -7, np.int32)
+        for r, sh in enumerate(shards):
+            lab = torch.full((sh.n_owned,), -9, dtype=torch.int32, device="cuda")
+            fec.slab_merge(allrec, world, r, 1, HUGE, lab, wss[r], states[r])
+            torch.cuda.synchronize()
+            labels[sh.gidx[:sh.n_owned].cpu().numpy()] = lab.cpu().numpy()
+        assert_same(labels, oracle.fec(pts, d, 1, HUGE), f"mode B case {k} world {world}")

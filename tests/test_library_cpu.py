@@ -89,7 +89,11 @@ def test_node_id_guard(libpath):
     """Union-find node ids are n + 8 * (dense cells) in int32: n beyond the bound is rejected on
     the host (and its workspace size is 0), before any CUDA call."""
     L = fec.lib()
-    kmax = (2**31 - 1) // 8 * 7 - 1024
+    kmax = L.fec_max_points()
+    # node ids: n points + 8 slots per dense record, record capacity n // 7 + 16 rounded up to a
+    # power of two -- all below 2^31 at kmax, not at kmax + 1
+    cap = lambda n: 1 << (n // 7 + 16 - 1).bit_length()
+    assert kmax + 8 * cap(kmax) < 2**31 - 1 <= kmax + 1 + 8 * cap(kmax + 1)
     assert fec.workspace_bytes(kmax + 1) == 0 and fec.workspace_bytes(kmax) > 0
     assert L.fec_cluster_ws(None, kmax + 1, 1.0, 1, 4, None, None, 0, None) == fec.ERR_INVALID_ARGUMENT
     assert b"node ids" in L.fec_last_error()
