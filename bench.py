@@ -861,16 +861,35 @@ def main():
     dom = max(rs, key=lambda k: rs[k])
     peak, peak_src = load_peaks()
     ach = algorithmic_bytes(dom, n, st) / (rs[dom] * 1e-3) / 1e9
-    traffic = None
+    tinfo = {}
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(args.config, {}).get(dom)
+            tinfo = json.load(open(tfile)).get(args.config, {})
         except Exception:
-            traffic = None
+            tinfo = {}
+
+    def traffic_of(stage):
+        e = tinfo.get(stage)
+        return e.get("dram_bytes") if isinstance(e, dict) else None
+
     roofline = {"bound": "hbm", "kernel": dom, "kernels": STAGE_KERNELS.get(dom, dom), "achieved": ach,
-                "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes": algorithmic_bytes(dom, n, st), "stage_ms": rs[dom]}
+                "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic_of(dom), "peak_source": peak_src,
+                "algorithmic_bytes": algorithmic_bytes(dom, n, st), "stage_ms": rs[dom],
+                "traffic_source": tinfo.get("source")}
+    # the north star's target stage (neighbour scan + union-find, 28 B/pt), reported
+    # whether or not it dominates; its dense-dense links run on a side stream concurrently with
+    # the scatter, so its main-stream stage time excludes them -- the ncu sum of its kernels
+    # (serialised, cold cache) is given beside it
+    a67 = rs.get("a6a7_scan_union", 0.0)
+    a67_bytes = algorithmic_bytes("a6a7_scan_union", n, st)
+    e67 = tinfo.get("a6a7_scan_union") if isinstance(tinfo.get("a6a7_scan_union"), dict) else {}
+    roofline_a6a7 = {"bound": "hbm", "kernel": "a6a7_scan_union", "kernels": STAGE_KERNELS["a6a7_scan_union"],
+                     "achieved": a67_bytes / (a67 * 1e-3) / 1e9 if a67 > 0 else None, "peak": peak, "unit": "GB/s",
+                     "frac": a67_bytes / (a67 * 1e-3) / 1e9 / peak if a67 > 0 else None,
+                     "traffic": e67.get("dram_bytes"), "stage_ms": a67,
+                     "ncu_kernels_us_incl_side_stream": e67.get("ncu_us"),
+                     "algorithmic_bytes": a67_bytes}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -897,6 +916,7 @@ def main():
                        "grid_dims": st["dims"]},
             "e2e": e2e,
             "roofline": roofline,
+            "roofline_a6a7": roofline_a6a7,
             "cpu_baseline": cpu,
             "gpu_launches": st["launches"] * args.steps,
             "clocks": clk.summary(),

@@ -3,6 +3,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1251,6 +1252,25 @@ const char* fec_last_error(void) { return g_err.c_str(); }
 // the other C-ABI translation units (fec_ground.cu) report through the same thread-local slot
 void fec::set_last_error(const std::string& msg) { g_err = msg; }
 bool fec::timing_enabled() { return g_timing != 0; }
+bool fec::debug_sync_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FEC_DEBUG_SYNC");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+cudaError_t fec::debug_sync_after(const void* kernel, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return cudaSuccess;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        const char* name = "?";
+        cudaFuncGetName(&name, kernel);
+        std::fprintf(stderr, "[fec] FEC_DEBUG_SYNC: kernel %s failed: %s\n", name, cudaGetErrorString(e));
+        g_err = std::string("kernel ") + name + ": " + cudaGetErrorString(e);
+    }
+    return e;
+}
 bool fec::pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("FEC_PDL");

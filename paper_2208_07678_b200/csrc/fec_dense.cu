@@ -1375,7 +1375,7 @@ __global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent,
         const int s = node_of(nbase, rmask, (int)(t >> 3), (int)(t & 7));
         int curr = ld_parent(parent, s), next;
         if (curr == s) continue;
-        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
         st_parent(parent, s, curr);
     }
 }

@@ -23,6 +23,10 @@ __device__ __forceinline__ void pdl_prologue() {
 }
 
 bool pdl_enabled();  // FEC_PDL=0 in the environment turns it off (A/B measurements)
+// FEC_DEBUG_SYNC=1: synchronise the stream after every launch (outside stream capture) and
+// report the first failing kernel by name on stderr and in fec_last_error() (debugging aid)
+bool debug_sync_enabled();
+cudaError_t debug_sync_after(const void* kernel, cudaStream_t st);
 
 template <typename... KArgs>
 struct PdlLaunch {
@@ -33,7 +37,9 @@ struct PdlLaunch {
     cudaError_t operator()(Args&&... args) {
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 1 : 0;
-        return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+        if (e == cudaSuccess && debug_sync_enabled()) return debug_sync_after(reinterpret_cast<const void*>(k), cfg.stream);
+        return e;
     }
 };
 template <typename... KArgs>
@@ -134,16 +140,31 @@ __device__ __forceinline__ u64 hash_cell(u64 pc) {
 }
 
 // ---- union-find over sorted positions (ECL-CC style) ----------------------------------
-// Invariant: parent[x] >= x, and a root r has parent[r] == r.  Hooks attach the SMALLER
-// root under the larger one with atomicCAS (performed at L2, always on the current value);
-// path compression only ever raises a parent.  Roots are therefore the highest sorted
-// position of their set: the kernels sweep the sorted order upwards, so the roots that
-// finds reach sit near the sweep front (in L2), not at the far start of the array.
+// Invariant: parents are strictly "above" their children in a fixed total order and a root r
+// has parent[r] == r.  Hooks attach the lower root under the higher one with atomicCAS
+// (performed at L2, always on the current value); path compression only ever moves a parent
+// up.  FEC_UF_MINROOT (default): "above" = smaller id, so a set's root is its SMALLEST sorted
+// position.  The union kernels sweep the sorted order upwards, so a component's root is
+// established early and the points met later hook straight under it: trees stay shallow
+// (the opposite order moves the root up with the sweep and deepens the tree at every hook).
+// Component nodes (ids above every point) then hang under a point whenever a dense cell's
+// component touches a sparse cell's point; nothing depends on roots being nodes.
 // Reads are plain (L1-cacheable) loads: a stale value is still an ancestor, so a find may
 // return a non-root; the hook's CAS then fails and returns the current parent, and the loop
-// continues from there (values strictly increase, so it terminates).  Two finds that return
+// continues from there (values move strictly up, so it terminates).  Two finds that return
 // the same node prove the inputs are connected, so skipping on equal roots is always
 // sound.  The loads/stores are inline PTX so the compiler cannot merge or hoist them.
+#ifndef FEC_UF_MINROOT
+#define FEC_UF_MINROOT 1
+#endif
+// true iff `a` lies strictly above `b` in the union-find order
+__host__ __device__ __forceinline__ bool uf_above(int a, int b) {
+#if FEC_UF_MINROOT
+    return a < b;
+#else
+    return a > b;
+#endif
+}
 __device__ __forceinline__ int ld_parent(const int* p, int x) {
     int v;
     asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p + x) : "memory");
@@ -152,12 +173,18 @@ __device__ __forceinline__ int ld_parent(const int* p, int x) {
 __device__ __forceinline__ void st_parent(int* p, int x, int v) {
     asm volatile("st.global.b32 [%0], %1;" ::"l"(p + x), "r"(v) : "memory");
 }
+// The root of v by a read-only walk (no writes: callers store the result themselves).
+__device__ __forceinline__ int uf_root(const int* parent, int v) {
+    int curr = ld_parent(parent, v), next;
+    while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
+    return curr;
+}
 
 __device__ __forceinline__ int uf_find(int* parent, int v) {
     int curr = ld_parent(parent, v);
     if (curr != v) {
         int prev = v, next;
-        while (curr < (next = ld_parent(parent, curr))) {
+        while (uf_above(next = ld_parent(parent, curr), curr)) {
             st_parent(parent, prev, next);  // pointer jumping: prev skips to its grandparent
             prev = curr;
             curr = next;
@@ -169,8 +196,8 @@ __device__ __forceinline__ int uf_find(int* parent, int v) {
 __device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
     int ra = uf_find(parent, a), rb = uf_find(parent, b);
     while (ra != rb) {
-        if (ra > rb) { int t = ra; ra = rb; rb = t; }
-        int old = atomicCAS(parent + ra, ra, rb);  // hook smaller root under larger
+        if (uf_above(ra, rb)) { int t = ra; ra = rb; rb = t; }
+        int old = atomicCAS(parent + ra, ra, rb);  // hook the lower root under the higher one
         if (old == ra) return;
         ra = uf_find(parent, old);
         rb = uf_find(parent, rb);

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) k_flatten(int* __restrict__ parent, int64
             minidx[s] = 0x7fffffff;
             continue;
         }
-        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
         st_parent(parent, (int)s, curr);
     }
 }
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, in
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         int curr = ld_parent(parent, (int)s), next;
         if (curr == (int)s) continue;
-        while (curr < (next = ld_parent(parent, curr))) curr = next;
+        while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
         st_parent(parent, (int)s, curr);
     }
 }
@@ -435,7 +435,7 @@ __device__ __forceinline__ void node_stats_body(int* __restrict__ parent, const 
             if (curr == node) {  // a root keeps its own totals
                 if (meta->instrument) atomicAdd(&meta->components, 1ull);
             } else {
-                while (curr < (next = ld_parent(parent, curr))) curr = next;
+                while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
                 st_parent(parent, node, curr);
                 c = size[node];
                 if (c) {
@@ -479,7 +479,7 @@ __device__ __forceinline__ void sparse_stats_body(int* __restrict__ parent, cons
                 curr = ld_parent(parent, s);
                 int next;
                 if (curr != s) {
-                    while (curr < (next = ld_parent(parent, curr))) curr = next;
+                    while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
                     st_parent(parent, s, curr);
                 } else if (meta->instrument) {
                     atomicAdd(&meta->components, 1ull);

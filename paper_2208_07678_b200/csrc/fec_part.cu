@@ -31,8 +31,8 @@ __device__ __forceinline__ float ord2f(unsigned u) {
 __global__ void __launch_bounds__(256) k_part_init(unsigned* __restrict__ state, int* __restrict__ hist) {
     pdl_prologue();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < 3) state[t] = 0xffffffffu;
-    else if (t < 6) state[t] = 0u;
+    if (t < 3) state[t] = f2ord(__int_as_float(0x7f800000));        // +inf: an empty shard's min
+    else if (t < 6) state[t] = f2ord(__int_as_float(0xff800000));   // -inf: an empty shard's max
     else if (t < 8) state[t] = 0u;
     for (int i = t; i < kPartMaxLayers; i += gridDim.x * blockDim.x) hist[i] = 0;
 }
@@ -141,8 +141,11 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int* __restrict__ hist
     __shared__ long long wsum[32];
     __shared__ long long carry;
     const int nl = info[1];
-    if (info[2]) return;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (info[2]) {  // the cloud cannot be cut: a deterministic empty plan (k_part_status adds why)
+        for (int i = tid; i < 4 * world + 2; i += blockDim.x) plan[i] = 0;
+        return;
+    }
     if (tid == 0) carry = 0;
     __syncthreads();
     for (int b = 0; b < nl; b += 1024) {  // block scan in chunks: cum[k] = sum hist[< k]

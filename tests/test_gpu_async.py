@@ -179,3 +179,20 @@ def test_foreign_stream_ordering(fec):
         lab = fec.cluster(x, w.d_th, w.min_size, w.max_size, stream=s, check=False)
         s.synchronize()
         assert_same(lab.cpu().numpy(), want, "foreign stream")
+
+
+def test_debug_sync_flag_reports_nothing_on_a_clean_run(fec):
+    """FEC_DEBUG_SYNC=1 (synchronise after every launch, name the failing kernel) on a clean run:
+    same labels, no report."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); import numpy as np, torch, synth, oracle; "
+            "import paper_2208_07678_b200 as fec; w = synth.make_config('C2'); "
+            "lab = fec.cluster(torch.from_numpy(w.points).cuda(), w.d_th, w.min_size, w.max_size).cpu().numpy(); "
+            "assert np.array_equal(lab, oracle.fec(w.points, w.d_th, w.min_size, w.max_size)); print('ok')")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "FEC_DEBUG_SYNC": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+    assert "FEC_DEBUG_SYNC" not in r.stderr
