@@ -23,7 +23,7 @@ NVCC_FLAGS = [
     "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-v",
-]
+] + [f"-D{k}={v}" for k, v in (("FEC_UF_RELAXED", os.environ.get("FEC_UF_RELAXED")),) if v is not None]
 
 
 def _stale() -> bool:

@@ -504,7 +504,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const Grid* gp = L.grid;
     const int* gstatus = &L.grid->status;
     const int* gkeysort = &L.grid->key_sort;
-    pdl(k_zero, di.sms * 4, 256, 0, st)(gp, L.cw, L.hkey, L.slots, L.arena, L.arena_words);
+    // (small clouds: a small grid -- the device-sized words are few and launch latency dominates)
+    const bool small = n <= kSmallN;
+    pdl(k_zero, small ? 64 : di.sms * 4, 256, 0, st)(gp, L.cw, L.hkey, L.slots, L.arena, L.arena_words);
     ++launches;
 
     const unsigned ew = grid_for(n, 256, cap * 4);
@@ -512,7 +514,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const int64_t dwords = n / 32 + 1;
     const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
     const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
-    const unsigned cs_blocks = (unsigned)std::min<int64_t>(L.cs_tiles, di.sms * 8);
+    const unsigned cs_blocks = (unsigned)std::min<int64_t>(L.cs_tiles, small ? 32 : di.sms * 8);
     DenseCtx dctx{};
     dctx.spts = L.spts;
     dctx.cstart = L.cstart;
@@ -577,7 +579,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // the dense-dense certain unions need no point: they run on the side stream while the
     // points are scattered and initialised
     SideStream* side = nullptr;
-    FEC_CUDA_RC(side_stream(&side));
+    if (!small) FEC_CUDA_RC(side_stream(&side));  // (small clouds: the fork/join would cost more)
     if (side) {
         FEC_CUDA(cudaEventRecord(side->fork, st));
         FEC_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_zero(const Grid* __restrict__ gp, uint2
                                              u64* __restrict__ hkey, int64_t slots, uint32_t* __restrict__ arena,
                                              int64_t arena_words) {
     pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_LOAD_GRID(gp);  // (right after k_bbox: the Grid is only safe after the wait)
     if (g.status) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -229,8 +229,7 @@ __global__ void __launch_bounds__(256) k_zero(const Grid* __restrict__ gp, uint2
 // counting path) makes the runs long and the distinct words per warp few.
 __global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
                                               uint2* __restrict__ cw) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int lane = threadIdx.x & 31;
@@ -287,8 +286,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, ui
                                                      u64* __restrict__ ccoord, const Grid* __restrict__ gp,
                                                      Meta* __restrict__ meta, unsigned long long* __restrict__ state,
                                                      unsigned int* __restrict__ counter) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     __shared__ uint32_t s[CS_TILE];
     __shared__ uint32_t sbits[CS_TILE];  // the tile's words, for the emission (no reload)
@@ -437,8 +435,7 @@ __device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int
 __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
                                                 const uint2* __restrict__ cw, uint32_t* __restrict__ count,
                                                 u64* __restrict__ cocc, int* __restrict__ cmin) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
@@ -525,8 +522,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
 __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n,
                                                  const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                  uint32_t* __restrict__ cursor, float4* __restrict__ spts) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots];
@@ -593,8 +589,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                                               int* __restrict__ size, int* __restrict__ minidx,
                                               int* __restrict__ sidx, const Meta* __restrict__ meta,
                                               int all_parents) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     // node-tail clouds of the single-GPU path read no sorted-order array of the dense points
     // (node statistics, k_relabel_in): k_slist initialises the points of sparse cells instead
@@ -676,8 +671,7 @@ __global__ void __launch_bounds__(256) k_lkey(const float* __restrict__ p, int64
                                              uint32_t* __restrict__ key, int* __restrict__ val,
                                              uint32_t* __restrict__ ghist, uint32_t* __restrict__ state0,
                                              int64_t state_words) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || !g.key_sort) return;
     __shared__ uint32_t h[4][256];
     for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
@@ -748,8 +742,7 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
                                                 u64* __restrict__ cocc, int* __restrict__ parent,
                                                 int* __restrict__ sidx, int* __restrict__ size,
                                                 int* __restrict__ minidx, const Meta* __restrict__ meta) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || !g.key_sort) return;
     const uint32_t* __restrict__ key = (g.passes & 1) ? key1 : key0;  // the sort's output buffers
     const int* __restrict__ val = (g.passes & 1) ? val1 : val0;
@@ -952,8 +945,7 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
                                                uint32_t* __restrict__ oflags, DenseCtx C, uint4* __restrict__ litems,
                                                int lhalf, const int* __restrict__ cmin, const int* __restrict__ sidx,
                                                int node_stats) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     // node-level statistics of single-component records come from their cell: the count is
     // the cell's size and the minimum input index was taken while counting (counting path;
@@ -1087,8 +1079,7 @@ __global__ void __launch_bounds__(256) k_dparent(const float4* __restrict__ spts
                                                 int nbase, int* __restrict__ parent, const Meta* __restrict__ meta,
                                                 const int* __restrict__ sidx, int* __restrict__ size,
                                                 int* __restrict__ minidx, int node_stats, int64_t n) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     const int lane = threadIdx.x & 31;
     const int nd = meta->ndense;
@@ -1262,8 +1253,7 @@ __device__ __forceinline__ void dense_link_serial(int r, int k, const Grid& g, c
 __global__ void __launch_bounds__(256, 4) k_dense_link(const Grid* __restrict__ gp, const int* __restrict__ crec,
                                                    const int* __restrict__ ncomp, uint32_t* __restrict__ oflags,
                                                    DenseCtx C, const uint4* __restrict__ litems, int lhalf, int which) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || C.meta->list_overflow) return;
     __shared__ signed char soff[26][3];
     if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
@@ -1285,8 +1275,7 @@ __global__ void __launch_bounds__(256) k_dense_link_all(const Grid* __restrict__
                                                        const int* __restrict__ crec, const int* __restrict__ ncomp,
                                                        const u64* __restrict__ dcoord,
                                                        uint32_t* __restrict__ oflags, DenseCtx C) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || !C.meta->list_overflow) return;
     const int64_t total = 27 * (int64_t)C.meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -1311,8 +1300,7 @@ __global__ void __launch_bounds__(256) k_dense_overflow(const Grid* __restrict__
                                                        const int* __restrict__ crec, const int* __restrict__ ncomp,
                                                        const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
                                                        DenseCtx C) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     const int nd = C.meta->ndense;
     if (C.meta->nitems <= C.item_cap) return;  // nothing overflowed
@@ -1388,8 +1376,7 @@ constexpr int kAPer = 4;
 __global__ void __launch_bounds__(256) k_dense_items(const Grid* __restrict__ gp, DenseCtx C,
                                                     const int4* __restrict__ items2,
                                                     const int4* __restrict__ slices2, int* __restrict__ idone) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     __shared__ float4 abuf_all[256 / kWarp][32 * kAPer];
     const int lane = threadIdx.x & 31;
@@ -1653,8 +1640,7 @@ __global__ void __launch_bounds__(256, 8) k_union_sparse(const float4* __restric
                                                      const uint32_t* __restrict__ cstart, const Grid* __restrict__ gp,
                                                      int* __restrict__ parent, Meta* __restrict__ meta, int64_t n,
                                                      int local_only) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     union_sparse_body(spts, cw, ccoord, cstart, g, parent, meta, n, local_only);
 }
 // Node-level tail (see node_accumulate): every used component node finds its root, is
@@ -1682,8 +1668,7 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
                                                            const Grid* __restrict__ gp,
                                                            int* __restrict__ parent, Meta* __restrict__ meta,
                                                            int64_t n, int local_only) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || (!local_only && 4 * (int64_t)meta->cells > n)) return;
     const uint32_t nitems = (uint32_t)meta->nsparse;
     const int lane = threadIdx.x & 31, sub = lane & 15, half = lane >> 4;
@@ -1778,8 +1763,7 @@ __global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p,
                                                    const float4* __restrict__ spts, const int* __restrict__ parent,
                                                    const int* __restrict__ minidx, int* __restrict__ labels,
                                                    const Meta* __restrict__ meta) {
-    pdl_prologue();
-    FEC_LOAD_GRID(gp);
+    FEC_PROLOGUE_GRID(gp);
     if (g.status || 4 * (int64_t)meta->cells > n) return;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t groups = (n + 3) / 4;

@@ -120,6 +120,18 @@ struct Grid {
     __syncthreads();                                            \
     const Grid& g = fec_grid_sh_
 
+// The same, with the PDL prologue in between: the Grid is written once per call, by a1 (k_bbox)
+// or by the host (batch mode, a copy that ends the PDL chain), and a kernel starts only after the
+// kernel two places before it has completed (every kernel triggers its dependents after its own
+// wait).  So every kernel except the one right after k_bbox (k_zero) may read the Grid BEFORE its
+// wait, overlapping that load's latency with the previous kernel's tail.
+#define FEC_PROLOGUE_GRID(gp)                                   \
+    __shared__ Grid fec_grid_sh_;                               \
+    if (threadIdx.x == 0) fec_grid_sh_ = *(gp);                 \
+    pdl_prologue();                                             \
+    __syncthreads();                                            \
+    const Grid& g = fec_grid_sh_
+
 // Sub-cell coordinate on one axis: floor((x - lo) * inv_h).  Cell = sub >> 1 and the octant
 // bit = sub & 1, so cell and sub-cell always agree.  Monotone in x (DESIGN.md §4.2 shows
 // that pred-true pairs differ by <= 2 sub-cells and <= 1 cell on every axis).
@@ -165,13 +177,27 @@ __host__ __device__ __forceinline__ bool uf_above(int a, int b) {
     return a > b;
 #endif
 }
+// FEC_UF_RELAXED=1 makes the racing parent loads / stores PTX relaxed atomics at GPU scope
+// (the memory model's well-defined form of a racy access; they bypass L1), instead of weak
+// accesses (L1-cacheable; a stale value is still an ancestor, see above).
+#ifndef FEC_UF_RELAXED
+#define FEC_UF_RELAXED 0
+#endif
 __device__ __forceinline__ int ld_parent(const int* p, int x) {
     int v;
+#if FEC_UF_RELAXED
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p + x) : "memory");
+#else
     asm volatile("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p + x) : "memory");
+#endif
     return v;
 }
 __device__ __forceinline__ void st_parent(int* p, int x, int v) {
+#if FEC_UF_RELAXED
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p + x), "r"(v) : "memory");
+#else
     asm volatile("st.global.b32 [%0], %1;" ::"l"(p + x), "r"(v) : "memory");
+#endif
 }
 // The root of v by a read-only walk (no writes: callers store the result themselves).
 __device__ __forceinline__ int uf_root(const int* parent, int v) {

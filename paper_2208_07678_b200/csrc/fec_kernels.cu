@@ -95,15 +95,29 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ p, PlanA
         // 4 points = 12 floats = 3 float4 per quad; the pointer is 16-byte aligned
         const float4* q = reinterpret_cast<const float4*>(p);
         const int64_t nq = n >> 2;
-        for (int64_t i = t0; i < nq; i += stride) {
-            float4 u = __ldg(q + 3 * i), v4 = __ldg(q + 3 * i + 1), w4 = __ldg(q + 3 * i + 2);
-            float v[12] = {u.x, u.y, u.z, u.w, v4.x, v4.y, v4.z, v4.w, w4.x, w4.y, w4.z, w4.w};
+        // two quads (96 bytes) in flight per thread and iteration
+        for (int64_t i = t0; i < nq; i += 2 * stride) {
+            const bool two = i + stride < nq;
+            float4 u[2], v4[2], w4[2];
 #pragma unroll
-            for (int k = 0; k < 12; ++k) bb_acc(v[k], mn[k % 3], mx[k % 3], bad);
+            for (int h = 0; h < 2; ++h) {
+                const int64_t ii = h ? (two ? i + stride : i) : i;
+                u[h] = __ldg(q + 3 * ii);
+                v4[h] = __ldg(q + 3 * ii + 1);
+                w4[h] = __ldg(q + 3 * ii + 2);
+            }
 #pragma unroll
-            for (int j = 0; j < 3; ++j)
-                nearc += fabsf(v[3 * j + 3] - v[3 * j]) <= near && fabsf(v[3 * j + 4] - v[3 * j + 1]) <= near &&
-                         fabsf(v[3 * j + 5] - v[3 * j + 2]) <= near;
+            for (int h = 0; h < 2; ++h) {
+                if (h && !two) break;
+                float v[12] = {u[h].x, u[h].y, u[h].z, u[h].w, v4[h].x, v4[h].y, v4[h].z, v4[h].w,
+                               w4[h].x, w4[h].y, w4[h].z, w4[h].w};
+#pragma unroll
+                for (int k = 0; k < 12; ++k) bb_acc(v[k], mn[k % 3], mx[k % 3], bad);
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    nearc += fabsf(v[3 * j + 3] - v[3 * j]) <= near && fabsf(v[3 * j + 4] - v[3 * j + 1]) <= near &&
+                             fabsf(v[3 * j + 5] - v[3 * j + 2]) <= near;
+            }
         }
         tail_start = nq << 2;
     }
