@@ -181,6 +181,7 @@ struct Layout {
     int* crec;          // [n]   dense record id of a dense cell
     uint32_t* slot;     // [n]   per-cell scatter cursors
     int* sidx;          // [n]   input index of each sorted position
+    uint32_t* pcode;    // [n]   counting path: compact cell id << 6 | fine sub-cell per input point
     int* dlist;         // dense record -> compact cell id
     uint32_t* dwpos;    // [n/32+2] popcount prefix of the dense bits
     u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
@@ -240,6 +241,7 @@ Layout carve(char* base, int64_t n) {
     L.crec = cv.take<int>(n);
     L.slot = cv.take<uint32_t>(n);
     L.sidx = cv.take<int>(n);
+    L.pcode = cv.take<uint32_t>(n);
     L.dlist = cv.take<int>(dense_max(n));
     L.dwpos = cv.take<uint32_t>(dwords + 1);
     L.cocc = cv.take<u64>(n);
@@ -555,7 +557,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
                                         L.ctr + 0);
     ++launches;
     if (count_path) {
-        pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin);
+        pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin, L.pcode, L.meta);
         launches += 1 + exclusive_scan_lb(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.sa_state, L.ctr + 1, cap,
                                           gstatus, gkeysort, st);
         pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta, gp, L.crec);
@@ -592,7 +594,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     mark(3, st);
     if (count_path) {
         // slot = per-cell cursors here
-        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts);
+        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts, L.pcode, L.meta);
         pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, gp, L.cw, L.crec, L.cmask, (int)n, L.parent, L.size, L.minidx,
                                      L.sidx, L.meta, C.node_stats ? 0 : 1);
         ++launches;
@@ -727,7 +729,7 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     // the two returns at once)
     pdl(k_relabel_in, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(pts, n, L.grid, L.cw, L.crec, L.cmask,
                                                                       L.cstart, L.spts, L.parent, L.minidx, labels,
-                                                                      L.meta);
+                                                                      L.meta, L.pcode);
     pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(L.parent, C.val, L.minidx, n, labels, L.meta,
                                                                    B ? B->off_dev : nullptr, B ? B->nclouds : 0);
     ++C.launches;

@@ -409,6 +409,66 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, ui
 // Warp per tile of 128 consecutive points (4 per lane), aggregated through a per-warp
 // shared-memory table: one global atomicAdd (+ atomicOr) per distinct cell per tile and only
 // warp-level synchronisation (the input order is spatially coherent on this path).
+//
+// (Measured alternatives: group reductions with __reduce_*_sync over __match_any_sync peer
+// masks serialise per distinct mask -- 3x slower on C4; a segmented shuffle scan instead of the
+// table, 1.3x slower.)
+//
+// A lane's 4 points fall into at most 4 runs of one compact cell id (k_dscatter's rounds).
+struct PointRuns {
+    uint32_t cid[4];  // compact cell id of each point (~0u past the end)
+    int ri[4];        // run index of each point (runs of equal cid among the lane's 4 points)
+    int off[4];       // position of the point inside its run
+    int q[4];         // fine sub-cell of the point
+};
+__device__ __forceinline__ void point_runs(const Pts4& P, int64_t b4, int64_t n, const Grid& g,
+                                           const uint2* __restrict__ cw, PointRuns& R) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        R.cid[j] = 0xffffffffu;
+        R.q[j] = 0;
+        if (b4 + j < n) {
+            uint32_t lin;
+            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, R.q[j]);
+            R.cid[j] = cid_of(cw, lin);
+        }
+        const bool fresh = j == 0 || R.cid[j] != R.cid[j > 0 ? j - 1 : 0];
+        R.ri[j] = j == 0 ? 0 : R.ri[j > 0 ? j - 1 : 0] + (fresh ? 1 : 0);
+        R.off[j] = fresh ? 0 : R.off[j > 0 ? j - 1 : 0] + 1;
+    }
+}
+
+// 4 consecutive u32 of a per-point array (one 16-byte store when aligned and complete).
+__device__ __forceinline__ void store4(uint32_t* __restrict__ a, int64_t b4, int64_t n, const uint32_t v[4]) {
+    if (b4 + 4 <= n && (reinterpret_cast<uintptr_t>(a + b4) & 15u) == 0) {
+        *reinterpret_cast<uint4*>(a + b4) = make_uint4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (b4 + j < n) a[b4 + j] = v[j];
+    }
+}
+__device__ __forceinline__ void load4(const uint32_t* __restrict__ a, int64_t b4, int64_t n, uint32_t v[4]) {
+    if (b4 + 4 <= n && (reinterpret_cast<uintptr_t>(a + b4) & 15u) == 0) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(a + b4));
+        v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = b4 + j < n ? __ldg(a + b4 + j) : 0u;
+    }
+}
+// PointRuns from the codes k_dcount2 wrote (no coordinates needed).
+__device__ __forceinline__ void point_runs_code(const uint32_t code[4], int64_t b4, int64_t n, PointRuns& R) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        R.cid[j] = b4 + j < n ? code[j] >> 6 : 0xffffffffu;
+        R.q[j] = (int)(code[j] & 63u);
+        const bool fresh = j == 0 || R.cid[j] != R.cid[j > 0 ? j - 1 : 0];
+        R.ri[j] = j == 0 ? 0 : R.ri[j > 0 ? j - 1 : 0] + (fresh ? 1 : 0);
+        R.off[j] = fresh ? 0 : R.off[j > 0 ? j - 1 : 0] + 1;
+    }
+}
+
 constexpr int kWTile = 128;
 constexpr int kWSlots = 256;
 
@@ -434,9 +494,11 @@ __device__ __forceinline__ int wbin_slot(int* keys, uint32_t key, int* used, int
 // by k_dscatter against per-cell cursors.
 __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
                                                 const uint2* __restrict__ cw, uint32_t* __restrict__ count,
-                                                u64* __restrict__ cocc, int* __restrict__ cmin) {
+                                                u64* __restrict__ cocc, int* __restrict__ cmin,
+                                                uint32_t* __restrict__ pcode, const Meta* __restrict__ meta) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
+    const bool wcode = meta->cells <= kCodeCells;
     __shared__ int keys_all[256 / kWarp][kWSlots];
     __shared__ uint32_t cnt_all[256 / kWarp][kWSlots], olo_all[256 / kWarp][kWSlots], ohi_all[256 / kWarp][kWSlots];
     __shared__ int mn_all[256 / kWarp][kWSlots];
@@ -459,6 +521,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         load_pts4(p, n, b4, vec, P);
         // runs of this thread's points in one cell take one table update
         // (a run's first point has its smallest input index)
+        uint32_t code[4] = {0u, 0u, 0u, 0u};
         uint32_t rc = 0xffffffffu, rn = 0u;
         int rfirst = 0;
         u64 rb = 0ull;
@@ -469,6 +532,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
                 int q;
                 dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
                 const uint32_t cid = cid_of(cw, lin);
+                code[j] = (cid << 6) | (uint32_t)q;
                 if (cid != rc) {
                     if (rn) {
                         const int h = wbin_slot(keys, rc, used, nused);
@@ -493,6 +557,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
             if ((uint32_t)rb) atomicOr(olo + h, (uint32_t)rb);
             if ((uint32_t)(rb >> 32)) atomicOr(ohi + h, (uint32_t)(rb >> 32));
         }
+        if (wcode) store4(pcode, b4, n, code);
         __syncwarp();
         const int nu = *nused;
         for (int e = lane; e < nu; e += 32) {
@@ -513,68 +578,72 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
     }
 }
 
-// Counting path, a3: scatter into cell order.  Per warp tile (128 consecutive input points), a
-// shared-memory table of the tile's distinct cells gives each point its rank among the tile's
-// points of its cell; one atomicAdd per distinct cell on the cell's cursor (initialised to the
-// cell start) gives the tile's base inside the cell.  Only the float4 (x, y, z, idx) is written
-// here: the scattered store is the expensive part, and k_dinit derives everything else from
-// the sorted float4s with coalesced accesses.
+// Counting path, a3: scatter into cell order, no shared memory.  Round r of a tile takes every
+// lane's r-th run and groups the lanes holding the same cell with one __match_any_sync
+// (coherent input: usually one or two rounds).  Per round, a group's base inside the cell is
+// one atomicAdd on the cell's cursor (initialised to the cell start) by the group's lowest
+// lane, issued for every round before any result is used; a lane's offset inside the group
+// is the run lengths of the group's lower lanes (three ballots: lengths are 1-4).  A cell's
+// points of one warp tile land contiguously.  Only the float4 (x, y, z, idx) is written here:
+// the scattered store is the expensive part, and k_dinit derives everything else from the
+// sorted float4s with coalesced accesses.
 __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n,
                                                  const Grid* __restrict__ gp, const uint2* __restrict__ cw,
-                                                 uint32_t* __restrict__ cursor, float4* __restrict__ spts) {
+                                                 uint32_t* __restrict__ cursor, float4* __restrict__ spts,
+                                                 const uint32_t* __restrict__ pcode, const Meta* __restrict__ meta) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
-    __shared__ int keys_all[256 / kWarp][kWSlots];
-    __shared__ uint32_t cnt_all[256 / kWarp][kWSlots];
-    __shared__ int used_all[256 / kWarp][kWTile];
-    __shared__ int nused_all[256 / kWarp];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int* keys = keys_all[wid];
-    uint32_t* cnt = cnt_all[wid];
-    int* used = used_all[wid];
-    int* nused = nused_all + wid;
-    for (int k = lane; k < kWSlots; k += 32) { keys[k] = -1; cnt[k] = 0u; }
-    if (lane == 0) *nused = 0;
-    __syncwarp();
+    const bool rcode = meta->cells <= kCodeCells;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWTile; t0 < n; t0 += nw * kWTile) {
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; t0 < n; t0 += nw * 128) {
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
-        int hs[4];
-        uint32_t rk[4];
+        PointRuns R;
+        if (rcode) {
+            uint32_t code[4];
+            load4(pcode, b4, n, code);
+            point_runs_code(code, b4, n, R);
+        } else {
+            point_runs(P, b4, n, g, cw, R);
+        }
+        const int rounds = __reduce_max_sync(0xffffffffu, R.ri[3] + 1);
+        uint32_t base[4] = {0u, 0u, 0u, 0u}, pre[4] = {0u, 0u, 0u, 0u};
+        int lead[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            hs[j] = -1;
-            rk[j] = 0u;
-            if (b4 + j < n) {
-                uint32_t lin;
-                int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
-                const int h = wbin_slot(keys, cid_of(cw, lin), used, nused);
-                hs[j] = h;
-                rk[j] = atomicAdd(cnt + h, 1u);
-            }
+        for (int r = 0; r < 4; ++r) {
+            if (r >= rounds) continue;  // (warp-uniform)
+            uint32_t key = 0xffffffffu, len = 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (R.ri[j] == r && R.cid[j] != 0xffffffffu) {
+                    key = R.cid[j];
+                    ++len;
+                }
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            const unsigned b0 = __ballot_sync(0xffffffffu, len & 1u), b1 = __ballot_sync(0xffffffffu, len & 2u),
+                           b2 = __ballot_sync(0xffffffffu, len & 4u);
+            pre[r] = __popc(peers & lt & b0) + 2 * __popc(peers & lt & b1) + 4 * __popc(peers & lt & b2);
+            lead[r] = __ffs(peers) - 1;
+            if (key != 0xffffffffu && lane == lead[r])
+                base[r] = atomicAdd(cursor + key, __popc(peers & b0) + 2 * __popc(peers & b1) + 4 * __popc(peers & b2));
         }
-        __syncwarp();
-        const int nu = *nused;
-        for (int e = lane; e < nu; e += 32) {
-            const int k = used[e];
-            cnt[k] = atomicAdd(cursor + keys[k], cnt[k]);  // the tile's base inside the cell
+        uint32_t pos[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r >= rounds) continue;
+            const uint32_t b = __shfl_sync(0xffffffffu, base[r], lead[r]) + pre[r];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (R.ri[j] == r) pos[j] = b + (uint32_t)R.off[j];
         }
-        __syncwarp();
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (hs[j] >= 0) spts[cnt[hs[j]] + rk[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
-        __syncwarp();
-        for (int e = lane; e < nu; e += 32) {
-            const int k = used[e];
-            keys[k] = -1;
-            cnt[k] = 0u;
-        }
-        if (lane == 0) *nused = 0;
-        __syncwarp();
+            if (R.cid[j] != 0xffffffffu)
+                spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
     }
 }
 
@@ -1762,26 +1831,42 @@ __global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p,
                                                    const uint32_t* __restrict__ cstart,
                                                    const float4* __restrict__ spts, const int* __restrict__ parent,
                                                    const int* __restrict__ minidx, int* __restrict__ labels,
-                                                   const Meta* __restrict__ meta) {
+                                                   const Meta* __restrict__ meta, const uint32_t* __restrict__ pcode) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status || 4 * (int64_t)meta->cells > n) return;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+    // (codes exist on the counting path when cells <= kCodeCells; node-tail clouds have
+    // cells <= n/4 and the key-sort path writes none)
+    const bool rcode = !g.key_sort && meta->cells <= kCodeCells;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b4 = 4 * gi;
-        Pts4 P;
-        load_pts4(p, n, b4, vec, P);
         int rv[4], q[4];
         uint32_t cid[4];
+        if (rcode) {
+            load4(pcode, b4, n, cid);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                q[j] = (int)(cid[j] & 63u);
+                cid[j] >>= 6;
+            }
+        } else {
+            Pts4 P;
+            load_pts4(p, n, b4, vec, P);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                q[j] = 0;
+                cid[j] = 0;
+                if (b4 + j >= n) continue;
+                uint32_t lin;
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q[j]);
+                cid[j] = cid_of(cw, lin);
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             rv[j] = 0;
-            q[j] = 0;
-            cid[j] = 0;
             if (b4 + j >= n) continue;
-            uint32_t lin;
-            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q[j]);
-            cid[j] = cid_of(cw, lin);
             // -1 sparse cell; <= -2 single-component dense cell: -(label + 3) (k_rootlab);
             // >= 0 several components: record << 3 | (components - 1)
             rv[j] = __ldg(crec + cid[j]);

@@ -80,10 +80,14 @@ __global__ void k_sgather(const float* p, const uint32_t* key0, const int* val0,
                           const int* val1, int64_t n, const Grid* gp, const uint2* cw, float4* spts, uint32_t* cstart,
                           u64* cocc, int* parent, int* sidx, int* size, int* minidx, const Meta* meta);
 __global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* meta, const Grid* gp, int* crec);
+// Counting path, per input point: compact cell id << 6 | fine sub-cell, written by k_dcount2
+// when the cloud has at most kCodeCells occupied cells (read by k_dscatter and k_relabel_in
+// instead of recomputing the cell from the coordinates).
+constexpr int kCodeCells = 1 << 26;
 __global__ void k_dcount2(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* count, u64* cocc,
-                          int* cmin);
+                          int* cmin, uint32_t* pcode, const Meta* meta);
 __global__ void k_dscatter(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* cursor,
-                           float4* spts);
+                           float4* spts, const uint32_t* pcode, const Meta* meta);
 __global__ void k_dinit(const float4* spts, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                         const u64* cmask, int nbase, int* parent, int* size, int* minidx, int* sidx, const Meta* meta,
                         int all_parents);
@@ -125,7 +129,7 @@ __global__ void k_tail_stats(int* parent, const int* val, int64_t n, int* size, 
                              const float4* spts);
 __global__ void k_relabel_in(const float* p, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                              const u64* cmask, const uint32_t* cstart, const float4* spts, const int* parent,
-                             const int* minidx, int* labels, const Meta* meta);
+                             const int* minidx, int* labels, const Meta* meta, const uint32_t* pcode);
 // local_only != 0 (small clouds, host-chosen): the sparse cells always go through the compact
 // list and k_union_sparse_local (more parallel per cell), whatever their share of the cells.
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,

@@ -17,7 +17,7 @@ if len(sys.argv) > 2:
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", kern], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(src)))
     # may contain several kernels; take the first table
-    h = rr[1]; data = [x for x in rr[2:] if len(x) == len(h)]
+    h = next(x for x in rr if 'Source' in x); data = [x for x in rr if len(x) == len(h) and x != h and x[h.index('Warp Stall Sampling (All Samples)')].replace('.', '', 1).isdigit()]
     i_src = h.index('Source'); i_st = h.index('Warp Stall Sampling (All Samples)'); i_ex = h.index('Instructions Executed')
     tot = sum(float(x[i_st] or 0) for x in data) or 1
     for x in sorted(data, key=lambda x: -float(x[i_st] or 0))[:int(sys.argv[3]) if len(sys.argv) > 3 else 20]:
