@@ -166,13 +166,13 @@ struct Layout {
     // arena zeroed by k_zero every call: counters, look-back states, histograms, dense bits
     uint32_t* arena;
     int64_t arena_words;
-    unsigned int* ctr;             // [0] k_cscan, [1] scan A, [2] scan B, [4..7] onesweep passes
-    unsigned long long* cs_state;  // k_cscan look-back
+    unsigned int* ctr;             // [1] scan A, [2] scan B, [4..7] onesweep passes
     unsigned long long* sa_state;  // cell starts scan
     unsigned long long* sb_state;  // dense-bits popcount scan
     uint32_t* ghist;               // onesweep: [4][256] digit histograms
     uint32_t* dbits;               // [n/32+2] bitmap of dense compact ids
     int64_t cs_tiles;              // k_cscan tiles (worst case over both cell-index modes)
+    uint32_t* ctile;               // [cs_tiles] occupied cells per k_cscan tile, then their prefix
     uint2* cw;                     // occupancy words {bits, occupied cells before the word}
     u64* hkey;                     // hash mode: packed cell coordinates per slot
     int64_t slots;
@@ -226,7 +226,6 @@ Layout carve(char* base, int64_t n) {
     const size_t a0 = ar.off;
     L.arena = reinterpret_cast<uint32_t*>(base + a0);
     L.ctr = ar.take<unsigned int>(64);
-    L.cs_state = ar.take<unsigned long long>(L.cs_tiles + 32);
     L.sa_state = ar.take<unsigned long long>(scan_lb_tiles(n + 1) + 32);
     L.sb_state = ar.take<unsigned long long>(scan_lb_tiles(dwords + 1) + 32);
     L.ghist = ar.take<uint32_t>(4 * 256);
@@ -235,6 +234,7 @@ Layout carve(char* base, int64_t n) {
     L.arena_words = (int64_t)((ar.off - a0) / 4);
     cv.off = ar.off;
     L.cw = cv.take<uint2>(w_max + 4);
+    L.ctile = cv.take<uint32_t>(L.cs_tiles + 1);
     L.hkey = cv.take<u64>(L.slots);
     L.clin = cv.take<uint32_t>(n);
     L.cstart = cv.take<uint32_t>(n + 1);
@@ -553,9 +553,12 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         pdl(k_smark, grid_for(n, 256, di.sms * 4), 256, 0, st)(L.skey0, L.skey1, n, L.cw, gp);
         ++launches;
     }
-    pdl(k_cscan, cs_blocks, 256, 0, st)(L.cw, L.clin, L.cstart, L.cocc, L.cmin, L.ccoord, gp, L.meta, L.cs_state,
-                                        L.ctr + 0);
-    ++launches;
+    pdl(k_cpop, cs_blocks, 256, 0, st)(L.cw, L.ctile, gp);
+    pdl(k_tscan, 1, 1024, 0, st)(L.ctile, gp, L.meta, L.cstart);
+    pdl(k_cscan, cs_blocks, 256, 0, st)(L.cw, gp, L.ctile);
+    pdl(k_cemit, grid_for(n, 256, small ? 32 : cap * 2), 256, 0, st)(L.cw, L.ctile, L.clin, L.cstart, L.cocc, L.cmin,
+                                                                   L.ccoord, gp, L.meta);
+    launches += 4;
     if (count_path) {
         pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin, L.pcode, L.meta);
         launches += 1 + exclusive_scan_lb(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.sa_state, L.ctr + 1, cap,

@@ -273,44 +273,113 @@ __global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int6
     }
 }
 
-// Fused word bases + cell list: a single-pass scan with decoupled look-back over the popcounts
-// of the occupancy words (tiles of 2048 words, taken in order from an atomic counter), the
-// exclusive prefix stored next to each word's bits, then the tile's occupied cells emitted:
-// lane per cell of each nonzero word, so consecutive occupied cells are written by consecutive
-// lanes.  One pass over the bitmap, one launch (+ the state memset).
+// Word bases + cell list in four launches, no look-back chain and no serial per-word loop:
+// k_cpop sums the popcounts of each tile of 2048 occupancy words (every tile in parallel),
+// k_tscan (one block) turns the tile sums into exclusive tile prefixes and the total U,
+// k_cscan stores each word's base next to its bits, and k_cemit takes one thread per occupied
+// cell (compact id k): binary searches over the tile prefixes and the tile's word bases find
+// its word, the bit is the word's (k - base)-th set bit.  Consecutive compact ids are written
+// by consecutive threads.  (A single-pass look-back scan that also emitted each tile's cells
+// with a serial loop over the nonzero words spent ~58 us on C4: the densest tiles, one block
+// each, set the kernel time while most SMs idled.)
 constexpr int CS_THREADS = 256, CS_ITEMS = 8, CS_TILE = CS_THREADS * CS_ITEMS;
 
-__global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, uint32_t* __restrict__ clin,
-                                                     uint32_t* __restrict__ count, u64* __restrict__ cocc,
-                                                     int* __restrict__ cmin,
-                                                     u64* __restrict__ ccoord, const Grid* __restrict__ gp,
-                                                     Meta* __restrict__ meta, unsigned long long* __restrict__ state,
-                                                     unsigned int* __restrict__ counter) {
+__device__ __forceinline__ uint32_t block_sum_256(uint32_t v, uint32_t* red) {  // all threads get the sum
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < CS_THREADS / kWarp; ++k) t += red[k];
+    return t;
+}
+
+__global__ void __launch_bounds__(CS_THREADS) k_cpop(const uint2* __restrict__ cw, uint32_t* __restrict__ tsum,
+                                                    const Grid* __restrict__ gp) {
+    FEC_PROLOGUE_GRID(gp);
+    if (g.status) return;
+    __shared__ uint32_t red[CS_THREADS / kWarp];
+    const int64_t words = g.words;
+    const int64_t tiles = (words + 1 + CS_TILE - 1) / CS_TILE;
+    const uint4* c4 = reinterpret_cast<const uint4*>(cw);  // two words {bits, base} per uint4
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < CS_ITEMS / 2; ++k) {
+            const int64_t i2 = t * (CS_TILE / 2) + k * CS_THREADS + threadIdx.x;  // word pair
+            if (2 * i2 < words) {
+                const uint4 v = __ldg(c4 + i2);
+                c += __popc(v.x) + (2 * i2 + 1 < words ? __popc(v.z) : 0);
+            }
+        }
+        c = block_sum_256(c, red);
+        if (threadIdx.x == 0) tsum[t] = c;
+    }
+}
+
+// One block: exclusive prefix of the tile sums in place, the total U -> meta.
+__global__ void __launch_bounds__(1024) k_tscan(uint32_t* __restrict__ tsum, const Grid* __restrict__ gp,
+                                               Meta* __restrict__ meta, uint32_t* __restrict__ count) {
+    pdl_prologue();
+    if (gp->status) return;
+    __shared__ uint32_t wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t tiles = (gp->words + 1 + CS_TILE - 1) / CS_TILE;
+    const int64_t per = (tiles + 1023) / 1024;  // contiguous chunk per thread
+    const int64_t b = tid * per, e = min(tiles, b + per);
+    uint32_t run = 0;
+    for (int64_t t = b; t < e; ++t) run += tsum[t];
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t v = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    uint32_t pre = (x - run) + (w > 0 ? wsum[w - 1] : 0u);
+    for (int64_t t = b; t < e; ++t) {
+        const uint32_t v = tsum[t];
+        tsum[t] = pre;
+        pre += v;
+    }
+    if (tid == 1023) {
+        const uint32_t U = wsum[31];
+        meta->cells = (int)U;
+        meta->cells1 = (int)U + 1;
+        count[U] = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, const Grid* __restrict__ gp,
+                                                     const uint32_t* __restrict__ tpre) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
     __shared__ uint32_t s[CS_TILE];
-    __shared__ uint32_t sbits[CS_TILE];  // the tile's words, for the emission (no reload)
     __shared__ uint32_t wsum[CS_THREADS / kWarp];
-    __shared__ unsigned int tile_sh;
-    __shared__ uint32_t prefix_sh;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t words = g.words;
-    const int64_t n = words + 1;  // the extra element yields U = the total
-    // persistent blocks take tiles in order from the counter (a tile only ever waits on
-    // earlier tiles, which blocks already running hold)
-    while (true) {
-    __syncthreads();
-    if (tid == 0) tile_sh = atomicAdd(counter, 1u);
-    __syncthreads();
-    const unsigned tile = tile_sh;
-    const int64_t base = (int64_t)tile * CS_TILE;
-    if (base >= n) return;
+    const int64_t tiles = (words + 1 + CS_TILE - 1) / CS_TILE;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t base = tile * CS_TILE;
+    __syncthreads();  // (the previous tile's stores read s)
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
         const int64_t i = base + k * CS_THREADS + tid;
-        const uint32_t b = i < words ? cw[i].x : 0u;
-        sbits[k * CS_THREADS + tid] = b;
-        s[k * CS_THREADS + tid] = (uint32_t)__popc(b);
+        s[k * CS_THREADS + tid] = i < words ? (uint32_t)__popc(cw[i].x) : 0u;
     }
     __syncthreads();
     uint32_t loc[CS_ITEMS];
@@ -337,72 +406,56 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, ui
             if (lane >= o) v += y;
         }
         if (lane < CS_THREADS / kWarp) wsum[lane] = v;
-        const unsigned long long agg = __shfl_sync(0xffffffffu, v, CS_THREADS / kWarp - 1);
-        constexpr unsigned long long A = 1ull << 62, P = 2ull << 62, VAL = (1ull << 62) - 1;
-        unsigned long long prefix = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(state, P | agg);
-        } else {
-            if (lane == 0) atomicExch(state + tile, A | agg);
-            int j = (int)tile - 1;
-            while (true) {
-                const int idx = j - lane;
-                const unsigned long long sv = idx >= 0 ? *reinterpret_cast<volatile unsigned long long*>(state + idx) : P;
-                const unsigned pmask = __ballot_sync(0xffffffffu, (sv & ~VAL) == P);
-                const int upto = pmask ? __ffs(pmask) - 1 : 31;
-                if (!__all_sync(0xffffffffu, lane > upto || (sv & ~VAL) != 0)) continue;
-                unsigned long long val = lane <= upto ? (sv & VAL) : 0ull;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-                prefix += val;
-                if (pmask) break;
-                j -= 32;
-            }
-            if (lane == 0) atomicExch(state + tile, P | (prefix + agg));
-        }
-        if (lane == 0) prefix_sh = (uint32_t)prefix;
     }
     __syncthreads();
-    const uint32_t pre = prefix_sh + (x - run) + (w > 0 ? wsum[w - 1] : 0u);
+    const uint32_t pre = __ldg(tpre + tile) + (x - run) + (w > 0 ? wsum[w - 1] : 0u);
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) s[tid * CS_ITEMS + k] = pre + loc[k];
     __syncthreads();
-    // word bases next to the bits; then warp w emits the cells of words [w*256, w*256 + 256)
+    // word bases next to the bits
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
         const int64_t i = base + k * CS_THREADS + tid;
-        if (i < words) {
-            cw[i].y = s[k * CS_THREADS + tid];
-        } else if (i == words) {
-            const uint32_t U = s[k * CS_THREADS + tid];
-            meta->cells = (int)U;
-            meta->cells1 = (int)U + 1;
-            count[U] = 0u;
-        }
-    }
-    for (int c = 0; c < CS_ITEMS; ++c) {
-        const int li = w * (CS_ITEMS * kWarp) + c * kWarp + lane;
-        const uint32_t bits = sbits[li];
-        unsigned m = __ballot_sync(0xffffffffu, bits != 0u);
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1;
-            const uint32_t b = __shfl_sync(0xffffffffu, bits, j);
-            const uint32_t r0 = s[w * (CS_ITEMS * kWarp) + c * kWarp + j];
-            if ((b >> lane) & 1u) {
-                const uint32_t r = r0 + (uint32_t)__popc(b & ((1u << lane) - 1u));
-                const uint32_t lin = (uint32_t)((base + w * (CS_ITEMS * kWarp) + c * kWarp + j) * 32 + lane);
-                int cc[3];
-                dense_decode(lin, g, cc);
-                clin[r] = lin;
-                ccoord[r] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
-                count[r] = 0u;
-                cocc[r] = 0ull;
-                cmin[r] = 0x7fffffff;
-            }
-        }
+        if (i < words) cw[i].y = s[k * CS_THREADS + tid];
     }
     }  // tiles
+}
+
+__global__ void __launch_bounds__(256) k_cemit(const uint2* __restrict__ cw, const uint32_t* __restrict__ tpre,
+                                              uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
+                                              u64* __restrict__ cocc, int* __restrict__ cmin,
+                                              u64* __restrict__ ccoord, const Grid* __restrict__ gp,
+                                              const Meta* __restrict__ meta) {
+    FEC_PROLOGUE_GRID(gp);
+    if (g.status) return;
+    const uint32_t U = (uint32_t)meta->cells;
+    const int64_t words = g.words;
+    const int tiles = (int)((words + 1 + CS_TILE - 1) / CS_TILE);
+    for (int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < U; kk += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)kk;
+        int lo = 0, hi = tiles;  // the last tile whose prefix is <= k
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(tpre + mid) <= k) lo = mid;
+            else hi = mid;
+        }
+        // the last word of the tile whose base is <= k: the word holding cell k
+        int64_t wl = (int64_t)lo * CS_TILE, wh = min(words, wl + CS_TILE);
+        while (wh - wl > 1) {
+            const int64_t mid = (wl + wh) >> 1;
+            if (__ldg(&cw[mid].y) <= k) wl = mid;
+            else wh = mid;
+        }
+        const uint2 v = __ldg(cw + wl);
+        const uint32_t lin = (uint32_t)(wl * 32) + (uint32_t)__fns(v.x, 0u, (int)(k - v.y) + 1);
+        int cc[3];
+        dense_decode(lin, g, cc);
+        clin[k] = lin;
+        ccoord[k] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
+        count[k] = 0u;
+        cocc[k] = 0ull;
+        cmin[k] = 0x7fffffff;
+    }
 }
 
 // ---- a2: per-cell counts, slot[i] = rank of point i inside its cell, fine occupancy ------

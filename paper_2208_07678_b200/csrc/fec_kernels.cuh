@@ -71,8 +71,11 @@ __global__ void k_relabel(const int* parent, const int* val, const int* minidx, 
 __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
                               unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, const Grid* gp, uint2* cw);
-__global__ void k_cscan(uint2* cw, uint32_t* clin, uint32_t* count, u64* cocc, int* cmin, u64* ccoord, const Grid* gp,
-                        Meta* meta, unsigned long long* state, unsigned int* counter);
+__global__ void k_cpop(const uint2* cw, uint32_t* tsum, const Grid* gp);
+__global__ void k_tscan(uint32_t* tsum, const Grid* gp, Meta* meta, uint32_t* count);
+__global__ void k_cscan(uint2* cw, const Grid* gp, const uint32_t* tpre);
+__global__ void k_cemit(const uint2* cw, const uint32_t* tpre, uint32_t* clin, uint32_t* count, u64* cocc, int* cmin,
+                        u64* ccoord, const Grid* gp, const Meta* meta);
 __global__ void k_lkey(const float* p, int64_t n, const Grid* gp, uint32_t* key, int* val, uint32_t* ghist,
                        uint32_t* state0, int64_t state_words);
 __global__ void k_smark(const uint32_t* key0, const uint32_t* key1, int64_t n, uint2* cw, const Grid* gp);
