@@ -142,12 +142,13 @@ STAGE_KERNELS = {
     "a2_bin_keys": "k_lkey + k_onesweep x passes (key path)",
     "a3_sort": "k_cmark / k_smark, k_cpop + k_tscan + k_cscan + k_cemit, k_dcount2 + k_scan_lb + k_ccount / k_sgather + k_scount, k_dbits_*, "
                "k_dcomps",
-    "a4_gather_init": "k_dscatter (count path: scatter + sorted-order init) / k_dparent (key path)",
+    "a4_gather_init": "k_dscatter phase 0 (+ phase 1, enqueued after the dense links; node-tail clouds scatter "
+                      "only the cells later kernels read), k_dinit, k_dparent",
     "a6a7_scan_union": "k_union_sparse(_local), k_slist, k_dense_link x2, k_dense_overflow, k_flatten_nodes, "
                        "k_dense_filter, k_dense_items",
     "a8_flatten": "k_flatten_if",
     "a9_stats": "k_tail_stats",
-    "a10_relabel": "k_rootlab, k_relabel",
+    "a10_relabel": "k_rootlab, k_relabel_in / k_relabel",
 }
 
 

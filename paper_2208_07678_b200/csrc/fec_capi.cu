@@ -43,6 +43,14 @@ struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
+// FEC_FULL_SCATTER=1 scatters every point in phase 0 (A/B measurements, debugging)
+bool full_scatter() {
+    static const bool v = [] {
+        const char* e = std::getenv("FEC_FULL_SCATTER");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
 thread_local SideStream g_side[64];
 thread_local int g_side_off = -1;  // FEC_SIDE_STREAM=0 turns the fork off (A/B measurements)
 fec_status_t side_stream(SideStream** out) {
@@ -76,8 +84,10 @@ const char* const kStageNames[kStages] = {"a1_bbox_validate", "a2_bin_keys",    
                                           "a10_relabel"};  // a8 = flatten (sparse-dominated clouds), a9 = k_tail_stats
 struct StageEvents {
     cudaEvent_t ev[kStages + 1] = {};
+    cudaEvent_t sub[2] = {};  // partial scatter phase 1: a4 work enqueued inside the a6a7 interval
     bool created = false;
     bool recorded = false;
+    bool sub_recorded = false;
 };
 thread_local StageEvents g_ev;
 
@@ -86,10 +96,18 @@ inline void mark(int i, cudaStream_t st) {
     if (!g_timing) return;
     if (!g_ev.created) {
         for (auto& e : g_ev.ev) cudaEventCreate(&e);
+        for (auto& e : g_ev.sub) cudaEventCreate(&e);
         g_ev.created = true;
     }
     cudaEventRecord(g_ev.ev[i], st);
+    if (i == 0) g_ev.sub_recorded = false;
     if (i == kStages) g_ev.recorded = true;
+}
+// Sub-interval j (0 = begin, 1 = end) of a4 work enqueued later (counted to a4, not a6a7).
+inline void mark_sub(int j, cudaStream_t st) {
+    if (!g_timing || !g_ev.created) return;
+    cudaEventRecord(g_ev.sub[j], st);
+    if (j == 1) g_ev.sub_recorded = true;
 }
 
 constexpr int kMaxBBoxBlocks = 148 * 8;
@@ -171,6 +189,7 @@ struct Layout {
     unsigned long long* sb_state;  // dense-bits popcount scan
     uint32_t* ghist;               // onesweep: [4][256] digit histograms
     uint32_t* dbits;               // [n/32+2] bitmap of dense compact ids
+    uint32_t* cneed1;              // [n/32+2] partial scatter phase 1: cells a queued item reads
     int64_t cs_tiles;              // k_cscan tiles (worst case over both cell-index modes)
     uint32_t* ctile;               // [cs_tiles] occupied cells per k_cscan tile, then their prefix
     uint2* cw;                     // occupancy words {bits, occupied cells before the word}
@@ -184,6 +203,7 @@ struct Layout {
     uint32_t* pcode;    // [n]   counting path: compact cell id << 6 | fine sub-cell per input point
     int* dlist;         // dense record -> compact cell id
     uint32_t* dwpos;    // [n/32+2] popcount prefix of the dense bits
+    uint32_t* cneed0;   // [n/32+2] partial scatter phase 0: sparse and multi-component cells
     u64* cocc;          // [n]   fine (4x4x4) occupancy mask of each occupied cell
     int* cmin;          // [n]   counting path: smallest input index in each occupied cell
     u64* ccoord;        // [n]   cell coordinates of each occupied cell, 21 bits each
@@ -230,6 +250,7 @@ Layout carve(char* base, int64_t n) {
     L.sb_state = ar.take<unsigned long long>(scan_lb_tiles(dwords + 1) + 32);
     L.ghist = ar.take<uint32_t>(4 * 256);
     L.dbits = ar.take<uint32_t>(dwords + 1);
+    L.cneed1 = ar.take<uint32_t>(dwords + 1);
     ar.off = (ar.off + 255) & ~size_t(255);
     L.arena_words = (int64_t)((ar.off - a0) / 4);
     cv.off = ar.off;
@@ -244,6 +265,7 @@ Layout carve(char* base, int64_t n) {
     L.pcode = cv.take<uint32_t>(n);
     L.dlist = cv.take<int>(dense_max(n));
     L.dwpos = cv.take<uint32_t>(dwords + 1);
+    L.cneed0 = cv.take<uint32_t>(dwords + 1);
     L.cocc = cv.take<u64>(n);
     L.cmin = cv.take<int>(n);
     L.ccoord = cv.take<u64>(n);
@@ -529,6 +551,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     dctx.nbase = (int)n;
     dctx.rmask = (uint32_t)(rec_pow2(n) - 1);
     dctx.meta = L.meta;
+    dctx.cneed0 = L.cneed0;
+    dctx.cneed1 = L.cneed1;
     // single cloud: the counting path is always enqueued (hash mode has no key sort); batch
     // mode planned on the host enqueues only the chosen path
     const bool count_path = !B || !key_path;
@@ -563,7 +587,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin, L.pcode, L.meta);
         launches += 1 + exclusive_scan_lb(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.sa_state, L.ctr + 1, cap,
                                           gstatus, gkeysort, st);
-        pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta, gp, L.crec);
+        pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta, gp, L.crec, L.cneed0);
         ++launches;
     }
     if (key_path) {
@@ -597,7 +621,8 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     mark(3, st);
     if (count_path) {
         // slot = per-cell cursors here
-        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts, L.pcode, L.meta);
+        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts, L.pcode, L.meta, L.cneed0, L.cneed1, 0,
+                                        C.node_stats && !full_scatter(), dctx.item_cap);
         pdl(k_dinit, ew4, 256, 0, st)(L.spts, n, gp, L.cw, L.crec, L.cmask, (int)n, L.parent, L.size, L.minidx,
                                      L.sidx, L.meta, C.node_stats ? 0 : 1);
         ++launches;
@@ -628,12 +653,23 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, st)(gp, L.crec, L.ncomp, L.oflag, dctx,
                                                                             L.litems, L.lhalf, side ? 2 : 3);
     if (side) FEC_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+    // (a litems list overflowed: every (record, slot) again, queueing like k_dense_link)
     pdl(k_dense_link_all, di.sms * 2, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
-    // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
-    pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
+    // queued pairs still apart after the certain unions (they mark the records whose points
+    // they need), then partial scatter phase 1, the item-queue overflow fallback (in-place
+    // point tests) and the queued point tests
     pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta,
                                                                             (uint32_t)(rec_pow2(n) - 1));
     pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(dctx, L.items2, L.slices2, L.idone);
+    if (count_path && C.node_stats) {
+        mark_sub(0, st);
+        pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts, L.pcode, L.meta, L.cneed0, L.cneed1, 1,
+                                        C.node_stats && !full_scatter(), dctx.item_cap);
+        mark_sub(1, st);
+        ++launches;
+    }
+    // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
+    pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
     pdl(k_dense_items, di.sms * 8, 256, 0, st)(gp, dctx, L.items2, L.slices2, L.idone);
     launches += local_only ? 8 : 9;
     if (g_instrument) {
@@ -1231,9 +1267,13 @@ int32_t fec_get_stage_times(float* ms_out, int32_t max_stages) {
     if (!g_ev.recorded) { g_err = "no timed call on this thread (fec_set_timing(1) first)"; return -1; }
     cudaError_t e = cudaEventSynchronize(g_ev.ev[kStages]);
     if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return -1; }
+    float sub = 0.f;
+    if (g_ev.sub_recorded) cudaEventElapsedTime(&sub, g_ev.sub[0], g_ev.sub[1]);
     for (int i = 0; i < kStages && i < max_stages; ++i) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, g_ev.ev[i], g_ev.ev[i + 1]);
+        if (i == 3) ms += sub;  // a4_gather_init: + partial scatter phase 1
+        if (i == 6) ms -= sub;  // a6a7_union_dense: - the same interval
         ms_out[i] = ms;
     }
     return kStages;

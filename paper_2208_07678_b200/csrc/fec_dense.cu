@@ -643,10 +643,20 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
 __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, int64_t n,
                                                  const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                  uint32_t* __restrict__ cursor, float4* __restrict__ spts,
-                                                 const uint32_t* __restrict__ pcode, const Meta* __restrict__ meta) {
+                                                 const uint32_t* __restrict__ pcode, const Meta* __restrict__ meta,
+                                                 const uint32_t* __restrict__ cneed0,
+                                                 const uint32_t* __restrict__ cneed1, int phase, int node_stats,
+                                                 int item_cap) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     const bool rcode = meta->cells <= kCodeCells;
+    // partial scatter (node-tail clouds of the single-GPU path): phase 0 writes the points of
+    // sparse and multi-component cells, phase 1 those of single-component dense records that
+    // a surviving queued item references (k_dense_filter marks them) -- every remaining one
+    // if the item queue overflowed (k_dense_overflow then tests pairs in place)
+    const bool partial = node_stats && 4 * (int64_t)meta->cells <= n;
+    if (phase == 1 && !partial) return;
+    const bool all1 = phase == 1 && meta->nitems > item_cap;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
@@ -654,15 +664,27 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
     for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; t0 < n; t0 += nw * 128) {
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
-        load_pts4(p, n, b4, vec, P);
         PointRuns R;
         if (rcode) {
             uint32_t code[4];
             load4(pcode, b4, n, code);
             point_runs_code(code, b4, n, R);
         } else {
+            load_pts4(p, n, b4, vec, P);
             point_runs(P, b4, n, g, cw, R);
         }
+        if (partial) {  // drop the points this phase does not write (their runs stay split)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (R.cid[j] == 0xffffffffu) continue;
+                const uint32_t c = R.cid[j];
+                const bool in0 = (__ldg(cneed0 + (c >> 5)) >> (c & 31)) & 1u;  // small bitmaps: L1 hits
+                const bool keep = phase == 0 ? in0 : (!in0 && (all1 || ((__ldg(cneed1 + (c >> 5)) >> (c & 31)) & 1u)));
+                if (!keep) R.cid[j] = 0xffffffffu;
+            }
+        }
+        if (rcode && (R.cid[0] & R.cid[1] & R.cid[2] & R.cid[3]) != 0xffffffffu) load_pts4(p, n, b4, vec, P);
+        if (partial && !__any_sync(0xffffffffu, (R.cid[0] & R.cid[1] & R.cid[2] & R.cid[3]) != 0xffffffffu)) continue;
         const int rounds = __reduce_max_sync(0xffffffffu, R.ri[3] + 1);
         uint32_t base[4] = {0u, 0u, 0u, 0u}, pre[4] = {0u, 0u, 0u, 0u};
         int lead[4] = {0, 0, 0, 0};
@@ -699,6 +721,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
                 spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
     }
 }
+
 
 // Counting path, a4: sorted-order initialisation (coalesced, 4 positions per thread): the
 // point's cell from its coordinates, the cell's record word (crec: -1 for a sparse cell) gives
@@ -765,7 +788,8 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
 // Dense bits of the occupied cells from the cell starts; also the scatter cursors.
 __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
                                                uint32_t* __restrict__ cursor, const Meta* __restrict__ meta,
-                                               const Grid* __restrict__ gp, int* __restrict__ crec) {
+                                               const Grid* __restrict__ gp, int* __restrict__ crec,
+                                               uint32_t* __restrict__ cneed0) {
     pdl_prologue();
     if (gp->status || gp->key_sort) return;
     const int64_t U = meta->cells;
@@ -779,7 +803,11 @@ __global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cst
             if (!dense) crec[u] = -1;  // dense cells get their record word in k_dcomps
         }
         const unsigned m = __ballot_sync(0xffffffffu, dense);
-        if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
+        const unsigned sp = __ballot_sync(0xffffffffu, u < U && !dense);  // sparse: partial scatter phase 0
+        if ((threadIdx.x & 31) == 0) {
+            dbits[u >> 5] = m;
+            cneed0[u >> 5] = sp;  // (k_dcomps adds the multi-component cells)
+        }
     }
 }
 
@@ -1099,7 +1127,8 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
             kp = sc_components(occ, comp, rest);
             if (rest) atomicOr(&C.meta->internal_error, 1);  // impossible by the 8-component bound
             ncomp[r] = kp;
-            crec[cid] = (r << 3) | (kp - 1);  // the cell's record word (k_dscatter, k_dense_link)
+            crec[cid] = (r << 3) | (kp - 1);  // the cell's record word (k_dense_link, k_relabel_in)
+            if (kp > 1 && C.cneed0) atomicOr(C.cneed0 + (cid >> 5), 1u << (cid & 31));  // (k_dparent reads its points)
 #pragma unroll
             for (int j = 0; j < kMaxComp; ++j) {
                 const int node = node_of(C.nbase, C.rmask, r, j);
@@ -1453,7 +1482,14 @@ __global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restri
         const int na = node_of(C.nbase, C.rmask, it.x, it.y);
         const int nb = it.w >= 0 ? node_of(C.nbase, C.rmask, it.z, it.w) : it.z;
         if (uf_find(C.parent, na) == uf_find(C.parent, nb)) continue;
+        // the records whose points k_dense_items reads (partial scatter, phase 1; an item
+        // naming a sparse point references a sorted position written in phase 0)
         const int cp = __ldg(C.dlist + it.x);
+        atomicOr(C.cneed1 + (cp >> 5), 1u << (cp & 31));
+        if (it.w >= 0) {
+            const int cq = __ldg(C.dlist + it.z);
+            atomicOr(C.cneed1 + (cq >> 5), 1u << (cq & 31));
+        }
         const int wa = (int)(__ldg(C.cstart + cp + 1) - __ldg(C.cstart + cp));
         int wb = 1;
         if (it.w >= 0) {

@@ -90,12 +90,13 @@ constexpr int kCodeCells = 1 << 26;
 __global__ void k_dcount2(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* count, u64* cocc,
                           int* cmin, uint32_t* pcode, const Meta* meta);
 __global__ void k_dscatter(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* cursor,
-                           float4* spts, const uint32_t* pcode, const Meta* meta);
+                           float4* spts, const uint32_t* pcode, const Meta* meta, const uint32_t* cneed0,
+                           const uint32_t* cneed1, int phase, int node_stats, int item_cap);
 __global__ void k_dinit(const float4* spts, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                         const u64* cmask, int nbase, int* parent, int* size, int* minidx, int* sidx, const Meta* meta,
                         int all_parents);
 __global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta,
-                         const Grid* gp, int* crec);
+                         const Grid* gp, int* crec, uint32_t* cneed0);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount, const Meta* meta);
 __global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
                              Meta* meta);
@@ -120,6 +121,8 @@ struct DenseCtx {
     int nbase;          // node id of component k of record r: node_of(nbase, rmask, r, k)
     uint32_t rmask;
     Meta* meta;
+    uint32_t* cneed0;   // partial scatter: bit per compact id, points written in phase 0
+    uint32_t* cneed1;   // ... and in phase 1 (cells a surviving queued item reads)
 };
 __global__ void k_dcomps(const Grid* gp, const uint2* cw, int* crec, const u64* cocc, const u64* ccoord, int* ncomp, int* size,
                          int* minidx, u64* dcoord, uint32_t* oflags, DenseCtx C, uint4* litems, int lhalf,
