@@ -661,6 +661,74 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
     const unsigned lt = (1u << lane) - 1u;
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (rcode && partial) {  // the usual case: a lean loop over the codes
+        const int64_t nt = (n + 127) / 128;
+        for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nw) {
+            const int64_t b4 = t * 128 + 4 * lane;
+            uint32_t code[4];
+            load4(pcode, b4, n, code);
+            uint32_t cid[4];
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t c = code[j] >> 6;
+                bool keep = false;
+                if (b4 + j < n) {
+                    const uint32_t w0 = __ldg(cneed0 + (c >> 5));  // small bitmaps: L1 hits
+                    const bool in0 = (w0 >> (c & 31)) & 1u;
+                    keep = phase == 0 ? in0 : (!in0 && (all1 || ((__ldg(cneed1 + (c >> 5)) >> (c & 31)) & 1u)));
+                }
+                cid[j] = keep ? c : 0xffffffffu;
+                any |= keep;
+            }
+            if (!__any_sync(0xffffffffu, any)) continue;
+            PointRuns R;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                R.cid[j] = cid[j];
+                const bool fresh = j == 0 || cid[j] != cid[j > 0 ? j - 1 : 0];
+                R.ri[j] = j == 0 ? 0 : R.ri[j > 0 ? j - 1 : 0] + (fresh ? 1 : 0);
+                R.off[j] = fresh ? 0 : R.off[j > 0 ? j - 1 : 0] + 1;
+            }
+            Pts4 P;
+            if (any) load_pts4(p, n, b4, vec, P);
+            const int rounds = __reduce_max_sync(0xffffffffu, R.ri[3] + 1);
+            uint32_t base[4] = {0u, 0u, 0u, 0u}, pre[4] = {0u, 0u, 0u, 0u};
+            int lead[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r >= rounds) continue;  // (warp-uniform)
+                uint32_t key = 0xffffffffu, len = 0u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (R.ri[j] == r && R.cid[j] != 0xffffffffu) {
+                        key = R.cid[j];
+                        ++len;
+                    }
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                const unsigned b0 = __ballot_sync(0xffffffffu, len & 1u), b1 = __ballot_sync(0xffffffffu, len & 2u),
+                               b2 = __ballot_sync(0xffffffffu, len & 4u);
+                pre[r] = __popc(peers & lt & b0) + 2 * __popc(peers & lt & b1) + 4 * __popc(peers & lt & b2);
+                lead[r] = __ffs(peers) - 1;
+                if (key != 0xffffffffu && lane == lead[r])
+                    base[r] = atomicAdd(cursor + key, __popc(peers & b0) + 2 * __popc(peers & b1) + 4 * __popc(peers & b2));
+            }
+            uint32_t pos[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (r >= rounds) continue;
+                const uint32_t b = __shfl_sync(0xffffffffu, base[r], lead[r]) + pre[r];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (R.ri[j] == r) pos[j] = b + (uint32_t)R.off[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (R.cid[j] != 0xffffffffu)
+                    spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
+        }
+        return;
+    }
     for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; t0 < n; t0 += nw * 128) {
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;

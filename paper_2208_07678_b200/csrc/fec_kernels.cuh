@@ -86,7 +86,7 @@ __global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* me
 // Counting path, per input point: compact cell id << 6 | fine sub-cell, written by k_dcount2
 // when the cloud has at most kCodeCells occupied cells (read by k_dscatter and k_relabel_in
 // instead of recomputing the cell from the coordinates).
-constexpr int kCodeCells = 1 << 26;
+constexpr int kCodeCells = (1 << 26) - 1;  // (the code ~0u >> 6 is never a valid compact id)
 __global__ void k_dcount2(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* count, u64* cocc,
                           int* cmin, uint32_t* pcode, const Meta* meta);
 __global__ void k_dscatter(const float* p, int64_t n, const Grid* gp, const uint2* cw, uint32_t* cursor,
