@@ -598,7 +598,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     }
     // dense records: compact ids of the dense cells, their components and nodes
     pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.meta);
-    launches += 1 + exclusive_scan_lb(L.dwpos, L.dwpos, dwords + 1, nullptr, L.sb_state, L.ctr + 2, cap, gstatus,
+    launches += 1 + exclusive_scan_lb(L.dwpos, L.dwpos, dwords + 1, &L.meta->dwords1, L.sb_state, L.ctr + 2, cap, gstatus,
                                       nullptr, st);
     pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
     pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(gp, L.cw, L.crec, L.cocc, L.ccoord, L.ncomp, L.size,

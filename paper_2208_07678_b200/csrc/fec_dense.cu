@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(1024) k_tscan(uint32_t* __restrict__ tsum, con
         const uint32_t U = wsum[31];
         meta->cells = (int)U;
         meta->cells1 = (int)U + 1;
+        meta->dwords1 = (int)((U + 31) / 32) + 1;
         count[U] = 0u;
     }
 }
@@ -1034,6 +1035,7 @@ __global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__
                                                    uint32_t* __restrict__ wcount, const Meta* __restrict__ meta) {
     pdl_prologue();
     if (meta->status) return;
+    words = min(words, (int64_t)meta->dwords1 - 1);  // the words that hold occupied cells
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
         wcount[w] = w < words ? (uint32_t)__popc(__ldg(dbits + w)) : 0u;
 }
@@ -1043,6 +1045,7 @@ __global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__
                                                    int* __restrict__ crec, Meta* __restrict__ meta) {
     pdl_prologue();
     if (meta->status) return;
+    words = min(words, (int64_t)meta->dwords1 - 1);
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
         if (w == words) { meta->ndense = (int)wpos[words]; continue; }
         uint32_t bits = __ldg(dbits + w);

@@ -30,6 +30,7 @@ struct Meta {
     int nheavy, nlight;               // dense-grid mode: schedule of the dense cells
     int work2;                        // second dynamic work counter
     int cells1;                       // dense-grid mode: occupied cells + 1 (scan length)
+    int dwords1;                      // dense-grid mode: words of the dense-cell bitmap + 1 (scan length)
     int nitems;                       // dense-grid mode: uncertain component pairs pushed
     int internal_error;               // != 0: an internal invariant failed (never expected)
     int nitems2;                      // dense-grid mode: queued pairs still apart after the certain unions
