@@ -140,7 +140,7 @@ class ClockSampler:
 STAGE_KERNELS = {
     "a1_bbox_validate": "k_bbox (its last block plans the grid on the device), k_zero",
     "a2_bin_keys": "k_lkey + k_onesweep x passes (key path)",
-    "a3_sort": "k_cmark / k_smark, k_cpop + k_tscan + k_cscan + k_cemit, k_dcount2 + k_scan_lb + k_ccount / k_sgather + k_scount, k_dbits_*, "
+    "a3_sort": "k_cmark / k_smark, k_cpop + k_tscan + k_cscan, k_dcount2 / k_sgather, k_cellred + k_celltscan + k_cellscan, "
                "k_dcomps",
     "a4_gather_init": "k_dscatter phase 0 (+ phase 1, enqueued after the dense links; node-tail clouds scatter "
                       "only the cells later kernels read), k_dinit, k_dparent",

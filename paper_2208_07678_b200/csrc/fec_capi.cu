@@ -579,32 +579,30 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     }
     pdl(k_cpop, cs_blocks, 256, 0, st)(L.cw, L.ctile, gp);
     pdl(k_tscan, 1, 1024, 0, st)(L.ctile, gp, L.meta, L.cstart);
-    pdl(k_cscan, cs_blocks, 256, 0, st)(L.cw, gp, L.ctile);
-    pdl(k_cemit, grid_for(n, 256, small ? 32 : cap * 2), 256, 0, st)(L.cw, L.ctile, L.clin, L.cstart, L.cocc, L.cmin,
-                                                                   L.ccoord, gp, L.meta);
-    launches += 4;
+    pdl(k_cscan, cs_blocks, 256, 0, st)(L.cw, gp, L.ctile, L.clin, L.cstart, L.cocc, L.cmin, L.ccoord);
+    launches += 3;
     if (count_path) {
         pdl(k_dcount2, wt, 256, 0, st)(pts, n, gp, L.cw, L.cstart, L.cocc, L.cmin, L.pcode, L.meta);
-        launches += 1 + exclusive_scan_lb(L.cstart, L.cstart, n + 1, &L.meta->cells1, L.sa_state, L.ctr + 1, cap,
-                                          gstatus, gkeysort, st);
-        pdl(k_ccount, ew, 256, 0, st)(L.cstart, L.dbits, L.slot, L.meta, gp, L.crec, L.cneed0);
         ++launches;
     }
     if (key_path) {
         pdl(k_sgather, grid_for((n + 3) / 4, 256, di.sms * 8), 256, 0, st)(pts, L.skey0, L.sval0, L.skey1, L.sval1, n, gp, L.cw, L.spts, L.cstart, L.cocc,
                                        L.parent, L.sidx, L.size, L.minidx, L.meta);
-        pdl(k_scount, grid_for(n, 256, di.sms * 4), 256, 0, st)(L.cstart, L.dbits, L.meta, gp, L.crec);
-        launches += 2;
+        ++launches;
     }
-    // dense records: compact ids of the dense cells, their components and nodes
-    pdl(k_dbits_popc, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.meta);
-    launches += 1 + exclusive_scan_lb(L.dwpos, L.dwpos, dwords + 1, &L.meta->dwords1, L.sb_state, L.ctr + 2, cap, gstatus,
-                                      nullptr, st);
-    pdl(k_dbits_list, wb, 256, 0, st)(L.dbits, dwords, L.dwpos, L.dlist, L.crec, L.meta);
+    // cell starts + scatter cursors + dense records (dlist, crec) in one scan over the cells
+    {
+        const unsigned cl_blocks = (unsigned)std::min<int64_t>(scan_lb_tiles(n + 1), small ? 32 : cap);
+        pdl(k_cellred, cl_blocks, 256, 0, st)(L.cstart, L.meta, gp, L.sa_state);
+        pdl(k_celltscan, 1, 1024, 0, st)(L.sa_state, L.meta, gp, L.cstart);
+        pdl(k_cellscan, cl_blocks, 256, 0, st)(L.cstart, L.slot, L.dlist, L.crec, L.cneed0, L.meta, gp, L.sa_state);
+        launches += 3;
+    }
+    // dense records: their components and nodes
     pdl(k_dcomps, grid_for(dense_max(n), 256, cap), 256, 0, st)(gp, L.cw, L.crec, L.cocc, L.ccoord, L.ncomp, L.size,
                                                               L.minidx, L.dcoord, L.oflag, dctx, L.litems, L.lhalf,
                                                               L.cmin, L.sidx, C.node_stats);
-    launches += 2;
+    ++launches;
     // the dense-dense certain unions need no point: they run on the side stream while the
     // points are scattered and initialised
     SideStream* side = nullptr;

@@ -273,15 +273,15 @@ __global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int6
     }
 }
 
-// Word bases + cell list in four launches, no look-back chain and no serial per-word loop:
-// k_cpop sums the popcounts of each tile of 2048 occupancy words (every tile in parallel),
-// k_tscan (one block) turns the tile sums into exclusive tile prefixes and the total U,
-// k_cscan stores each word's base next to its bits, and k_cemit takes one thread per occupied
-// cell (compact id k): binary searches over the tile prefixes and the tile's word bases find
-// its word, the bit is the word's (k - base)-th set bit.  Consecutive compact ids are written
-// by consecutive threads.  (A single-pass look-back scan that also emitted each tile's cells
-// with a serial loop over the nonzero words spent ~58 us on C4: the densest tiles, one block
-// each, set the kernel time while most SMs idled.)
+// Word bases + cell list in three launches, no look-back chain: k_cpop sums the popcounts of
+// each tile of 2048 occupancy words (every tile in parallel), k_tscan (one block) turns the
+// tile sums into exclusive tile prefixes and the total U, and k_cscan stores each word's base
+// next to its bits and emits the cells: each warp the cells of its 256 words, lane per cell
+// (a binary search over the warp's word bases in shared memory), which keeps sparse (C4: 0.4%
+// of the grid) and dense (C5: half) occupancy balanced and the stores coalesced.  (Measured
+// alternatives: a look-back scan emitting word by word per warp, ~58 us on C4 -- the densest
+// tiles serialised; a thread per cell with two global binary searches, 1.6 ms on C5; a
+// thread per word, 3.9 ms on C5 -- uncoalesced stores, 6.9 GB of DRAM traffic for 2 GB.)
 constexpr int CS_THREADS = 256, CS_ITEMS = 8, CS_TILE = CS_THREADS * CS_ITEMS;
 
 __device__ __forceinline__ uint32_t block_sum_256(uint32_t v, uint32_t* red) {  // all threads get the sum
@@ -365,29 +365,38 @@ __global__ void __launch_bounds__(1024) k_tscan(uint32_t* __restrict__ tsum, con
     }
 }
 
+// Shared-memory index with one pad word per 8: the thread-serial scan reads 8 consecutive
+// entries per thread (stride 8 words: an 8-way bank conflict unpadded, none padded).
+__device__ __forceinline__ int pad8(int j) { return j + (j >> 3); }
+
 __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, const Grid* __restrict__ gp,
-                                                     const uint32_t* __restrict__ tpre) {
+                                                     const uint32_t* __restrict__ tpre, uint32_t* __restrict__ clin,
+                                                     uint32_t* __restrict__ count, u64* __restrict__ cocc,
+                                                     int* __restrict__ cmin, u64* __restrict__ ccoord) {
     FEC_PROLOGUE_GRID(gp);
     if (g.status) return;
-    __shared__ uint32_t s[CS_TILE];
+    __shared__ uint32_t s[CS_TILE + CS_TILE / 8 + 1];      // word bases (padded), + the tile's end
+    __shared__ uint32_t sbits[CS_TILE + CS_TILE / 8 + 1];  // the words (padded)
     __shared__ uint32_t wsum[CS_THREADS / kWarp];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t words = g.words;
     const int64_t tiles = (words + 1 + CS_TILE - 1) / CS_TILE;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t base = tile * CS_TILE;
-    __syncthreads();  // (the previous tile's stores read s)
+    __syncthreads();  // (the previous tile's emission read s / sbits)
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
         const int64_t i = base + k * CS_THREADS + tid;
-        s[k * CS_THREADS + tid] = i < words ? (uint32_t)__popc(cw[i].x) : 0u;
+        const uint32_t b = i < words ? cw[i].x : 0u;
+        sbits[pad8(k * CS_THREADS + tid)] = b;
+        s[pad8(k * CS_THREADS + tid)] = (uint32_t)__popc(b);
     }
     __syncthreads();
     uint32_t loc[CS_ITEMS];
     uint32_t run = 0;
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
-        const uint32_t v = s[tid * CS_ITEMS + k];
+        const uint32_t v = s[pad8(tid * CS_ITEMS + k)];
         loc[k] = run;
         run += v;
     }
@@ -409,54 +418,40 @@ __global__ void __launch_bounds__(CS_THREADS) k_cscan(uint2* __restrict__ cw, co
         if (lane < CS_THREADS / kWarp) wsum[lane] = v;
     }
     __syncthreads();
-    const uint32_t pre = __ldg(tpre + tile) + (x - run) + (w > 0 ? wsum[w - 1] : 0u);
+    const uint32_t t0 = __ldg(tpre + tile);
+    const uint32_t pre = t0 + (x - run) + (w > 0 ? wsum[w - 1] : 0u);
 #pragma unroll
-    for (int k = 0; k < CS_ITEMS; ++k) s[tid * CS_ITEMS + k] = pre + loc[k];
+    for (int k = 0; k < CS_ITEMS; ++k) s[pad8(tid * CS_ITEMS + k)] = pre + loc[k];
+    if (tid == 0) s[pad8(CS_TILE)] = t0 + wsum[CS_THREADS / kWarp - 1];  // the tile's end
     __syncthreads();
     // word bases next to the bits
 #pragma unroll
     for (int k = 0; k < CS_ITEMS; ++k) {
         const int64_t i = base + k * CS_THREADS + tid;
-        if (i < words) cw[i].y = s[k * CS_THREADS + tid];
+        if (i < words) cw[i].y = s[pad8(k * CS_THREADS + tid)];
     }
-    }  // tiles
-}
-
-__global__ void __launch_bounds__(256) k_cemit(const uint2* __restrict__ cw, const uint32_t* __restrict__ tpre,
-                                              uint32_t* __restrict__ clin, uint32_t* __restrict__ count,
-                                              u64* __restrict__ cocc, int* __restrict__ cmin,
-                                              u64* __restrict__ ccoord, const Grid* __restrict__ gp,
-                                              const Meta* __restrict__ meta) {
-    FEC_PROLOGUE_GRID(gp);
-    if (g.status) return;
-    const uint32_t U = (uint32_t)meta->cells;
-    const int64_t words = g.words;
-    const int tiles = (int)((words + 1 + CS_TILE - 1) / CS_TILE);
-    for (int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < U; kk += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = (uint32_t)kk;
-        int lo = 0, hi = tiles;  // the last tile whose prefix is <= k
+    // cells: warp w owns words [256w, 256w + 256); its cells [r0, r1) go 32 at a time, lane per
+    // cell (coalesced stores), the word found by a binary search over the warp's word bases
+    const int j0 = w * 256;
+    const uint32_t r0 = s[pad8(j0)], r1 = s[pad8(j0 + 256)];
+    for (uint32_t c = r0 + lane; c < r1; c += 32) {
+        int lo = j0, hi = j0 + 256;  // the last word whose base is <= c
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (__ldg(tpre + mid) <= k) lo = mid;
+            if (s[pad8(mid)] <= c) lo = mid;
             else hi = mid;
         }
-        // the last word of the tile whose base is <= k: the word holding cell k
-        int64_t wl = (int64_t)lo * CS_TILE, wh = min(words, wl + CS_TILE);
-        while (wh - wl > 1) {
-            const int64_t mid = (wl + wh) >> 1;
-            if (__ldg(&cw[mid].y) <= k) wl = mid;
-            else wh = mid;
-        }
-        const uint2 v = __ldg(cw + wl);
-        const uint32_t lin = (uint32_t)(wl * 32) + (uint32_t)__fns(v.x, 0u, (int)(k - v.y) + 1);
+        const uint32_t bw = sbits[pad8(lo)];
+        const uint32_t lin = (uint32_t)((base + lo) * 32) + (uint32_t)__fns(bw, 0u, (int)(c - s[pad8(lo)]) + 1);
         int cc[3];
         dense_decode(lin, g, cc);
-        clin[k] = lin;
-        ccoord[k] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
-        count[k] = 0u;
-        cocc[k] = 0ull;
-        cmin[k] = 0x7fffffff;
+        clin[c] = lin;
+        ccoord[c] = (u64)cc[0] | ((u64)cc[1] << 21) | ((u64)cc[2] << 42);
+        count[c] = 0u;
+        cocc[c] = 0ull;
+        cmin[c] = 0x7fffffff;
     }
+    }  // tiles
 }
 
 // ---- a2: per-cell counts, slot[i] = rank of point i inside its cell, fine occupancy ------
@@ -852,6 +847,169 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
                 }
         }
     }
+}
+
+// Cell starts, scatter cursors and the dense record numbering in one reduce-then-scan over the
+// occupied cells of the pair (points in the cell, cell is dense) packed in 64 bits -- point
+// count low, dense flag high (< 2^32 points, so the low half never carries): k_cellred sums
+// each tile of 2048 cells (every tile in parallel), k_celltscan (one block) scans the tile
+// sums, k_cellscan scans each tile again from its prefix and writes, per cell, the start and
+// the cursor (counting path: the counts are replaced in place; key path: the starts exist
+// already and only the dense rank is scanned), dlist / crec (record, or -1 for a sparse cell)
+// and the partial-scatter phase-0 bits of the sparse cells.  Replaces a counts scan, a
+// dense-flag pass, a popcount pass, a second scan and a list pass.  (A single-pass
+// decoupled look-back version took 0.7 ms on C5's 73M cells: the look-back chain.)
+constexpr int CL_THREADS = 256, CL_ITEMS = 8, CL_TILE = CL_THREADS * CL_ITEMS;
+__device__ __forceinline__ unsigned long long cell_pair(const uint32_t* __restrict__ cstart, int64_t i, int64_t U,
+                                                        bool ks) {
+    if (i >= U) return 0ull;
+    const uint32_t c = ks ? __ldg(cstart + i + 1) - __ldg(cstart + i) : cstart[i];
+    return (ks ? 0ull : (unsigned long long)c) | ((unsigned long long)(c > (uint32_t)SPARSE_MAX) << 32);
+}
+__global__ void __launch_bounds__(CL_THREADS) k_cellred(const uint32_t* __restrict__ cstart,
+                                                      const Meta* __restrict__ meta, const Grid* __restrict__ gp,
+                                                      unsigned long long* __restrict__ tsum) {
+    pdl_prologue();
+    if (gp->status) return;
+    __shared__ unsigned long long red[CL_THREADS / kWarp];
+    const int64_t U = meta->cells;
+    const bool ks = gp->key_sort;
+    const int64_t tiles = (U + 1 + CL_TILE - 1) / CL_TILE;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        unsigned long long v = 0ull;
+#pragma unroll
+        for (int k = 0; k < CL_ITEMS; ++k) v += cell_pair(cstart, t * CL_TILE + k * CL_THREADS + threadIdx.x, U, ks);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tot = 0ull;
+#pragma unroll
+            for (int k = 0; k < CL_THREADS / kWarp; ++k) tot += red[k];
+            tsum[t] = tot;
+        }
+    }
+}
+// One block: exclusive prefix of the tile sums in place; the totals -> ndense, cstart[U].
+__global__ void __launch_bounds__(1024) k_celltscan(unsigned long long* __restrict__ tsum, Meta* __restrict__ meta,
+                                                  const Grid* __restrict__ gp, uint32_t* __restrict__ cstart) {
+    pdl_prologue();
+    if (gp->status) return;
+    __shared__ unsigned long long wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t U = meta->cells;
+    const int64_t tiles = (U + 1 + CL_TILE - 1) / CL_TILE;
+    const int64_t per = (tiles + 1023) / 1024;
+    const int64_t b = tid * per, e = min(tiles, b + per);
+    unsigned long long run = 0ull;
+    for (int64_t t = b; t < e; ++t) run += tsum[t];
+    unsigned long long x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long v = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    unsigned long long pre = (x - run) + (w > 0 ? wsum[w - 1] : 0ull);
+    for (int64_t t = b; t < e; ++t) {
+        const unsigned long long v = tsum[t];
+        tsum[t] = pre;
+        pre += v;
+    }
+    if (tid == 1023) {
+        const unsigned long long tot = wsum[31];
+        meta->ndense = (int)(tot >> 32);
+        if (!gp->key_sort) cstart[U] = (uint32_t)tot;  // = n
+    }
+}
+__global__ void __launch_bounds__(CL_THREADS) k_cellscan(uint32_t* __restrict__ cstart, uint32_t* __restrict__ cursor,
+                                                       int* __restrict__ dlist, int* __restrict__ crec,
+                                                       uint32_t* __restrict__ cneed0, const Meta* __restrict__ meta,
+                                                       const Grid* __restrict__ gp,
+                                                       const unsigned long long* __restrict__ tpre) {
+    pdl_prologue();
+    if (gp->status) return;
+    __shared__ unsigned long long sv[CL_TILE + CL_TILE / 8];  // padded (pad8)
+    __shared__ unsigned long long wsum[CL_THREADS / kWarp];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t U = meta->cells;
+    const bool ks = gp->key_sort;
+    const int64_t tiles = (U + 1 + CL_TILE - 1) / CL_TILE;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t base = tile * CL_TILE;
+    __syncthreads();  // (the previous tile's writes read sv)
+#pragma unroll
+    for (int k = 0; k < CL_ITEMS; ++k) sv[pad8(k * CL_THREADS + tid)] = cell_pair(cstart, base + k * CL_THREADS + tid, U, ks);
+    __syncthreads();
+    // thread-serial over 8 consecutive elements, then warp and block scans
+    unsigned long long loc[CL_ITEMS];
+    unsigned long long run = 0ull;
+#pragma unroll
+    for (int k = 0; k < CL_ITEMS; ++k) {
+        loc[k] = run;
+        run += sv[pad8(tid * CL_ITEMS + k)];
+    }
+    unsigned long long x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long v = lane < CL_THREADS / kWarp ? wsum[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane < CL_THREADS / kWarp) wsum[lane] = v;
+    }
+    __syncthreads();
+    const unsigned long long pre = __ldg(tpre + tile) + (x - run) + (w > 0 ? wsum[w - 1] : 0ull);
+    // exclusive prefix of each element, keeping its own dense flag in bit 63 (free: < 2^62)
+#pragma unroll
+    for (int k = 0; k < CL_ITEMS; ++k) {
+        const unsigned long long own = sv[pad8(tid * CL_ITEMS + k)];
+        sv[pad8(tid * CL_ITEMS + k)] = (pre + loc[k]) | ((own >> 32) << 63);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CL_ITEMS; ++k) {
+        const int64_t i = base + k * CL_THREADS + tid;  // a warp: 32 consecutive cells
+        const unsigned long long e = sv[pad8(k * CL_THREADS + tid)];
+        const bool dense = (e >> 63) != 0;
+        if (i < U) {
+            if (!ks) {
+                cstart[i] = (uint32_t)e;
+                cursor[i] = (uint32_t)e;
+            }
+            if (dense) {
+                const int r = (int)((e >> 32) & 0x3fffffffull);
+                dlist[r] = (int)i;
+                crec[i] = r;  // (k_dcomps replaces it by the record word)
+            } else {
+                crec[i] = -1;
+            }
+        }
+        const unsigned sp = __ballot_sync(0xffffffffu, i < U && !dense);
+        if (lane == 0 && i < ((U + 31) & ~int64_t(31))) cneed0[i >> 5] = sp;  // (k_dcomps adds multi-component cells)
+    }
+    }  // tiles
 }
 
 // Dense bits of the occupied cells from the cell starts; also the scatter cursors.

@@ -74,9 +74,8 @@ __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int
 __global__ void k_cmark(const float* p, int64_t n, const Grid* gp, uint2* cw);
 __global__ void k_cpop(const uint2* cw, uint32_t* tsum, const Grid* gp);
 __global__ void k_tscan(uint32_t* tsum, const Grid* gp, Meta* meta, uint32_t* count);
-__global__ void k_cscan(uint2* cw, const Grid* gp, const uint32_t* tpre);
-__global__ void k_cemit(const uint2* cw, const uint32_t* tpre, uint32_t* clin, uint32_t* count, u64* cocc, int* cmin,
-                        u64* ccoord, const Grid* gp, const Meta* meta);
+__global__ void k_cscan(uint2* cw, const Grid* gp, const uint32_t* tpre, uint32_t* clin, uint32_t* count, u64* cocc,
+                        int* cmin, u64* ccoord);
 __global__ void k_lkey(const float* p, int64_t n, const Grid* gp, uint32_t* key, int* val, uint32_t* ghist,
                        uint32_t* state0, int64_t state_words);
 __global__ void k_smark(const uint32_t* key0, const uint32_t* key1, int64_t n, uint2* cw, const Grid* gp);
@@ -96,6 +95,10 @@ __global__ void k_dscatter(const float* p, int64_t n, const Grid* gp, const uint
 __global__ void k_dinit(const float4* spts, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                         const u64* cmask, int nbase, int* parent, int* size, int* minidx, int* sidx, const Meta* meta,
                         int all_parents);
+__global__ void k_cellred(const uint32_t* cstart, const Meta* meta, const Grid* gp, unsigned long long* tsum);
+__global__ void k_celltscan(unsigned long long* tsum, Meta* meta, const Grid* gp, uint32_t* cstart);
+__global__ void k_cellscan(uint32_t* cstart, uint32_t* cursor, int* dlist, int* crec, uint32_t* cneed0, const Meta* meta,
+                           const Grid* gp, const unsigned long long* tpre);
 __global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta,
                          const Grid* gp, int* crec, uint32_t* cneed0);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount, const Meta* meta);
