@@ -111,7 +111,8 @@ inline void mark_sub(int j, cudaStream_t st) {
 }
 
 constexpr int kMaxBBoxBlocks = 148 * 8;
-constexpr int64_t kSmallN = int64_t(1) << 17;  // below: the counting path only (no key-sort launches)
+constexpr int64_t kSmallN = int64_t(1) << 17;
+constexpr int64_t kRelabelBucketN = int64_t(1) << 22;  // from here: the two-pass bucketed relabel  // below: the counting path only (no key-sort launches)
 
 fec_status_t fail_cuda(cudaError_t e, const char* where) {
     g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -190,6 +191,7 @@ struct Layout {
     uint32_t* ghist;               // onesweep: [4][256] digit histograms
     uint32_t* dbits;               // [n/32+2] bitmap of dense compact ids
     uint32_t* cneed1;              // [n/32+2] partial scatter phase 1: cells a queued item reads
+    unsigned int* rlcur;           // [RL_MAX_BUCKETS] bucketed relabel: per-bucket cursors
     int64_t cs_tiles;              // k_cscan tiles (worst case over both cell-index modes)
     uint32_t* ctile;               // [cs_tiles] occupied cells per k_cscan tile, then their prefix
     uint2* cw;                     // occupancy words {bits, occupied cells before the word}
@@ -251,6 +253,7 @@ Layout carve(char* base, int64_t n) {
     L.ghist = ar.take<uint32_t>(4 * 256);
     L.dbits = ar.take<uint32_t>(dwords + 1);
     L.cneed1 = ar.take<uint32_t>(dwords + 1);
+    L.rlcur = ar.take<unsigned int>(n >= kRelabelBucketN ? (size_t)RL_CUR_STRIDE * ((n >> RL_SHIFT) + 1) : 1);
     ar.off = (ar.off + 255) & ~size_t(255);
     L.arena_words = (int64_t)((ar.off - a0) / 4);
     cv.off = ar.off;
@@ -563,7 +566,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         pdl(k_lkey, grid_for((n + 3) / 4, 256, di.sms * 4), 256, 0, st)(pts, n, gp, L.skey0, L.sval0, L.ghist, L.os_state, L.os_tiles * 256);
         ++launches;
         for (int pass = 0; pass < 4; ++pass) {  // passes beyond the planned count return at once
-            pdl(k_onesweep, (unsigned)std::min<int64_t>(L.os_tiles, di.sms * 2), RS_THREADS, 0, st)(gp, pass, L.skey0, L.sval0, L.skey1, L.sval1, n,
+            pdl(k_onesweep, (unsigned)std::min<int64_t>(L.os_tiles, di.sms * 3), RS_THREADS, 0, st)(gp, pass, L.skey0, L.sval0, L.skey1, L.sval1, n,
                                                                     L.ghist, L.os_state, L.os_tiles, L.ctr + 4);
             ++launches;
         }
@@ -611,7 +614,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         FEC_CUDA(cudaEventRecord(side->fork, st));
         FEC_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
         pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, side->s)(
-            gp, L.crec, L.ncomp, L.oflag, dctx, L.litems, L.lhalf, 1);
+            gp, L.crec, L.ncomp, L.oflag, dctx, L.litems, L.lhalf, 1, L.cw, L.dcoord);
         FEC_CUDA(cudaEventRecord(side->join, side->s));
         ++launches;
     }
@@ -649,10 +652,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // dense pairs on the side stream (forked after k_dcomps); the fallback runs only if a list
     // overflowed
     pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, st)(gp, L.crec, L.ncomp, L.oflag, dctx,
-                                                                            L.litems, L.lhalf, side ? 2 : 3);
+                                                                            L.litems, L.lhalf, side ? 2 : 3,
+                                                                            L.cw, L.dcoord);
     if (side) FEC_CUDA(cudaStreamWaitEvent(st, side->join, 0));
-    // (a litems list overflowed: every (record, slot) again, queueing like k_dense_link)
-    pdl(k_dense_link_all, di.sms * 2, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
     // queued pairs still apart after the certain unions (they mark the records whose points
     // they need), then partial scatter phase 1, the item-queue overflow fallback (in-place
     // point tests) and the queued point tests
@@ -669,7 +671,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
     pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
     pdl(k_dense_items, di.sms * 8, 256, 0, st)(gp, dctx, L.items2, L.slices2, L.idone);
-    launches += local_only ? 8 : 9;
+    launches += local_only ? 7 : 8;
     if (g_instrument) {
         pdl(k_dense_count, grid_for(dense_max(n), 256, cap), 256, 0, st)(L.ncomp, L.dlist, L.cstart, dctx);
         ++launches;
@@ -762,13 +764,19 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     mark(9, st);
     pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta,
                                      (uint32_t)(rec_pow2(n) - 1), L.cstart, L.slist, L.ncomp, L.dlist, L.crec);
-    // labels: input order for node-tail clouds, sorted order for sparse-dominated ones (one of
-    // the two returns at once)
+    // labels: input order for node-tail clouds, sorted order for sparse-dominated ones (large
+    // ones through the bucket pass inside k_relabel_in and k_relabel_b2; the kernels of the
+    // variant not chosen return at once)
+    const bool bucketed = n >= kRelabelBucketN;
+    uint2* tmp = bucketed ? reinterpret_cast<uint2*>(L.skey0) : nullptr;  // (the sort buffers are free again)
     pdl(k_relabel_in, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(pts, n, L.grid, L.cw, L.crec, L.cmask,
                                                                       L.cstart, L.spts, L.parent, L.minidx, labels,
-                                                                      L.meta, L.pcode);
-    pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(L.parent, C.val, L.minidx, n, labels, L.meta,
-                                                                   B ? B->off_dev : nullptr, B ? B->nclouds : 0);
+                                                                      L.meta, L.pcode, C.val, tmp, L.rlcur);
+    if (bucketed)
+        pdl(k_relabel_b2, grid_for((n + 1) / 2, 256, cap), 256, 0, st)(tmp, n, labels, L.meta);
+    else
+        pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(L.parent, C.val, L.minidx, n, labels, L.meta,
+                                                                       B ? B->off_dev : nullptr, B ? B->nclouds : 0);
     ++C.launches;
     C.launches += 4;
     mark(10, st);

@@ -1315,7 +1315,7 @@ __device__ __forceinline__ bool queue_item(const DenseCtx& C, int4 it) {
 // direction, plus slot 26 = its own component pairs when it has several ("DS" list).  Absent
 // and backward-dense neighbours produce nothing, so the link kernel's threads all have work.
 // Items are block-aggregated (one atomic per list per block) into two halves of `litems`; if a
-// half overflows, meta->list_overflow makes k_dense_link_all redo every (record, slot).
+// half overflows, meta->list_overflow makes k_dense_link (main stream) redo every (record, slot).
 __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                int* __restrict__ crec,
                                                const u64* __restrict__ cocc, const u64* __restrict__ ccoord,
@@ -1623,40 +1623,13 @@ __device__ __forceinline__ void dense_link_serial(int r, int k, const Grid& g, c
     dense_link_pair<true>(r, k, ox, oy, oz, cq, g, crec, ncomp, oflags, C);
 }
 
-// a6+a7 for dense cells: one thread per listed item (k_dcomps), the forward dense pairs first,
-// then the sparse neighbours and own pairs.  Certain component pairs are united at once;
-// non-certain pairs within reach whose nodes are still apart are queued (k_dense_filter
-// re-checks them after every certain union).
-// `which`: 1 = the forward dense pairs only (they touch no point: this launch may run on a side
-// stream concurrently with the scatter of the points), 2 = the sparse neighbours and own pairs
-// only, 3 = both lists.
-__global__ void __launch_bounds__(256, 4) k_dense_link(const Grid* __restrict__ gp, const int* __restrict__ crec,
-                                                   const int* __restrict__ ncomp, uint32_t* __restrict__ oflags,
-                                                   DenseCtx C, const uint4* __restrict__ litems, int lhalf, int which) {
-    FEC_PROLOGUE_GRID(gp);
-    if (g.status || C.meta->list_overflow) return;
-    __shared__ signed char soff[26][3];
-    if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
-    __syncthreads();
-    const int ndd = (which & 1) ? min(C.meta->ndd, lhalf) : 0, nds = (which & 2) ? min(C.meta->nds, lhalf) : 0;
-    const int tot = ndd + nds;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
-        const uint4 it = __ldg(litems + (i < ndd ? i : lhalf + (i - ndd)));
-        const int k = (int)it.y;
-        const int ox = k < 26 ? soff[k][0] : 0, oy = k < 26 ? soff[k][1] : 0, oz = k < 26 ? soff[k][2] : 0;
-        dense_link_pair<false>((int)it.x, k, ox, oy, oz, (int)it.z, g, crec, ncomp, oflags, C);
-    }
-}
-
 // Fallback when the item lists overflowed (never on the configs measured): every (record,
 // slot) is processed by its own thread, looking its neighbour up itself.  Unions are
 // idempotent and queued duplicates are filtered, so items already handled do no harm.
-__global__ void __launch_bounds__(256) k_dense_link_all(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
-                                                       const int* __restrict__ crec, const int* __restrict__ ncomp,
-                                                       const u64* __restrict__ dcoord,
-                                                       uint32_t* __restrict__ oflags, DenseCtx C) {
-    FEC_PROLOGUE_GRID(gp);
-    if (g.status || !C.meta->list_overflow) return;
+__device__ __forceinline__ void dense_link_all_body(const Grid& g, const uint2* __restrict__ cw,
+                                                    const int* __restrict__ crec, const int* __restrict__ ncomp,
+                                                    const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
+                                                    const DenseCtx& C) {
     const int64_t total = 27 * (int64_t)C.meta->ndense;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(t / 27), k = (int)(t % 27);
@@ -1675,7 +1648,40 @@ __global__ void __launch_bounds__(256) k_dense_link_all(const Grid* __restrict__
     }
 }
 
+// a6+a7 for dense cells: one thread per listed item (k_dcomps), the forward dense pairs first,
+// then the sparse neighbours and own pairs.  Certain component pairs are united at once;
+// non-certain pairs within reach whose nodes are still apart are queued (k_dense_filter
+// re-checks them after every certain union).
+// `which`: 1 = the forward dense pairs only (they touch no point: this launch may run on a side
+// stream concurrently with the scatter of the points), 2 = the sparse neighbours and own pairs
+// only, 3 = both lists.  If an item list overflowed, the launch with the sparse neighbours
+// (which & 2) runs the fallback over every (record, slot) instead (concurrent unions with a
+// side-stream launch are harmless: they commute) and the other returns at once.
+__global__ void __launch_bounds__(256, 4) k_dense_link(const Grid* __restrict__ gp, const int* __restrict__ crec,
+                                                   const int* __restrict__ ncomp, uint32_t* __restrict__ oflags,
+                                                   DenseCtx C, const uint4* __restrict__ litems, int lhalf, int which,
+                                                   const uint2* __restrict__ cw, const u64* __restrict__ dcoord) {
+    FEC_PROLOGUE_GRID(gp);
+    if (g.status) return;
+    if (C.meta->list_overflow) {
+        if (which & 2) dense_link_all_body(g, cw, crec, ncomp, dcoord, oflags, C);
+        return;
+    }
+    __shared__ signed char soff[26][3];
+    if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
+    __syncthreads();
+    const int ndd = (which & 1) ? min(C.meta->ndd, lhalf) : 0, nds = (which & 2) ? min(C.meta->nds, lhalf) : 0;
+    const int tot = ndd + nds;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+        const uint4 it = __ldg(litems + (i < ndd ? i : lhalf + (i - ndd)));
+        const int k = (int)it.y;
+        const int ox = k < 26 ? soff[k][0] : 0, oy = k < 26 ? soff[k][1] : 0, oz = k < 26 ? soff[k][2] : 0;
+        dense_link_pair<false>((int)it.x, k, ox, oy, oz, (int)it.z, g, crec, ncomp, oflags, C);
+    }
+}
+
 // Queue overflow: the marked slots' pairs are tested in place (one thread per record).
+// (A separate launch: folded into k_dense_items it raised that kernel's registers 64 -> 80.)
 __global__ void __launch_bounds__(256) k_dense_overflow(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                        const int* __restrict__ crec, const int* __restrict__ ncomp,
                                                        const u64* __restrict__ dcoord, uint32_t* __restrict__ oflags,
@@ -1910,6 +1916,57 @@ __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ nco
 // Loops are warp-uniform with a reconvergence point per neighbour (SIMT efficiency).
 constexpr int SP_CHUNK = 32;
 
+// The pair tests of a warp, dealt out evenly: lane l brings m_l pairs -- the rectangle
+// [ps, ps+np) x [qs, qs+nq) of its cell and a neighbour, or (nq < 0) the triangle of its own
+// cell's pairs -- the warp numbers all of them by a scan and takes them 32 at a time (a lane
+// finds its pair's owner by a binary search over the scan), so it runs ceil(sum m / 32)
+// rounds instead of max np x max nq lock-step iterations (C5: ~1 pair per lane and neighbour,
+// 10% SIMT efficiency in the nested form).  Returns this lane's tests.
+__device__ __forceinline__ int warp_pairs(const float4* __restrict__ spts, int* __restrict__ parent, float t2,
+                                          int lane, int ps, int np, int qs, int nq) {
+    const int m = nq >= 0 ? np * nq : np * (np - 1) / 2;
+    int incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int tests = 0;
+    for (int b0 = 0; b0 < total; b0 += 32) {
+        const int idx = b0 + lane;
+        int lo = 0;  // owner = number of lanes whose inclusive count is <= idx
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+            if (__shfl_sync(0xffffffffu, incl, lo + step - 1) <= idx) lo += step;
+        const int ex = __shfl_sync(0xffffffffu, incl - m, lo);
+        const int ops = __shfl_sync(0xffffffffu, ps, lo);
+        const int oqs = __shfl_sync(0xffffffffu, qs, lo);
+        const int onq = __shfl_sync(0xffffffffu, nq, lo);
+        const int onp = __shfl_sync(0xffffffffu, np, lo);
+        if (idx < total) {
+            int k = idx - ex, s, t;
+            if (onq > 0) {  // k < 36: k / onq = (k * ceil(256 / onq)) >> 8 (exact for k < 37)
+                const int mg = (int)((0x5634201590100ull >> (9 * (onq - 1))) & 511u);
+                const int q = (k * mg) >> 8;
+                s = ops + q;
+                t = oqs + (k - q * onq);
+            } else {
+                int i = 0;
+                while (k >= onp - 1 - i) {
+                    k -= onp - 1 - i;
+                    ++i;
+                }
+                s = ops + i;
+                t = s + 1 + k;
+            }
+            ++tests;
+            if (pred(__ldg(spts + s), __ldg(spts + t), t2)) uf_unite(parent, s, t);
+        }
+    }
+    return tests;
+}
+
 // Sparse-dominated clouds (occupied cells > n/4, ~1-2 points per cell): lane per sparse
 // cell, its own pairs and every sparse forward neighbour's points (dense neighbours are
 // handled by k_dense_link).  Clouds with few sparse cells use k_union_sparse_local instead;
@@ -1947,35 +2004,21 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
             const bool v = e < total;
             const uint32_t P = v ? list[e] : 0u;
             const int ps = v ? (int)__ldg(cstart + P) : 0;
-            const int pe = v ? (int)__ldg(cstart + P + 1) : 0;
-            for (int s = ps; s < pe; ++s) {
-                const float4 a = __ldg(spts + s);
-                for (int t = s + 1; t < pe; ++t) {
-                    ++n_tests;
-                    if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-                }
-            }
-            __syncwarp();
+            const int np = v ? (int)__ldg(cstart + P + 1) - ps : 0;
+            n_tests += warp_pairs(spts, parent, t2, lane, ps, np, 0, -1);  // own pairs
             const u64 pc = v ? __ldg(ccoord + P) : 0ull;
             const int c[3] = {(int)(pc & 0x1fffff), (int)((pc >> 21) & 0x1fffff), (int)(pc >> 42)};
 #pragma unroll 1
             for (int k = 0; k < 13; ++k) {
                 uint32_t Q;
-                int qs = 0, qe = 0, qc = -1;
+                int qs = 0, nq = 0, qc = -1;
                 if (v && dense_neighbor(g, c, c_fwd[k][0], c_fwd[k][1], c_fwd[k][2], Q)) qc = cid_lookup(cw, Q);
                 if (qc >= 0) {
                     qs = (int)__ldg(cstart + qc);
-                    qe = (int)__ldg(cstart + qc + 1);
-                    if (qe - qs > SPARSE_MAX) qe = qs;  // dense neighbours are handled by k_dense_link
+                    nq = (int)__ldg(cstart + qc + 1) - qs;
+                    if (nq > SPARSE_MAX) nq = 0;  // dense neighbours are handled by k_dense_link
                 }
-                for (int s = ps; s < pe && qe > qs; ++s) {
-                    const float4 a = __ldg(spts + s);
-                    for (int t = qs; t < qe; ++t) {
-                        ++n_tests;
-                        if (pred(a, __ldg(spts + t), t2)) uf_unite(parent, s, t);
-                    }
-                }
-                __syncwarp();
+                n_tests += warp_pairs(spts, parent, t2, lane, ps, np, qs, nq);
             }
         }
         __syncwarp();
@@ -2143,15 +2186,77 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
 // takes the folded label of its component's node (its fine sub-cell picks the component); a point
 // of a sparse cell is found among the cell's <= 6 sorted points (by its index) and takes its
 // root's folded label.  (The sorted-order pass below serves sparse-dominated clouds.)
-__global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p, int64_t n,
+// a10 for large sparse-dominated clouds, in two passes.  k_relabel's label stores go to random
+// input positions (shuffled input): each 4-byte store dirties a whole 32-byte sector and the
+// sectors leave L2 long before their neighbours arrive (C5: 3.4 GB written for 0.44 GB of
+// labels), and the store stream evicts the roots' labels the loads need.  Pass 1 computes the
+// labels in sorted order (coalesced reads, roots nearby) and writes (input index, label) pairs
+// bucket-major into a temporary: bucket b = input index >> RL_SHIFT owns the temporary's range
+// [b << RL_SHIFT, ...) -- the sorted positions are a permutation of the input indices, so a
+// bucket holds exactly as many pairs as its index range -- and a block reserves one run per
+// bucket and tile (one global atomic each).  Pass 2 streams the temporary in order: the blocks
+// in flight write into one or two buckets' 1 MB label ranges, which stay in L2 until their
+// sectors are complete.
+__device__ __forceinline__ void relabel_bucket_body(const int* __restrict__ parent, const int* __restrict__ val,
+                                                    const int* __restrict__ minidx, int64_t n,
+                                                    uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
+                                                    const int64_t* __restrict__ boff, int nclouds) {
+    __shared__ unsigned int hist[RL_MAX_BUCKETS];  // per tile: counts, then the runs' starts
+    const int nb = (int)((n + (int64_t(1) << RL_SHIFT) - 1) >> RL_SHIFT);
+    constexpr int PER = RL_TILE / 256;
+    for (int64_t t0 = (int64_t)blockIdx.x * RL_TILE; t0 < n; t0 += (int64_t)gridDim.x * RL_TILE) {
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+        __syncthreads();
+        int v[PER], lab[PER];
+        unsigned int rank[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int64_t s = t0 + j * 256 + threadIdx.x;
+            v[j] = -1;
+            if (s < n) {
+                v[j] = __ldg(val + s);
+                int l = __ldg(minidx + __ldg(parent + s));
+                if (boff && l >= 0) {  // batch mode: index inside the point's own cloud
+                    int lo = 0, hi = nclouds;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (__ldg(boff + mid) <= (int64_t)v[j]) lo = mid;
+                        else hi = mid;
+                    }
+                    l -= (int)__ldg(boff + lo);
+                }
+                lab[j] = l;
+                rank[j] = atomicAdd(&hist[v[j] >> RL_SHIFT], 1u);
+            }
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const unsigned int c = hist[b];
+            if (c) hist[b] = (b << RL_SHIFT) + atomicAdd(cursor + b * RL_CUR_STRIDE, c);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (v[j] >= 0) tmp[hist[v[j] >> RL_SHIFT] + rank[j]] = make_uint2((unsigned)v[j], (unsigned)lab[j]);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256, 8) k_relabel_in(const float* __restrict__ p, int64_t n,
                                                    const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                    const int* __restrict__ crec, const u64* __restrict__ cmask,
                                                    const uint32_t* __restrict__ cstart,
                                                    const float4* __restrict__ spts, const int* __restrict__ parent,
                                                    const int* __restrict__ minidx, int* __restrict__ labels,
-                                                   const Meta* __restrict__ meta, const uint32_t* __restrict__ pcode) {
+                                                   const Meta* __restrict__ meta, const uint32_t* __restrict__ pcode,
+                                                   const int* __restrict__ val, uint2* __restrict__ tmp,
+                                                   unsigned int* __restrict__ cursor) {
     FEC_PROLOGUE_GRID(gp);
-    if (g.status || 4 * (int64_t)meta->cells > n) return;
+    if (g.status) return;
+    if (4 * (int64_t)meta->cells > n) {  // sparse-dominated: labels from the sorted order
+        if (tmp) relabel_bucket_body(parent, val, minidx, n, tmp, cursor, g.batch ? g.boff : nullptr, g.nclouds);
+        return;
+    }
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     // (codes exist on the counting path when cells <= kCodeCells; node-tail clouds have
     // cells <= n/4 and the key-sort path writes none)

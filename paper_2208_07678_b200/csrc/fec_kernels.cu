@@ -371,40 +371,47 @@ __device__ __forceinline__ void stats_body(const int* __restrict__ parent, const
     __syncthreads();
     const int lane = threadIdx.x & 31;
     unsigned long long roots = 0;
-    const int64_t chunk = ((n + nblk - 1) / nblk + 255) / 256 * 256;
+    // each thread takes 4 consecutive positions per round (int4 loads: 4 loads in flight); the
+    // lanes of one distinct root meet in one __match_any_sync per position slot, and their
+    // leader adds the group's count and minimum once: into the block's table if the root owns
+    // its slot (the giant component claims one early), else straight to the root
+    const int64_t chunk = ((n + nblk - 1) / nblk + 1023) / 1024 * 1024;
     const int64_t b0 = (int64_t)bid * chunk, b1 = min(n, b0 + chunk);
-    for (int64_t s0 = b0; s0 < b1; s0 += blockDim.x) {
-        const int64_t s = s0 + threadIdx.x;
-        const bool ok = s < b1;
-        const int r = ok ? __ldg(parent + s) : -1;
-        const int v = ok ? __ldg(val + s) : 0x7fffffff;
-        roots += (ok && r == (int)s) ? 1ull : 0ull;
-        unsigned todo = __ballot_sync(0xffffffffu, ok);
-        while (todo) {
-            const int leader = __ffs(todo) - 1;
-            const int key = __shfl_sync(0xffffffffu, r, leader);
-            const bool mem = ok && r == key;
-            const unsigned peers = __ballot_sync(0xffffffffu, mem);
-            const int mn = __reduce_min_sync(0xffffffffu, mem ? v : 0x7fffffff);
-            if (lane == leader) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(parent) | reinterpret_cast<uintptr_t>(val)) & 15u) == 0;
+    for (int64_t s0 = b0; s0 < b1; s0 += 4 * (int64_t)blockDim.x) {
+        const int64_t sb = s0 + 4 * (int64_t)threadIdx.x;
+        int r[4], v[4];
+        if (vec && sb + 4 <= b1) {
+            const int4 pr = __ldg(reinterpret_cast<const int4*>(parent + sb));
+            const int4 vv = __ldg(reinterpret_cast<const int4*>(val + sb));
+            r[0] = pr.x; r[1] = pr.y; r[2] = pr.z; r[3] = pr.w;
+            v[0] = vv.x; v[1] = vv.y; v[2] = vv.z; v[3] = vv.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                r[j] = sb + j < b1 ? __ldg(parent + sb + j) : -1;
+                v[j] = sb + j < b1 ? __ldg(val + sb + j) : 0x7fffffff;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int key = r[j];
+            roots += (key >= 0 && key == (int)(sb + j)) ? 1ull : 0ull;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            const int mn = __reduce_min_sync(peers, v[j]);
+            if (key >= 0 && lane == __ffs(peers) - 1) {
                 const int cnt = __popc(peers);
-                unsigned h = ((unsigned)key * 2654435761u) >> 24;  // 256 slots
-                bool done = false;
-                for (int probe = 0; probe < 4 && !done; ++probe, h = (h + 1) & (HH_SLOTS - 1)) {
-                    int cur = hkey[h];
-                    if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
-                    if (cur == -1 || cur == key) {
-                        atomicAdd(&hcnt[h], cnt);
-                        atomicMin(&hmin[h], mn);
-                        done = true;
-                    }
-                }
-                if (!done) {
+                const unsigned h = ((unsigned)key * 2654435761u) >> 24;  // 256 slots
+                int cur = hkey[h];
+                if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
+                if (cur == -1 || cur == key) {
+                    atomicAdd(&hcnt[h], cnt);
+                    atomicMin(&hmin[h], mn);
+                } else {
                     atomicAdd(size + key, cnt);
                     atomicMin(minidx + key, mn);
                 }
             }
-            todo &= ~peers;
         }
     }
     __syncthreads();
@@ -635,6 +642,30 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
             }
             labels[v[j]] = l;
         }
+    }
+}
+
+// a10 for large sparse-dominated clouds, second pass (the first one is the bucket pass inside
+// k_relabel_in, fec_dense.cu): the temporary streamed in order; the blocks in flight write into
+// one or two buckets' 1 MB label ranges, which stay in L2 until their sectors are complete.
+__global__ void __launch_bounds__(256) k_relabel_b2(const uint2* __restrict__ tmp, int64_t n,
+                                                   int* __restrict__ labels, const Meta* __restrict__ meta) {
+    pdl_prologue();
+    if (meta->status || 4 * (int64_t)meta->cells <= n) return;
+    const int64_t pairs = n / 2;  // two entries per 16-byte load (tmp is 256-B aligned)
+    const uint4* t4 = reinterpret_cast<const uint4*>(tmp);
+    // the label stores carry an L2 evict-last hint, the temporary's loads evict-first, so the
+    // partially written label sectors are the last lines L2 gives up
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 e = __ldcs(t4 + i);
+        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(labels + e.x), "r"(e.y), "l"(pol) : "memory");
+        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(labels + e.z), "r"(e.w), "l"(pol) : "memory");
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+        const uint2 e = tmp[n - 1];
+        labels[e.x] = (int)e.y;
     }
 }
 

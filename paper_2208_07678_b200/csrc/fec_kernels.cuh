@@ -38,7 +38,7 @@ struct Meta {
     int nsparse;                      // dense-grid mode: occupied cells with <= SPARSE_MAX points
     int nslices_extra;                // dense-grid mode: extra slices of heavy uncertain pairs
     int ndd, nds;                     // dense link items: forward dense pairs / sparse neighbours + own pairs
-    int list_overflow;                // != 0: a link item list overflowed (k_dense_link_all redoes all)
+    int list_overflow;                // != 0: a link item list overflowed (k_dense_link redoes all)
 };
 
 // What the host passes to a1 (k_bbox); its last block turns the bbox into the Grid (plan_grid).
@@ -69,6 +69,12 @@ __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64
                           const int* slist, const int* ncomp, const int* dlist, int* crec);
 __global__ void k_relabel(const int* parent, const int* val, const int* minidx, int64_t n, int* labels,
                           const Meta* meta, const int64_t* boff, int nclouds);
+// bucketed relabel (large sparse-dominated clouds): RL_SHIFT bits of input index per bucket
+constexpr int RL_SHIFT = 18;
+constexpr int RL_TILE = 2048;
+constexpr int RL_MAX_BUCKETS = 4096;  // n <= 2^30 (fec_max_points < 2^30)
+constexpr int RL_CUR_STRIDE = 32;     // one bucket cursor per 128-byte line (L2 slices in parallel)
+__global__ void k_relabel_b2(const uint2* tmp, int64_t n, int* labels, const Meta* meta);
 __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
                               unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, const Grid* gp, uint2* cw);
@@ -139,7 +145,8 @@ __global__ void k_tail_stats(int* parent, const int* val, int64_t n, int* size, 
                              const float4* spts);
 __global__ void k_relabel_in(const float* p, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                              const u64* cmask, const uint32_t* cstart, const float4* spts, const int* parent,
-                             const int* minidx, int* labels, const Meta* meta, const uint32_t* pcode);
+                             const int* minidx, int* labels, const Meta* meta, const uint32_t* pcode,
+                             const int* val, uint2* tmp, unsigned int* cursor);
 // local_only != 0 (small clouds, host-chosen): the sparse cells always go through the compact
 // list and k_union_sparse_local (more parallel per cell), whatever their share of the cells.
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
@@ -150,12 +157,10 @@ __global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const 
 __global__ void k_slist(const uint32_t* cstart, int* slist, Meta* meta, int64_t n, int local_only, const Grid* gp,
                         int all_parents, int* parent, int* size, int* minidx);
 __global__ void k_dense_link(const Grid* gp, const int* crec, const int* ncomp, uint32_t* oflags, DenseCtx C,
-                             const uint4* litems, int lhalf, int which);
-__global__ void k_dense_link_all(const Grid* gp, const uint2* cw, const int* crec, const int* ncomp,
-                                 const u64* dcoord, uint32_t* oflags, DenseCtx C);
+                             const uint4* litems, int lhalf, int which, const uint2* cw, const u64* dcoord);
+__global__ void k_dense_filter(DenseCtx C, int4* items2, int4* slices2, int* idone);
 __global__ void k_dense_overflow(const Grid* gp, const uint2* cw, const int* crec, const int* ncomp,
                                  const u64* dcoord, uint32_t* oflags, DenseCtx C);
-__global__ void k_dense_filter(DenseCtx C, int4* items2, int4* slices2, int* idone);
 __global__ void k_dense_items(const Grid* gp, DenseCtx C, const int4* items2, const int4* slices2, int* idone);
 __global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta, uint32_t rmask);
 __global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);

@@ -18,6 +18,9 @@ namespace fec {
 
 constexpr int OS_THREADS = 256, OS_ITEMS = 16, OS_TILE = OS_THREADS * OS_ITEMS;
 constexpr uint32_t OS_PREFIX = 0x80000000u;
+// 3 resident blocks per SM (registers <= 85): the look-back and the digit-run stores of
+// one tile overlap the loads and ranking of the others (2 blocks: 1.4 TB/s per pass on C5)
+constexpr int OS_MIN_BLOCKS = 3;
 static_assert(OS_TILE == RS_TILE, "onesweep tiles = radix tiles (workspace sizing)");
 
 __device__ __forceinline__ uint32_t ld_state(const uint32_t* p) {
@@ -29,7 +32,7 @@ __device__ __forceinline__ void st_state(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(const Grid* __restrict__ gp, int pass, uint32_t* __restrict__ k0,
+__global__ void __launch_bounds__(OS_THREADS, OS_MIN_BLOCKS) k_onesweep(const Grid* __restrict__ gp, int pass, uint32_t* __restrict__ k0,
                                                         int* __restrict__ v0, uint32_t* __restrict__ k1,
                                                         int* __restrict__ v1, int64_t n,
                                                         const uint32_t* __restrict__ ghist,
@@ -67,19 +70,18 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(const Grid* __restrict_
     uint32_t k[OS_ITEMS];
     int v[OS_ITEMS];
     uint32_t rank[OS_ITEMS];
-    int dig[OS_ITEMS];
+    const int64_t nvalid = n - base;  // items it with it * kWarp + lane < nvalid are keys
 #pragma unroll
     for (int it = 0; it < OS_ITEMS; ++it) {
         const int64_t i = base + it * kWarp + lane;
         const bool ok = i < n;
         k[it] = ok ? __ldg(kin + i) : 0u;
         v[it] = ok ? __ldg(vin + i) : 0;
-        dig[it] = ok ? (int)((k[it] >> shift) & 255u) : 256;
     }
     // rank inside the warp's 512 keys (iteration-major, lane-minor = input order)
 #pragma unroll
     for (int it = 0; it < OS_ITEMS; ++it) {
-        const int d = dig[it];
+        const int d = (it * kWarp + lane < nvalid) ? (int)((k[it] >> shift) & 255u) : 256;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t c = d < 256 ? wcnt[w][d] : 0u;
         __syncwarp();
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(const Grid* __restrict_
     // stage the tile in digit order
 #pragma unroll
     for (int it = 0; it < OS_ITEMS; ++it) {
-        const int dd = dig[it];
+        const int dd = (it * kWarp + lane < nvalid) ? (int)((k[it] >> shift) & 255u) : 256;
         if (dd < 256) {
             const uint32_t lp = tstart[dd] + wcnt[w][dd] + rank[it];
             sk[lp] = k[it];

@@ -24,10 +24,10 @@ def raw(rep):
 L = launch_table(launches_csv)
 ids = sorted(L)
 # last complete step = kernels after the last k_bbox_partial
-last = max(i for i in ids if L[i]['k'] == 'k_bbox_partial')
+last = max(i for i in ids if L[i]['k'] in ('k_bbox', 'k_bbox_partial'))
 step = [i for i in ids if i >= last]
 tot = sum(L[i]['gpu__time_duration.sum'] for i in step)
-lines = [f"# {rnd}: C4 launch list and ncu summary", "",
+lines = [f"# {rnd}: launch list and ncu summary", "",
          "Source: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
          "--clock-control none -c 400 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e` "
          "(cold-cache, serialised launches: compare shares, not absolutes).  Raw CSV: "

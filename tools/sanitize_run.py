@@ -15,6 +15,11 @@ cases = [("C1",) + tuple(synth.make_config("C1").__dict__[k] for k in ("points",
 for s in range(20):
     p, d, geom = synth.random_cloud(s, n=int(np.random.default_rng(s).integers(200, 4000)))
     cases.append((f"seed{s}-{geom}", p, d, 2, 10**6))
+# clouds above the small-cloud threshold: the counting path with dense cells and the side
+# stream (C4 at 1%), and the key-sort path of shuffled input (C5 at 0.2%)
+for name, scale in (("C4", 0.01), ("C5", 0.002)):
+    w = synth.make_config(name, scale=scale)
+    cases.append((f"{name}@{scale}", w.points, w.d_th, w.min_size, w.max_size))
 for mode in (0, 1, 2, 3):
     fec.set_grid_mode(mode)
     for name, p, d, mn, mx in cases:
