@@ -148,8 +148,8 @@ STAGE_KERNELS = {
                        "overflow fallback), k_flatten_nodes, k_dense_filter, k_dense_overflow, k_dense_items",
     "a8_flatten": "k_flatten_if",
     "a9_stats": "k_tail_stats",
-    "a10_relabel": "k_rootlab, k_relabel_in (node-tail clouds; large sparse-dominated ones: the bucket pass) + "
-                   "k_relabel_b2 / k_relabel",
+    "a10_relabel": "k_rootlab (large sparse-dominated clouds: the bucket pass), k_relabel_in (node-tail clouds) + "
+                   "k_relabel_b2c (a cluster per bucket) / k_relabel",
 }
 
 

@@ -72,6 +72,8 @@ typedef struct {
     int32_t dense_table;    /* 1: dense cell grid (counting sort), 0: Morton radix sort + hash */
     int32_t dims[3];        /* cells per axis */
     int32_t launches;       /* kernel launches of the call (all of them the library's own) */
+    int32_t binning;        /* 0: counting sort (coherent input), 1: key sort (shuffled input
+                               above 2^17 points, grid mode 2); -1 unless instrumented */
 } fec_stats_t;
 
 /* Bytes of device workspace fec_cluster_ws needs for n points (an upper bound that does

@@ -49,7 +49,7 @@ class FecStats(ctypes.Structure):
                 ("dense_points", ctypes.c_int64), ("dense_tests", ctypes.c_int64),
                 ("key_bits", ctypes.c_int64),
                 ("radix_passes", ctypes.c_int32), ("dense_table", ctypes.c_int32),
-                ("dims", ctypes.c_int32 * 3), ("launches", ctypes.c_int32)]
+                ("dims", ctypes.c_int32 * 3), ("launches", ctypes.c_int32), ("binning", ctypes.c_int32)]
 
 
 class SlabState(ctypes.Structure):

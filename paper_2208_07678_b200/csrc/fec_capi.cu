@@ -112,7 +112,8 @@ inline void mark_sub(int j, cudaStream_t st) {
 
 constexpr int kMaxBBoxBlocks = 148 * 8;
 constexpr int64_t kSmallN = int64_t(1) << 17;
-constexpr int64_t kRelabelBucketN = int64_t(1) << 22;  // from here: the two-pass bucketed relabel  // below: the counting path only (no key-sort launches)
+constexpr int64_t kRelabelBucketN = int64_t(1) << 22;  // from here: the two-pass bucketed relabel
+  // below: the counting path only (no key-sort launches)
 
 fec_status_t fail_cuda(cudaError_t e, const char* where) {
     g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -693,6 +694,7 @@ fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
     g_stats.key_bits = -1;
     g_stats.radix_passes = -1;
     g_stats.dense_table = -1;
+    g_stats.binning = -1;
     for (int a = 0; a < 3; ++a) g_stats.dims[a] = -1;
     g_stats.launches = C.launches;
     if (g_instrument) {
@@ -709,6 +711,7 @@ fec_status_t finish_stats(const Core& C, int64_t n, cudaStream_t st) {
         g_stats.key_bits = g.key_bits;
         g_stats.radix_passes = g.passes;
         g_stats.dense_table = g.hashed ? 0 : 1;
+        g_stats.binning = g.key_sort ? 1 : 0;
         for (int a = 0; a < 3; ++a) g_stats.dims[a] = g.dims[a];
         g_stats.cells = m.cells;
         g_stats.groups = -1;
@@ -759,21 +762,36 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     pdl(k_flatten_if, wave, 256, 0, st)(L.parent, n, L.meta);
     mark(8, st);
     // (at least two blocks: the node tail splits the grid in halves)
+    // large sparse-dominated clouds: the bucket pass of k_relabel_in applies the size filter
+    // (k_rootlab returns at once for them), and a filter keeping every size needs no counts
+    const bool bucketed = n >= kRelabelBucketN;
+    const int count_sizes = (bucketed && min_size <= 1 && max_size >= n) ? 0 : 1;
+    uint2* tmp = bucketed ? reinterpret_cast<uint2*>(L.skey0) : nullptr;  // (the sort buffers are free again)
     pdl(k_tail_stats, std::max(ew, 2u), 256, 0, st)(L.parent, C.val, n, L.size, L.minidx, L.meta, L.ncomp,
-                                                   L.cstart, L.slist, (uint32_t)(rec_pow2(n) - 1), L.spts);
+                                                   L.cstart, L.slist, (uint32_t)(rec_pow2(n) - 1), L.spts,
+                                                   count_sizes);
     mark(9, st);
     pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta,
-                                     (uint32_t)(rec_pow2(n) - 1), L.cstart, L.slist, L.ncomp, L.dlist, L.crec);
+                                     (uint32_t)(rec_pow2(n) - 1), L.cstart, L.slist, L.ncomp, L.dlist, L.crec,
+                                     C.val, tmp, L.rlcur, L.grid);
     // labels: input order for node-tail clouds, sorted order for sparse-dominated ones (large
-    // ones through the bucket pass inside k_relabel_in and k_relabel_b2; the kernels of the
-    // variant not chosen return at once)
-    const bool bucketed = n >= kRelabelBucketN;
-    uint2* tmp = bucketed ? reinterpret_cast<uint2*>(L.skey0) : nullptr;  // (the sort buffers are free again)
+    // ones: the bucket pass in k_rootlab, then k_relabel_b2c); the kernels of the variant
+    // not chosen return at once
     pdl(k_relabel_in, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(pts, n, L.grid, L.cw, L.crec, L.cmask,
                                                                       L.cstart, L.spts, L.parent, L.minidx, labels,
-                                                                      L.meta, L.pcode, C.val, tmp, L.rlcur);
-    if (bucketed)
-        pdl(k_relabel_b2, grid_for((n + 1) / 2, 256, cap), 256, 0, st)(tmp, n, labels, L.meta);
+                                                                      L.meta, L.pcode);
+    if (bucketed) {
+        static bool attr_set[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!attr_set[dev & 63]) {
+            FEC_CUDA(cudaFuncSetAttribute(k_relabel_b2c, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RL_CTA_SHIFT));
+            attr_set[dev & 63] = true;
+        }
+        const int64_t nb = (n + (1 << RL_SHIFT) - 1) >> RL_SHIFT;
+        const int64_t clusters = std::min<int64_t>(nb, dev_info().sms / RL_CLUSTER);
+        pdl(k_relabel_b2c, (unsigned)(clusters * RL_CLUSTER), 1024, 4 << RL_CTA_SHIFT, st)(tmp, n, labels, L.meta);
+    }
     else
         pdl(k_relabel, grid_for((n + 3) / 4, 256, cap * 4), 256, 0, st)(L.parent, C.val, L.minidx, n, labels, L.meta,
                                                                        B ? B->off_dev : nullptr, B ? B->nclouds : 0);

@@ -144,8 +144,11 @@ __device__ __forceinline__ bool dense_neighbor(const Grid& g, const int c[3], in
 // aligned (more bytes in flight per thread than one scalar load per coordinate).
 struct Pts4 {
     float x[4], y[4], z[4];
+    int i[4];  // input indices
 };
 __device__ __forceinline__ void load_pts4(const float* __restrict__ p, int64_t n, int64_t base, bool vec, Pts4& P) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) P.i[j] = (int)(base + j);
     if (vec && base + 4 <= n) {
         const float4* q = reinterpret_cast<const float4*>(p + 3 * base);
         const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -478,7 +481,7 @@ __device__ __forceinline__ void point_runs(const Pts4& P, int64_t b4, int64_t n,
         R.q[j] = 0;
         if (b4 + j < n) {
             uint32_t lin;
-            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, R.q[j]);
+            dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, R.q[j]);
             R.cid[j] = cid_of(cw, lin);
         }
         const bool fresh = j == 0 || R.cid[j] != R.cid[j > 0 ? j - 1 : 0];
@@ -568,8 +571,8 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
-        // runs of this thread's points in one cell take one table update
-        // (a run's first point has its smallest input index)
+        // runs of this thread's points in one cell take one table update (and the run's
+        // smallest input index)
         uint32_t code[4] = {0u, 0u, 0u, 0u};
         uint32_t rc = 0xffffffffu, rn = 0u;
         int rfirst = 0;
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, q);
                 const uint32_t cid = cid_of(cw, lin);
                 code[j] = (cid << 6) | (uint32_t)q;
                 if (cid != rc) {
@@ -593,8 +596,9 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
                     rc = cid;
                     rn = 0u;
                     rb = 0ull;
-                    rfirst = (int)(b4 + j);
+                    rfirst = P.i[j];
                 }
+                rfirst = min(rfirst, P.i[j]);
                 ++rn;
                 rb |= 1ull << q;
             }
@@ -721,7 +725,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (R.cid[j] != 0xffffffffu)
-                    spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
+                    spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float(P.i[j]));
         }
         return;
     }
@@ -782,7 +786,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (R.cid[j] != 0xffffffffu)
-                spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
+                spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float(P.i[j]));
     }
 }
 
@@ -2186,77 +2190,15 @@ __global__ void __launch_bounds__(256) k_union_sparse_local(const float4* __rest
 // takes the folded label of its component's node (its fine sub-cell picks the component); a point
 // of a sparse cell is found among the cell's <= 6 sorted points (by its index) and takes its
 // root's folded label.  (The sorted-order pass below serves sparse-dominated clouds.)
-// a10 for large sparse-dominated clouds, in two passes.  k_relabel's label stores go to random
-// input positions (shuffled input): each 4-byte store dirties a whole 32-byte sector and the
-// sectors leave L2 long before their neighbours arrive (C5: 3.4 GB written for 0.44 GB of
-// labels), and the store stream evicts the roots' labels the loads need.  Pass 1 computes the
-// labels in sorted order (coalesced reads, roots nearby) and writes (input index, label) pairs
-// bucket-major into a temporary: bucket b = input index >> RL_SHIFT owns the temporary's range
-// [b << RL_SHIFT, ...) -- the sorted positions are a permutation of the input indices, so a
-// bucket holds exactly as many pairs as its index range -- and a block reserves one run per
-// bucket and tile (one global atomic each).  Pass 2 streams the temporary in order: the blocks
-// in flight write into one or two buckets' 1 MB label ranges, which stay in L2 until their
-// sectors are complete.
-__device__ __forceinline__ void relabel_bucket_body(const int* __restrict__ parent, const int* __restrict__ val,
-                                                    const int* __restrict__ minidx, int64_t n,
-                                                    uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
-                                                    const int64_t* __restrict__ boff, int nclouds) {
-    __shared__ unsigned int hist[RL_MAX_BUCKETS];  // per tile: counts, then the runs' starts
-    const int nb = (int)((n + (int64_t(1) << RL_SHIFT) - 1) >> RL_SHIFT);
-    constexpr int PER = RL_TILE / 256;
-    for (int64_t t0 = (int64_t)blockIdx.x * RL_TILE; t0 < n; t0 += (int64_t)gridDim.x * RL_TILE) {
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
-        __syncthreads();
-        int v[PER], lab[PER];
-        unsigned int rank[PER];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int64_t s = t0 + j * 256 + threadIdx.x;
-            v[j] = -1;
-            if (s < n) {
-                v[j] = __ldg(val + s);
-                int l = __ldg(minidx + __ldg(parent + s));
-                if (boff && l >= 0) {  // batch mode: index inside the point's own cloud
-                    int lo = 0, hi = nclouds;
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (__ldg(boff + mid) <= (int64_t)v[j]) lo = mid;
-                        else hi = mid;
-                    }
-                    l -= (int)__ldg(boff + lo);
-                }
-                lab[j] = l;
-                rank[j] = atomicAdd(&hist[v[j] >> RL_SHIFT], 1u);
-            }
-        }
-        __syncthreads();
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-            const unsigned int c = hist[b];
-            if (c) hist[b] = (b << RL_SHIFT) + atomicAdd(cursor + b * RL_CUR_STRIDE, c);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < PER; ++j)
-            if (v[j] >= 0) tmp[hist[v[j] >> RL_SHIFT] + rank[j]] = make_uint2((unsigned)v[j], (unsigned)lab[j]);
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256, 8) k_relabel_in(const float* __restrict__ p, int64_t n,
+__global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p, int64_t n,
                                                    const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                    const int* __restrict__ crec, const u64* __restrict__ cmask,
                                                    const uint32_t* __restrict__ cstart,
                                                    const float4* __restrict__ spts, const int* __restrict__ parent,
                                                    const int* __restrict__ minidx, int* __restrict__ labels,
-                                                   const Meta* __restrict__ meta, const uint32_t* __restrict__ pcode,
-                                                   const int* __restrict__ val, uint2* __restrict__ tmp,
-                                                   unsigned int* __restrict__ cursor) {
+                                                   const Meta* __restrict__ meta, const uint32_t* __restrict__ pcode) {
     FEC_PROLOGUE_GRID(gp);
-    if (g.status) return;
-    if (4 * (int64_t)meta->cells > n) {  // sparse-dominated: labels from the sorted order
-        if (tmp) relabel_bucket_body(parent, val, minidx, n, tmp, cursor, g.batch ? g.boff : nullptr, g.nclouds);
-        return;
-    }
+    if (g.status || 4 * (int64_t)meta->cells > n) return;  // (sparse-dominated: from the sorted order)
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     // (codes exist on the counting path when cells <= kCodeCells; node-tail clouds have
     // cells <= n/4 and the key-sort path writes none)
@@ -2282,7 +2224,7 @@ __global__ void __launch_bounds__(256, 8) k_relabel_in(const float* __restrict__
                 cid[j] = 0;
                 if (b4 + j >= n) continue;
                 uint32_t lin;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q[j]);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, q[j]);
                 cid[j] = cid_of(cw, lin);
             }
         }

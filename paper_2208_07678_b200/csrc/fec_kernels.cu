@@ -5,6 +5,8 @@
 
 #include "fec_internal.cuh"
 #include "fec_kernels.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace fec {
 
@@ -364,7 +366,8 @@ constexpr int HH_SLOTS = 256;
 // flattened by k_flatten_if), where per-lane aggregation of this form is the faster one.
 __device__ __forceinline__ void stats_body(const int* __restrict__ parent, const int* __restrict__ val, int64_t n,
                                               int* __restrict__ size, int* __restrict__ minidx,
-                                              Meta* __restrict__ meta, int only_sparse, int bid, int nblk) {
+                                              Meta* __restrict__ meta, int only_sparse, int bid, int nblk,
+                                              bool count_sizes) {
     if (only_sparse && 4 * (int64_t)meta->cells <= n) return;
     __shared__ int hkey[HH_SLOTS], hcnt[HH_SLOTS], hmin[HH_SLOTS];
     for (int k = threadIdx.x; k < HH_SLOTS; k += blockDim.x) { hkey[k] = -1; hcnt[k] = 0; hmin[k] = 0x7fffffff; }
@@ -405,10 +408,10 @@ __device__ __forceinline__ void stats_body(const int* __restrict__ parent, const
                 int cur = hkey[h];
                 if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
                 if (cur == -1 || cur == key) {
-                    atomicAdd(&hcnt[h], cnt);
+                    if (count_sizes) atomicAdd(&hcnt[h], cnt);
                     atomicMin(&hmin[h], mn);
                 } else {
-                    atomicAdd(size + key, cnt);
+                    if (count_sizes) atomicAdd(size + key, cnt);
                     atomicMin(minidx + key, mn);
                 }
             }
@@ -527,17 +530,104 @@ __global__ void __launch_bounds__(256) k_tail_stats(int* __restrict__ parent, co
                                                    int* __restrict__ size, int* __restrict__ minidx,
                                                    Meta* __restrict__ meta, const int* __restrict__ ncomp,
                                                    const uint32_t* __restrict__ cstart, const int* __restrict__ slist,
-                                                   uint32_t rmask, const float4* __restrict__ spts) {
+                                                   uint32_t rmask, const float4* __restrict__ spts, int count_sizes) {
     pdl_prologue();
     if (meta->status) return;
     if (4 * (int64_t)meta->cells > n) {
-        stats_body(parent, val, n, size, minidx, meta, 1, blockIdx.x, gridDim.x);
+        // (count_sizes == 0: the size filter keeps every size -- min <= 1, max >= n -- and the
+        // bucketed relabel reads no size, so only the minimum index is reduced)
+        stats_body(parent, val, n, size, minidx, meta, 1, blockIdx.x, gridDim.x, count_sizes != 0);
     } else {
         const int half = (int)(gridDim.x >> 1);  // >= 1: the host launches >= 2 blocks
         if ((int)blockIdx.x < half)
             node_stats_body(parent, ncomp, size, minidx, (int)n, meta, n, blockIdx.x, half, rmask);
         else
             sparse_stats_body(parent, cstart, slist, spts, size, minidx, meta, n, blockIdx.x - half, gridDim.x - half);
+    }
+}
+
+// a10 for large sparse-dominated clouds, in two passes.  k_relabel's label stores go to random
+// input positions (shuffled input): each 4-byte store dirties a whole 32-byte sector and the
+// sectors leave L2 long before their neighbours arrive (C5: 3.4 GB written for 0.44 GB of
+// labels), and the store stream evicts the roots' labels the loads need.  Pass 1 computes the
+// labels in sorted order (coalesced reads, roots nearby) and writes (input index, label) pairs
+// bucket-major into a temporary: bucket b = input index >> RL_SHIFT owns the temporary's range
+// [b << RL_SHIFT, ...) -- the sorted positions are a permutation of the input indices, so a
+// bucket holds exactly as many pairs as its index range -- and a block reserves one run per
+// bucket and tile (one global atomic each).  Pass 2 streams the temporary in order: the blocks
+// in flight write into one or two buckets' 1 MB label ranges, which stay in L2 until their
+// sectors are complete.
+__device__ __forceinline__ void relabel_bucket_body(const int* __restrict__ parent, const int* __restrict__ val,
+                                                    const int* __restrict__ size, const int* __restrict__ minidx,
+                                                    int64_t n, long long min_size, long long max_size,
+                                                    uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
+                                                    const int64_t* __restrict__ boff, int nclouds, int sh) {
+    // block k owns the tiles k, k + G, ... (G = the grid, one resident wave: the tiles in
+    // flight are a narrow window of the sorted order, so the roots' labels stay in L2).  Pass A
+    // counts the block's pairs per bucket and reserves one run per bucket (G atomics per
+    // cursor; tile-wise reservations serialised ~50k on each cursor's L2 slice), pass B
+    // re-reads the tiles and writes the pairs.
+    __shared__ unsigned int base[RL_MAX_BUCKETS], cnt[RL_MAX_BUCKETS];
+    const int nb = (int)((n + (int64_t(1) << sh) - 1) >> sh);
+    const int64_t stride = (int64_t)gridDim.x * RL_TILE;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0u;
+    __syncthreads();
+    constexpr int PER = RL_TILE / 256;
+    for (int64_t t0 = (int64_t)blockIdx.x * RL_TILE; t0 < n; t0 += stride) {
+        int v[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {  // all loads in flight before the counts
+            const int64_t s = t0 + j * 256 + threadIdx.x;
+            v[j] = s < n ? __ldg(val + s) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (v[j] >= 0) atomicAdd(&cnt[v[j] >> sh], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const unsigned int c = cnt[b];
+        base[b] = c ? ((unsigned)b << sh) + atomicAdd(cursor + b * RL_CUR_STRIDE, c) : 0u;
+    }
+    // the size filter applied here (k_rootlab runs this pass instead of its own for these clouds); a filter that keeps every
+    // size (min <= 1, max >= n) reads no size
+    const bool filt = min_size > 1 || max_size < n;
+    for (int64_t t0 = (int64_t)blockIdx.x * RL_TILE; t0 < n; t0 += stride) {
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0u;
+        __syncthreads();
+        int v[PER], lab[PER];
+        unsigned int rank[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int64_t s = t0 + j * 256 + threadIdx.x;
+            v[j] = -1;
+            if (s < n) {
+                v[j] = __ldg(val + s);
+                const int r = __ldg(parent + s);  // the root (flattened by k_flatten_if)
+                int l = __ldg(minidx + r);
+                if (filt) {
+                    const long long sz = __ldg(size + r);
+                    if (sz < min_size || sz > max_size) l = -1;
+                }
+                if (boff && l >= 0) {  // batch mode: index inside the point's own cloud
+                    int lo = 0, hi = nclouds;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (__ldg(boff + mid) <= (int64_t)v[j]) lo = mid;
+                        else hi = mid;
+                    }
+                    l -= (int)__ldg(boff + lo);
+                }
+                lab[j] = l;
+                rank[j] = atomicAdd(&cnt[v[j] >> sh], 1u);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (v[j] >= 0) tmp[base[v[j] >> sh] + rank[j]] = make_uint2((unsigned)v[j], (unsigned)lab[j]);
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) base[b] += cnt[b];
     }
 }
 
@@ -558,10 +648,17 @@ __global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent,
                                                 long long max_size, const Meta* __restrict__ meta, uint32_t rmask,
                                                 const uint32_t* __restrict__ cstart, const int* __restrict__ slist,
                                                 const int* __restrict__ ncomp, const int* __restrict__ dlist,
-                                                int* __restrict__ crec) {
+                                                int* __restrict__ crec, const int* __restrict__ val,
+                                                uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
+                                                const Grid* __restrict__ gp) {
     pdl_prologue();
     if (meta->status) return;
     const bool sparse_dom = 4 * (int64_t)meta->cells > n;
+    if (sparse_dom && tmp) {  // large sparse-dominated clouds: the bucket pass (filter included)
+        relabel_bucket_body(parent, val, size, minidx, n, min_size, max_size, tmp, cursor,
+                            gp->batch ? gp->boff : nullptr, gp->nclouds, RL_SHIFT);
+        return;
+    }
     const int64_t nslot = 8 * (int64_t)meta->ndense;
     const int64_t npts = sparse_dom ? n : (int64_t)meta->nsparse * SPARSE_MAX;  // points, or sparse-cell slots
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < npts + nslot;
@@ -645,27 +742,55 @@ __global__ void __launch_bounds__(256) k_relabel(const int* __restrict__ parent,
     }
 }
 
-// a10 for large sparse-dominated clouds, second pass (the first one is the bucket pass inside
-// k_relabel_in, fec_dense.cu): the temporary streamed in order; the blocks in flight write into
-// one or two buckets' 1 MB label ranges, which stay in L2 until their sectors are complete.
-__global__ void __launch_bounds__(256) k_relabel_b2(const uint2* __restrict__ tmp, int64_t n,
-                                                   int* __restrict__ labels, const Meta* __restrict__ meta) {
+// Staged form: a cluster of RL_CLUSTER CTAs per bucket holds the bucket's 1 MB label range in
+// its distributed shared memory (CTA r: labels [r * 2^15, (r + 1) * 2^15) of the bucket); every
+// CTA streams an eighth of the bucket's pairs and stores each label into the owning CTA's
+// shared memory, then each CTA writes its 128 KB slice out coalesced -- no partial sector ever
+// reaches L2.  (Every index of a bucket occurs exactly once: the sorted positions are a
+// permutation of the input indices.)
+__global__ void __cluster_dims__(RL_CLUSTER, 1, 1) __launch_bounds__(1024)
+    k_relabel_b2c(const uint2* __restrict__ tmp, int64_t n, int* __restrict__ labels, const Meta* __restrict__ meta) {
     pdl_prologue();
-    if (meta->status || 4 * (int64_t)meta->cells <= n) return;
-    const int64_t pairs = n / 2;  // two entries per 16-byte load (tmp is 256-B aligned)
-    const uint4* t4 = reinterpret_cast<const uint4*>(tmp);
-    // the label stores carry an L2 evict-last hint, the temporary's loads evict-first, so the
-    // partially written label sectors are the last lines L2 gives up
-    unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint4 e = __ldcs(t4 + i);
-        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(labels + e.x), "r"(e.y), "l"(pol) : "memory");
-        asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(labels + e.z), "r"(e.w), "l"(pol) : "memory");
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
-        const uint2 e = tmp[n - 1];
-        labels[e.x] = (int)e.y;
+    if (meta->status || 4 * (int64_t)meta->cells <= n) return;  // (uniform over the cluster)
+    extern __shared__ int stage[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    constexpr int B = 1 << RL_SHIFT, S = 1 << RL_CTA_SHIFT;
+    const int64_t nb = (n + B - 1) / B;
+    const int64_t ncl = gridDim.x / RL_CLUSTER;
+    for (int64_t b = blockIdx.x / RL_CLUSTER; b < nb; b += ncl) {
+        const int64_t e0 = b * B;
+        const int cnt = (int)min((int64_t)B, n - e0);
+        const int per = (cnt + RL_CLUSTER - 1) / RL_CLUSTER;
+        const int i0 = min(cnt, rank * per), i1 = min(cnt, i0 + per);
+        // 8 pairs in flight per thread (the remote stores are fire-and-forget)
+        constexpr int U = 8;
+        for (int i = i0 + threadIdx.x; i < i1; i += U * blockDim.x) {
+            uint2 e[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = i + u * blockDim.x;
+                e[u] = k < i1 ? __ldcs(tmp + e0 + k) : make_uint2(0xffffffffu, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (e[u].x == 0xffffffffu) continue;
+                const int loc = (int)(e[u].x - (unsigned)e0);
+                int* dst = cluster.map_shared_rank(stage, loc >> RL_CTA_SHIFT);
+                dst[loc & (S - 1)] = (int)e[u].y;
+            }
+        }
+        cluster.sync();
+        const int o0 = rank * S, oc = max(0, min(S, cnt - o0));
+        if ((reinterpret_cast<uintptr_t>(labels) & 15u) == 0) {
+            int4* out4 = reinterpret_cast<int4*>(labels + e0 + o0);  // (e0 + o0: a multiple of 4)
+            for (int i = threadIdx.x; i < oc / 4; i += blockDim.x)
+                out4[i] = make_int4(stage[4 * i], stage[4 * i + 1], stage[4 * i + 2], stage[4 * i + 3]);
+            for (int i = (oc / 4) * 4 + threadIdx.x; i < oc; i += blockDim.x) labels[e0 + o0 + i] = stage[i];
+        } else {
+            for (int i = threadIdx.x; i < oc; i += blockDim.x) labels[e0 + o0 + i] = stage[i];
+        }
+        cluster.sync();  // (the next bucket's stores into this CTA wait for its slice to be out)
     }
 }
 

@@ -66,15 +66,20 @@ __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx, const 
 __global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
 __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
                           long long max_size, const Meta* meta, uint32_t rmask, const uint32_t* cstart,
-                          const int* slist, const int* ncomp, const int* dlist, int* crec);
+                          const int* slist, const int* ncomp, const int* dlist, int* crec, const int* val, uint2* tmp, unsigned int* cursor, const Grid* gp);
 __global__ void k_relabel(const int* parent, const int* val, const int* minidx, int64_t n, int* labels,
                           const Meta* meta, const int64_t* boff, int nclouds);
 // bucketed relabel (large sparse-dominated clouds): RL_SHIFT bits of input index per bucket
+// bucket = input index >> RL_SHIFT: 2^18 labels = 1 MB, staged by k_relabel_b2c in the
+// distributed shared memory of a cluster of RL_CLUSTER CTAs (128 KB each)
 constexpr int RL_SHIFT = 18;
+constexpr int RL_CLUSTER = 8;
+constexpr int RL_CTA_SHIFT = 15;  // labels per CTA of the cluster: 2^15 (128 KB)
 constexpr int RL_TILE = 2048;
 constexpr int RL_MAX_BUCKETS = 4096;  // n <= 2^30 (fec_max_points < 2^30)
 constexpr int RL_CUR_STRIDE = 32;     // one bucket cursor per 128-byte line (L2 slices in parallel)
-__global__ void k_relabel_b2(const uint2* tmp, int64_t n, int* labels, const Meta* meta);
+static_assert(RL_CTA_SHIFT + 3 == RL_SHIFT, "a cluster of 8 CTAs holds one bucket");
+__global__ void k_relabel_b2c(const uint2* tmp, int64_t n, int* labels, const Meta* meta);
 __global__ void k_bbox_clouds(const float* p, const int64_t* off, float* bb, int* nonfinite, float near,
                               unsigned long long* near_pairs);
 __global__ void k_cmark(const float* p, int64_t n, const Grid* gp, uint2* cw);
@@ -142,11 +147,10 @@ __global__ void k_dparent(const float4* spts, const uint32_t* cstart, const int*
                           int* size, int* minidx, int node_stats, int64_t n);
 __global__ void k_tail_stats(int* parent, const int* val, int64_t n, int* size, int* minidx, Meta* meta,
                              const int* ncomp, const uint32_t* cstart, const int* slist, uint32_t rmask,
-                             const float4* spts);
+                             const float4* spts, int count_sizes);
 __global__ void k_relabel_in(const float* p, int64_t n, const Grid* gp, const uint2* cw, const int* crec,
                              const u64* cmask, const uint32_t* cstart, const float4* spts, const int* parent,
-                             const int* minidx, int* labels, const Meta* meta, const uint32_t* pcode,
-                             const int* val, uint2* tmp, unsigned int* cursor);
+                             const int* minidx, int* labels, const Meta* meta, const uint32_t* pcode);
 // local_only != 0 (small clouds, host-chosen): the sparse cells always go through the compact
 // list and k_union_sparse_local (more parallel per cell), whatever their share of the cells.
 __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,

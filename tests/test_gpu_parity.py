@@ -154,6 +154,34 @@ def test_async_host_api_pipelined_over_two_streams(fec):
         assert_same(outs[k].numpy(), oracle.fec(c, ds[k], 2, 10**6), f"async cloud {k}")
 
 
+@pytest.mark.parametrize("name,scale", [("C4", 0.02), ("C3", 0.05), ("C5", 0.01)])
+def test_shuffled_input_key_path(fec, name, scale):
+    """Shuffled input above 2^17 points takes the key-sort path (the a1 coherence test):
+    node-tail clouds (shuffled C4 / C3: labels written in input order by k_relabel_in through
+    the cell codes of the key path) and a sparse-dominated one (C5), filtered and not --
+    bit-exact against the oracle, and the instrumented stats confirm the path."""
+    w = synth.make_config(name, scale=scale)
+    pts = w.points[np.random.default_rng(11).permutation(w.n)]
+    fec.set_instrumentation(True)
+    try:
+        got = run_gpu(fec, pts, w.d_th, w.min_size, w.max_size)
+        assert fec.stats()["binning"] == 1
+    finally:
+        fec.set_instrumentation(False)
+    assert_same(got, oracle.fec(pts, w.d_th, w.min_size, w.max_size), f"shuffled {name}@{scale}")
+    assert_same(run_gpu(fec, pts, w.d_th), oracle.fec(pts, w.d_th), f"shuffled {name}@{scale} unfiltered")
+
+
+@pytest.mark.parametrize("mn,mx", [(1, 10**9), (3, 40)])
+def test_large_sparse_dominated_bucketed_relabel(fec, mn, mx):
+    """Sparse-dominated clouds of >= 2^22 points take the bucketed relabel (the size filter
+    applied in the bucket pass; a filter keeping every size reduces no counts): C5 at 4% (4.4M
+    points, shuffled: the key-sort path), with a no-op and a real size filter."""
+    w = synth.make_config("C5", scale=0.04)
+    assert w.n >= 1 << 22
+    assert_same(run_gpu(fec, w.points, w.d_th, mn, mx), oracle.fec(w.points, w.d_th, mn, mx), f"C5@0.04 [{mn},{mx}]")
+
+
 def test_deterministic_repeats(fec):
     w = synth.make_config("C5", scale=0.01)
     first = run_gpu(fec, w.points, w.d_th)
