@@ -148,7 +148,7 @@ STAGE_KERNELS = {
                        "overflow fallback), k_flatten_nodes, k_dense_filter, k_dense_overflow, k_dense_items",
     "a8_flatten": "k_flatten_if",
     "a9_stats": "k_tail_stats",
-    "a10_relabel": "k_rootlab (large sparse-dominated clouds: the bucket pass), k_relabel_in (node-tail clouds) + "
+    "a10_relabel": "k_rootlab, k_relabel_in (node-tail clouds) / k_relabel_b1 (the bucket pass of large sparse-dominated clouds) + "
                    "k_relabel_b2c (a cluster per bucket) / k_relabel",
 }
 

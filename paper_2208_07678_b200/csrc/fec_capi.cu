@@ -773,7 +773,12 @@ fec_status_t run(const float* pts, int64_t n, float d, int64_t min_size, int64_t
     mark(9, st);
     pdl(k_rootlab, wave, 256, 0, st)(L.parent, L.size, L.minidx, n, (long long)min_size, (long long)max_size, L.meta,
                                      (uint32_t)(rec_pow2(n) - 1), L.cstart, L.slist, L.ncomp, L.dlist, L.crec,
-                                     C.val, tmp, L.rlcur, L.grid);
+                                     bucketed ? 1 : 0);
+    if (bucketed) {
+        pdl(k_relabel_b1, wave, 256, 0, st)(L.parent, C.val, L.size, L.minidx, n, (long long)min_size,
+                                            (long long)max_size, tmp, L.rlcur, L.meta, L.grid);
+        ++C.launches;
+    }
     // labels: input order for node-tail clouds, sorted order for sparse-dominated ones (large
     // ones: the bucket pass in k_rootlab, then k_relabel_b2c); the kernels of the variant
     // not chosen return at once

@@ -144,11 +144,8 @@ __device__ __forceinline__ bool dense_neighbor(const Grid& g, const int c[3], in
 // aligned (more bytes in flight per thread than one scalar load per coordinate).
 struct Pts4 {
     float x[4], y[4], z[4];
-    int i[4];  // input indices
 };
 __device__ __forceinline__ void load_pts4(const float* __restrict__ p, int64_t n, int64_t base, bool vec, Pts4& P) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) P.i[j] = (int)(base + j);
     if (vec && base + 4 <= n) {
         const float4* q = reinterpret_cast<const float4*>(p + 3 * base);
         const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -481,7 +478,7 @@ __device__ __forceinline__ void point_runs(const Pts4& P, int64_t b4, int64_t n,
         R.q[j] = 0;
         if (b4 + j < n) {
             uint32_t lin;
-            dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, R.q[j]);
+            dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, R.q[j]);
             R.cid[j] = cid_of(cw, lin);
         }
         const bool fresh = j == 0 || R.cid[j] != R.cid[j > 0 ? j - 1 : 0];
@@ -571,8 +568,8 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         const int64_t b4 = t0 + 4 * lane;
         Pts4 P;
         load_pts4(p, n, b4, vec, P);
-        // runs of this thread's points in one cell take one table update (and the run's
-        // smallest input index)
+        // runs of this thread's points in one cell take one table update
+        // (a run's first point has its smallest input index)
         uint32_t code[4] = {0u, 0u, 0u, 0u};
         uint32_t rc = 0xffffffffu, rn = 0u;
         int rfirst = 0;
@@ -582,7 +579,7 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
             if (b4 + j < n) {
                 uint32_t lin;
                 int q;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, q);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q);
                 const uint32_t cid = cid_of(cw, lin);
                 code[j] = (cid << 6) | (uint32_t)q;
                 if (cid != rc) {
@@ -596,9 +593,8 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
                     rc = cid;
                     rn = 0u;
                     rb = 0ull;
-                    rfirst = P.i[j];
+                    rfirst = (int)(b4 + j);
                 }
-                rfirst = min(rfirst, P.i[j]);
                 ++rn;
                 rb |= 1ull << q;
             }
@@ -725,7 +721,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (R.cid[j] != 0xffffffffu)
-                    spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float(P.i[j]));
+                    spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
         }
         return;
     }
@@ -786,7 +782,7 @@ __global__ void __launch_bounds__(256) k_dscatter(const float* __restrict__ p, i
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (R.cid[j] != 0xffffffffu)
-                spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float(P.i[j]));
+                spts[pos[j]] = make_float4(P.x[j], P.y[j], P.z[j], __int_as_float((int)(b4 + j)));
     }
 }
 
@@ -2224,7 +2220,7 @@ __global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p,
                 cid[j] = 0;
                 if (b4 + j >= n) continue;
                 uint32_t lin;
-                dense_cell_of(P.x[j], P.y[j], P.z[j], P.i[j], g, lin, q[j]);
+                dense_cell_of(P.x[j], P.y[j], P.z[j], b4 + j, g, lin, q[j]);
                 cid[j] = cid_of(cw, lin);
             }
         }

@@ -557,11 +557,18 @@ __global__ void __launch_bounds__(256) k_tail_stats(int* __restrict__ parent, co
 // bucket and tile (one global atomic each).  Pass 2 streams the temporary in order: the blocks
 // in flight write into one or two buckets' 1 MB label ranges, which stay in L2 until their
 // sectors are complete.
-__device__ __forceinline__ void relabel_bucket_body(const int* __restrict__ parent, const int* __restrict__ val,
-                                                    const int* __restrict__ size, const int* __restrict__ minidx,
-                                                    int64_t n, long long min_size, long long max_size,
-                                                    uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
-                                                    const int64_t* __restrict__ boff, int nclouds, int sh) {
+// (A separate launch, enqueued only for clouds of >= 2^22 points: folded into k_rootlab its
+// shared tables and registers slowed that kernel on node-tail clouds, C4 25 -> 42 us.)
+__global__ void __launch_bounds__(256) k_relabel_b1(const int* __restrict__ parent, const int* __restrict__ val,
+                                                   const int* __restrict__ size, const int* __restrict__ minidx,
+                                                   int64_t n, long long min_size, long long max_size,
+                                                   uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
+                                                   const Meta* __restrict__ meta, const Grid* __restrict__ gp) {
+    pdl_prologue();
+    if (meta->status || 4 * (int64_t)meta->cells <= n) return;
+    const int64_t* __restrict__ boff = gp->batch ? gp->boff : nullptr;
+    const int nclouds = gp->nclouds;
+    constexpr int sh = RL_SHIFT;
     // block k owns the tiles k, k + G, ... (G = the grid, one resident wave: the tiles in
     // flight are a narrow window of the sorted order, so the roots' labels stay in L2).  Pass A
     // counts the block's pairs per bucket and reserves one run per bucket (G atomics per
@@ -589,7 +596,7 @@ __device__ __forceinline__ void relabel_bucket_body(const int* __restrict__ pare
         const unsigned int c = cnt[b];
         base[b] = c ? ((unsigned)b << sh) + atomicAdd(cursor + b * RL_CUR_STRIDE, c) : 0u;
     }
-    // the size filter applied here (k_rootlab runs this pass instead of its own for these clouds); a filter that keeps every
+    // the size filter applied here (k_rootlab returns at once for these clouds); a filter that keeps every
     // size (min <= 1, max >= n) reads no size
     const bool filt = min_size > 1 || max_size < n;
     for (int64_t t0 = (int64_t)blockIdx.x * RL_TILE; t0 < n; t0 += stride) {
@@ -648,17 +655,11 @@ __global__ void __launch_bounds__(256) k_rootlab(const int* __restrict__ parent,
                                                 long long max_size, const Meta* __restrict__ meta, uint32_t rmask,
                                                 const uint32_t* __restrict__ cstart, const int* __restrict__ slist,
                                                 const int* __restrict__ ncomp, const int* __restrict__ dlist,
-                                                int* __restrict__ crec, const int* __restrict__ val,
-                                                uint2* __restrict__ tmp, unsigned int* __restrict__ cursor,
-                                                const Grid* __restrict__ gp) {
+                                                int* __restrict__ crec, int bucketed) {
     pdl_prologue();
     if (meta->status) return;
     const bool sparse_dom = 4 * (int64_t)meta->cells > n;
-    if (sparse_dom && tmp) {  // large sparse-dominated clouds: the bucket pass (filter included)
-        relabel_bucket_body(parent, val, size, minidx, n, min_size, max_size, tmp, cursor,
-                            gp->batch ? gp->boff : nullptr, gp->nclouds, RL_SHIFT);
-        return;
-    }
+    if (sparse_dom && bucketed) return;  // (large sparse-dominated clouds: k_relabel_b1)
     const int64_t nslot = 8 * (int64_t)meta->ndense;
     const int64_t npts = sparse_dom ? n : (int64_t)meta->nsparse * SPARSE_MAX;  // points, or sparse-cell slots
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < npts + nslot;

@@ -66,7 +66,10 @@ __global__ void k_flatten(int* parent, int64_t n, int* size, int* minidx, const 
 __global__ void k_flatten_if(int* parent, int64_t n, const Meta* meta);
 __global__ void k_rootlab(const int* parent, const int* size, int* minidx, int64_t n, long long min_size,
                           long long max_size, const Meta* meta, uint32_t rmask, const uint32_t* cstart,
-                          const int* slist, const int* ncomp, const int* dlist, int* crec, const int* val, uint2* tmp, unsigned int* cursor, const Grid* gp);
+                          const int* slist, const int* ncomp, const int* dlist, int* crec, int bucketed);
+__global__ void k_relabel_b1(const int* parent, const int* val, const int* size, const int* minidx, int64_t n,
+                             long long min_size, long long max_size, uint2* tmp, unsigned int* cursor,
+                             const Meta* meta, const Grid* gp);
 __global__ void k_relabel(const int* parent, const int* val, const int* minidx, int64_t n, int* labels,
                           const Meta* meta, const int64_t* boff, int nclouds);
 // bucketed relabel (large sparse-dominated clouds): RL_SHIFT bits of input index per bucket

@@ -57,35 +57,26 @@ __global__ void __launch_bounds__(256) k_slab_stats(const int* __restrict__ pare
         const bool owned = ok && i < n_owned;
         const bool bnd = ok && (i < n_first || i >= n_owned);
         roots += (ok && r == (int)s) ? 1ull : 0ull;
-        unsigned todo = __ballot_sync(0xffffffffu, ok);
-        while (todo) {
-            const int leader = __ffs(todo) - 1;
-            const int key = __shfl_sync(0xffffffffu, r, leader);
-            const bool mem = ok && r == key;
-            const unsigned peers = __ballot_sync(0xffffffffu, mem);
-            const int cnt = __popc(__ballot_sync(0xffffffffu, mem && owned));
-            const int mn = __reduce_min_sync(0xffffffffu, (mem && owned) ? gv : 0x7fffffff);
-            const int bk = __reduce_max_sync(0xffffffffu, (mem && bnd) ? gv : -1);
-            if (lane == leader) {
-                unsigned h = ((unsigned)key * 2654435761u) >> 24;
-                bool done = false;
-                for (int probe = 0; probe < 4 && !done; ++probe, h = (h + 1) & (SL_SLOTS - 1)) {
-                    int cur = hkey[h];
-                    if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
-                    if (cur == -1 || cur == key) {
-                        if (cnt) atomicAdd(&hcnt[h], cnt);
-                        if (mn != 0x7fffffff) atomicMin(&hmin[h], mn);
-                        if (bk >= 0) atomicMax(&hbk[h], bk);
-                        done = true;
-                    }
-                }
-                if (!done) {
-                    if (cnt) atomicAdd(size + key, cnt);
-                    if (mn != 0x7fffffff) atomicMin(minidx + key, mn);
-                    if (bk >= 0) atomicMax(ckey + key, bk);
-                }
+        // the lanes of one root meet in one __match_any_sync; the group's leader adds once (into
+        // the block's table if the root owns its slot -- a big component -- else to the root)
+        const int key = ok ? r : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int cnt = __popc(peers & __ballot_sync(0xffffffffu, owned));
+        const int mn = __reduce_min_sync(peers, owned ? gv : 0x7fffffff);
+        const int bk = __reduce_max_sync(peers, bnd ? gv : -1);
+        if (key >= 0 && lane == __ffs(peers) - 1) {
+            const unsigned h = ((unsigned)key * 2654435761u) >> 24;
+            int cur = hkey[h];
+            if (cur == -1) cur = atomicCAS(&hkey[h], -1, key);
+            if (cur == -1 || cur == key) {
+                if (cnt) atomicAdd(&hcnt[h], cnt);
+                if (mn != 0x7fffffff) atomicMin(&hmin[h], mn);
+                if (bk >= 0) atomicMax(&hbk[h], bk);
+            } else {
+                if (cnt) atomicAdd(size + key, cnt);
+                if (mn != 0x7fffffff) atomicMin(minidx + key, mn);
+                if (bk >= 0) atomicMax(ckey + key, bk);
             }
-            todo &= ~peers;
         }
     }
     __syncthreads();

@@ -18,7 +18,7 @@ STAGES = {
                         "k_dense_overflow", "k_flatten_nodes", "k_dense_filter", "k_dense_items"],
     "a8_flatten": ["k_flatten_if"],
     "a9_stats": ["k_tail_stats"],
-    "a10_relabel": ["k_rootlab", "k_relabel_in", "k_relabel", "k_relabel_b2c"],
+    "a10_relabel": ["k_rootlab", "k_relabel_in", "k_relabel", "k_relabel_b1", "k_relabel_b2c"],
 }
 
 
