@@ -144,8 +144,8 @@ STAGE_KERNELS = {
                "k_dcomps",
     "a4_gather_init": "k_dscatter phase 0 (+ phase 1, enqueued after the dense links; node-tail clouds scatter "
                       "only the cells later kernels read), k_dinit, k_dparent",
-    "a6a7_scan_union": "k_union_sparse(_local), k_slist, k_dense_link x2 (the main-stream one also runs the "
-                       "overflow fallback), k_flatten_nodes, k_dense_filter, k_dense_overflow, k_dense_items",
+    "a6a7_scan_union": "k_union_sparse(_local), k_dense_link x2 (the main-stream one also runs the "
+                       "overflow fallback), k_dense_filter (with the node flattening), k_dense_overflow, k_dense_items",
     "a8_flatten": "k_flatten_if",
     "a9_stats": "k_tail_stats",
     "a10_relabel": "k_rootlab, k_relabel_in (node-tail clouds) / k_relabel_b1 (the bucket pass of large sparse-dominated clouds) + "

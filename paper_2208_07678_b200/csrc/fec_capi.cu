@@ -41,7 +41,7 @@ thread_local cudaEvent_t g_batch_copied = nullptr;  // batch mode: the pinned bu
 // captured into a graph when the caller's stream is being captured).
 struct SideStream {
     cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr;
 };
 // FEC_FULL_SCATTER=1 scatters every point in phase 0 (A/B measurements, debugging)
 bool full_scatter() {
@@ -68,7 +68,8 @@ fec_status_t side_stream(SideStream** out) {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi) != cudaSuccess ||
             cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork2, cudaEventDisableTiming) != cudaSuccess) {
             g_err = "side stream creation failed";
             return FEC_ERR_CUDA;
         }
@@ -534,6 +535,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     const int* gkeysort = &L.grid->key_sort;
     // (small clouds: a small grid -- the device-sized words are few and launch latency dominates)
     const bool small = n <= kSmallN;
+    const int local_only = small ? 1 : 0;  // sparse cells: always the compact list + k_union_sparse_local
     pdl(k_zero, small ? 64 : di.sms * 4, 256, 0, st)(gp, L.cw, L.hkey, L.slots, L.arena, L.arena_words);
     ++launches;
 
@@ -599,7 +601,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         const unsigned cl_blocks = (unsigned)std::min<int64_t>(scan_lb_tiles(n + 1), small ? 32 : cap);
         pdl(k_cellred, cl_blocks, 256, 0, st)(L.cstart, L.meta, gp, L.sa_state);
         pdl(k_celltscan, 1, 1024, 0, st)(L.sa_state, L.meta, gp, L.cstart);
-        pdl(k_cellscan, cl_blocks, 256, 0, st)(L.cstart, L.slot, L.dlist, L.crec, L.cneed0, L.meta, gp, L.sa_state);
+        pdl(k_cellscan, cl_blocks, 256, 0, st)(L.cstart, L.slot, L.dlist, L.crec, L.cneed0, L.meta, gp, L.sa_state,
+                                               L.slist, n, local_only, C.node_stats ? 0 : 1, L.parent, L.size,
+                                               L.minidx);
         launches += 3;
     }
     // dense records: their components and nodes
@@ -616,7 +620,6 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
         FEC_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
         pdl(k_dense_link, grid_for(dense_max(n) * 4, 256, di.sms * 8), 256, 0, side->s)(
             gp, L.crec, L.ncomp, L.oflag, dctx, L.litems, L.lhalf, 1, L.cw, L.dcoord);
-        FEC_CUDA(cudaEventRecord(side->join, side->s));
         ++launches;
     }
     // ---- a4: sorted-order init (counting path: scatter + init; key path: dense re-parenting)
@@ -639,15 +642,22 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // ---- a6+a7: sparse-sparse point pairs; dense cells: certain component unions, then the
     // queued uncertain pairs
     mark(5, st);
-    const int local_only = n <= kSmallN ? 1 : 0;
+    // the sparse-cell unions and the dense records' sparse-neighbour links are independent
+    // (unions commute): with a side stream the former run there, concurrently with the latter
+    // (both are latency-bound chains of dependent loads)
+    cudaStream_t us = st;
+    if (side) {
+        FEC_CUDA(cudaEventRecord(side->fork2, st));
+        FEC_CUDA(cudaStreamWaitEvent(side->s, side->fork2, 0));
+        us = side->s;
+    }
     if (!local_only)
-        pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart, gp,
+        pdl(k_union_sparse, di.sms * di.sparse_blocks_per_sm, 256, 0, us)(L.spts, L.cw, L.ccoord, L.cstart, gp,
                                                                          L.parent, L.meta, n, local_only);
-    pdl(k_slist, grid_for(n, 256, cap * 4), 256, 0, st)(L.cstart, L.slist, L.meta, n, local_only, gp,
-                                                       C.node_stats ? 0 : 1, L.parent, L.size, L.minidx);
-    pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, st)(L.spts, L.cw, L.ccoord, L.cstart,
+    pdl(k_union_sparse_local, di.sms * di.sparse_blocks_per_sm, 256, 0, us)(L.spts, L.cw, L.ccoord, L.cstart,
                                                                            L.slist, gp, L.parent, L.meta, n,
                                                                            local_only);
+    if (side) FEC_CUDA(cudaEventRecord(side->join, side->s));
     mark(6, st);
     // thread per listed item (k_dcomps): the sparse neighbours and own pairs here, the forward
     // dense pairs on the side stream (forked after k_dcomps); the fallback runs only if a list
@@ -659,9 +669,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // queued pairs still apart after the certain unions (they mark the records whose points
     // they need), then partial scatter phase 1, the item-queue overflow fallback (in-place
     // point tests) and the queued point tests
-    pdl(k_flatten_nodes, grid_for(8 * dense_max(n), 256, cap * 4), 256, 0, st)(L.parent, (int)n, L.meta,
-                                                                            (uint32_t)(rec_pow2(n) - 1));
-    pdl(k_dense_filter, grid_for(L.item_cap, 256, cap * 4), 256, 0, st)(dctx, L.items2, L.slices2, L.idone);
+    pdl(k_dense_filter, grid_for(std::max<int64_t>(L.item_cap, 8 * dense_max(n)), 256, cap * 4), 256, 0, st)(dctx, L.items2, L.slices2, L.idone);
     if (count_path && C.node_stats) {
         mark_sub(0, st);
         pdl(k_dscatter, wt, 256, 0, st)(pts, n, gp, L.cw, L.slot, L.spts, L.pcode, L.meta, L.cneed0, L.cneed1, 1,
@@ -672,7 +680,7 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     // almost always a no-op (nothing overflowed): a small grid keeps its launch cheap
     pdl(k_dense_overflow, di.sms, 256, 0, st)(gp, L.cw, L.crec, L.ncomp, L.dcoord, L.oflag, dctx);
     pdl(k_dense_items, di.sms * 8, 256, 0, st)(gp, dctx, L.items2, L.slices2, L.idone);
-    launches += local_only ? 7 : 8;
+    launches += local_only ? 5 : 6;
     if (g_instrument) {
         pdl(k_dense_count, grid_for(dense_max(n), 256, cap), 256, 0, st)(L.ncomp, L.dlist, L.cstart, dctx);
         ++launches;

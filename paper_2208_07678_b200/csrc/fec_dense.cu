@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(256) k_dinit(const float4* __restrict__ spts, 
     FEC_PROLOGUE_GRID(gp);
     if (g.status || g.key_sort) return;
     // node-tail clouds of the single-GPU path read no sorted-order array of the dense points
-    // (node statistics, k_relabel_in): k_slist initialises the points of sparse cells instead
+    // (node statistics, k_relabel_in): k_cellscan initialises the points of sparse cells instead
     if (!all_parents && 4 * (int64_t)meta->cells <= n) return;
     const int64_t groups = (n + 3) / 4;
     for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
@@ -937,9 +937,12 @@ __global__ void __launch_bounds__(1024) k_celltscan(unsigned long long* __restri
 }
 __global__ void __launch_bounds__(CL_THREADS) k_cellscan(uint32_t* __restrict__ cstart, uint32_t* __restrict__ cursor,
                                                        int* __restrict__ dlist, int* __restrict__ crec,
-                                                       uint32_t* __restrict__ cneed0, const Meta* __restrict__ meta,
+                                                       uint32_t* __restrict__ cneed0, Meta* __restrict__ meta,
                                                        const Grid* __restrict__ gp,
-                                                       const unsigned long long* __restrict__ tpre) {
+                                                       const unsigned long long* __restrict__ tpre,
+                                                       int* __restrict__ slist, int64_t n, int local_only,
+                                                       int all_parents, int* __restrict__ parent,
+                                                       int* __restrict__ size, int* __restrict__ minidx) {
     pdl_prologue();
     if (gp->status) return;
     __shared__ unsigned long long sv[CL_TILE + CL_TILE / 8];  // padded (pad8)
@@ -948,6 +951,12 @@ __global__ void __launch_bounds__(CL_THREADS) k_cellscan(uint32_t* __restrict__ 
     const int64_t U = meta->cells;
     const bool ks = gp->key_sort;
     const int64_t tiles = (U + 1 + CL_TILE - 1) / CL_TILE;
+    // the compact list of the sparse cells (LOCAL clouds and small clouds: k_union_sparse_local
+    // and the node tail walk it) and, on the counting path of node-tail clouds, the union-find
+    // init of their points (k_dinit does not run there)
+    const bool node_tail = 4 * U <= n;
+    const bool list = local_only || node_tail;
+    const bool init = list && !ks && !all_parents && node_tail;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t base = tile * CL_TILE;
     __syncthreads();  // (the previous tile's writes read sv)
@@ -1008,6 +1017,24 @@ __global__ void __launch_bounds__(CL_THREADS) k_cellscan(uint32_t* __restrict__ 
         }
         const unsigned sp = __ballot_sync(0xffffffffu, i < U && !dense);
         if (lane == 0 && i < ((U + 31) & ~int64_t(31))) cneed0[i >> 5] = sp;  // (k_dcomps adds multi-component cells)
+        if (list && sp) {
+            int lbase = 0;
+            if (lane == 0) lbase = atomicAdd(&meta->nsparse, __popc(sp));
+            lbase = __shfl_sync(0xffffffffu, lbase, 0);
+            const bool mine = (sp >> lane) & 1u;
+            if (mine) slist[lbase + __popc(sp & ((1u << lane) - 1u))] = (int)i;
+            if (init && mine) {  // the cell's points: [its start, the next cell's start)
+                const bool last = k == CL_ITEMS - 1 && tid == CL_THREADS - 1;
+                const uint32_t s0 = (uint32_t)e;
+                const uint32_t s1 = last ? (uint32_t)(__ldg(tpre + tile) + wsum[CL_THREADS / kWarp - 1])
+                                         : (uint32_t)sv[pad8(k * CL_THREADS + tid + 1)];
+                for (uint32_t t = s0; t < s1; ++t) {
+                    parent[t] = (int)t;
+                    size[t] = 0;
+                    minidx[t] = 0x7fffffff;
+                }
+            }
+        }
     }
     }  // tiles
 }
@@ -1707,10 +1734,20 @@ __global__ void __launch_bounds__(256) k_dense_overflow(const Grid* __restrict__
 constexpr int kSliceWork = 4096;   // cell-size product per slice
 constexpr int kMaxSlices = 128;
 
+// Also (first) component nodes -> their roots, which shortens the finds here and in
+// k_dense_items (one launch: concurrent finds and flattening only ever move parents up).
 __global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restrict__ items2,
                                                      int4* __restrict__ slices2, int* __restrict__ idone) {
     pdl_prologue();
     if (C.meta->status) return;
+    const int64_t nn = 8 * (int64_t)C.meta->ndense;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
+        const int s = node_of(C.nbase, C.rmask, (int)(t >> 3), (int)(t & 7));
+        int curr = ld_parent(C.parent, s), next;
+        if (curr == s) continue;
+        while (uf_above(next = ld_parent(C.parent, curr), curr)) curr = next;
+        st_parent(C.parent, s, curr);
+    }
     const int ni = min(C.meta->nitems, C.item_cap);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ni; e += gridDim.x * blockDim.x) {
         const int4 it = C.items[e];  // queued before every certain union was done: re-check
@@ -1743,21 +1780,6 @@ __global__ void __launch_bounds__(256) k_dense_filter(DenseCtx C, int4* __restri
             items2[base + k] = it;
             slices2[base + k] = make_int4(k, K, e, 0);
         }
-    }
-}
-
-// Component nodes -> their roots (shortens the finds of the uncertain pass).
-__global__ void __launch_bounds__(256) k_flatten_nodes(int* __restrict__ parent, int nbase, const Meta* __restrict__ meta,
-                                                      uint32_t rmask) {
-    pdl_prologue();
-    if (meta->status) return;
-    const int64_t nn = 8 * (int64_t)meta->ndense;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += (int64_t)gridDim.x * blockDim.x) {
-        const int s = node_of(nbase, rmask, (int)(t >> 3), (int)(t & 7));
-        int curr = ld_parent(parent, s), next;
-        if (curr == s) continue;
-        while (uf_above(next = ld_parent(parent, curr), curr)) curr = next;
-        st_parent(parent, s, curr);
     }
 }
 
@@ -2029,42 +2051,6 @@ __device__ __forceinline__ void union_sparse_body(const float4* __restrict__ spt
     }
 }
 
-// LOCAL clouds (and small clouds): the sparse cells in one compact list, so every lane of the
-// union kernel owns a real sparse cell and all of them run in one wave.
-// Also (counting path without k_dinit) the union-find init of the sparse cells' points.
-__global__ void __launch_bounds__(256) k_slist(const uint32_t* __restrict__ cstart, int* __restrict__ slist,
-                                              Meta* __restrict__ meta, int64_t n, int local_only,
-                                              const Grid* __restrict__ gp, int all_parents, int* __restrict__ parent,
-                                              int* __restrict__ size, int* __restrict__ minidx) {
-    pdl_prologue();
-    if (meta->status || (!local_only && 4 * (int64_t)meta->cells > n)) return;  // sparse-dominated: k_union_sparse
-    const bool init = !gp->key_sort && !all_parents && 4 * (int64_t)meta->cells <= n;
-    const int64_t U = meta->cells;
-    const int64_t ur = (U + 31) & ~int64_t(31);
-    const int lane = threadIdx.x & 31;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
-        bool sp = false;
-        if (u < U) {
-            const uint32_t c = __ldg(cstart + u + 1) - __ldg(cstart + u);
-            sp = c > 0 && c <= (uint32_t)SPARSE_MAX;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, sp);
-        if (!m) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&meta->nsparse, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (sp) slist[base + __popc(m & ((1u << lane) - 1u))] = (int)u;
-        if (sp && init) {
-            const int s0 = (int)__ldg(cstart + u), s1 = (int)__ldg(cstart + u + 1);
-            for (int t = s0; t < s1; ++t) {
-                parent[t] = t;
-                size[t] = 0;
-                minidx[t] = 0x7fffffff;
-            }
-        }
-    }
-}
-
 __global__ void __launch_bounds__(256, 8) k_union_sparse(const float4* __restrict__ spts, const uint2* __restrict__ cw,
                                                      const u64* __restrict__ ccoord,
                                                      const uint32_t* __restrict__ cstart, const Grid* __restrict__ gp,
@@ -2075,7 +2061,7 @@ __global__ void __launch_bounds__(256, 8) k_union_sparse(const float4* __restric
 }
 // Node-level tail (see node_accumulate): every used component node finds its root, is
 // flattened onto it, and adds its own totals to the root's; then the points of sparse cells
-// (the compact list of k_slist) find their roots, are flattened and counted one by one.
+// (the compact list of k_cellscan) find their roots, are flattened and counted one by one.
 // Only for dense-grid clouds with few sparse cells; the others run k_flat_stats / k_stats.
 
 

@@ -111,8 +111,9 @@ __global__ void k_dinit(const float4* spts, int64_t n, const Grid* gp, const uin
                         int all_parents);
 __global__ void k_cellred(const uint32_t* cstart, const Meta* meta, const Grid* gp, unsigned long long* tsum);
 __global__ void k_celltscan(unsigned long long* tsum, Meta* meta, const Grid* gp, uint32_t* cstart);
-__global__ void k_cellscan(uint32_t* cstart, uint32_t* cursor, int* dlist, int* crec, uint32_t* cneed0, const Meta* meta,
-                           const Grid* gp, const unsigned long long* tpre);
+__global__ void k_cellscan(uint32_t* cstart, uint32_t* cursor, int* dlist, int* crec, uint32_t* cneed0, Meta* meta,
+                           const Grid* gp, const unsigned long long* tpre, int* slist, int64_t n, int local_only,
+                           int all_parents, int* parent, int* size, int* minidx);
 __global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta,
                          const Grid* gp, int* crec, uint32_t* cneed0);
 __global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount, const Meta* meta);
@@ -161,15 +162,12 @@ __global__ void k_union_sparse(const float4* spts, const uint2* cw, const u64* c
 __global__ void k_union_sparse_local(const float4* spts, const uint2* cw, const u64* ccoord, const uint32_t* cstart,
                                      const int* slist, const Grid* gp, int* parent, Meta* meta, int64_t n,
                                      int local_only);
-__global__ void k_slist(const uint32_t* cstart, int* slist, Meta* meta, int64_t n, int local_only, const Grid* gp,
-                        int all_parents, int* parent, int* size, int* minidx);
 __global__ void k_dense_link(const Grid* gp, const int* crec, const int* ncomp, uint32_t* oflags, DenseCtx C,
                              const uint4* litems, int lhalf, int which, const uint2* cw, const u64* dcoord);
 __global__ void k_dense_filter(DenseCtx C, int4* items2, int4* slices2, int* idone);
 __global__ void k_dense_overflow(const Grid* gp, const uint2* cw, const int* crec, const int* ncomp,
                                  const u64* dcoord, uint32_t* oflags, DenseCtx C);
 __global__ void k_dense_items(const Grid* gp, DenseCtx C, const int4* items2, const int4* slices2, int* idone);
-__global__ void k_flatten_nodes(int* parent, int nbase, const Meta* meta, uint32_t rmask);
 __global__ void k_dense_count(const int* ncomp, const int* dlist, const uint32_t* cstart, DenseCtx C);
 cudaError_t ensure_subcell_tables();  // host: upload the fine sub-cell tables (once per device)
 __global__ void k_debug_pred(const float* a, const float* b, int64_t m, float t2, uint8_t* out, float* d2out);

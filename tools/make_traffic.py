@@ -14,8 +14,8 @@ STAGES = {
                 "k_dbits_popc", "k_dbits_list", "k_dcomps"],
     "a4_gather_init": ["k_dscatter", "k_dinit", "k_dparent"],
     # SURVEY's a6+a7 row: every union kernel, the dense-dense links on the side stream included
-    "a6a7_scan_union": ["k_union_sparse", "k_slist", "k_union_sparse_local", "k_dense_link",
-                        "k_dense_overflow", "k_flatten_nodes", "k_dense_filter", "k_dense_items"],
+    "a6a7_scan_union": ["k_union_sparse", "k_union_sparse_local", "k_dense_link",
+                        "k_dense_overflow", "k_dense_filter", "k_dense_items"],
     "a8_flatten": ["k_flatten_if"],
     "a9_stats": ["k_tail_stats"],
     "a10_relabel": ["k_rootlab", "k_relabel_in", "k_relabel", "k_relabel_b1", "k_relabel_b2c"],
