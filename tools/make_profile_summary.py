@@ -11,7 +11,7 @@ def launch_table(path):
     ik, im, iv, iid = hdr.index('Kernel Name'), hdr.index('Metric Name'), hdr.index('Metric Value'), hdr.index('ID')
     d = OrderedDict()
     for r in rows[1:]:
-        d.setdefault(int(r[iid]), {'k': r[ik].split('(')[0].replace('void ', '')})[r[im]] = float(r[iv].replace(',', ''))
+        d.setdefault(int(r[iid]), {'k': r[ik].split('(')[0].replace('void ', '').replace('fec::', '')})[r[im]] = float(r[iv].replace(',', ''))
     return d
 
 
