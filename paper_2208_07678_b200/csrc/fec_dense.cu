@@ -1039,32 +1039,6 @@ __global__ void __launch_bounds__(CL_THREADS) k_cellscan(uint32_t* __restrict__ 
     }  // tiles
 }
 
-// Dense bits of the occupied cells from the cell starts; also the scatter cursors.
-__global__ void __launch_bounds__(256) k_ccount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
-                                               uint32_t* __restrict__ cursor, const Meta* __restrict__ meta,
-                                               const Grid* __restrict__ gp, int* __restrict__ crec,
-                                               uint32_t* __restrict__ cneed0) {
-    pdl_prologue();
-    if (gp->status || gp->key_sort) return;
-    const int64_t U = meta->cells;
-    const int64_t ur = (U + 31) & ~int64_t(31);
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
-        bool dense = false;
-        if (u < U) {
-            const uint32_t c0 = __ldg(cstart + u);
-            dense = __ldg(cstart + u + 1) - c0 > (uint32_t)SPARSE_MAX;
-            cursor[u] = c0;
-            if (!dense) crec[u] = -1;  // dense cells get their record word in k_dcomps
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, dense);
-        const unsigned sp = __ballot_sync(0xffffffffu, u < U && !dense);  // sparse: partial scatter phase 0
-        if ((threadIdx.x & 31) == 0) {
-            dbits[u >> 5] = m;
-            cneed0[u >> 5] = sp;  // (k_dcomps adds the multi-component cells)
-        }
-    }
-}
-
 // ---- a2/a3, sort path (shuffled inputs) ----------------------------------------------------
 // For inputs without spatial coherence (C1, C5) the counting sort's per-point atomics and
 // scatter hit random DRAM sectors; instead the linear cell ids are radix-sorted (coalesced
@@ -1198,53 +1172,6 @@ __global__ void __launch_bounds__(256) k_sgather(const float* __restrict__ p, co
     }
 }
 
-// Dense bits of the occupied cells from the run lengths (lanes = consecutive compact ids,
-// so a warp fills one bitmap word with a plain store).
-__global__ void __launch_bounds__(256) k_scount(const uint32_t* __restrict__ cstart, uint32_t* __restrict__ dbits,
-                                               const Meta* __restrict__ meta, const Grid* __restrict__ gp,
-                                               int* __restrict__ crec) {
-    pdl_prologue();
-    if (gp->status || !gp->key_sort) return;
-    const int64_t U = meta->cells;
-    const int64_t ur = (U + 31) & ~int64_t(31);
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < ur; u += (int64_t)gridDim.x * blockDim.x) {
-        const bool dense = u < U && __ldg(cstart + u + 1) - __ldg(cstart + u) > (uint32_t)SPARSE_MAX;
-        if (u < U && !dense) crec[u] = -1;  // dense cells get their record word in k_dcomps
-        const unsigned m = __ballot_sync(0xffffffffu, dense);
-        if ((threadIdx.x & 31) == 0) dbits[u >> 5] = m;
-    }
-}
-
-// ---- dense records: compact ids of the dense cells in ascending order -----------------------
-__global__ void __launch_bounds__(256) k_dbits_popc(const uint32_t* __restrict__ dbits, int64_t words,
-                                                   uint32_t* __restrict__ wcount, const Meta* __restrict__ meta) {
-    pdl_prologue();
-    if (meta->status) return;
-    words = min(words, (int64_t)meta->dwords1 - 1);  // the words that hold occupied cells
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x)
-        wcount[w] = w < words ? (uint32_t)__popc(__ldg(dbits + w)) : 0u;
-}
-
-__global__ void __launch_bounds__(256) k_dbits_list(const uint32_t* __restrict__ dbits, int64_t words,
-                                                   const uint32_t* __restrict__ wpos, int* __restrict__ dlist,
-                                                   int* __restrict__ crec, Meta* __restrict__ meta) {
-    pdl_prologue();
-    if (meta->status) return;
-    words = min(words, (int64_t)meta->dwords1 - 1);
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w <= words; w += (int64_t)gridDim.x * blockDim.x) {
-        if (w == words) { meta->ndense = (int)wpos[words]; continue; }
-        uint32_t bits = __ldg(dbits + w);
-        int r = (int)__ldg(wpos + w);
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int cell = (int)(w * 32 + b);
-            dlist[r] = cell;
-            crec[cell] = r;
-            ++r;
-        }
-    }
-}
 
 // ---- uncertain component pairs: queued, or tested in place when the queue is full ----------
 // item = (P record, P component, Q record or point, Q component or -1 for a point)
@@ -1909,7 +1836,7 @@ __global__ void __launch_bounds__(256) k_dense_items(const Grid* __restrict__ gp
 }
 
 // Instrumentation: dense-mode roots that are component nodes (points count themselves in
-// k_stats) and the number of dense points.
+// the stats kernels) and the number of dense points.
 __global__ void __launch_bounds__(256) k_dense_count(const int* __restrict__ ncomp, const int* __restrict__ dlist,
                                                     const uint32_t* __restrict__ cstart, DenseCtx C) {
     pdl_prologue();
@@ -2062,7 +1989,7 @@ __global__ void __launch_bounds__(256, 8) k_union_sparse(const float4* __restric
 // Node-level tail (see node_accumulate): every used component node finds its root, is
 // flattened onto it, and adds its own totals to the root's; then the points of sparse cells
 // (the compact list of k_cellscan) find their roots, are flattened and counted one by one.
-// Only for dense-grid clouds with few sparse cells; the others run k_flat_stats / k_stats.
+// Only for dense-grid clouds with few sparse cells; the others run k_flatten_if + k_tail_stats.
 
 
 

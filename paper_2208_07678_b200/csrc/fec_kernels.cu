@@ -430,7 +430,7 @@ __device__ __forceinline__ void stats_body(const int* __restrict__ parent, const
     }
 }
 // Sparse-dominated clouds (many small components, deep forests: occupied cells > n/4)
-// flatten in a separate pass first; k_flat_stats's walks are then one load each.
+// flatten in a separate pass first; k_tail_stats's walks are then one load each.
 __global__ void __launch_bounds__(256) k_flatten_if(int* __restrict__ parent, int64_t n, const Meta* __restrict__ meta) {
     pdl_prologue();
     if (meta->status || 4 * (int64_t)meta->cells <= n) return;

@@ -96,7 +96,6 @@ __global__ void k_smark(const uint32_t* key0, const uint32_t* key1, int64_t n, u
 __global__ void k_sgather(const float* p, const uint32_t* key0, const int* val0, const uint32_t* key1,
                           const int* val1, int64_t n, const Grid* gp, const uint2* cw, float4* spts, uint32_t* cstart,
                           u64* cocc, int* parent, int* sidx, int* size, int* minidx, const Meta* meta);
-__global__ void k_scount(const uint32_t* cstart, uint32_t* dbits, const Meta* meta, const Grid* gp, int* crec);
 // Counting path, per input point: compact cell id << 6 | fine sub-cell, written by k_dcount2
 // when the cloud has at most kCodeCells occupied cells (read by k_dscatter and k_relabel_in
 // instead of recomputing the cell from the coordinates).
@@ -114,11 +113,6 @@ __global__ void k_celltscan(unsigned long long* tsum, Meta* meta, const Grid* gp
 __global__ void k_cellscan(uint32_t* cstart, uint32_t* cursor, int* dlist, int* crec, uint32_t* cneed0, Meta* meta,
                            const Grid* gp, const unsigned long long* tpre, int* slist, int64_t n, int local_only,
                            int all_parents, int* parent, int* size, int* minidx);
-__global__ void k_ccount(const uint32_t* cstart, uint32_t* dbits, uint32_t* cursor, const Meta* meta,
-                         const Grid* gp, int* crec, uint32_t* cneed0);
-__global__ void k_dbits_popc(const uint32_t* dbits, int64_t words, uint32_t* wcount, const Meta* meta);
-__global__ void k_dbits_list(const uint32_t* dbits, int64_t words, const uint32_t* wpos, int* dlist, int* crec,
-                             Meta* meta);
 // Component node of dense record r, component c (rmask: R - 1 for the record capacity R, a
 // power of two; node ids stay below nbase + 8R).
 __host__ __device__ __forceinline__ int node_of(int nbase, uint32_t rmask, int r, int c) {

@@ -28,7 +28,7 @@ constexpr int SL_SLOTS = 256;
 
 // Per local root r (a sorted position): size[r] = owned members, minidx[r] = min gidx of
 // owned members, ckey[r] = max gidx of boundary members (-1: none).  size/minidx arrive
-// initialised to 0 / INT_MAX by a4; ckey to -1.  Warp- then block-aggregated like k_stats.
+// initialised to 0 / INT_MAX by a4; ckey to -1.  Warp- then block-aggregated like k_tail_stats.
 __global__ void __launch_bounds__(256) k_slab_stats(const int* __restrict__ parent, const int* __restrict__ val,
                                                    const int* __restrict__ gidx, int64_t n, int n_owned,
                                                    int n_first, int* __restrict__ size,

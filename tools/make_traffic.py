@@ -10,8 +10,8 @@ from collections import OrderedDict
 STAGES = {
     "a1_bbox_validate": ["k_bbox", "k_zero"],
     "a2_bin_keys": ["k_lkey", "k_onesweep"],
-    "a3_sort": ["k_cmark", "k_smark", "k_cpop", "k_tscan", "k_cscan", "k_cemit", "k_dcount2", "k_sgather", "k_cellred", "k_celltscan", "k_cellscan", "k_scan_lb", "k_ccount", "k_scount",
-                "k_dbits_popc", "k_dbits_list", "k_dcomps"],
+    "a3_sort": ["k_cmark", "k_smark", "k_cpop", "k_tscan", "k_cscan", "k_cemit", "k_dcount2", "k_sgather", "k_cellred", "k_celltscan", "k_cellscan", "k_scan_lb",
+                "k_dcomps"],
     "a4_gather_init": ["k_dscatter", "k_dinit", "k_dparent"],
     # SURVEY's a6+a7 row: every union kernel, the dense-dense links on the side stream included
     "a6a7_scan_union": ["k_union_sparse", "k_union_sparse_local", "k_dense_link",
