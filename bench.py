@@ -803,6 +803,7 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
     fec.raise_status(status)  # the device status of the timed calls (read after the timed region)
+    digest = full_size_digest(args, w, out) if rank == 0 else None
     # per-stage times (library events at the stage boundaries) in a second pass of the same
     # steps: the events split the stream, so they are kept out of the timed loop
     fec.set_timing(True)
@@ -926,9 +927,31 @@ def main():
         }
         if check is not None:
             line["parity_bit_exact"] = check
+        if digest is not None:
+            line["parity_digest"] = digest
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def full_size_digest(args, w, out):
+    """The last timed step's labels against the ORACLE's stored full-size digest
+    (tests/golden/full_size.json, written by tools/make_full_size_digests.py from synth/ and
+    oracle/ only), after the timed region: the bench line itself says whether the input was
+    the stored cloud and whether the measured step produced the oracle's labels."""
+    if args.scale != 1.0 or args.grid_mode != "auto":
+        return None
+    import hashlib
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "full_size.json")
+    try:
+        ref = json.load(open(path))["configs"][args.config]
+    except (OSError, KeyError, ValueError):
+        return None
+    in_sha = synth.sha256_f32(w.points)
+    lab = np.ascontiguousarray(out.cpu().numpy(), dtype="<i4")
+    return {"input_sha256": in_sha, "input_matches_golden": in_sha == ref["input_sha256"],
+            "labels_match_oracle_digest": hashlib.sha256(lab.tobytes()).hexdigest() == ref["labels_sha256"],
+            "source": "tests/golden/full_size.json (oracle labels, sha256)"}
 
 
 if __name__ == "__main__":

@@ -49,6 +49,9 @@ def test_default_arm_line_small_config():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    # the timed step's labels against the oracle's stored full-size digest (tests/golden)
+    pd = d["parity_digest"]
+    assert pd["input_matches_golden"] is True and pd["labels_match_oracle_digest"] is True
 
 
 @pytest.mark.gpu
