@@ -234,15 +234,10 @@ __global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int6
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // software-pipelined: the next tile's 48 bytes per lane are in flight while this tile's
-    // cells are computed and marked
-    int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128;
-    Pts4 P;
-    if (t0 < n) load_pts4(p, n, t0 + 4 * lane, vec, P);
-    for (; t0 < n; t0 += nw * 128) {
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; t0 < n; t0 += nw * 128) {
         const int64_t b4 = t0 + 4 * lane;
-        Pts4 Pn;
-        if (t0 + nw * 128 < n) load_pts4(p, n, b4 + nw * 128, vec, Pn);
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
         uint32_t w0 = 0xffffffffu, bits0 = 0u;  // the thread's first run
         uint32_t w = 0xffffffffu, bits = 0u;     // the current (later) run
         u64 prev_pc = ~0ull;
@@ -275,7 +270,6 @@ __global__ void __launch_bounds__(256) k_cmark(const float* __restrict__ p, int6
         const unsigned peers = __match_any_sync(0xffffffffu, w0);
         const uint32_t all = __reduce_or_sync(peers, bits0);
         if (w0 != 0xffffffffu && lane == __ffs(peers) - 1) atomicOr(reinterpret_cast<unsigned int*>(cw + w0), all);
-        P = Pn;
     }
 }
 
@@ -570,13 +564,10 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
     __syncwarp();
     const bool vec = (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWTile;
-    Pts4 P;  // software-pipelined like k_cmark
-    if (t0 < n) load_pts4(p, n, t0 + 4 * lane, vec, P);
-    for (; t0 < n; t0 += nw * kWTile) {
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kWTile; t0 < n; t0 += nw * kWTile) {
         const int64_t b4 = t0 + 4 * lane;
-        Pts4 Pn;
-        if (t0 + nw * kWTile < n) load_pts4(p, n, b4 + nw * kWTile, vec, Pn);
+        Pts4 P;
+        load_pts4(p, n, b4, vec, P);
         // runs of this thread's points in one cell take one table update
         // (a run's first point has its smallest input index)
         uint32_t code[4] = {0u, 0u, 0u, 0u};
@@ -633,7 +624,6 @@ __global__ void __launch_bounds__(256) k_dcount2(const float* __restrict__ p, in
         __syncwarp();
         if (lane == 0) *nused = 0;
         __syncwarp();
-        P = Pn;
     }
 }
 
@@ -2123,20 +2113,12 @@ __global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p,
     // cells <= n/4 and the key-sort path writes none)
     const bool rcode = !g.key_sort && meta->cells <= kCodeCells;
     const int64_t groups = (n + 3) / 4;
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    // codes software-pipelined: the next group's 16 bytes are in flight during this group's
-    // dependent record / label loads
-    uint32_t cnext[4] = {0u, 0u, 0u, 0u};
-    int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (rcode && gi < groups) load4(pcode, 4 * gi, n, cnext);
-    for (; gi < groups; gi += gstride) {
+    for (int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b4 = 4 * gi;
         int rv[4], q[4];
         uint32_t cid[4];
         if (rcode) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) cid[j] = cnext[j];
-            if (gi + gstride < groups) load4(pcode, b4 + 4 * gstride, n, cnext);
+            load4(pcode, b4, n, cid);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 q[j] = (int)(cid[j] & 63u);
