@@ -1289,7 +1289,7 @@ __device__ __forceinline__ bool queue_item(const DenseCtx& C, int4 it) {
 // k_dense_link: every forward dense neighbour ("DD" list) and every sparse neighbour in either
 // direction, plus slot 26 = its own component pairs when it has several ("DS" list).  Absent
 // and backward-dense neighbours produce nothing, so the link kernel's threads all have work.
-// Items are block-aggregated (one atomic per list per block) into two halves of `litems`; if a
+// Items are warp-aggregated (one atomic per list per warp) into two halves of `litems`; if a
 // half overflows, meta->list_overflow makes k_dense_link (main stream) redo every (record, slot).
 __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, const uint2* __restrict__ cw,
                                                int* __restrict__ crec,
@@ -1306,11 +1306,9 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
     // the key path's stable sort puts it first in the cell)
     const bool nstats = node_stats && 4 * (int64_t)C.meta->cells <= (int64_t)C.nbase;
     __shared__ signed char soff[26][3];
-    __shared__ int wsum[256 / kWarp][2];
-    __shared__ int bbase[2];
     if (threadIdx.x < 26 * 3) (&soff[0][0])[threadIdx.x] = (&c_slot[0][0])[threadIdx.x];
     __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int nd = C.meta->ndense;
     for (int r0 = blockIdx.x * blockDim.x; r0 < nd; r0 += gridDim.x * blockDim.x) {  // block-uniform
         const int r = r0 + threadIdx.x;
@@ -1379,23 +1377,16 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
                 xds += yds;
             }
         }
+        // warp-aggregated reservation (no block barrier waits on the atomics' round trip)
+        int bdd = 0, bds = 0;
         if (lane == 31) {
-            wsum[w][0] = xdd;
-            wsum[w][1] = xds;
+            bdd = xdd ? atomicAdd(&C.meta->ndd, xdd) : 0;
+            bds = xds ? atomicAdd(&C.meta->nds, xds) : 0;
+            if ((xdd && bdd + xdd > lhalf) || (xds && bds + xds > lhalf)) atomicOr(&C.meta->list_overflow, 1);
         }
-        __syncthreads();
-        if (threadIdx.x < 2) {
-            int tot = 0;
-            for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) {
-                const int t = wsum[ww][threadIdx.x];
-                wsum[ww][threadIdx.x] = tot;
-                tot += t;
-            }
-            bbase[threadIdx.x] = tot ? atomicAdd(threadIdx.x == 0 ? &C.meta->ndd : &C.meta->nds, tot) : 0;
-            if (tot && bbase[threadIdx.x] + tot > lhalf) atomicOr(&C.meta->list_overflow, 1);
-        }
-        __syncthreads();
-        int pdd = bbase[0] + wsum[w][0] + xdd - cdd, pds = bbase[1] + wsum[w][1] + xds - cds;
+        bdd = __shfl_sync(0xffffffffu, bdd, 31);
+        bds = __shfl_sync(0xffffffffu, bds, 31);
+        int pdd = bdd + xdd - cdd, pds = bds + xds - cds;
         if (pdd + cdd <= lhalf && pds + cds <= lhalf) {
             uint32_t m = mdd;
             while (m) {
@@ -1418,7 +1409,6 @@ __global__ void __launch_bounds__(256) k_dcomps(const Grid* __restrict__ gp, con
                 litems[lhalf + pds++] = make_uint4((uint32_t)r, (uint32_t)k, cq, 0u);
             }
         }
-        __syncthreads();  // wsum / bbase are reused
     }
 }
 
