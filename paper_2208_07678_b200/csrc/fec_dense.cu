@@ -2131,7 +2131,7 @@ __global__ void __launch_bounds__(256) k_relabel_in(const float* __restrict__ p,
         int rv[4], q[4];
         uint32_t cid[4];
         if (rcode) {
-            load4(pcode, b4, n, cid);
+            load4_stream(pcode, b4, n, cid);  // (read once: no L1 allocation, the L1 keeps crec)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 q[j] = (int)(cid[j] & 63u);
