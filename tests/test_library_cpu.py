@@ -169,3 +169,19 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in src.replace("oracle/", "").lower() or f == "__init__.py" and "import oracle" not in src, f
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_schedule_switches_of_the_t6_test_exist_in_the_library():
+    """tests/test_gpu_schedules.py perturbs the launch schedule through environment switches; a
+    renamed switch would silently turn that test into a plain rerun."""
+    import glob
+    import importlib.util
+    import re
+    here = os.path.dirname(os.path.abspath(__file__))
+    spec = importlib.util.spec_from_file_location("t6", os.path.join(here, "test_gpu_schedules.py"))
+    t6 = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(t6)
+    src = "".join(open(f).read() for f in glob.glob(os.path.join(here, "..", "paper_2208_07678_b200", "csrc", "*.cu*")))
+    known = set(re.findall(r'getenv\("(FEC_[A-Z_]+)"\)', src))
+    used = {k for env in t6.SCHEDULES.values() for k in env if not k.startswith("_")}
+    assert used and used <= known, (used - known)
