@@ -118,6 +118,25 @@ def test_full_size_label_digest(fec, name):
         f"{name}: labels differ from the oracle's (noise {(lab < 0).sum()} vs {ref['noise']})")
 
 
+@pytest.mark.parametrize("name,gmode", [("C3", 1), ("C3", 2), ("C3", 3), ("C4", 1), ("C4", 2), ("C4", 3)])
+def test_full_size_label_digest_forced_grid_modes(fec, name, gmode):
+    """The paths the automatic plan does not take at full size -- hashed cell index (1), key
+    sort (2), counting sort (3) forced on the 9M / 27M-point configs -- against the same stored
+    oracle digests (the scaled configs reach these paths too, but with 50x fewer cells, tiles
+    and radix buckets)."""
+    import hashlib
+    ref = json.load(open(os.path.join(GOLDEN, "full_size.json")))["configs"][name]
+    w = synth.make_config(name)
+    assert synth.sha256_f32(w.points) == ref["input_sha256"], f"{name}: input differs"
+    fec.set_grid_mode(gmode)
+    try:
+        lab = np.ascontiguousarray(run_gpu(fec, w.points, w.d_th, w.min_size, w.max_size), dtype="<i4")
+    finally:
+        fec.set_grid_mode(0)
+    assert hashlib.sha256(lab.tobytes()).hexdigest() == ref["labels_sha256"], (
+        f"{name} mode {gmode}: labels differ from the oracle's (noise {(lab < 0).sum()} vs {ref['noise']})")
+
+
 @pytest.mark.parametrize("name,scale", [("C3", 0.05), ("C4", 0.02), ("C5", 0.02)])
 def test_config_scaled(fec, mode, name, scale):
     w = synth.make_config(name, scale=scale)
