@@ -540,7 +540,9 @@ fec_status_t run_core(const float* pts, int64_t n, float d, float t2, void* ws, 
     ++launches;
 
     const unsigned ew = grid_for(n, 256, cap * 4);
-    const unsigned ew4 = grid_for((n + 3) / 4, 256, cap * 4);  // kernels taking 4 points per thread
+    // k_dinit (4 points per thread, grid-stride): one full-occupancy wave -- on node-tail clouds the
+    // device plan turns it into a no-op, and a 4-wave grid of returning blocks cost ~11 us there
+    const unsigned ew4 = grid_for((n + 3) / 4, 256, cap);
     const int64_t dwords = n / 32 + 1;
     const unsigned wb = grid_for(dwords + 1, 256, cap * 4);
     const unsigned wt = grid_for((n + kWarp * 4 - 1) / (kWarp * 4) * kWarp, 256, cap * 4);  // warp tiles
